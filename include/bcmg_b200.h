@@ -1,0 +1,135 @@
+/*
+ * bcmg_b200.h -- C ABI of the B200-native (sm_100a) multi-GPU Cholesky path.
+ *
+ * This is the drop-in boundary for the path named by BASELINE.json's north
+ * star: the row-sharded -> 1D block-cyclic column redistribution and the
+ * tiled potrf + potrs / potri that run on that layout.  It replaces, entry by
+ * entry:
+ *
+ *   bcmg_open / bcmg_close      reference pkg/frontend/src/api.ts:44-62
+ *                               (session = device binding + NCCL communicator
+ *                               instead of a scratch directory)
+ *   bcmg_last_error             api.ts:35-42; codes = errors.ts:9-23 (same
+ *                               numbers, plus BCMG_ERR_CUDA)
+ *   bcmg_potrs                  api.ts:137-154 -> solvers.py:931-985
+ *                               (solve_positive_definite pipeline)
+ *   bcmg_potri                  api.ts:157-165 -> solvers.py:988-1016
+ *                               (invert_positive_definite pipeline)
+ *   bcmg_redistribute           solvers.py:262-273 (redistribute_in/out)
+ *                               -> layout.py:191-256 (execute_plan)
+ *   bcmg_potrf                  solvers.py:341-406 (potrf, LAPACK info)
+ *   bcmg_potrs_factored         solvers.py:430-474 (potrs on the factor)
+ *   bcmg_potri_factored         solvers.py:487-594 (potri on the factor)
+ *   bcmg_build_permutation      layout.py:126-145
+ *   bcmg_decompose_cycles       layout.py:148-172
+ *   bcmg_invert_cycles          layout.py:175-183
+ *   bcmg_column_counts          layout.py:82-95
+ *
+ * Conventions
+ *   - dtype codes follow the reference's ElementType (core.py:69-72):
+ *     0 real32, 1 real64, 2 complex64, 3 complex128 (interleaved re, im).
+ *   - Matrices are column-major.  A distributed matrix of order n is held as
+ *     `ndev` logical-device shards, shard d being n rows x counts[d] columns
+ *     (bcmg_column_counts), leading dimension n.  Each process passes the
+ *     shards of ITS logical devices: ndev/world of them, devices
+ *     rank*ndev/world .. (rank+1)*ndev/world-1.  With world == 1 all logical
+ *     devices live on the session's GPU ("virtual devices").
+ *   - All data pointers are device pointers on the session's GPU; `stream`
+ *     is the caller's cudaStream_t (NULL = legacy default stream).  Work is
+ *     ordered after prior work on `stream` and `stream` is ordered after it;
+ *     calls returning `info` synchronise on `stream`.
+ *   - A session is single-caller: a call that overlaps another call on the
+ *     same session fails with BCMG_ERR_CONFIG (reference ConcurrentCallError,
+ *     runtime.py:449-466).
+ *   - Return value: BCMG_OK or an error code; bcmg_last_error() /
+ *     bcmg_last_error_message() describe the last failure on this thread.
+ */
+#ifndef BCMG_B200_H
+#define BCMG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BCMG_OK 0
+#define BCMG_ERR_NOT_POSITIVE_DEFINITE 1
+#define BCMG_ERR_CONFIG 2
+#define BCMG_ERR_NO_CONVERGENCE 3
+#define BCMG_ERR_OUT_OF_MEMORY 4
+#define BCMG_ERR_CHECK_FAILED 5
+#define BCMG_ERR_STALE_SESSION 6
+#define BCMG_ERR_IO 7
+#define BCMG_ERR_CUDA 8
+
+#define BCMG_R32 0
+#define BCMG_R64 1
+#define BCMG_C64 2
+#define BCMG_C128 3
+
+/* redistribution direction */
+#define BCMG_TO_CYCLIC 0   /* contiguous -> block-cyclic (redistribute_in)  */
+#define BCMG_TO_CONTIG 1   /* block-cyclic -> contiguous (redistribute_out) */
+
+/* pipeline flags */
+#define BCMG_FLAG_ROW_SHARDED 1 /* shards are row blocks of a ROW-major matrix (the
+                                   JAX P("x", None) layout): for complex Hermitian
+                                   input the bytes hold conj(A); handled by solving
+                                   conj(A) conj(x) = conj(b). */
+
+typedef struct bcmg_session bcmg_session;
+
+int bcmg_version(void);
+int bcmg_last_error(void);
+const char* bcmg_last_error_message(void);
+
+/* ---- layout planning (host only, no GPU needed) ---- */
+int bcmg_column_counts(int64_t n_cols, int64_t tile, int ndev, int64_t* counts /* [ndev] */);
+int bcmg_build_permutation(int64_t n_cols, int64_t tile, int ndev, int64_t* dest_of /* [n_cols] */);
+/* members: [n] (cycles concatenated, rotation order); offsets: [n+1] CSR */
+int bcmg_decompose_cycles(int64_t n, const int64_t* dest_of, int64_t* members, int64_t* offsets,
+                          int64_t* n_cycles);
+int bcmg_invert_cycles(int64_t n_cycles, const int64_t* offsets, int64_t* members);
+/* segment width S used by the device plan (S = T at tile-aligned shapes) and
+   the number of moved columns */
+int bcmg_segment_plan_info(int64_t n_cols, int64_t tile, int ndev, int64_t* seg_width, int64_t* n_cycles,
+                           int64_t* moved_columns);
+
+/* ---- sessions ---- */
+int bcmg_nccl_unique_id(unsigned char* id /* [128] */);
+int bcmg_open(int cuda_device, int rank, int world, const unsigned char* nccl_id /* NULL if world==1 */,
+              bcmg_session** out);
+int bcmg_close(bcmg_session* s);
+
+/* ---- pipelines (the reference's FFI routines) ---- */
+/* x overwrites b (n x nrhs, ldb, replicated on every process); A's shards are
+   overwritten by the factor in block-cyclic order. *info = LAPACK pivot. */
+int bcmg_potrs(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t nrhs, int64_t tile, int ndev,
+               void* const* shards, void* b, int64_t ldb, int flags, int* info);
+/* A's shards (contiguous layout) are overwritten by the full Hermitian inverse,
+   contiguous layout. */
+int bcmg_potri(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev, void* const* shards,
+               int flags, int* info);
+
+/* ---- building blocks (the reference's solvers.py routines) ---- */
+int bcmg_redistribute(bcmg_session* s, void* stream, int dtype, int64_t n_rows, int64_t n_cols, int64_t tile,
+                      int ndev, void* const* shards, int direction);
+int bcmg_potrf(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev, void* const* shards,
+               int* info);
+int bcmg_potrs_factored(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t nrhs, int64_t tile, int ndev,
+                        void* const* shards, void* b, int64_t ldb);
+int bcmg_potri_factored(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev,
+                        void* const* shards);
+
+/* ---- measurement ---- */
+/* milliseconds of the last pipeline call: [0] redistribute_in, [1] potrf,
+   [2] potrs/potri(+redistribute_out), [3] total (CUDA events on `stream`) */
+int bcmg_last_timings(bcmg_session* s, float* ms /* [4] */);
+/* algorithmic bytes (read + write) moved by the last redistribution */
+int64_t bcmg_last_moved_bytes(bcmg_session* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BCMG_B200_H */

@@ -1,0 +1,278 @@
+// extern "C" surface of libbcmg_b200.so (declared in include/bcmg_b200.h).
+// Every entry point converts exceptions into the reference's stable error
+// codes (pkg/frontend/src/errors.ts:9-23) and records a per-thread message.
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+
+#include "../../include/bcmg_b200.h"
+#include "ops.h"
+#include "solver.h"
+
+struct bcmg_session {
+  bcmg::Session* impl;
+};
+
+namespace {
+thread_local int g_err = BCMG_OK;
+thread_local std::string g_msg;
+
+int fail(int code, const std::string& msg) {
+  g_err = code;
+  g_msg = msg;
+  return code;
+}
+int ok() {
+  g_err = BCMG_OK;
+  g_msg.clear();
+  return BCMG_OK;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return ok();
+  } catch (const bcmg::Error& e) {
+    return fail(e.code, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(BCMG_ERR_OUT_OF_MEMORY, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(BCMG_ERR_CONFIG, e.what());
+  }
+}
+
+bcmg::Session* live(bcmg_session* s) {
+  if (!s || !s->impl) throw bcmg::Error(BCMG_ERR_STALE_SESSION, "no open session");
+  return s->impl;
+}
+
+// Single-caller contract (reference runtime.py:449-466).
+struct Entry {
+  bcmg::Session* s;
+  explicit Entry(bcmg::Session* s_, void* stream) : s(s_) {
+    bool expected = false;
+    if (!s->busy.compare_exchange_strong(expected, true))
+      throw bcmg::Error(BCMG_ERR_CONFIG, "concurrent call on a single-caller session");
+    s->begin(static_cast<cudaStream_t>(stream));
+  }
+  ~Entry() { s->busy.store(false); }
+};
+
+void check_common(int dtype, int ndev, void* const* shards) {
+  if (bcmg::dtype_size(dtype) == 0) throw bcmg::Error(BCMG_ERR_CONFIG, "unknown element-type code " + std::to_string(dtype));
+  if (ndev < 1) throw bcmg::Error(BCMG_ERR_CONFIG, "need at least one device");
+  if (!shards) throw bcmg::Error(BCMG_ERR_CONFIG, "null shard table");
+}
+
+void finish_timings(bcmg::Session* s, bool has_redist_out) {
+  (void)has_redist_out;
+  BCMG_CUDA(cudaEventSynchronize(s->ev_time[bcmg::T_SOLVE]));
+  float a = 0, b = 0, c = 0;
+  BCMG_CUDA(cudaEventElapsedTime(&a, s->ev_time[bcmg::T_BEGIN], s->ev_time[bcmg::T_REDIST]));
+  BCMG_CUDA(cudaEventElapsedTime(&b, s->ev_time[bcmg::T_REDIST], s->ev_time[bcmg::T_POTRF]));
+  BCMG_CUDA(cudaEventElapsedTime(&c, s->ev_time[bcmg::T_POTRF], s->ev_time[bcmg::T_SOLVE]));
+  s->phase_ms[0] = a;
+  s->phase_ms[1] = b;
+  s->phase_ms[2] = c;
+  s->phase_ms[3] = a + b + c;
+}
+}  // namespace
+
+extern "C" {
+
+int bcmg_version(void) { return 1; }
+int bcmg_last_error(void) { return g_err; }
+const char* bcmg_last_error_message(void) { return g_msg.c_str(); }
+
+int bcmg_column_counts(int64_t n_cols, int64_t tile, int ndev, int64_t* counts) {
+  return guarded([&] {
+    auto c = bcmg::column_counts(n_cols, tile, ndev);
+    std::memcpy(counts, c.data(), c.size() * sizeof(int64_t));
+  });
+}
+
+int bcmg_build_permutation(int64_t n_cols, int64_t tile, int ndev, int64_t* dest_of) {
+  return guarded([&] {
+    bcmg::column_counts(n_cols, tile, ndev);  // validates
+    bcmg::build_dest(n_cols, tile, ndev, dest_of);
+  });
+}
+
+int bcmg_decompose_cycles(int64_t n, const int64_t* dest_of, int64_t* members, int64_t* offsets, int64_t* n_cycles) {
+  return guarded([&] {
+    if (n < 0) throw bcmg::Error(BCMG_ERR_CONFIG, "negative size");
+    std::vector<int64_t> m, o;
+    bcmg::decompose(n, dest_of, m, o);
+    std::memcpy(members, m.data(), m.size() * sizeof(int64_t));
+    std::memcpy(offsets, o.data(), o.size() * sizeof(int64_t));
+    *n_cycles = (int64_t)o.size() - 1;
+  });
+}
+
+int bcmg_invert_cycles(int64_t n_cycles, const int64_t* offsets, int64_t* members) {
+  return guarded([&] {
+    std::vector<int64_t> o(offsets, offsets + n_cycles + 1);
+    std::vector<int64_t> m(members, members + o.back());
+    bcmg::invert_cycles(m, o);
+    std::memcpy(members, m.data(), m.size() * sizeof(int64_t));
+  });
+}
+
+int bcmg_segment_plan_info(int64_t n_cols, int64_t tile, int ndev, int64_t* seg_width, int64_t* n_cycles,
+                           int64_t* moved_columns) {
+  return guarded([&] {
+    auto p = bcmg::segment_plan(n_cols, tile, ndev, false);
+    *seg_width = p.seg;
+    *n_cycles = (int64_t)p.offsets.size() - 1;
+    *moved_columns = (int64_t)p.members.size() * p.seg;
+  });
+}
+
+int bcmg_nccl_unique_id(unsigned char* id) {
+  return guarded([&] {
+    ncclUniqueId u;
+    ncclResult_t r = ncclGetUniqueId(&u);
+    if (r != ncclSuccess) throw bcmg::Error(BCMG_ERR_CUDA, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(u) == 128, "NCCL unique id is 128 bytes");
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+int bcmg_open(int cuda_device, int rank, int world, const unsigned char* nccl_id, bcmg_session** out) {
+  return guarded([&] {
+    if (!out) throw bcmg::Error(BCMG_ERR_CONFIG, "null output handle");
+    *out = nullptr;
+    auto* s = new bcmg_session{nullptr};
+    try {
+      s->impl = new bcmg::Session(cuda_device, rank, world, nccl_id);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int bcmg_close(bcmg_session* s) {
+  return guarded([&] {
+    if (!s || !s->impl) throw bcmg::Error(BCMG_ERR_STALE_SESSION, "no open session");
+    delete s->impl;
+    s->impl = nullptr;
+    delete s;
+  });
+}
+
+int bcmg_redistribute(bcmg_session* s, void* stream, int dtype, int64_t n_rows, int64_t n_cols, int64_t tile, int ndev,
+                      void* const* shards, int direction) {
+  return guarded([&] {
+    auto* S = live(s);
+    check_common(dtype, ndev, shards);
+    if (direction != BCMG_TO_CYCLIC && direction != BCMG_TO_CONTIG)
+      throw bcmg::Error(BCMG_ERR_CONFIG, "unknown redistribution direction");
+    Entry e(S, stream);
+    S->redistribute(dtype, n_rows, n_cols, tile, ndev, shards, direction == BCMG_TO_CONTIG);
+  });
+}
+
+int bcmg_potrf(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev, void* const* shards,
+               int* info) {
+  return guarded([&] {
+    auto* S = live(s);
+    check_common(dtype, ndev, shards);
+    Entry e(S, stream);
+    *info = S->potrf(dtype, n, tile, ndev, shards);
+  });
+}
+
+int bcmg_potrs_factored(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t nrhs, int64_t tile, int ndev,
+                        void* const* shards, void* b, int64_t ldb) {
+  return guarded([&] {
+    auto* S = live(s);
+    check_common(dtype, ndev, shards);
+    Entry e(S, stream);
+    S->potrs(dtype, n, nrhs, tile, ndev, shards, b, ldb);
+  });
+}
+
+int bcmg_potri_factored(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev,
+                        void* const* shards) {
+  return guarded([&] {
+    auto* S = live(s);
+    check_common(dtype, ndev, shards);
+    Entry e(S, stream);
+    S->potri(dtype, n, tile, ndev, shards);
+  });
+}
+
+int bcmg_potrs(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t nrhs, int64_t tile, int ndev,
+               void* const* shards, void* b, int64_t ldb, int flags, int* info) {
+  int rc = guarded([&] {
+    auto* S = live(s);
+    check_common(dtype, ndev, shards);
+    if (nrhs < 1) throw bcmg::Error(BCMG_ERR_CONFIG, "right-hand side must be non-empty");
+    if (ldb < n) throw bcmg::Error(BCMG_ERR_CONFIG, "ldb < n");
+    if (tile < 1 || tile > n) throw bcmg::Error(BCMG_ERR_CONFIG, "tile width out of range");
+    Entry e(S, stream);
+    const bool conj = (flags & BCMG_FLAG_ROW_SHARDED) && bcmg::dtype_complex(dtype);
+    S->mark(bcmg::T_BEGIN);
+    if (conj) bcmg::conj2d(dtype, b, ldb, n, nrhs, S->user);
+    S->redistribute(dtype, n, n, tile, ndev, shards, false);
+    S->mark(bcmg::T_REDIST);
+    *info = S->potrf(dtype, n, tile, ndev, shards);
+    S->mark(bcmg::T_POTRF);
+    if (*info) {
+      S->mark(bcmg::T_SOLVE);
+      finish_timings(S, false);
+      throw bcmg::Error(BCMG_ERR_NOT_POSITIVE_DEFINITE,
+                        "matrix is not positive definite: leading minor of order " + std::to_string(*info) +
+                            " (pivot=" + std::to_string(*info) + ")");
+    }
+    S->begin(S->user);
+    S->potrs(dtype, n, nrhs, tile, ndev, shards, b, ldb);
+    if (conj) bcmg::conj2d(dtype, b, ldb, n, nrhs, S->user);
+    S->mark(bcmg::T_SOLVE);
+    finish_timings(S, false);
+  });
+  return rc;
+}
+
+int bcmg_potri(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev, void* const* shards,
+               int flags, int* info) {
+  (void)flags;  // inv(conj(A)) = conj(inv(A)) is the row-major view of inv(A): no fix-up needed
+  return guarded([&] {
+    auto* S = live(s);
+    check_common(dtype, ndev, shards);
+    if (tile < 1 || tile > n) throw bcmg::Error(BCMG_ERR_CONFIG, "tile width out of range");
+    Entry e(S, stream);
+    S->mark(bcmg::T_BEGIN);
+    S->redistribute(dtype, n, n, tile, ndev, shards, false);
+    S->mark(bcmg::T_REDIST);
+    *info = S->potrf(dtype, n, tile, ndev, shards);
+    S->mark(bcmg::T_POTRF);
+    if (*info) {
+      S->mark(bcmg::T_SOLVE);
+      finish_timings(S, true);
+      throw bcmg::Error(BCMG_ERR_NOT_POSITIVE_DEFINITE,
+                        "matrix is not positive definite: leading minor of order " + std::to_string(*info) +
+                            " (pivot=" + std::to_string(*info) + ")");
+    }
+    S->begin(S->user);
+    S->potri(dtype, n, tile, ndev, shards);
+    S->redistribute(dtype, n, n, tile, ndev, shards, true);
+    S->mark(bcmg::T_SOLVE);
+    finish_timings(S, true);
+  });
+}
+
+int bcmg_last_timings(bcmg_session* s, float* ms) {
+  return guarded([&] {
+    auto* S = live(s);
+    for (int i = 0; i < 4; ++i) ms[i] = S->phase_ms[i];
+  });
+}
+
+int64_t bcmg_last_moved_bytes(bcmg_session* s) { return (s && s->impl) ? s->impl->last_moved_bytes : -1; }
+
+}  // extern "C"

@@ -1,0 +1,378 @@
+// FP64 tensor-core (DMMA) block GEMM for sm_100a.
+//
+// The only dense contraction of the Cholesky path is a GEMM of the form
+//     C := alpha * Ahat * Bhat^T + beta * C
+// where Ahat (M x K) and Bhat (N x K) are logical views of column-major
+// storage (see Operand).  On sm_100a there is no tcgen05 kind::f64, so FP64
+// tensor work is warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), fed from
+// shared memory laid out k-major ([k][i], i contiguous) with a 4-word row
+// pad so every 8x4 fragment load is bank-conflict free.  Complex operands are
+// split into re/im planes and contracted with 4 real DMMAs per step;
+// float/complex64 storage is widened to FP64 on the way into shared memory.
+//
+// Two operand feeders:
+//   * CP  : cp.async 16-byte copies into a STAGES-deep ring (real double,
+//           natural orientation, 16-byte aligned) -- the hot trailing update
+//           and panel TRSM of potrf;
+//   * REG : register-staged loads with conversion / conjugation /
+//           transposition / triangular masks, double buffered -- every other
+//           shape.
+#pragma once
+
+#include "common.cuh"
+
+namespace bcmg {
+
+enum Op : int { OP_N = 0, OP_C = 1 };
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ int ld_flag(const int* p) { return p ? *(volatile const int*)p : 0; }
+
+// Logical operand: element (i, k) of Xhat.
+struct Operand {
+  const void* ptr;
+  int64_t ld;
+  int trans;         // 0: Xhat(i,k) = X[i + k*ld]   1: Xhat(i,k) = X[k + i*ld]
+  int conj;          // conjugate on load
+  int mask;          // 1: element read as 0 unless storage_row + mask_off >= storage_col
+  int64_t mask_off;  //    (a lower-triangular view of the stored matrix)
+};
+
+// op(A): A is M x K (op N) or K x M (op C) column-major.
+inline Operand opA(const void* p, int64_t ld, int op) {
+  return Operand{p, ld, op == OP_C ? 1 : 0, op == OP_C ? 1 : 0, 0, 0};
+}
+// op(B): B is K x N (op N) or N x K (op C) column-major.
+inline Operand opB(const void* p, int64_t ld, int op) {
+  return Operand{p, ld, op == OP_N ? 1 : 0, op == OP_C ? 1 : 0, 0, 0};
+}
+
+struct Epilogue {
+  void* C;
+  int64_t ldc;
+  double alpha, beta;
+  int lower_only;      // store only where row - col >= lower_off
+  int64_t lower_off;
+};
+
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+struct Tile {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
+  static constexpr int FM = WM / 8, FN = WN / 8;
+  static constexpr int LDA = BM + 4, LDB = BN + 4;  // 8-byte words; == 4 (mod 16)
+  static_assert(LDA % 16 == 4 && LDB % 16 == 4, "row pad must be 4 words mod 16");
+  static constexpr int A_WORDS = BK * LDA, B_WORDS = BK * LDB;
+  static constexpr int STAGE_WORDS = A_WORDS + B_WORDS;
+};
+
+template <class TL, bool CPLX, bool CP>
+constexpr size_t gemm_smem_bytes() {
+  return CP ? (size_t)TL::STAGES * TL::STAGE_WORDS * 8 : (size_t)2 * TL::STAGE_WORDS * 8 * (CPLX ? 2 : 1);
+}
+
+// ----------------------------------------------------------------- accumulators
+template <class TL, bool CPLX>
+struct Acc {
+  double re[TL::FM][TL::FN][2];
+  double im[CPLX ? TL::FM : 1][CPLX ? TL::FN : 1][2];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int a = 0; a < TL::FM; ++a)
+#pragma unroll
+      for (int b = 0; b < TL::FN; ++b) {
+        re[a][b][0] = re[a][b][1] = 0.0;
+        if constexpr (CPLX) im[a][b][0] = im[a][b][1] = 0.0;
+      }
+  }
+};
+
+// One BK slice of DMMAs out of shared memory (planes: real or re/im).
+template <class TL, bool CPLX>
+__device__ __forceinline__ void mma_slice(Acc<TL, CPLX>& acc, const double* __restrict__ As,
+                                          const double* __restrict__ Bs, const double* __restrict__ Asi,
+                                          const double* __restrict__ Bsi, int wm0, int wn0, int lane) {
+  const int r = lane >> 2, q = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < TL::BK; kk += 4) {
+    double a[TL::FM], b[TL::FN];
+    double ai[CPLX ? TL::FM : 1], bi[CPLX ? TL::FN : 1];
+#pragma unroll
+    for (int f = 0; f < TL::FM; ++f) {
+      a[f] = As[(kk + q) * TL::LDA + wm0 + f * 8 + r];
+      if constexpr (CPLX) ai[f] = Asi[(kk + q) * TL::LDA + wm0 + f * 8 + r];
+    }
+#pragma unroll
+    for (int f = 0; f < TL::FN; ++f) {
+      b[f] = Bs[(kk + q) * TL::LDB + wn0 + f * 8 + r];
+      if constexpr (CPLX) bi[f] = Bsi[(kk + q) * TL::LDB + wn0 + f * 8 + r];
+    }
+#pragma unroll
+    for (int fm = 0; fm < TL::FM; ++fm)
+#pragma unroll
+      for (int fn = 0; fn < TL::FN; ++fn) {
+        dmma(acc.re[fm][fn][0], acc.re[fm][fn][1], a[fm], b[fn]);
+        if constexpr (CPLX) {
+          dmma(acc.re[fm][fn][0], acc.re[fm][fn][1], -ai[fm], bi[fn]);
+          dmma(acc.im[fm][fn][0], acc.im[fm][fn][1], a[fm], bi[fn]);
+          dmma(acc.im[fm][fn][0], acc.im[fm][fn][1], ai[fm], b[fn]);
+        }
+      }
+  }
+}
+
+// ----------------------------------------------------------------- REG feeder
+template <class S, int BI, int BK, int THREADS>
+struct RegFeed {
+  static constexpr bool CPLX = Traits<S>::cplx;
+  static constexpr int E = BI * BK / THREADS;
+  static_assert(E * THREADS == BI * BK, "tile not divisible by threads");
+  double vr[E];
+  double vi[CPLX ? E : 1];
+
+  __device__ __forceinline__ void load(const Operand& op, int64_t I, int64_t K, int64_t i0, int64_t k0, int tid) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int idx = tid + e * THREADS;
+      const int il = op.trans ? idx / BK : idx % BI;
+      const int kl = op.trans ? idx % BK : idx / BI;
+      const int64_t i = i0 + il, k = k0 + kl;
+      double2 v = make_double2(0.0, 0.0);
+      // storage coordinates: natural (row i, col k), transposed (row k, col i)
+      const int64_t srow = op.trans ? k : i, scol = op.trans ? i : k;
+      if (i < I && k < K && (!op.mask || srow + op.mask_off >= scol)) {
+        const S* p = reinterpret_cast<const S*>(op.ptr) + (op.trans ? (k + i * op.ld) : (i + k * op.ld));
+        v = to_c(*p);
+        if (op.conj) v.y = -v.y;
+      }
+      vr[e] = v.x;
+      if constexpr (CPLX) vi[e] = v.y;
+    }
+  }
+  __device__ __forceinline__ void store(const Operand& op, double* Xs, double* Xsi, int LD, int tid) const {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int idx = tid + e * THREADS;
+      const int il = op.trans ? idx / BK : idx % BI;
+      const int kl = op.trans ? idx % BK : idx / BI;
+      Xs[kl * LD + il] = vr[e];
+      if constexpr (CPLX) Xsi[kl * LD + il] = vi[e];
+    }
+  }
+};
+
+// ----------------------------------------------------------------- CP feeder
+// Real double, natural orientation (Xhat(i,k) = X[i + k*ld]), X 16B aligned,
+// ld even.  Out-of-range elements are zero-filled by cp.async src-size.
+template <int BI, int BK, int THREADS>
+__device__ __forceinline__ void cp_feed(const Operand& op, int64_t I, int64_t K, int64_t i0, int64_t k0,
+                                        double* Xs, int LD, int tid) {
+  constexpr int CH = (BI / 2) * BK;  // 16-byte chunks per stage
+  static_assert(CH % THREADS == 0, "chunks not divisible by threads");
+  const double* base = reinterpret_cast<const double*>(op.ptr);
+#pragma unroll
+  for (int c = 0; c < CH / THREADS; ++c) {
+    const int idx = tid + c * THREADS;
+    const int il = (idx % (BI / 2)) * 2, kl = idx / (BI / 2);
+    const int64_t i = i0 + il, k = k0 + kl;
+    int64_t rem = I - i;
+    int bytes = (k < K && rem > 0) ? (rem >= 2 ? 16 : 8) : 0;
+    const double* src = bytes ? base + i + k * op.ld : base;
+    cp_async16(Xs + kl * LD + il, src, bytes);
+  }
+}
+
+// ----------------------------------------------------------------- epilogue
+template <class S, class TL, bool CPLX>
+__device__ __forceinline__ void store_block(const Acc<TL, CPLX>& acc, const Epilogue& ep, int64_t M, int64_t N,
+                                            int64_t m0, int64_t n0, int wm0, int wn0, int lane) {
+  const int r = lane >> 2, q = lane & 3;
+  S* C = reinterpret_cast<S*>(ep.C);
+#pragma unroll
+  for (int fm = 0; fm < TL::FM; ++fm)
+#pragma unroll
+    for (int fn = 0; fn < TL::FN; ++fn)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int64_t row = m0 + wm0 + fm * 8 + r;
+        const int64_t col = n0 + wn0 + fn * 8 + 2 * q + j;
+        if (row < M && col < N && (!ep.lower_only || row - col >= ep.lower_off)) {
+          S* c = C + row + col * ep.ldc;
+          double2 v = make_double2(ep.alpha * acc.re[fm][fn][j], 0.0);
+          if constexpr (CPLX) v.y = ep.alpha * acc.im[fm][fn][j];
+          if (ep.beta != 0.0) {
+            double2 o = to_c(*c);
+            v.x += ep.beta * o.x;
+            v.y += ep.beta * o.y;
+          }
+          *c = from_c<S>(v);
+        }
+      }
+}
+
+// ----------------------------------------------------------------- block GEMM
+// Computes the BM x BN block at (m0, n0) of C := alpha*Ahat*Bhat^T + beta*C.
+template <class S, class TL, bool CP>
+__device__ __forceinline__ void gemm_block(const Operand& A, const Operand& B, int64_t M, int64_t N, int64_t K,
+                                           int64_t m0, int64_t n0, const Epilogue& ep, double* smem) {
+  constexpr bool CPLX = Traits<S>::cplx;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm0 = (warp % TL::WARPS_M) * TL::WM, wn0 = (warp / TL::WARPS_M) * TL::WN;
+  const int KT = (int)((K + TL::BK - 1) / TL::BK);
+  Acc<TL, CPLX> acc;
+  acc.zero();
+
+  if constexpr (CP) {
+    static_assert(!CPLX, "cp.async feeder is real-only");
+    // prologue: STAGES-1 slices in flight
+#pragma unroll
+    for (int s = 0; s < TL::STAGES - 1; ++s) {
+      if (s < KT) {
+        double* st = smem + s * TL::STAGE_WORDS;
+        cp_feed<TL::BM, TL::BK, TL::THREADS>(A, M, K, m0, (int64_t)s * TL::BK, st, TL::LDA, tid);
+        cp_feed<TL::BN, TL::BK, TL::THREADS>(B, N, K, n0, (int64_t)s * TL::BK, st + TL::A_WORDS, TL::LDB, tid);
+      }
+      cp_async_commit();
+    }
+    for (int kt = 0; kt < KT; ++kt) {
+      cp_async_wait<TL::STAGES - 2>();
+      __syncthreads();
+      const int nk = kt + TL::STAGES - 1;
+      if (nk < KT) {
+        double* st = smem + (nk % TL::STAGES) * TL::STAGE_WORDS;
+        cp_feed<TL::BM, TL::BK, TL::THREADS>(A, M, K, m0, (int64_t)nk * TL::BK, st, TL::LDA, tid);
+        cp_feed<TL::BN, TL::BK, TL::THREADS>(B, N, K, n0, (int64_t)nk * TL::BK, st + TL::A_WORDS, TL::LDB, tid);
+      }
+      cp_async_commit();
+      const double* st = smem + (kt % TL::STAGES) * TL::STAGE_WORDS;
+      mma_slice<TL, false>(acc, st, st + TL::A_WORDS, nullptr, nullptr, wm0, wn0, lane);
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+  } else {
+    RegFeed<S, TL::BM, TL::BK, TL::THREADS> fa;
+    RegFeed<S, TL::BN, TL::BK, TL::THREADS> fb;
+    constexpr int PLANE = TL::STAGE_WORDS;  // re plane size per buffer
+    auto bufA = [&](int b) { return smem + b * PLANE * (CPLX ? 2 : 1); };
+    fa.load(A, M, K, m0, 0, tid);
+    fb.load(B, N, K, n0, 0, tid);
+    {
+      double* s0 = bufA(0);
+      fa.store(A, s0, s0 + PLANE, TL::LDA, tid);
+      fb.store(B, s0 + TL::A_WORDS, s0 + PLANE + TL::A_WORDS, TL::LDB, tid);
+    }
+    __syncthreads();
+    for (int kt = 0; kt < KT; ++kt) {
+      const bool more = kt + 1 < KT;
+      if (more) {
+        fa.load(A, M, K, m0, (int64_t)(kt + 1) * TL::BK, tid);
+        fb.load(B, N, K, n0, (int64_t)(kt + 1) * TL::BK, tid);
+      }
+      const double* s = bufA(kt & 1);
+      mma_slice<TL, CPLX>(acc, s, s + TL::A_WORDS, s + PLANE, s + PLANE + TL::A_WORDS, wm0, wn0, lane);
+      if (more) {
+        double* d = bufA((kt + 1) & 1);
+        fa.store(A, d, d + PLANE, TL::LDA, tid);
+        fb.store(B, d + TL::A_WORDS, d + PLANE + TL::A_WORDS, TL::LDB, tid);
+      }
+      __syncthreads();
+    }
+  }
+  store_block<S, TL, CPLX>(acc, ep, M, N, m0, n0, wm0, wn0, lane);
+}
+
+// ----------------------------------------------------------------- front-ends
+// Single GEMM: grid (ceil(M/BM), ceil(N/BN)).
+template <class S, class TL, bool CP>
+__global__ void __launch_bounds__(TL::THREADS) gemm_kernel(Operand A, Operand B, int64_t M, int64_t N, int64_t K,
+                                                            Epilogue ep, const int* info) {
+  if (ld_flag(info)) return;
+  extern __shared__ __align__(16) double smem[];
+  gemm_block<S, TL, CP>(A, B, M, N, K, (int64_t)blockIdx.x * TL::BM, (int64_t)blockIdx.y * TL::BN, ep, smem);
+}
+
+// Trailing update of potrf step k on this process's shards:
+//   for every local tile m in [m_first, m_last):
+//     A_m[ms:N, :] -= P[ms:N, :] * P[ms:ms+tc_m, :]^H
+// (reference solvers.py:395-405, restricted to the rows the lower triangle
+// reads).  Persistent grid, static round-robin over the lower-trapezoid
+// blocks of all tiles, tile-major so co-resident CTAs share panel rows.
+constexpr int MAX_LOCAL_DEV = 16;
+struct TrailParams {
+  const void* P;      // panel, element (r, c) at P[r + c*ldp], r = global row - prow0
+  int64_t ldp, prow0;
+  int64_t N, T, K;    // matrix order, tile width, panel width
+  int D, dev0, nloc;  // logical devices; this launch owns dev0 .. dev0+nloc-1
+  void* shards[MAX_LOCAL_DEV];
+  int64_t m_first, m_last;
+};
+
+template <int B>
+__device__ __forceinline__ int64_t trail_blocks(int64_t rows, int64_t tc) {
+  const int64_t nrb = (rows + B - 1) / B, ncb = (tc + B - 1) / B;
+  return nrb <= ncb ? nrb * (nrb + 1) / 2 : ncb * (ncb + 1) / 2 + (nrb - ncb) * ncb;
+}
+
+template <class S, class TL, bool CP>
+__global__ void __launch_bounds__(TL::THREADS) trail_kernel(TrailParams p, const int* info) {
+  static_assert(TL::BM == TL::BN, "trailing decode assumes square blocks");
+  constexpr int B = TL::BM;
+  if (ld_flag(info)) return;
+  extern __shared__ __align__(16) double smem[];
+  const S* P = reinterpret_cast<const S*>(p.P);
+  int64_t m = p.m_first, base = 0, cnt = -1;
+  for (int64_t item = blockIdx.x;; item += gridDim.x) {
+    // advance the tile cursor (monotone: items only grow)
+    for (;;) {
+      if (m >= p.m_last) return;
+      const int dev = (int)(m % p.D);
+      const bool local = dev >= p.dev0 && dev < p.dev0 + p.nloc;
+      if (local) {
+        if (cnt < 0) {
+          const int64_t ms = m * p.T;
+          cnt = trail_blocks<B>(p.N - ms, (p.T < p.N - ms ? p.T : p.N - ms));
+        }
+        if (item < base + cnt) break;
+        base += cnt;
+      }
+      ++m;
+      cnt = -1;
+    }
+    const int64_t ms = m * p.T, rows = p.N - ms, tc = p.T < rows ? p.T : rows;
+    const int64_t ncb = (tc + B - 1) / B;
+    int64_t b = item - base, rb, cb;
+    const int64_t tri = ncb * (ncb + 1) / 2;
+    if (b < tri) {
+      rb = 0;
+      while ((rb + 1) * (rb + 2) / 2 <= b) ++rb;
+      cb = b - rb * (rb + 1) / 2;
+    } else {
+      rb = ncb + (b - tri) / ncb;
+      cb = (b - tri) % ncb;
+    }
+    const int dev = (int)(m % p.D);
+    S* shard = reinterpret_cast<S*>(p.shards[dev - p.dev0]);
+    const int64_t loc = (m / p.D) * p.T;
+    Operand A{P + (ms - p.prow0), p.ldp, 0, 0, 0, 0};
+    Operand Bo{P + (ms - p.prow0), p.ldp, 0, 1, 0, 0};
+    Epilogue ep{shard + ms + loc * p.N, p.N, -1.0, 1.0, 0, 0};
+    gemm_block<S, TL, CP>(A, Bo, rows, tc, p.K, rb * B, cb * B, ep, smem);
+    __syncthreads();
+  }
+}
+
+}  // namespace bcmg

@@ -1,0 +1,478 @@
+// Kernels and launchers of the bcmg B200 library (sm_100a):
+//   * GEMM dispatch onto the DMMA block kernels of gemm.cuh,
+//   * the potrf trailing update launcher,
+//   * the diagonal-tile factor+inverse (leaf kernel + recursive GEMM driver),
+//   * the in-place cycle rotation of the block-cyclic redistribution,
+//   * small copy / conjugate / mirror helpers.
+#include <algorithm>
+#include <type_traits>
+
+#include "ops.h"
+
+namespace bcmg {
+
+// ============================================================== GEMM dispatch
+using TileBig = Tile<128, 128, 16, 64, 32, 4>;    // 256 threads, hot real path
+using TileMed = Tile<64, 64, 16, 32, 32, 3>;      // 128 threads, general
+using TileNarrow = Tile<128, 16, 16, 32, 16, 3>;  // 128 threads, N <= 16 (RHS blocks)
+
+static int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+template <class K>
+static void set_smem(K kernel, size_t bytes) {
+  // idempotent; cheap enough to call per launch but cache per kernel anyway
+  static thread_local std::vector<const void*> done;
+  const void* key = reinterpret_cast<const void*>(kernel);
+  if (std::find(done.begin(), done.end(), key) != done.end()) return;
+  BCMG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  done.push_back(key);
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static bool cp_ok(const Operand& X) {
+  return !X.trans && !X.mask && aligned16(X.ptr) && (X.ld % 2 == 0);
+}
+
+template <class S, class TL, bool CP>
+static void launch_gemm(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+                        const int* info, cudaStream_t st) {
+  constexpr size_t smem = gemm_smem_bytes<TL, Traits<S>::cplx, CP>();
+  auto kern = gemm_kernel<S, TL, CP>;
+  set_smem(kern, smem);
+  dim3 grid((unsigned)((M + TL::BM - 1) / TL::BM), (unsigned)((N + TL::BN - 1) / TL::BN));
+  kern<<<grid, TL::THREADS, smem, st>>>(A, B, M, N, K, ep, info);
+  BCMG_CHECK_LAUNCH();
+}
+
+template <class S>
+static void gemm_t(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+                   const int* info, cudaStream_t st) {
+  if constexpr (std::is_same_v<S, double>) {
+    const bool cp = cp_ok(A) && cp_ok(B);
+    if (cp) {
+      if (N <= 16) return launch_gemm<S, TileNarrow, true>(M, N, K, A, B, ep, info, st);
+      const int64_t big_blocks = ((M + 127) / 128) * ((N + 127) / 128);
+      if (big_blocks >= num_sms()) return launch_gemm<S, TileBig, true>(M, N, K, A, B, ep, info, st);
+      return launch_gemm<S, TileMed, true>(M, N, K, A, B, ep, info, st);
+    }
+  }
+  if (N <= 16) return launch_gemm<S, TileNarrow, false>(M, N, K, A, B, ep, info, st);
+  return launch_gemm<S, TileMed, false>(M, N, K, A, B, ep, info, st);
+}
+
+void gemm(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+          const int* info, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return;
+  if (K <= 0) {
+    // C := beta*C only; with beta==1 nothing to do, beta==0 handled by a zero-K GEMM
+    if (ep.beta == 1.0) return;
+  }
+  dispatch_dtype(dt, [&](auto s) { gemm_t<decltype(s)>(M, N, std::max<int64_t>(K, 0), A, B, ep, info, st); });
+}
+
+// ============================================================== trailing update
+template <class S, class TL, bool CP>
+static void launch_trail(const TrailParams& p, const int* info, cudaStream_t st) {
+  constexpr int B = TL::BM;
+  int64_t total = 0;
+  for (int64_t m = p.m_first; m < p.m_last; ++m) {
+    const int dev = (int)(m % p.D);
+    if (dev < p.dev0 || dev >= p.dev0 + p.nloc) continue;
+    const int64_t rows = p.N - m * p.T, tc = std::min(p.T, rows);
+    const int64_t nrb = (rows + B - 1) / B, ncb = (tc + B - 1) / B;
+    total += nrb <= ncb ? nrb * (nrb + 1) / 2 : ncb * (ncb + 1) / 2 + (nrb - ncb) * ncb;
+  }
+  if (total == 0) return;
+  constexpr size_t smem = gemm_smem_bytes<TL, Traits<S>::cplx, CP>();
+  auto kern = trail_kernel<S, TL, CP>;
+  set_smem(kern, smem);
+  int per_sm = 0;
+  BCMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TL::THREADS, smem));
+  per_sm = std::max(per_sm, 1);
+  const int64_t grid = std::min<int64_t>(total, (int64_t)num_sms() * per_sm);
+  kern<<<(unsigned)grid, TL::THREADS, smem, st>>>(p, info);
+  BCMG_CHECK_LAUNCH();
+}
+
+void trailing_update(int dt, const TrailParams& p, const int* info, cudaStream_t st) {
+  if (p.m_first >= p.m_last || p.K <= 0) return;
+  dispatch_dtype(dt, [&](auto s) {
+    using S = decltype(s);
+    if constexpr (std::is_same_v<S, double>) {
+      const bool cp = aligned16(p.P) && p.ldp % 2 == 0 && p.T % 2 == 0 && (p.prow0 % 2 == 0);
+      if (cp) return launch_trail<S, TileBig, true>(p, info, st);
+    }
+    launch_trail<S, TileMed, false>(p, info, st);
+  });
+}
+
+// ============================================================== diagonal leaf
+// n <= 64: in-place lower Cholesky + X = L^-1 in shared memory, right-looking
+// (the reference's unblocked factor is solvers.py:322-338; same pivot test:
+// d = Re a_jj after the updates, fail unless d > 0 and finite).
+constexpr int LEAF = 64;
+constexpr int LEAF_LD = LEAF + 1;
+
+template <bool C> struct V_ { using type = double; };
+template <> struct V_<true> { using type = double2; };
+
+__device__ __forceinline__ double v_re(double a) { return a; }
+__device__ __forceinline__ double v_re(double2 a) { return a.x; }
+__device__ __forceinline__ double v_scale(double a, double s) { return a * s; }
+__device__ __forceinline__ double2 v_scale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double v_fnms(double c, double a, double b) { return c - a * b; }            // c - a*b
+__device__ __forceinline__ double2 v_fnms(double2 c, double2 a, double2 b) {
+  double2 p = cmul(a, b);
+  return make_double2(c.x - p.x, c.y - p.y);
+}
+__device__ __forceinline__ double v_fnmsc(double c, double a, double b) { return c - a * b; }           // c - a*conj(b)
+__device__ __forceinline__ double2 v_fnmsc(double2 c, double2 a, double2 b) {
+  double2 p = cmulc(a, b);
+  return make_double2(c.x - p.x, c.y - p.y);
+}
+template <class V> __device__ __forceinline__ V v_from(double2 x);
+template <> __device__ __forceinline__ double v_from<double>(double2 x) { return x.x; }
+template <> __device__ __forceinline__ double2 v_from<double2>(double2 x) { return x; }
+__device__ __forceinline__ double2 v_to(double a) { return make_double2(a, 0.0); }
+__device__ __forceinline__ double2 v_to(double2 a) { return a; }
+
+template <class S>
+__global__ void __launch_bounds__(256) leaf_kernel(S* A, int64_t lda, S* X, int64_t ldx, int n, int64_t goff,
+                                                   int* info) {
+  using V = typename V_<Traits<S>::cplx>::type;
+  if (*(volatile int*)info) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* Ls = reinterpret_cast<V*>(smem_raw);
+  V* Xs = Ls + LEAF * LEAF_LD;
+  __shared__ double s_inv;
+  __shared__ int s_bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    const int i = idx % n, c = idx / n;
+    Ls[i * LEAF_LD + c] = (i >= c) ? v_from<V>(to_c(A[i + (int64_t)c * lda])) : v_from<V>(make_double2(0, 0));
+    Xs[i * LEAF_LD + c] = v_from<V>(make_double2(i == c ? 1.0 : 0.0, 0.0));
+  }
+  if (tid == 0) s_bad = -1;
+  __syncthreads();
+  int j = 0;
+  for (; j < n; ++j) {
+    if (tid == 0) {
+      const double d = v_re(Ls[j * LEAF_LD + j]);
+      if (!(d > 0.0) || !isfinite(d)) {
+        s_bad = j;
+      } else {
+        const double l = sqrt(d);
+        Ls[j * LEAF_LD + j] = v_from<V>(make_double2(l, 0.0));
+        s_inv = 1.0 / l;
+      }
+    }
+    __syncthreads();
+    if (s_bad >= 0) break;
+    const double inv = s_inv;
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) Ls[i * LEAF_LD + j] = v_scale(Ls[i * LEAF_LD + j], inv);
+    for (int c = tid; c <= j; c += blockDim.x) Xs[j * LEAF_LD + c] = v_scale(Xs[j * LEAF_LD + c], inv);
+    __syncthreads();
+    for (int i = j + 1 + warp; i < n; i += blockDim.x / 32) {
+      const V lij = Ls[i * LEAF_LD + j];
+      for (int c = lane; c <= i; c += 32) {
+        if (c <= j)
+          Xs[i * LEAF_LD + c] = v_fnms(Xs[i * LEAF_LD + c], lij, Xs[j * LEAF_LD + c]);
+        else
+          Ls[i * LEAF_LD + c] = v_fnmsc(Ls[i * LEAF_LD + c], lij, Ls[c * LEAF_LD + j]);
+      }
+    }
+    __syncthreads();
+  }
+  const int done = j;  // columns [0, done) of L are final
+  if (done < n && tid == 0) atomicCAS(info, 0, (int)(goff + done + 1));
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    const int i = idx % n, c = idx / n;
+    if (c < done && i >= c) A[i + (int64_t)c * lda] = from_c<S>(v_to(Ls[i * LEAF_LD + c]));
+    if (done == n) X[i + (int64_t)c * ldx] = from_c<S>(i >= c ? v_to(Xs[i * LEAF_LD + c]) : make_double2(0, 0));
+  }
+}
+
+template <class S>
+static void launch_leaf(S* A, int64_t lda, S* X, int64_t ldx, int n, int64_t goff, int* info, cudaStream_t st) {
+  using V = typename V_<Traits<S>::cplx>::type;
+  const size_t smem = 2 * LEAF * LEAF_LD * sizeof(V);
+  auto kern = leaf_kernel<S>;
+  set_smem(kern, smem);
+  kern<<<1, 256, smem, st>>>(A, lda, X, ldx, n, goff, info);
+  BCMG_CHECK_LAUNCH();
+}
+
+// Recursive diagonal factor + inverse:
+//   [L11 0; L21 L22] = chol(A),  X = [X11 0; X21 X22] = L^-1
+//   L21 = A21 X11^H,  A22 -= L21 L21^H,  X21 = -X22 (L21 X11)
+void diag_factor(int dt, void* A, int64_t lda, void* X, int64_t ldx, void* W, int64_t n, int64_t goff, int* info,
+                 cudaStream_t st) {
+  const int esz = dtype_size(dt);
+  auto at = [esz](void* base, int64_t ld, int64_t r, int64_t c) {
+    return static_cast<void*>(static_cast<char*>(base) + (r + c * ld) * esz);
+  };
+  if (n <= LEAF) {
+    dispatch_dtype(dt, [&](auto s) {
+      using S = decltype(s);
+      launch_leaf<S>(static_cast<S*>(A), lda, static_cast<S*>(X), ldx, (int)n, goff, info, st);
+    });
+    return;
+  }
+  int64_t n1 = ((n + 1) / 2 + LEAF - 1) / LEAF * LEAF;
+  if (n1 >= n) n1 = n - LEAF;
+  const int64_t n2 = n - n1;
+  void* A11 = A;
+  void* A21 = at(A, lda, n1, 0);
+  void* A22 = at(A, lda, n1, n1);
+  void* X11 = X;
+  void* X21 = at(X, ldx, n1, 0);
+  void* X22 = at(X, ldx, n1, n1);
+  const int64_t ldw = n2;  // W holds n2 x n1 and n2 x n1 temporaries
+  diag_factor(dt, A11, lda, X11, ldx, W, n1, goff, info, st);
+  // L21 = A21 * X11^H  -> W, then back into A21
+  gemm(dt, n2, n1, n1, opA(A21, lda, OP_N), opB(X11, ldx, OP_C), Epilogue{W, ldw, 1.0, 0.0, 0, 0}, info, st);
+  copy2d(dt, W, ldw, A21, lda, n2, n1, false, info, st);
+  // A22 -= L21 * L21^H (lower triangle)
+  gemm(dt, n2, n2, n1, opA(A21, lda, OP_N), opB(A21, lda, OP_C), Epilogue{A22, lda, -1.0, 1.0, 1, 0}, info, st);
+  diag_factor(dt, A22, lda, X22, ldx, W, n2, goff + n1, info, st);
+  // X21 = -X22 * (L21 * X11)
+  gemm(dt, n2, n1, n1, opA(A21, lda, OP_N), opB(X11, ldx, OP_N), Epilogue{X21, ldx, 1.0, 0.0, 0, 0}, info, st);
+  gemm(dt, n2, n1, n2, opA(X22, ldx, OP_N), opB(X21, ldx, OP_N), Epilogue{W, ldw, -1.0, 0.0, 0, 0}, info, st);
+  copy2d(dt, W, ldw, X21, ldx, n2, n1, false, info, st);
+  // X's strict upper block (X12) must read as zero for later GEMM operands
+  zero_upper(dt, at(X, ldx, 0, n1), ldx, n1, n2, n1, st);
+}
+
+// ============================================================== elementwise helpers
+template <class S>
+__global__ void copy2d_kernel(const S* __restrict__ src, int64_t lds, S* __restrict__ dst, int64_t ldd, int64_t rows,
+                              int64_t cols, int conj, const int* info) {
+  if (ld_flag(info)) return;
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx % rows, c = idx / rows;
+    S v = src[r + c * lds];
+    if (conj) v = from_c<S>(cconj(to_c(v)));
+    dst[r + c * ldd] = v;
+  }
+}
+
+static unsigned ew_grid(int64_t total) {
+  int64_t g = (total + 255) / 256;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)num_sms() * 16));
+}
+
+void copy2d(int dt, const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols, bool conj,
+            const int* info, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  dispatch_dtype(dt, [&](auto s) {
+    using S = decltype(s);
+    copy2d_kernel<S><<<ew_grid(rows * cols), 256, 0, st>>>(static_cast<const S*>(src), lds, static_cast<S*>(dst), ldd,
+                                                           rows, cols, conj ? 1 : 0, info);
+  });
+  BCMG_CHECK_LAUNCH();
+}
+
+template <class S>
+__global__ void conj2d_kernel(S* a, int64_t lda, int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx % rows, c = idx / rows;
+    a[r + c * lda] = from_c<S>(cconj(to_c(a[r + c * lda])));
+  }
+}
+
+void conj2d(int dt, void* a, int64_t lda, int64_t rows, int64_t cols, cudaStream_t st) {
+  if (!dtype_complex(dt) || rows <= 0 || cols <= 0) return;
+  dispatch_dtype(dt, [&](auto s) {
+    using S = decltype(s);
+    conj2d_kernel<S><<<ew_grid(rows * cols), 256, 0, st>>>(static_cast<S*>(a), lda, rows, cols);
+  });
+  BCMG_CHECK_LAUNCH();
+}
+
+template <class S>
+__global__ void zero_upper_kernel(S* a, int64_t lda, int64_t rows, int64_t cols, int64_t off) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx % rows, c = idx / rows;
+    if (r < c + off) a[r + c * lda] = from_c<S>(make_double2(0, 0));
+  }
+}
+
+void zero_upper(int dt, void* a, int64_t lda, int64_t rows, int64_t cols, int64_t off, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  dispatch_dtype(dt, [&](auto s) {
+    using S = decltype(s);
+    zero_upper_kernel<S><<<ew_grid(rows * cols), 256, 0, st>>>(static_cast<S*>(a), lda, rows, cols, off);
+  });
+  BCMG_CHECK_LAUNCH();
+}
+
+template <class S>
+__global__ void conj_transpose_kernel(const S* __restrict__ src, int64_t lds, S* __restrict__ dst, int64_t ldd,
+                                      int64_t rows, int64_t cols) {
+  // dst (rows x cols) = src^H, src is cols x rows; 32x32 tiles through shared memory
+  __shared__ double2 t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    // read src rows (c0 + x), cols (r0 + y): coalesced along src rows
+    const int64_t sr = c0 + threadIdx.x, sc = r0 + y;
+    if (sr < cols && sc < rows) t[y][threadIdx.x] = to_c(src[sr + sc * lds]);
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t dr = r0 + threadIdx.x, dc = c0 + y;
+    if (dr < rows && dc < cols) dst[dr + dc * ldd] = from_c<S>(cconj(t[threadIdx.x][y]));
+  }
+}
+
+void conj_transpose(int dt, const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
+                    cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32)), block(32, 8);
+  dispatch_dtype(dt, [&](auto s) {
+    using S = decltype(s);
+    conj_transpose_kernel<S><<<grid, block, 0, st>>>(static_cast<const S*>(src), lds, static_cast<S*>(dst), ldd, rows,
+                                                     cols);
+  });
+  BCMG_CHECK_LAUNCH();
+}
+
+template <class S>
+__global__ void realify_diag_kernel(S* a, int64_t lda, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = to_c(a[i + i * lda]);
+    a[i + i * lda] = from_c<S>(make_double2(v.x, 0.0));
+  }
+}
+
+void realify_diag(int dt, void* a, int64_t lda, int64_t n, cudaStream_t st) {
+  if (!dtype_complex(dt) || n <= 0) return;
+  dispatch_dtype(dt, [&](auto s) {
+    using S = decltype(s);
+    realify_diag_kernel<S><<<ew_grid(n), 256, 0, st>>>(static_cast<S*>(a), lda, n);
+  });
+  BCMG_CHECK_LAUNCH();
+}
+
+template <class S>
+__global__ void reduce_parts_kernel(const S* __restrict__ parts, int64_t pstride, int nparts, S* dst, int64_t ldd,
+                                    int64_t rows, int64_t cols, double alpha) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx % rows, c = idx / rows;
+    double2 acc = make_double2(0, 0);
+    for (int s = 0; s < nparts; ++s) {  // fixed order: deterministic
+      double2 v = to_c(parts[s * pstride + r + c * rows]);
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    double2 o = to_c(dst[r + c * ldd]);
+    dst[r + c * ldd] = from_c<S>(make_double2(o.x + alpha * acc.x, o.y + alpha * acc.y));
+  }
+}
+
+void reduce_parts(int dt, const void* parts, int64_t part_stride, int nparts, void* dst, int64_t ldd, int64_t rows,
+                  int64_t cols, double alpha, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  dispatch_dtype(dt, [&](auto s) {
+    using S = decltype(s);
+    reduce_parts_kernel<S><<<ew_grid(rows * cols), 256, 0, st>>>(static_cast<const S*>(parts), part_stride, nparts,
+                                                                 static_cast<S*>(dst), ldd, rows, cols, alpha);
+  });
+  BCMG_CHECK_LAUNCH();
+}
+
+// ============================================================== cycle rotation
+// Each thread owns one vec-byte lane of one cycle and carries it around the
+// whole cycle: new[c1] = old[c0], ..., new[c0] = old[c_{m-1}] (the rotation
+// direction of layout.py:236-250).  Every address is read exactly once and
+// then written once by the same thread, so there is no hazard between
+// threads and no staging buffer beyond registers; loads of the next UNROLL
+// members are issued before the stores (each is still read before written).
+template <class W, int UNROLL>
+__global__ void __launch_bounds__(256) rotate_kernel(RotateJob j) {
+  for (int64_t lane = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; lane < j.total_lanes;
+       lane += (int64_t)gridDim.x * blockDim.x) {
+    // cycle owning this lane
+    int64_t lo = 0, hi = j.n_cycles;  // lane_pref[lo] <= lane < lane_pref[hi]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(j.lane_pref + mid) <= lane) lo = mid; else hi = mid;
+    }
+    const int64_t c = lo;
+    const int64_t off = (lane - __ldg(j.lane_pref + c)) * (int64_t)sizeof(W);
+    const int64_t b = __ldg(j.offsets + c), e = __ldg(j.offsets + c + 1);
+    W carry = *reinterpret_cast<const W*>(__ldg(j.addr + b) + off);
+    int64_t i = b + 1;
+    for (; i + UNROLL <= e; i += UNROLL) {
+      W v[UNROLL];
+      W* p[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        p[u] = reinterpret_cast<W*>(__ldg(j.addr + i + u) + off);
+        v[u] = *p[u];
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        *p[u] = carry;
+        carry = v[u];
+      }
+    }
+    for (; i < e; ++i) {
+      W* p = reinterpret_cast<W*>(__ldg(j.addr + i) + off);
+      W v = *p;
+      *p = carry;
+      carry = v;
+    }
+    *reinterpret_cast<W*>(__ldg(j.addr + b) + off) = carry;
+  }
+}
+
+void rotate_cycles(const RotateJob& j, cudaStream_t st) {
+  if (j.total_lanes <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>((j.total_lanes + 255) / 256, (int64_t)num_sms() * 8);
+  if (j.vec == 16) rotate_kernel<uint4, 4><<<grid, 256, 0, st>>>(j);
+  else if (j.vec == 8) rotate_kernel<uint2, 4><<<grid, 256, 0, st>>>(j);
+  else rotate_kernel<unsigned, 4><<<grid, 256, 0, st>>>(j);
+  BCMG_CHECK_LAUNCH();
+}
+
+
+// In-place Hermitian completion of a diagonal block: a(r,c) = conj(a(c,r))
+// for r < c, diagonal made exactly real (reference solvers.py:577-583).
+template <class S>
+__global__ void mirror_diag_kernel(S* a, int64_t lda, int64_t n) {
+  const int64_t total = n * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx % n, c = idx / n;
+    if (r < c) a[r + c * lda] = from_c<S>(cconj(to_c(a[c + r * lda])));
+    else if (r == c) a[r + c * lda] = from_c<S>(make_double2(to_c(a[r + c * lda]).x, 0.0));
+  }
+}
+
+void mirror_diag(int dt, void* a, int64_t lda, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  dispatch_dtype(dt, [&](auto s) {
+    using S = decltype(s);
+    mirror_diag_kernel<S><<<ew_grid(n * n), 256, 0, st>>>(static_cast<S*>(a), lda, n);
+  });
+  BCMG_CHECK_LAUNCH();
+}
+}  // namespace bcmg

@@ -1,0 +1,74 @@
+// Internal launcher interface between the drivers (solver.cu) and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <vector>
+
+#include "gemm.cuh"
+
+namespace bcmg {
+
+// C := alpha*op(A)*op(B) + beta*C, any dtype (dt), any shape; dispatches to
+// the cp.async DMMA kernel when the operands qualify, else the REG kernel.
+void gemm(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+          const int* info, cudaStream_t st);
+
+// Trailing update for potrf step (see trail_kernel).
+void trailing_update(int dt, const TrailParams& p, const int* info, cudaStream_t st);
+
+// Diagonal tile: in-place lower Cholesky of the n x n block at A (lda) and
+// X := L^-1 (n x n, ldx, zero upper).  goff = global column of the block's
+// first column; on a non-positive pivot writes the 1-based global pivot to
+// *info and leaves the columns before it factored.  W is n x n scratch.
+void diag_factor(int dt, void* A, int64_t lda, void* X, int64_t ldx, void* W, int64_t n, int64_t goff, int* info,
+                 cudaStream_t st);
+
+// dst(i,j) = src(i,j) (optionally conjugated), rows x cols, column-major.
+void copy2d(int dt, const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols, bool conj,
+            const int* info, cudaStream_t st);
+
+// In-place conjugation of a rows x cols block (complex only; no-op for real).
+void conj2d(int dt, void* a, int64_t lda, int64_t rows, int64_t cols, cudaStream_t st);
+
+// Zero the strict upper triangle (row < col + off) of a rows x cols block.
+void zero_upper(int dt, void* a, int64_t lda, int64_t rows, int64_t cols, int64_t off, cudaStream_t st);
+
+// Mirror: a(r, c) = conj(src(c, r)) for the block; diagonal forced real when diag.
+void conj_transpose(int dt, const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
+                    cudaStream_t st);
+void realify_diag(int dt, void* a, int64_t lda, int64_t n, cudaStream_t st);
+void mirror_diag(int dt, void* a, int64_t lda, int64_t n, cudaStream_t st);
+
+// Split-K deterministic reduction: dst += sum_s part[s] (fixed order).
+void reduce_parts(int dt, const void* parts, int64_t part_stride, int nparts, void* dst, int64_t ldd, int64_t rows,
+                  int64_t cols, double alpha, cudaStream_t st);
+
+// ----------------------------------------------------------------- redistribution
+// Segment-level plan of the contiguous <-> cyclic permutation (layout.py:126-256).
+struct SegPlan {
+  int64_t seg;                        // columns per segment (T when tile-aligned, else gcd-derived, >= 1)
+  std::vector<int64_t> members;       // segment positions, cycles concatenated in rotation order
+  std::vector<int64_t> offsets;       // CSR offsets into members, size n_cycles + 1
+  std::vector<int64_t> seg_cols;      // columns of each cycle's segments
+};
+// Column-level plan exactly as the reference (dest_of + cycles).
+void build_dest(int64_t n_cols, int64_t tile, int ndev, int64_t* dest);
+void decompose(int64_t n, const int64_t* dest, std::vector<int64_t>& members, std::vector<int64_t>& offsets);
+void invert_cycles(std::vector<int64_t>& members, const std::vector<int64_t>& offsets);
+SegPlan segment_plan(int64_t n_cols, int64_t tile, int ndev, bool inverse);
+std::vector<int64_t> column_counts(int64_t n_cols, int64_t tile, int ndev);
+
+// Rotate every cycle in place: members are absolute device addresses
+// (segments of seg_bytes[c] bytes), data moved in vec-byte lanes.
+struct RotateJob {
+  const uint64_t* addr;      // device: member addresses, cycles concatenated
+  const int64_t* offsets;    // device: CSR, n_cycles + 1
+  const int64_t* lane_pref;  // device: prefix sum of lanes per cycle, n_cycles + 1
+  const int64_t* seg_bytes;  // device: bytes per segment of each cycle
+  int64_t n_cycles, total_lanes;
+  int vec;                   // 16, 8 or 4
+};
+void rotate_cycles(const RotateJob& j, cudaStream_t st);
+
+}  // namespace bcmg

@@ -1,0 +1,466 @@
+// Session + drivers of the multi-GPU Cholesky path (B200, sm_100a).
+//
+// Process model: one process per GPU (torchrun), each process owning
+// ndev/world consecutive LOGICAL devices of the 1D block-cyclic layout
+// (tile k -> logical device k mod ndev, reference solvers.py:373).  With
+// world == 1 all logical devices are "virtual devices" sharing one GPU,
+// which keeps the reference's multi-device arithmetic testable on one B200.
+// Cross-process traffic is NCCL (panel broadcast per potrf step, solution
+// blocks in potrs); intra-process "peer copies" of the reference are plain
+// device memory accesses.
+//
+// Drivers:
+//   redistribute : segment-level cycle plan + in-place rotation kernel
+//                  (reference layout.py:191-256)
+//   potrf        : right-looking tiled Cholesky with depth-1 lookahead on a
+//                  high-priority stream (reference solvers.py:341-406)
+//   potrs        : forward/backward substitution over the tiles using the
+//                  diagonal-block inverses kept by potrf (solvers.py:430-474)
+//   potri        : W = L^-1 sweep, A^-1 = W^H W sweep, Hermitian mirror
+//                  (solvers.py:487-594)
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "ops.h"
+#include "solver.h"
+
+namespace bcmg {
+
+// ------------------------------------------------------------------ buffers
+void DevBuf::ensure(size_t n) {
+  if (n <= bytes) return;
+  release();
+  if (n == 0) return;
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(OUT_OF_MEMORY, "device workspace of " + std::to_string(n) + " bytes: " + cudaGetErrorString(e));
+  }
+  p = q;
+  bytes = n;
+}
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+#define BCMG_NCCL(call)                                                                  \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess) throw Error(CUDA, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+// ------------------------------------------------------------------ session
+Session::Session(int device_, int rank_, int world_, const unsigned char* nccl_id) : device(device_), rank(rank_), world(world_) {
+  if (world < 1 || rank < 0 || rank >= world) throw Error(CONFIG, "bad rank/world");
+  BCMG_CUDA(cudaSetDevice(device));
+  int lo = 0, hi = 0;
+  BCMG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  BCMG_CUDA(cudaStreamCreateWithPriority(&crit, cudaStreamNonBlocking, hi));
+  BCMG_CUDA(cudaStreamCreateWithPriority(&bulk, cudaStreamNonBlocking, lo));
+  BCMG_CUDA(cudaStreamCreateWithPriority(&comm, cudaStreamNonBlocking, hi));
+  for (auto& e : ev_pool) BCMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : ev_time) BCMG_CUDA(cudaEventCreate(&e));
+  BCMG_CUDA(cudaMallocHost(&info_host, sizeof(int)));
+  if (world > 1) {
+    if (!nccl_id) throw Error(CONFIG, "world > 1 needs an NCCL unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ncclComm_t c;
+    BCMG_NCCL(ncclCommInitRank(&c, world, id, rank));
+    nccl = c;
+  }
+}
+
+Session::~Session() {
+  cudaSetDevice(device);
+  cudaDeviceSynchronize();
+  if (nccl) ncclCommDestroy(static_cast<ncclComm_t>(nccl));
+  for (auto* b : {&panel[0], &panel[1], &dinv, &wdiag, &info_dev, &tmp, &acc, &plan_buf}) b->release();
+  for (auto& e : ev_pool) cudaEventDestroy(e);
+  for (auto& e : ev_time) cudaEventDestroy(e);
+  if (info_host) cudaFreeHost(info_host);
+  cudaStreamDestroy(crit);
+  cudaStreamDestroy(bulk);
+  cudaStreamDestroy(comm);
+}
+
+cudaEvent_t Session::ev(int i) { return ev_pool[i % kEvents]; }
+
+void Session::begin(cudaStream_t user_stream) {
+  user = user_stream;
+  BCMG_CUDA(cudaSetDevice(device));
+  BCMG_CUDA(cudaEventRecord(ev(kJoin + 4), user));
+  for (cudaStream_t s : {crit, bulk, comm}) BCMG_CUDA(cudaStreamWaitEvent(s, ev(kJoin + 4), 0));
+}
+
+void Session::join() {
+  // user stream waits for every internal stream
+  int i = 0;
+  for (cudaStream_t s : {crit, bulk, comm}) {
+    BCMG_CUDA(cudaEventRecord(ev(kJoin + i), s));
+    BCMG_CUDA(cudaStreamWaitEvent(user, ev(kJoin + i), 0));
+    ++i;
+  }
+}
+
+void Session::sync_streams(cudaStream_t waiter, cudaStream_t on) {
+  BCMG_CUDA(cudaEventRecord(ev(kJoin + 3), on));
+  BCMG_CUDA(cudaStreamWaitEvent(waiter, ev(kJoin + 3), 0));
+}
+
+void Session::mark(int phase) {
+  if (phase >= 0 && phase < kTimeEvents) BCMG_CUDA(cudaEventRecord(ev_time[phase], user));
+}
+
+void Session::bcast(void* buf, size_t bytes, int root, cudaStream_t st) {
+  if (world == 1 || bytes == 0) return;
+  BCMG_NCCL(ncclBroadcast(buf, buf, bytes, ncclUint8, root, static_cast<ncclComm_t>(nccl), st));
+}
+
+int Session::reduce_info(int local) {
+  if (world == 1) return local;
+  // smallest nonzero pivot over ranks (later tiles can only fail at larger pivots)
+  int* d = static_cast<int*>(tmp.p);
+  const int v = local ? local : 0x7fffffff;
+  BCMG_CUDA(cudaMemcpyAsync(d, &v, sizeof(int), cudaMemcpyHostToDevice, comm));
+  BCMG_NCCL(ncclAllReduce(d, d, 1, ncclInt32, ncclMin, static_cast<ncclComm_t>(nccl), comm));
+  int out = 0;
+  BCMG_CUDA(cudaMemcpyAsync(&out, d, sizeof(int), cudaMemcpyDeviceToHost, comm));
+  BCMG_CUDA(cudaStreamSynchronize(comm));
+  return out == 0x7fffffff ? 0 : out;
+}
+
+// ------------------------------------------------------------------ geometry
+struct Geo {
+  int64_t n, T, nt;
+  int D, nloc, dev0;
+  int esz;
+  bool owns(int64_t k) const {
+    const int d = (int)(k % D);
+    return d >= dev0 && d < dev0 + nloc;
+  }
+  int owner_rank(int64_t k) const { return (int)((k % D) / nloc); }
+  int64_t start(int64_t k) const { return k * T; }
+  int64_t stop(int64_t k) const { return std::min(n, (k + 1) * T); }
+  int64_t loc(int64_t k) const { return (k / D) * T; }  // local first column of tile k on its device
+};
+
+static Geo make_geo(const Session& s, int dt, int64_t n, int64_t T, int ndev) {
+  if (n < 1) throw Error(CONFIG, "matrix order must be positive");
+  if (T < 1 || T > n) throw Error(CONFIG, "tile width " + std::to_string(T) + " out of range for " + std::to_string(n) + " columns");
+  if (ndev < 1) throw Error(CONFIG, "need at least one device");
+  if (ndev % s.world) throw Error(CONFIG, "logical device count must be a multiple of the process count");
+  Geo g;
+  g.n = n;
+  g.T = T;
+  g.nt = (n + T - 1) / T;
+  g.D = ndev;
+  g.nloc = ndev / s.world;
+  g.dev0 = s.rank * g.nloc;
+  g.esz = dtype_size(dt);
+  if (!g.esz) throw Error(CONFIG, "unknown element-type code");
+  if (g.nloc > MAX_LOCAL_DEV) throw Error(CONFIG, "too many logical devices per process");
+  return g;
+}
+
+static char* colp(void* shard, const Geo& g, int64_t row, int64_t col) {
+  return static_cast<char*>(shard) + (row + col * g.n) * g.esz;
+}
+
+// ------------------------------------------------------------------ redistribution
+void Session::redistribute(int dt, int64_t n_rows, int64_t n_cols, int64_t T, int ndev, void* const* shards,
+                           bool inverse) {
+  if (n_rows < 1 || n_cols < 1) throw Error(CONFIG, "matrix dimensions must be positive");
+  if (T < 1 || T > n_cols) throw Error(CONFIG, "tile width out of range");
+  if (ndev < 1) throw Error(CONFIG, "need at least one device");
+  const int esz = dtype_size(dt);
+  if (!esz) throw Error(CONFIG, "unknown element-type code");
+  if (world > 1) throw Error(CONFIG, "multi-process redistribution is not implemented in this build");
+  last_moved_bytes = 0;
+  SegPlan plan = segment_plan(n_cols, T, ndev, inverse);
+  const int64_t nc = (int64_t)plan.offsets.size() - 1;
+  if (nc == 0) return;
+  const auto counts = column_counts(n_cols, T, ndev);
+  std::vector<int64_t> off(ndev, 0);
+  for (int d = 1; d < ndev; ++d) off[d] = off[d - 1] + counts[d - 1];
+  const int64_t col_bytes = n_rows * esz;
+  int vec = (col_bytes % 16 == 0) ? 16 : (col_bytes % 8 == 0 ? 8 : 4);
+  for (int d = 0; d < ndev; ++d)
+    if (reinterpret_cast<uintptr_t>(shards[d]) % vec) vec = (reinterpret_cast<uintptr_t>(shards[d]) % 8) ? 4 : 8;
+  // host tables: member addresses, CSR offsets, lane prefix, segment bytes
+  const size_t nm = plan.members.size();
+  std::vector<uint64_t> addr(nm);
+  for (size_t i = 0; i < nm; ++i) {
+    const int64_t pos = plan.members[i] * plan.seg;
+    int d = (int)(std::upper_bound(off.begin(), off.end(), pos) - off.begin()) - 1;
+    addr[i] = reinterpret_cast<uint64_t>(shards[d]) + (uint64_t)((pos - off[d]) * col_bytes);
+  }
+  std::vector<int64_t> lane_pref(nc + 1, 0), seg_bytes(nc);
+  for (int64_t c = 0; c < nc; ++c) {
+    seg_bytes[c] = plan.seg_cols[c] * col_bytes;
+    lane_pref[c + 1] = lane_pref[c] + seg_bytes[c] / vec;
+  }
+  const size_t bytes = nm * 8 + (nc + 1) * 8 * 2 + nc * 8;
+  plan_host.resize(bytes);
+  char* h = plan_host.data();
+  std::memcpy(h, addr.data(), nm * 8);
+  std::memcpy(h + nm * 8, plan.offsets.data(), (nc + 1) * 8);
+  std::memcpy(h + nm * 8 + (nc + 1) * 8, lane_pref.data(), (nc + 1) * 8);
+  std::memcpy(h + nm * 8 + (nc + 1) * 16, seg_bytes.data(), nc * 8);
+  plan_buf.ensure(bytes);
+  char* dptr = static_cast<char*>(plan_buf.p);
+  BCMG_CUDA(cudaMemcpyAsync(dptr, h, bytes, cudaMemcpyHostToDevice, crit));
+  RotateJob j;
+  j.addr = reinterpret_cast<const uint64_t*>(dptr);
+  j.offsets = reinterpret_cast<const int64_t*>(dptr + nm * 8);
+  j.lane_pref = reinterpret_cast<const int64_t*>(dptr + nm * 8 + (nc + 1) * 8);
+  j.seg_bytes = reinterpret_cast<const int64_t*>(dptr + nm * 8 + (nc + 1) * 16);
+  j.n_cycles = nc;
+  j.total_lanes = lane_pref[nc];
+  j.vec = vec;
+  rotate_cycles(j, crit);
+  // (cudaMemcpyAsync from pageable memory returns once the source is consumed)
+  last_moved_bytes = 2 * (int64_t)nm * plan.seg * col_bytes;
+  sync_streams(user, crit);
+}
+
+// ------------------------------------------------------------------ potrf
+// Panel k lives in panel[k % 2] with rows [stop_k, n) (ld = n - stop_k): only
+// the rows the trailing update reads (the reference copies the full-height
+// panel, solvers.py:389-394).  X_kk = L_kk^-1 is kept in dinv for potrs/potri.
+int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) {
+  const Geo g = make_geo(*this, dt, n, T, ndev);
+  const size_t panel_bytes = (size_t)n * T * g.esz;
+  panel[0].ensure(panel_bytes);
+  panel[1].ensure(panel_bytes);
+  dinv.ensure((size_t)g.nt * T * T * g.esz);
+  wdiag.ensure((size_t)T * T * g.esz);
+  info_dev.ensure(sizeof(int));
+  tmp.ensure(4096);
+  int* info = static_cast<int*>(info_dev.p);
+  BCMG_CUDA(cudaMemsetAsync(info, 0, sizeof(int), crit));
+  sync_streams(bulk, crit);
+  sync_streams(comm, crit);
+  last_dinv_T = T;
+
+  auto dinv_k = [&](int64_t k) { return static_cast<char*>(dinv.p) + (size_t)k * T * T * g.esz; };
+  auto shard_of = [&](int64_t k) { return shards[(k % g.D) - g.dev0]; };
+
+  // F(k): factor diagonal block + inverse, panel solve into panel[k%2]
+  auto factor = [&](int64_t k) {
+    const int64_t s0 = g.start(k), s1 = g.stop(k), tc = s1 - s0;
+    void* sh = shard_of(k);
+    void* Akk = colp(sh, g, s0, g.loc(k));
+    diag_factor(dt, Akk, n, dinv_k(k), T, wdiag.p, tc, s0, info, crit);
+    if (s1 < n) {
+      gemm(dt, n - s1, tc, tc, opA(colp(sh, g, s1, g.loc(k)), n, OP_N), opB(dinv_k(k), T, OP_C),
+           Epilogue{panel[k % 2].p, n - s1, 1.0, 0.0, 0, 0}, info, crit);
+    }
+  };
+  auto trail = [&](int64_t k, int64_t m_first, int64_t m_last, cudaStream_t st) {
+    TrailParams p{};
+    p.P = panel[k % 2].p;
+    p.prow0 = g.stop(k);
+    p.ldp = n - p.prow0;
+    p.N = n;
+    p.T = T;
+    p.K = g.stop(k) - g.start(k);
+    p.D = g.D;
+    p.dev0 = g.dev0;
+    p.nloc = g.nloc;
+    for (int i = 0; i < g.nloc; ++i) p.shards[i] = shards[i];
+    p.m_first = m_first;
+    p.m_last = m_last;
+    trailing_update(dt, p, info, st);
+  };
+
+  // Event slots: type*8 + k%8 (dependencies reach back at most two steps).
+  enum { R = 0, C = 1, B = 2, U = 3, FREE = 4 };
+  auto E = [&](int type, int64_t k) { return ev(type * 8 + (int)(k % 8)); };
+  if (g.owns(0)) {
+    factor(0);
+    BCMG_CUDA(cudaEventRecord(E(R, 0), crit));
+  }
+  for (int64_t k = 0; k < g.nt; ++k) {
+    const int64_t s1 = g.stop(k);
+    if (s1 >= n) break;  // last tile: nothing below it
+    const bool mine = g.owns(k);
+    const int b = (int)(k % 2);
+    // -- panel k reaches every rank (R[k]: usable here; C[k]: broadcast done)
+    if (world > 1) {
+      if (mine) BCMG_CUDA(cudaStreamWaitEvent(comm, E(R, k), 0));
+      else if (k >= 2) BCMG_CUDA(cudaStreamWaitEvent(comm, E(FREE, k - 2), 0));
+      bcast(panel[b].p, (size_t)(n - s1) * (s1 - g.start(k)) * g.esz, g.owner_rank(k), comm);
+      BCMG_CUDA(cudaEventRecord(E(C, k), comm));
+      if (!mine) BCMG_CUDA(cudaEventRecord(E(R, k), comm));
+    }
+    // -- lookahead: the owner of tile k+1 applies update k to it first (crit stream)
+    const bool look = g.owns(k + 1);
+    if (look) {
+      if (!mine) BCMG_CUDA(cudaStreamWaitEvent(crit, E(R, k), 0));
+      if (k >= 1) BCMG_CUDA(cudaStreamWaitEvent(crit, E(B, k - 1), 0));
+      trail(k, k + 1, k + 2, crit);
+      BCMG_CUDA(cudaEventRecord(E(U, k), crit));
+    }
+    // -- bulk update of the other local trailing tiles (bulk stream)
+    BCMG_CUDA(cudaStreamWaitEvent(bulk, E(R, k), 0));
+    trail(k, look ? k + 2 : k + 1, g.nt, bulk);
+    if (mine)  // factor below the diagonal back into A (potrs/potri read it there)
+      copy2d(dt, panel[b].p, n - s1, colp(shard_of(k), g, s1, g.loc(k)), n, n - s1, s1 - g.start(k), false, info,
+             bulk);
+    BCMG_CUDA(cudaEventRecord(E(B, k), bulk));
+    // -- panel buffer b is reusable once bulk(k), U(k) and the broadcast are done
+    if (look) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(U, k), 0));
+    if (world > 1) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(C, k), 0));
+    BCMG_CUDA(cudaEventRecord(E(FREE, k), bulk));
+    // -- F(k+1) overwrites panel buffer 1-b (last used by panel k-1)
+    if (look) {
+      if (k >= 1) BCMG_CUDA(cudaStreamWaitEvent(crit, E(FREE, k - 1), 0));
+      factor(k + 1);
+      BCMG_CUDA(cudaEventRecord(E(R, k + 1), crit));
+    }
+  }
+  join();
+  BCMG_CUDA(cudaMemcpyAsync(info_host, info, sizeof(int), cudaMemcpyDeviceToHost, user));
+  BCMG_CUDA(cudaStreamSynchronize(user));
+  return reduce_info(*info_host);
+}
+
+
+// ------------------------------------------------------------------ potrs
+// Substitution on the owners of each tile (no panel movement, unlike the
+// reference's _fetch_panel, solvers.py:412-427).  x (n x nrhs, ldx) is
+// replicated on every process; each step's arithmetic happens on the tile
+// owner only, in tile order, so the bits do not depend on the device count.
+//   forward : x_k <- X_kk x_k ; x[stop:] -= L[stop:, k] x_k      (solvers.py:455-461)
+//   backward: x_k -= L[stop:, k]^H x[stop:] ; x_k <- X_kk^H x_k   (solvers.py:462-469)
+// With world > 1 the owner broadcasts x[start:] (forward) / x_k (backward).
+void Session::potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* const* shards, void* x, int64_t ldx) {
+  const Geo g = make_geo(*this, dt, n, T, ndev);
+  if (nrhs < 1) throw Error(CONFIG, "right-hand side must be non-empty");
+  if (ldx < n) throw Error(CONFIG, "ldx < n");
+  if (last_dinv_T != T || dinv.bytes < (size_t)g.nt * T * T * g.esz)
+    throw Error(CONFIG, "potrs needs a potrf of the same tiling in this session");
+  constexpr int64_t KSPLIT = 8192;  // split-K chunk of the backward update
+  const int64_t max_parts = (n + KSPLIT - 1) / KSPLIT;
+  const size_t y_bytes = (size_t)T * nrhs * g.esz;
+  const size_t parts_bytes = (size_t)max_parts * T * nrhs * g.esz;
+  const size_t pack_bytes = world > 1 ? (size_t)n * nrhs * g.esz : 0;
+  tmp.ensure(std::max<size_t>(4096, y_bytes + parts_bytes + pack_bytes));
+  char* y = static_cast<char*>(tmp.p);
+  char* parts = y + y_bytes;
+  char* pack = parts + parts_bytes;
+  char* xb = static_cast<char*>(x);
+  auto xrow = [&](int64_t r) { return xb + r * g.esz; };
+  auto dinv_k = [&](int64_t k) { return static_cast<char*>(dinv.p) + (size_t)k * T * T * g.esz; };
+  cudaStream_t st = crit;
+  auto share = [&](int64_t r0, int64_t rows, int root) {  // broadcast x[r0:r0+rows, :]
+    if (world == 1 || rows <= 0) return;
+    if (rank == root) copy2d(dt, xrow(r0), ldx, pack, rows, rows, nrhs, false, nullptr, st);
+    bcast(pack, (size_t)rows * nrhs * g.esz, root, st);
+    if (rank != root) copy2d(dt, pack, rows, xrow(r0), ldx, rows, nrhs, false, nullptr, st);
+  };
+  for (int64_t k = 0; k < g.nt; ++k) {
+    const int64_t s0 = g.start(k), s1 = g.stop(k), tc = s1 - s0;
+    if (g.owns(k)) {
+      void* sh = shards[(k % g.D) - g.dev0];
+      gemm(dt, tc, nrhs, tc, opA(dinv_k(k), T, OP_N), opB(xrow(s0), ldx, OP_N), Epilogue{y, tc, 1.0, 0.0, 0, 0},
+           nullptr, st);
+      copy2d(dt, y, tc, xrow(s0), ldx, tc, nrhs, false, nullptr, st);
+      if (s1 < n)
+        gemm(dt, n - s1, nrhs, tc, opA(colp(sh, g, s1, g.loc(k)), n, OP_N), opB(xrow(s0), ldx, OP_N),
+             Epilogue{xrow(s1), ldx, -1.0, 1.0, 0, 0}, nullptr, st);
+    }
+    share(s0, n - s0, g.owner_rank(k));
+  }
+  for (int64_t k = g.nt - 1; k >= 0; --k) {
+    const int64_t s0 = g.start(k), s1 = g.stop(k), tc = s1 - s0;
+    if (g.owns(k)) {
+      void* sh = shards[(k % g.D) - g.dev0];
+      if (s1 < n) {
+        const int64_t K = n - s1, np = (K + KSPLIT - 1) / KSPLIT;
+        for (int64_t p = 0; p < np; ++p) {
+          const int64_t k0 = p * KSPLIT, kc = std::min(KSPLIT, K - k0);
+          gemm(dt, tc, nrhs, kc, opA(colp(sh, g, s1 + k0, g.loc(k)), n, OP_C), opB(xrow(s1 + k0), ldx, OP_N),
+               Epilogue{parts + (size_t)p * tc * nrhs * g.esz, tc, 1.0, 0.0, 0, 0}, nullptr, st);
+        }
+        reduce_parts(dt, parts, tc * nrhs, (int)np, xrow(s0), ldx, tc, nrhs, -1.0, st);
+      }
+      gemm(dt, tc, nrhs, tc, opA(dinv_k(k), T, OP_C), opB(xrow(s0), ldx, OP_N), Epilogue{y, tc, 1.0, 0.0, 0, 0},
+           nullptr, st);
+      copy2d(dt, y, tc, xrow(s0), ldx, tc, nrhs, false, nullptr, st);
+    }
+    share(s0, tc, g.owner_rank(k));
+  }
+  sync_streams(user, crit);
+}
+
+// ------------------------------------------------------------------ potri
+// In place on the cyclic shards (solvers.py:487-594):
+//   W sweep (last tile first):  acc = sum_{s>k} tril(W_s)[stop:] L21[s rows];
+//                               W21 = -acc X_kk;  W_kk = X_kk
+//   product sweep (first tile first): tile j <- sum_{s>=j} tril(W_s)^H tril(W_j)
+//   mirror: upper := conj-transpose of lower, diagonal exactly real.
+void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards) {
+  const Geo g = make_geo(*this, dt, n, T, ndev);
+  if (world > 1) throw Error(CONFIG, "multi-process potri is not implemented in this build");
+  if (last_dinv_T != T || dinv.bytes < (size_t)g.nt * T * T * g.esz)
+    throw Error(CONFIG, "potri needs a potrf of the same tiling in this session");
+  acc.ensure((size_t)n * T * g.esz);
+  char* accp = static_cast<char*>(acc.p);
+  cudaStream_t st = crit;
+  auto sh = [&](int64_t k) { return shards[(k % g.D) - g.dev0]; };
+  auto dinv_k = [&](int64_t k) { return static_cast<char*>(dinv.p) + (size_t)k * T * T * g.esz; };
+  for (int64_t k = g.nt - 1; k >= 0; --k) {
+    const int64_t s0 = g.start(k), s1 = g.stop(k), tc = s1 - s0;
+    if (s1 < n) {
+      const int64_t lda = n - s1;
+      for (int64_t s = k + 1; s < g.nt; ++s) {
+        const int64_t ss = g.start(s), tcs = g.stop(s) - ss;
+        Operand Ws = opA(colp(sh(s), g, ss, g.loc(s)), n, OP_N);
+        Ws.mask = 1;  // tril in global coordinates: row ss+i >= col ss+kk
+        gemm(dt, n - ss, tc, tcs, Ws, opB(colp(sh(k), g, ss, g.loc(k)), n, OP_N),
+             Epilogue{accp + (ss - s1) * g.esz, lda, 1.0, s == k + 1 ? 0.0 : 1.0, 0, 0}, nullptr, st);
+      }
+      gemm(dt, n - s1, tc, tc, opA(accp, lda, OP_N), opB(dinv_k(k), T, OP_N),
+           Epilogue{colp(sh(k), g, s1, g.loc(k)), n, -1.0, 0.0, 0, 0}, nullptr, st);
+    }
+    copy2d(dt, dinv_k(k), T, colp(sh(k), g, s0, g.loc(k)), n, tc, tc, false, nullptr, st);
+  }
+  for (int64_t j = 0; j < g.nt; ++j) {
+    const int64_t js = g.start(j), tcj = g.stop(j) - js, lda = n - js;
+    for (int64_t s = j; s < g.nt; ++s) {
+      const int64_t ss = g.start(s), tcs = g.stop(s) - ss;
+      Operand Ws = opA(colp(sh(s), g, ss, g.loc(s)), n, OP_C);
+      Ws.mask = 1;  // storage row ss+kk >= storage col ss+i
+      Operand Wj = opB(colp(sh(j), g, ss, g.loc(j)), n, OP_N);
+      Wj.mask = 1;
+      Wj.mask_off = ss - js;  // storage row ss+kk >= col js+nn
+      gemm(dt, tcs, tcj, n - ss, Ws, Wj, Epilogue{accp + (ss - js) * g.esz, lda, 1.0, 0.0, 0, 0}, nullptr, st);
+    }
+    copy2d(dt, accp, lda, colp(sh(j), g, js, g.loc(j)), n, n - js, tcj, false, nullptr, st);
+    zero_upper(dt, colp(sh(j), g, 0, g.loc(j)), n, js, tcj, js + 1, st);  // rows above the tile: 0
+  }
+  for (int64_t j = 0; j < g.nt; ++j) {
+    const int64_t js = g.start(j), tcj = g.stop(j) - js;
+    for (int64_t i = j; i < g.nt; ++i) {
+      const int64_t is = g.start(i), tci = g.stop(i) - is;
+      if (i == j) {
+        mirror_diag(dt, colp(sh(j), g, js, g.loc(j)), n, tcj, st);
+      } else {
+        conj_transpose(dt, colp(sh(j), g, is, g.loc(j)), n, colp(sh(i), g, js, g.loc(i)), n, tcj, tci, st);
+      }
+    }
+  }
+  sync_streams(user, crit);
+}
+}  // namespace bcmg
