@@ -129,6 +129,19 @@ int bcmg_last_timings(bcmg_session* s, float* ms /* [4] */);
 /* algorithmic bytes (read + write) moved by the last redistribution */
 int64_t bcmg_last_moved_bytes(bcmg_session* s);
 
+/* Per-kernel timing: when on, every launch of a kernel kind is bracketed by
+   CUDA events on the stream it is launched on.  kind: 0 trailing update
+   (DMMA GEMM), 1 panel TRSM, 2 diagonal factor+inverse, 3 cycle rotation.
+   stats[4] = {launches, total ms, algorithmic work (flops; bytes for kind 3),
+   max ms}; reading clears the record. */
+int bcmg_set_profiling(bcmg_session* s, int on);
+int bcmg_kernel_stats(bcmg_session* s, int kind, double* stats /* [4] */);
+/* kernels launched by this library in this process so far */
+int64_t bcmg_launch_count(void);
+/* FP64 tensor-core (DMMA) throughput of a register-resident mma.sync loop on
+   all SMs, TFLOP/s: the roofline denominator of the FP64 kernels */
+int bcmg_measure_fp64_peak(int cuda_device, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,7 +55,13 @@ SIGNATURES = {
     "bcmg_potri_factored": (C.c_int, [_vp, _vp, C.c_int, _i64, _i64, C.c_int, _vpp]),
     "bcmg_last_timings": (C.c_int, [_vp, C.POINTER(C.c_float)]),
     "bcmg_last_moved_bytes": (C.c_int64, [_vp]),
+    "bcmg_set_profiling": (C.c_int, [_vp, C.c_int]),
+    "bcmg_kernel_stats": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_double)]),
+    "bcmg_launch_count": (C.c_int64, []),
+    "bcmg_measure_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
 }
+
+KERNEL_KINDS = {"trailing_update": 0, "panel_trsm": 1, "diag_factor": 2, "rotate": 3}
 
 
 class LibraryMissingError(ImportError):

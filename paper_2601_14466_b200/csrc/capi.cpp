@@ -275,4 +275,21 @@ int bcmg_last_timings(bcmg_session* s, float* ms) {
 
 int64_t bcmg_last_moved_bytes(bcmg_session* s) { return (s && s->impl) ? s->impl->last_moved_bytes : -1; }
 
+int bcmg_set_profiling(bcmg_session* s, int on) {
+  return guarded([&] { live(s)->profiling = on != 0; });
+}
+
+int bcmg_kernel_stats(bcmg_session* s, int kind, double* stats) {
+  return guarded([&] { live(s)->kernel_stats(kind, stats); });
+}
+
+int64_t bcmg_launch_count(void) { return (int64_t)bcmg::launch_count(); }
+
+int bcmg_measure_fp64_peak(int cuda_device, double* tflops) {
+  return guarded([&] {
+    BCMG_CUDA(cudaSetDevice(cuda_device));
+    *tflops = bcmg::measure_dmma_peak(nullptr);
+  });
+}
+
 }  // extern "C"

@@ -55,7 +55,14 @@ struct Error : std::runtime_error {
     }                                                                                \
   } while (0)
 
-#define BCMG_CHECK_LAUNCH() BCMG_CUDA(cudaGetLastError())
+// Every kernel launch of the library goes through BCMG_CHECK_LAUNCH, which
+// also counts it (bcmg_launch_count(): evidence that the native path ran).
+void note_launch();
+#define BCMG_CHECK_LAUNCH()            \
+  do {                                 \
+    BCMG_CUDA(cudaGetLastError());     \
+    ::bcmg::note_launch();             \
+  } while (0)
 
 // ---------------------------------------------------------------- storage traits
 // Storage type S <-> compute value.  Real types compute in double; complex

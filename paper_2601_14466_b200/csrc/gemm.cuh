@@ -68,15 +68,25 @@ struct Epilogue {
   int64_t lower_off;
 };
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+// PAIR: fragment f covers rows {16(f/2) + 2r + f%2 : r = 0..7} instead of
+// {8f + r}, so a thread's rows for fragments 2p and 2p+1 are adjacent and one
+// LDS.128 feeds two DMMA fragments (rows of a GEMM are independent: the
+// permutation changes no arithmetic, only where the epilogue stores).
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, bool PAIR_ = false>
 struct Tile {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr bool PAIR = PAIR_;
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
   static constexpr int FM = WM / 8, FN = WN / 8;
-  static constexpr int LDA = BM + 4, LDB = BN + 4;  // 8-byte words; == 4 (mod 16)
-  static_assert(LDA % 16 == 4 && LDB % 16 == 4, "row pad must be 4 words mod 16");
-  static constexpr int A_WORDS = BK * LDA, B_WORDS = BK * LDB;
+  static_assert(!PAIR || (FM % 2 == 0 && FN % 2 == 0), "paired fragments need even counts");
+  // i-contiguous tiles [BK][BI+4] (operand stored with i contiguous) and
+  // k-contiguous tiles [BI][BK+4] (operand stored with k contiguous); the
+  // 4-word pad keeps both fragment read patterns bank-conflict free.
+  static constexpr int LDA = BM + 4, LDB = BN + 4, LDT = BK + 4;  // 8-byte words; == 4 (mod 16)
+  static_assert(LDA % 16 == 4 && LDB % 16 == 4 && LDT % 16 == 4, "row pad must be 4 words mod 16");
+  static constexpr int A_WORDS = (BK * LDA > BM * LDT) ? BK * LDA : BM * LDT;
+  static constexpr int B_WORDS = (BK * LDB > BN * LDT) ? BK * LDB : BN * LDT;
   static constexpr int STAGE_WORDS = A_WORDS + B_WORDS;
 };
 
@@ -101,8 +111,13 @@ struct Acc {
   }
 };
 
+template <class TL>
+__device__ __forceinline__ int frag_row(int f, int r) {
+  return TL::PAIR ? 16 * (f >> 1) + 2 * r + (f & 1) : 8 * f + r;
+}
+
 // One BK slice of DMMAs out of shared memory (planes: real or re/im).
-template <class TL, bool CPLX>
+template <class TL, bool CPLX, bool TA, bool TB>
 __device__ __forceinline__ void mma_slice(Acc<TL, CPLX>& acc, const double* __restrict__ As,
                                           const double* __restrict__ Bs, const double* __restrict__ Asi,
                                           const double* __restrict__ Bsi, int wm0, int wn0, int lane) {
@@ -111,15 +126,37 @@ __device__ __forceinline__ void mma_slice(Acc<TL, CPLX>& acc, const double* __re
   for (int kk = 0; kk < TL::BK; kk += 4) {
     double a[TL::FM], b[TL::FN];
     double ai[CPLX ? TL::FM : 1], bi[CPLX ? TL::FN : 1];
+    if constexpr (TL::PAIR && !TA && !CPLX) {
 #pragma unroll
-    for (int f = 0; f < TL::FM; ++f) {
-      a[f] = As[(kk + q) * TL::LDA + wm0 + f * 8 + r];
-      if constexpr (CPLX) ai[f] = Asi[(kk + q) * TL::LDA + wm0 + f * 8 + r];
+      for (int f = 0; f < TL::FM; f += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(As + (kk + q) * TL::LDA + wm0 + frag_row<TL>(f, r));
+        a[f] = v.x;
+        a[f + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int f = 0; f < TL::FM; ++f) {
+        const int m = wm0 + frag_row<TL>(f, r);
+        const int o = TA ? m * TL::LDT + kk + q : (kk + q) * TL::LDA + m;
+        a[f] = As[o];
+        if constexpr (CPLX) ai[f] = Asi[o];
+      }
     }
+    if constexpr (TL::PAIR && !TB && !CPLX) {
 #pragma unroll
-    for (int f = 0; f < TL::FN; ++f) {
-      b[f] = Bs[(kk + q) * TL::LDB + wn0 + f * 8 + r];
-      if constexpr (CPLX) bi[f] = Bsi[(kk + q) * TL::LDB + wn0 + f * 8 + r];
+      for (int f = 0; f < TL::FN; f += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(Bs + (kk + q) * TL::LDB + wn0 + frag_row<TL>(f, r));
+        b[f] = v.x;
+        b[f + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int f = 0; f < TL::FN; ++f) {
+        const int nn = wn0 + frag_row<TL>(f, r);
+        const int o = TB ? nn * TL::LDT + kk + q : (kk + q) * TL::LDB + nn;
+        b[f] = Bs[o];
+        if constexpr (CPLX) bi[f] = Bsi[o];
+      }
     }
 #pragma unroll
     for (int fm = 0; fm < TL::FM; ++fm)
@@ -163,14 +200,16 @@ struct RegFeed {
       if constexpr (CPLX) vi[e] = v.y;
     }
   }
-  __device__ __forceinline__ void store(const Operand& op, double* Xs, double* Xsi, int LD, int tid) const {
+  // LD: row length of the i-contiguous layout; LDT: of the k-contiguous one
+  __device__ __forceinline__ void store(const Operand& op, double* Xs, double* Xsi, int LD, int LDT, int tid) const {
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int idx = tid + e * THREADS;
       const int il = op.trans ? idx / BK : idx % BI;
       const int kl = op.trans ? idx % BK : idx / BI;
-      Xs[kl * LD + il] = vr[e];
-      if constexpr (CPLX) Xsi[kl * LD + il] = vi[e];
+      const int o = op.trans ? il * LDT + kl : kl * LD + il;
+      Xs[o] = vr[e];
+      if constexpr (CPLX) Xsi[o] = vi[e];
     }
   }
 };
@@ -196,6 +235,32 @@ __device__ __forceinline__ void cp_feed(const Operand& op, int64_t I, int64_t K,
   }
 }
 
+// k-contiguous operand (Xhat(i,k) = X[k + i*ld]) into [BI][BK+4].
+template <int BI, int BK, int LDT, int THREADS>
+__device__ __forceinline__ void cp_feed_t(const Operand& op, int64_t I, int64_t K, int64_t i0, int64_t k0,
+                                          double* Xs, int tid) {
+  constexpr int CH = BI * (BK / 2);
+  static_assert(CH % THREADS == 0, "chunks not divisible by threads");
+  const double* base = reinterpret_cast<const double*>(op.ptr);
+#pragma unroll
+  for (int c = 0; c < CH / THREADS; ++c) {
+    const int idx = tid + c * THREADS;
+    const int kl = (idx % (BK / 2)) * 2, il = idx / (BK / 2);
+    const int64_t i = i0 + il, k = k0 + kl;
+    int64_t rem = K - k;
+    int bytes = (i < I && rem > 0) ? (rem >= 2 ? 16 : 8) : 0;
+    const double* src = bytes ? base + k + i * op.ld : base;
+    cp_async16(Xs + il * LDT + kl, src, bytes);
+  }
+}
+
+template <bool T, int BI, int BK, int LD, int LDT, int THREADS>
+__device__ __forceinline__ void cp_feed_any(const Operand& op, int64_t I, int64_t K, int64_t i0, int64_t k0,
+                                            double* Xs, int tid) {
+  if constexpr (T) cp_feed_t<BI, BK, LDT, THREADS>(op, I, K, i0, k0, Xs, tid);
+  else cp_feed<BI, BK, THREADS>(op, I, K, i0, k0, Xs, LD, tid);
+}
+
 // ----------------------------------------------------------------- epilogue
 template <class S, class TL, bool CPLX>
 __device__ __forceinline__ void store_block(const Acc<TL, CPLX>& acc, const Epilogue& ep, int64_t M, int64_t N,
@@ -208,8 +273,8 @@ __device__ __forceinline__ void store_block(const Acc<TL, CPLX>& acc, const Epil
     for (int fn = 0; fn < TL::FN; ++fn)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const int64_t row = m0 + wm0 + fm * 8 + r;
-        const int64_t col = n0 + wn0 + fn * 8 + 2 * q + j;
+        const int64_t row = m0 + wm0 + frag_row<TL>(fm, r);
+        const int64_t col = n0 + wn0 + (TL::PAIR ? 16 * (fn >> 1) + 2 * (2 * q + j) + (fn & 1) : fn * 8 + 2 * q + j);
         if (row < M && col < N && (!ep.lower_only || row - col >= ep.lower_off)) {
           S* c = C + row + col * ep.ldc;
           double2 v = make_double2(ep.alpha * acc.re[fm][fn][j], 0.0);
@@ -226,7 +291,7 @@ __device__ __forceinline__ void store_block(const Acc<TL, CPLX>& acc, const Epil
 
 // ----------------------------------------------------------------- block GEMM
 // Computes the BM x BN block at (m0, n0) of C := alpha*Ahat*Bhat^T + beta*C.
-template <class S, class TL, bool CP>
+template <class S, class TL, bool CP, bool TA, bool TB>
 __device__ __forceinline__ void gemm_block(const Operand& A, const Operand& B, int64_t M, int64_t N, int64_t K,
                                            int64_t m0, int64_t n0, const Epilogue& ep, double* smem) {
   constexpr bool CPLX = Traits<S>::cplx;
@@ -243,8 +308,9 @@ __device__ __forceinline__ void gemm_block(const Operand& A, const Operand& B, i
     for (int s = 0; s < TL::STAGES - 1; ++s) {
       if (s < KT) {
         double* st = smem + s * TL::STAGE_WORDS;
-        cp_feed<TL::BM, TL::BK, TL::THREADS>(A, M, K, m0, (int64_t)s * TL::BK, st, TL::LDA, tid);
-        cp_feed<TL::BN, TL::BK, TL::THREADS>(B, N, K, n0, (int64_t)s * TL::BK, st + TL::A_WORDS, TL::LDB, tid);
+        cp_feed_any<TA, TL::BM, TL::BK, TL::LDA, TL::LDT, TL::THREADS>(A, M, K, m0, (int64_t)s * TL::BK, st, tid);
+        cp_feed_any<TB, TL::BN, TL::BK, TL::LDB, TL::LDT, TL::THREADS>(B, N, K, n0, (int64_t)s * TL::BK,
+                                                                        st + TL::A_WORDS, tid);
       }
       cp_async_commit();
     }
@@ -254,12 +320,13 @@ __device__ __forceinline__ void gemm_block(const Operand& A, const Operand& B, i
       const int nk = kt + TL::STAGES - 1;
       if (nk < KT) {
         double* st = smem + (nk % TL::STAGES) * TL::STAGE_WORDS;
-        cp_feed<TL::BM, TL::BK, TL::THREADS>(A, M, K, m0, (int64_t)nk * TL::BK, st, TL::LDA, tid);
-        cp_feed<TL::BN, TL::BK, TL::THREADS>(B, N, K, n0, (int64_t)nk * TL::BK, st + TL::A_WORDS, TL::LDB, tid);
+        cp_feed_any<TA, TL::BM, TL::BK, TL::LDA, TL::LDT, TL::THREADS>(A, M, K, m0, (int64_t)nk * TL::BK, st, tid);
+        cp_feed_any<TB, TL::BN, TL::BK, TL::LDB, TL::LDT, TL::THREADS>(B, N, K, n0, (int64_t)nk * TL::BK,
+                                                                        st + TL::A_WORDS, tid);
       }
       cp_async_commit();
       const double* st = smem + (kt % TL::STAGES) * TL::STAGE_WORDS;
-      mma_slice<TL, false>(acc, st, st + TL::A_WORDS, nullptr, nullptr, wm0, wn0, lane);
+      mma_slice<TL, false, TA, TB>(acc, st, st + TL::A_WORDS, nullptr, nullptr, wm0, wn0, lane);
     }
     cp_async_wait<0>();
     __syncthreads();
@@ -272,8 +339,8 @@ __device__ __forceinline__ void gemm_block(const Operand& A, const Operand& B, i
     fb.load(B, N, K, n0, 0, tid);
     {
       double* s0 = bufA(0);
-      fa.store(A, s0, s0 + PLANE, TL::LDA, tid);
-      fb.store(B, s0 + TL::A_WORDS, s0 + PLANE + TL::A_WORDS, TL::LDB, tid);
+      fa.store(A, s0, s0 + PLANE, TL::LDA, TL::LDT, tid);
+      fb.store(B, s0 + TL::A_WORDS, s0 + PLANE + TL::A_WORDS, TL::LDB, TL::LDT, tid);
     }
     __syncthreads();
     for (int kt = 0; kt < KT; ++kt) {
@@ -283,11 +350,11 @@ __device__ __forceinline__ void gemm_block(const Operand& A, const Operand& B, i
         fb.load(B, N, K, n0, (int64_t)(kt + 1) * TL::BK, tid);
       }
       const double* s = bufA(kt & 1);
-      mma_slice<TL, CPLX>(acc, s, s + TL::A_WORDS, s + PLANE, s + PLANE + TL::A_WORDS, wm0, wn0, lane);
+      mma_slice<TL, CPLX, TA, TB>(acc, s, s + TL::A_WORDS, s + PLANE, s + PLANE + TL::A_WORDS, wm0, wn0, lane);
       if (more) {
         double* d = bufA((kt + 1) & 1);
-        fa.store(A, d, d + PLANE, TL::LDA, tid);
-        fb.store(B, d + TL::A_WORDS, d + PLANE + TL::A_WORDS, TL::LDB, tid);
+        fa.store(A, d, d + PLANE, TL::LDA, TL::LDT, tid);
+        fb.store(B, d + TL::A_WORDS, d + PLANE + TL::A_WORDS, TL::LDB, TL::LDT, tid);
       }
       __syncthreads();
     }
@@ -297,12 +364,13 @@ __device__ __forceinline__ void gemm_block(const Operand& A, const Operand& B, i
 
 // ----------------------------------------------------------------- front-ends
 // Single GEMM: grid (ceil(M/BM), ceil(N/BN)).
-template <class S, class TL, bool CP>
+template <class S, class TL, bool CP, bool TA, bool TB>
 __global__ void __launch_bounds__(TL::THREADS) gemm_kernel(Operand A, Operand B, int64_t M, int64_t N, int64_t K,
                                                             Epilogue ep, const int* info) {
   if (ld_flag(info)) return;
   extern __shared__ __align__(16) double smem[];
-  gemm_block<S, TL, CP>(A, B, M, N, K, (int64_t)blockIdx.x * TL::BM, (int64_t)blockIdx.y * TL::BN, ep, smem);
+  gemm_block<S, TL, CP, TA, TB>(A, B, M, N, K, (int64_t)blockIdx.x * TL::BM, (int64_t)blockIdx.y * TL::BN, ep,
+                                smem);
 }
 
 // Trailing update of potrf step k on this process's shards:
@@ -370,7 +438,7 @@ __global__ void __launch_bounds__(TL::THREADS) trail_kernel(TrailParams p, const
     Operand A{P + (ms - p.prow0), p.ldp, 0, 0, 0, 0};
     Operand Bo{P + (ms - p.prow0), p.ldp, 0, 1, 0, 0};
     Epilogue ep{shard + ms + loc * p.N, p.N, -1.0, 1.0, 0, 0};
-    gemm_block<S, TL, CP>(A, Bo, rows, tc, p.K, rb * B, cb * B, ep, smem);
+    gemm_block<S, TL, CP, false, false>(A, Bo, rows, tc, p.K, rb * B, cb * B, ep, smem);
     __syncthreads();
   }
 }

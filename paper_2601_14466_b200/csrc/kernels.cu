@@ -5,14 +5,19 @@
 //   * the in-place cycle rotation of the block-cyclic redistribution,
 //   * small copy / conjugate / mirror helpers.
 #include <algorithm>
+#include <atomic>
 #include <type_traits>
 
 #include "ops.h"
 
 namespace bcmg {
 
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
+
 // ============================================================== GEMM dispatch
-using TileBig = Tile<128, 128, 16, 64, 32, 4>;    // 256 threads, hot real path
+using TileBig = Tile<128, 128, 32, 32, 32, 3, true>;  // 512 threads, hot real path (paired LDS.128)
 using TileMed = Tile<64, 64, 16, 32, 32, 3>;      // 128 threads, general
 using TileNarrow = Tile<128, 16, 16, 32, 16, 3>;  // 128 threads, N <= 16 (RHS blocks)
 
@@ -39,19 +44,29 @@ static void set_smem(K kernel, size_t bytes) {
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-static bool cp_ok(const Operand& X) {
-  return !X.trans && !X.mask && aligned16(X.ptr) && (X.ld % 2 == 0);
+static bool cp_ok(const Operand& X) { return !X.mask && aligned16(X.ptr) && (X.ld % 2 == 0); }
+
+template <class S, class TL, bool CP, bool TA, bool TB>
+static void launch_gemm_t(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+                          const int* info, cudaStream_t st) {
+  constexpr size_t smem = gemm_smem_bytes<TL, Traits<S>::cplx, CP>();
+  auto kern = gemm_kernel<S, TL, CP, TA, TB>;
+  set_smem(kern, smem);
+  dim3 grid((unsigned)((M + TL::BM - 1) / TL::BM), (unsigned)((N + TL::BN - 1) / TL::BN));
+  kern<<<grid, TL::THREADS, smem, st>>>(A, B, M, N, K, ep, info);
+  BCMG_CHECK_LAUNCH();
 }
 
 template <class S, class TL, bool CP>
 static void launch_gemm(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
                         const int* info, cudaStream_t st) {
-  constexpr size_t smem = gemm_smem_bytes<TL, Traits<S>::cplx, CP>();
-  auto kern = gemm_kernel<S, TL, CP>;
-  set_smem(kern, smem);
-  dim3 grid((unsigned)((M + TL::BM - 1) / TL::BM), (unsigned)((N + TL::BN - 1) / TL::BN));
-  kern<<<grid, TL::THREADS, smem, st>>>(A, B, M, N, K, ep, info);
-  BCMG_CHECK_LAUNCH();
+  if (A.trans) {
+    if (B.trans) launch_gemm_t<S, TL, CP, true, true>(M, N, K, A, B, ep, info, st);
+    else launch_gemm_t<S, TL, CP, true, false>(M, N, K, A, B, ep, info, st);
+  } else {
+    if (B.trans) launch_gemm_t<S, TL, CP, false, true>(M, N, K, A, B, ep, info, st);
+    else launch_gemm_t<S, TL, CP, false, false>(M, N, K, A, B, ep, info, st);
+  }
 }
 
 template <class S>
@@ -61,7 +76,7 @@ static void gemm_t(int64_t M, int64_t N, int64_t K, const Operand& A, const Oper
     const bool cp = cp_ok(A) && cp_ok(B);
     if (cp) {
       if (N <= 16) return launch_gemm<S, TileNarrow, true>(M, N, K, A, B, ep, info, st);
-      const int64_t big_blocks = ((M + 127) / 128) * ((N + 127) / 128);
+      const int64_t big_blocks = ((M + TileBig::BM - 1) / TileBig::BM) * ((N + TileBig::BN - 1) / TileBig::BN);
       if (big_blocks >= num_sms()) return launch_gemm<S, TileBig, true>(M, N, K, A, B, ep, info, st);
       return launch_gemm<S, TileMed, true>(M, N, K, A, B, ep, info, st);
     }
@@ -121,7 +136,6 @@ void trailing_update(int dt, const TrailParams& p, const int* info, cudaStream_t
 // (the reference's unblocked factor is solvers.py:322-338; same pivot test:
 // d = Re a_jj after the updates, fail unless d > 0 and finite).
 constexpr int LEAF = 64;
-constexpr int LEAF_LD = LEAF + 1;
 
 template <bool C> struct V_ { using type = double; };
 template <> struct V_<true> { using type = double2; };
@@ -146,69 +160,111 @@ template <> __device__ __forceinline__ double2 v_from<double2>(double2 x) { retu
 __device__ __forceinline__ double2 v_to(double a) { return make_double2(a, 0.0); }
 __device__ __forceinline__ double2 v_to(double2 a) { return a; }
 
+// Register-resident leaf: thread (ty, tx) = (tid/16, tid%16) owns the 4x4
+// elements (ty + 16a, tx + 16b) of both L and X = L^-1, so the only shared
+// traffic per column is a broadcast of the scaled column of L and row of X
+// (double buffered: two barriers per column, no shared-memory matrix).
+// Right-looking: step j takes the pivot d = Re a_jj after all earlier
+// updates -- the reference's test, failing unless d > 0 and finite.
 template <class S>
 __global__ void __launch_bounds__(256) leaf_kernel(S* A, int64_t lda, S* X, int64_t ldx, int n, int64_t goff,
                                                    int* info) {
   using V = typename V_<Traits<S>::cplx>::type;
   if (*(volatile int*)info) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* Ls = reinterpret_cast<V*>(smem_raw);
-  V* Xs = Ls + LEAF * LEAF_LD;
-  __shared__ double s_inv;
+  __shared__ V colL[2][LEAF];
+  __shared__ V rowX[2][LEAF];
+  __shared__ double s_inv[2];
   __shared__ int s_bad;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int idx = tid; idx < n * n; idx += blockDim.x) {
-    const int i = idx % n, c = idx / n;
-    Ls[i * LEAF_LD + c] = (i >= c) ? v_from<V>(to_c(A[i + (int64_t)c * lda])) : v_from<V>(make_double2(0, 0));
-    Xs[i * LEAF_LD + c] = v_from<V>(make_double2(i == c ? 1.0 : 0.0, 0.0));
-  }
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  V l[4][4], x[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, c = tx + 16 * b;
+      const bool in = i < n && c < n;
+      l[a][b] = v_from<V>(in && i >= c ? to_c(A[i + (int64_t)c * lda]) : make_double2(0, 0));
+      x[a][b] = v_from<V>(make_double2(in && i == c ? 1.0 : 0.0, 0.0));
+    }
   if (tid == 0) s_bad = -1;
   __syncthreads();
-  int j = 0;
-  for (; j < n; ++j) {
-    if (tid == 0) {
-      const double d = v_re(Ls[j * LEAF_LD + j]);
-      if (!(d > 0.0) || !isfinite(d)) {
-        s_bad = j;
-      } else {
-        const double l = sqrt(d);
-        Ls[j * LEAF_LD + j] = v_from<V>(make_double2(l, 0.0));
-        s_inv = 1.0 / l;
+  int done = n;
+#pragma unroll
+  for (int jo = 0; jo < 4; ++jo) {
+    for (int jl = 0; jl < 16; ++jl) {
+      const int j = 16 * jo + jl, buf = j & 1;
+      if (j >= n) goto finished;
+      // pivot (owner of (j, j))
+      if (ty == jl && tx == jl) {
+        const double d = v_re(l[jo][jo]);
+        if (!(d > 0.0) || !isfinite(d)) {
+          s_bad = j;
+        } else {
+          const double lv = sqrt(d);
+          l[jo][jo] = v_from<V>(make_double2(lv, 0.0));
+          s_inv[buf] = 1.0 / lv;
+        }
+      }
+      __syncthreads();
+      if (s_bad >= 0) {
+        done = j;
+        goto finished;
+      }
+      {
+        const double inv = s_inv[buf];
+        if (tx == jl) {  // column j of L, rows below the diagonal
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const int i = ty + 16 * a;
+            if (i > j && i < n) {
+              l[a][jo] = v_scale(l[a][jo], inv);
+              colL[buf][i] = l[a][jo];
+            }
+          }
+        }
+        if (ty == jl) {  // row j of X, columns up to the diagonal
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int c = tx + 16 * b;
+            if (c <= j) {
+              x[jo][b] = v_scale(x[jo][b], inv);
+              rowX[buf][c] = x[jo][b];
+            }
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int i = ty + 16 * a;
+        if (i > j && i < n) {
+          const V lij = colL[buf][i];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int c = tx + 16 * b;
+            if (c <= j) x[a][b] = v_fnms(x[a][b], lij, rowX[buf][c]);
+            else if (c <= i) l[a][b] = v_fnmsc(l[a][b], lij, colL[buf][c]);
+          }
+        }
       }
     }
-    __syncthreads();
-    if (s_bad >= 0) break;
-    const double inv = s_inv;
-    for (int i = j + 1 + tid; i < n; i += blockDim.x) Ls[i * LEAF_LD + j] = v_scale(Ls[i * LEAF_LD + j], inv);
-    for (int c = tid; c <= j; c += blockDim.x) Xs[j * LEAF_LD + c] = v_scale(Xs[j * LEAF_LD + c], inv);
-    __syncthreads();
-    for (int i = j + 1 + warp; i < n; i += blockDim.x / 32) {
-      const V lij = Ls[i * LEAF_LD + j];
-      for (int c = lane; c <= i; c += 32) {
-        if (c <= j)
-          Xs[i * LEAF_LD + c] = v_fnms(Xs[i * LEAF_LD + c], lij, Xs[j * LEAF_LD + c]);
-        else
-          Ls[i * LEAF_LD + c] = v_fnmsc(Ls[i * LEAF_LD + c], lij, Ls[c * LEAF_LD + j]);
-      }
-    }
-    __syncthreads();
   }
-  const int done = j;  // columns [0, done) of L are final
+finished:
   if (done < n && tid == 0) atomicCAS(info, 0, (int)(goff + done + 1));
-  for (int idx = tid; idx < n * n; idx += blockDim.x) {
-    const int i = idx % n, c = idx / n;
-    if (c < done && i >= c) A[i + (int64_t)c * lda] = from_c<S>(v_to(Ls[i * LEAF_LD + c]));
-    if (done == n) X[i + (int64_t)c * ldx] = from_c<S>(i >= c ? v_to(Xs[i * LEAF_LD + c]) : make_double2(0, 0));
-  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, c = tx + 16 * b;
+      if (i >= n || c >= n) continue;
+      if (c < done && i >= c) A[i + (int64_t)c * lda] = from_c<S>(v_to(l[a][b]));
+      if (done == n) X[i + (int64_t)c * ldx] = from_c<S>(i >= c ? v_to(x[a][b]) : make_double2(0, 0));
+    }
 }
 
 template <class S>
 static void launch_leaf(S* A, int64_t lda, S* X, int64_t ldx, int n, int64_t goff, int* info, cudaStream_t st) {
-  using V = typename V_<Traits<S>::cplx>::type;
-  const size_t smem = 2 * LEAF * LEAF_LD * sizeof(V);
-  auto kern = leaf_kernel<S>;
-  set_smem(kern, smem);
-  kern<<<1, 256, smem, st>>>(A, lda, X, ldx, n, goff, info);
+  leaf_kernel<S><<<1, 256, 0, st>>>(A, lda, X, ldx, n, goff, info);
   BCMG_CHECK_LAUNCH();
 }
 
@@ -474,5 +530,46 @@ void mirror_diag(int dt, void* a, int64_t lda, int64_t n, cudaStream_t st) {
     mirror_diag_kernel<S><<<ew_grid(n * n), 256, 0, st>>>(static_cast<S*>(a), lda, n);
   });
   BCMG_CHECK_LAUNCH();
+}
+
+// ============================================================== FP64 peak probe
+// Register-resident DMMA loop (8 independent accumulators per warp, 16 warps
+// per SM): the FP64 tensor roofline denominator, measured live by bench.py.
+__global__ void __launch_bounds__(512) dmma_peak_kernel(double* out, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma(c[i][0], c[i][1], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.0) out[threadIdx.x] = s;
+}
+
+double measure_dmma_peak(cudaStream_t st) {
+  double* out = nullptr;
+  BCMG_CUDA(cudaMalloc(&out, 4096 * sizeof(double)));
+  cudaEvent_t e0, e1;
+  BCMG_CUDA(cudaEventCreate(&e0));
+  BCMG_CUDA(cudaEventCreate(&e1));
+  const int grid = num_sms(), iters = 40000;
+  dmma_peak_kernel<<<grid, 512, 0, st>>>(out, 1000);  // warm-up
+  BCMG_CHECK_LAUNCH();
+  BCMG_CUDA(cudaEventRecord(e0, st));
+  dmma_peak_kernel<<<grid, 512, 0, st>>>(out, iters);
+  BCMG_CHECK_LAUNCH();
+  BCMG_CUDA(cudaEventRecord(e1, st));
+  BCMG_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  BCMG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  const double flops = 2.0 * 8 * 8 * 4 * 8.0 * iters * (double)grid * 16;
+  return flops / (ms * 1e-3) / 1e12;
 }
 }  // namespace bcmg

@@ -9,6 +9,9 @@
 
 namespace bcmg {
 
+long long launch_count();
+double measure_dmma_peak(cudaStream_t st);  // TFLOP/s
+
 // C := alpha*op(A)*op(B) + beta*C, any dtype (dt), any shape; dispatches to
 // the cp.async DMMA kernel when the operands qualify, else the REG kernel.
 void gemm(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,

@@ -87,6 +87,12 @@ Session::~Session() {
   for (auto* b : {&panel[0], &panel[1], &dinv, &wdiag, &info_dev, &tmp, &acc, &plan_buf}) b->release();
   for (auto& e : ev_pool) cudaEventDestroy(e);
   for (auto& e : ev_time) cudaEventDestroy(e);
+  for (auto& k : kstat)
+    for (auto& pr : k.ev) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+  for (auto& e : ev_spare) cudaEventDestroy(e);
   if (info_host) cudaFreeHost(info_host);
   cudaStreamDestroy(crit);
   cudaStreamDestroy(bulk);
@@ -94,6 +100,38 @@ Session::~Session() {
 }
 
 cudaEvent_t Session::ev(int i) { return ev_pool[i % kEvents]; }
+
+cudaEvent_t Session::take_event() {
+  if (!ev_spare.empty()) {
+    cudaEvent_t e = ev_spare.back();
+    ev_spare.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  BCMG_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void Session::kernel_stats(int kind, double* out) {
+  if (kind < 0 || kind >= K_KINDS) throw Error(CONFIG, "unknown kernel kind");
+  KStat& k = kstat[kind];
+  double tot = 0, mx = 0;
+  for (auto& pr : k.ev) {
+    BCMG_CUDA(cudaEventSynchronize(pr.second));
+    float ms = 0;
+    BCMG_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+    tot += ms;
+    mx = std::max(mx, (double)ms);
+    ev_spare.push_back(pr.first);
+    ev_spare.push_back(pr.second);
+  }
+  out[0] = (double)k.ev.size();
+  out[1] = tot;
+  out[2] = k.work;
+  out[3] = mx;
+  k.ev.clear();
+  k.work = 0;
+}
 
 void Session::begin(cudaStream_t user_stream) {
   user = user_stream;
@@ -227,7 +265,7 @@ void Session::redistribute(int dt, int64_t n_rows, int64_t n_cols, int64_t T, in
   j.n_cycles = nc;
   j.total_lanes = lane_pref[nc];
   j.vec = vec;
-  rotate_cycles(j, crit);
+  timed(K_ROTATE, crit, 2.0 * (double)nm * plan.seg * col_bytes, [&] { rotate_cycles(j, crit); });
   // (cudaMemcpyAsync from pageable memory returns once the source is consumed)
   last_moved_bytes = 2 * (int64_t)nm * plan.seg * col_bytes;
   sync_streams(user, crit);
@@ -260,10 +298,14 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
     const int64_t s0 = g.start(k), s1 = g.stop(k), tc = s1 - s0;
     void* sh = shard_of(k);
     void* Akk = colp(sh, g, s0, g.loc(k));
-    diag_factor(dt, Akk, n, dinv_k(k), T, wdiag.p, tc, s0, info, crit);
+    const double cf = dtype_complex(dt) ? 4.0 : 1.0;
+    timed(K_DIAG, crit, cf * (double)tc * tc * tc / 3.0,
+          [&] { diag_factor(dt, Akk, n, dinv_k(k), T, wdiag.p, tc, s0, info, crit); });
     if (s1 < n) {
-      gemm(dt, n - s1, tc, tc, opA(colp(sh, g, s1, g.loc(k)), n, OP_N), opB(dinv_k(k), T, OP_C),
-           Epilogue{panel[k % 2].p, n - s1, 1.0, 0.0, 0, 0}, info, crit);
+      timed(K_TRSM, crit, cf * 2.0 * (double)(n - s1) * tc * tc, [&] {
+        gemm(dt, n - s1, tc, tc, opA(colp(sh, g, s1, g.loc(k)), n, OP_N), opB(dinv_k(k), T, OP_C),
+             Epilogue{panel[k % 2].p, n - s1, 1.0, 0.0, 0, 0}, info, crit);
+      });
     }
   };
   auto trail = [&](int64_t k, int64_t m_first, int64_t m_last, cudaStream_t st) {
@@ -280,7 +322,14 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
     for (int i = 0; i < g.nloc; ++i) p.shards[i] = shards[i];
     p.m_first = m_first;
     p.m_last = m_last;
-    trailing_update(dt, p, info, st);
+    double flops = 0;  // algorithmic: lower trapezoid of every updated local tile
+    for (int64_t m = m_first; m < m_last; ++m) {
+      if (!g.owns(m)) continue;
+      const double rows = (double)(n - m * T), tcm = (double)std::min<int64_t>(T, n - m * T);
+      flops += 2.0 * (double)p.K * (rows * tcm - tcm * (tcm - 1) / 2);
+    }
+    if (dtype_complex(dt)) flops *= 4.0;
+    if (flops > 0) timed(K_TRAIL, st, flops, [&] { trailing_update(dt, p, info, st); });
   };
 
   // Event slots: type*8 + k%8 (dependencies reach back at most two steps).

@@ -36,6 +36,32 @@ struct Session {
   std::atomic<bool> busy{false};
   float phase_ms[kTimeEvents] = {0, 0, 0, 0, 0};
 
+  // Optional per-kernel timing (bcmg_set_profiling): CUDA events around each
+  // launch of a kind on the stream it is launched on, plus its algorithmic flops/bytes.
+  enum Kind : int { K_TRAIL = 0, K_TRSM = 1, K_DIAG = 2, K_ROTATE = 3, K_SUBST = 4, K_KINDS = 5 };
+  bool profiling = false;
+  struct KStat {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    double work = 0;
+  } kstat[K_KINDS];
+  std::vector<cudaEvent_t> ev_spare;
+  cudaEvent_t take_event();
+  template <class F>
+  void timed(int kind, cudaStream_t st, double work, F&& f) {
+    if (!profiling) {
+      f();
+      return;
+    }
+    cudaEvent_t a = take_event(), b = take_event();
+    BCMG_CUDA(cudaEventRecord(a, st));
+    f();
+    BCMG_CUDA(cudaEventRecord(b, st));
+    kstat[kind].ev.emplace_back(a, b);
+    kstat[kind].work += work;
+  }
+  // launches, total ms, work (flops or bytes), max ms; clears the record
+  void kernel_stats(int kind, double* out);
+
   Session(int device, int rank, int world, const unsigned char* nccl_id);
   ~Session();
 
