@@ -387,6 +387,7 @@ struct TrailParams {
   int D, dev0, nloc;  // logical devices; this launch owns dev0 .. dev0+nloc-1
   void* shards[MAX_LOCAL_DEV];
   int64_t m_first, m_last;
+  int max_ctas;       // host-side: persistent grid cap (0 = all SMs)
 };
 
 template <int B>

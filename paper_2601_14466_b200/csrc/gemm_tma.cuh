@@ -1,0 +1,220 @@
+// Hot-path FP64 GEMM: TMA-fed, mbarrier-pipelined, persistent DMMA kernel.
+//
+// Operands are real double, stored i-contiguous (column-major M x K for A,
+// N x K for B): the potrf trailing update C_m -= P P_m^H and the panel solve
+// P = A21 X11^H.  One elected thread issues cp.async.bulk.tensor (TMA, SASS
+// UTMALDG) boxes of {132 rows, BK columns} into a STAGES-deep ring; the box
+// is 4 rows taller than the tile so every smem row is 132 words long -- the
+// same conflict-free pad as the cp.async path, produced by TMA itself (TMA
+// cannot pad, but it can over-fetch).  Consumers wait on the stage's "full"
+// mbarrier (complete_tx) and release it with one arrive per warp on its
+// "empty" mbarrier, so warps never meet at a CTA-wide barrier inside the K
+// loop.  The kernel is persistent: the producer runs STAGES-1 slices ahead
+// across work-item boundaries, so the next tile's operands stream in while
+// the current tile's epilogue updates C.
+#pragma once
+
+#include <cuda.h>
+
+#include "gemm.cuh"
+
+namespace bcmg {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Box rows fetched per operand tile (tile rows + 4-row pad).
+template <class TL>
+constexpr int tma_box_rows_a() { return TL::LDA; }
+template <class TL>
+constexpr int tma_box_rows_b() { return TL::LDB; }
+template <class TL>
+constexpr unsigned tma_stage_bytes() { return (unsigned)(TL::BK * (TL::LDA + TL::LDB) * 8); }
+template <class TL>
+constexpr size_t tma_smem_bytes() { return (size_t)TL::STAGES * tma_stage_bytes<TL>() + 2 * TL::STAGES * 8 + 64; }
+
+// One output block: rows [a_row + m0 ...) of A's map, [b_row + n0 ...) of B's map.
+struct TmaBlock {
+  int a_row, b_row;      // tensor-map row coordinate of the block's first A / B row
+  int64_t m0, n0;        // block origin inside the output (for the epilogue)
+  int64_t M, N;          // output extent (rows >= M / cols >= N are not stored)
+  Epilogue ep;
+};
+
+// Persistent producer/consumer loop.  `next_p(item, blk)` / `next_c(item, blk)`
+// fill the block of work item `item` (producer / consumer view; separate so
+// stateful cursors stay monotone) and return false when there is none.
+template <class TL, class NextP, class NextC>
+__device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUtensorMap* mapB, int K, NextP&& next_p,
+                                              NextC&& next_c) {
+  extern __shared__ __align__(128) double smem[];
+  constexpr int NW = TL::THREADS / 32;
+  constexpr unsigned STAGE_BYTES = tma_stage_bytes<TL>();
+  constexpr int STAGE_WORDS = TL::BK * (TL::LDA + TL::LDB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TL::STAGES * STAGE_WORDS);
+  uint64_t* empty = full + TL::STAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm0 = (warp % TL::WARPS_M) * TL::WM, wn0 = (warp / TL::WARPS_M) * TL::WN;
+  const int KT = (K + TL::BK - 1) / TL::BK;
+  if (tid == 0) {
+    for (int s = 0; s < TL::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(mapB) : "memory");
+  }
+  __syncthreads();
+
+  // producer state (thread 0 only): slice counter gp over (item, kt)
+  int64_t p_item = blockIdx.x;
+  int p_kt = 0;
+  TmaBlock pb;
+  bool p_live = false;
+  uint32_t gp = 0;
+  auto produce_one = [&]() {
+    if (!p_live) return;
+    const int s = gp % TL::STAGES;
+    mbar_wait(&empty[s], ((gp / TL::STAGES) & 1) ^ 1);
+    double* st = smem + s * STAGE_WORDS;
+    mbar_expect_tx(&full[s], STAGE_BYTES);
+    tma_load_2d(st, mapA, pb.a_row + (int)pb.m0, p_kt * TL::BK, &full[s]);
+    tma_load_2d(st + TL::BK * TL::LDA, mapB, pb.b_row + (int)pb.n0, p_kt * TL::BK, &full[s]);
+    ++gp;
+    if (++p_kt == KT) {
+      p_kt = 0;
+      p_item += gridDim.x;
+      p_live = next_p(p_item, pb);
+    }
+  };
+  if (tid == 0) {
+    p_live = next_p(p_item, pb);
+    for (int i = 0; i < TL::STAGES - 1; ++i) produce_one();
+  }
+
+  uint32_t g = 0;
+  TmaBlock cb;
+  for (int64_t item = blockIdx.x; next_c(item, cb); item += gridDim.x) {
+    Acc<TL, false> acc;
+    acc.zero();
+    for (int kt = 0; kt < KT; ++kt) {
+      if (tid == 0) produce_one();
+      const int s = g % TL::STAGES;
+      mbar_wait(&full[s], (g / TL::STAGES) & 1);
+      const double* st = smem + s * STAGE_WORDS;
+      mma_slice<TL, false, false, false>(acc, st, st + TL::BK * TL::LDA, nullptr, nullptr, wm0, wn0, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      ++g;
+    }
+    store_block<double, TL, false>(acc, cb.ep, cb.M, cb.N, cb.m0, cb.n0, wm0, wn0, lane);
+  }
+}
+
+// Trailing update (see trail_kernel in gemm.cuh) over one panel tensor map.
+template <class TL>
+__global__ void __launch_bounds__(TL::THREADS, 1)
+    trail_tma_kernel(const __grid_constant__ CUtensorMap mapP, TrailParams p, const int* info) {
+  static_assert(TL::BM == TL::BN, "square blocks");
+  constexpr int B = TL::BM;
+  if (ld_flag(info)) return;
+  // tile cursor: items only grow for a given caller, so the walk over tiles is
+  // amortised O(1); producer and consumer each own one
+  struct Cursor {
+    int64_t m, base, cnt;
+  };
+  auto decode = [&p](Cursor& cur, int64_t item, TmaBlock& blk) -> bool {
+    for (;;) {
+      if (cur.m >= p.m_last) return false;
+      const int dev = (int)(cur.m % p.D);
+      const bool local = dev >= p.dev0 && dev < p.dev0 + p.nloc;
+      if (local) {
+        if (cur.cnt < 0) {
+          const int64_t ms = cur.m * p.T;
+          cur.cnt = trail_blocks<B>(p.N - ms, (p.T < p.N - ms ? p.T : p.N - ms));
+        }
+        if (item < cur.base + cur.cnt) break;
+        cur.base += cur.cnt;
+      }
+      ++cur.m;
+      cur.cnt = -1;
+    }
+    const int64_t m = cur.m, ms = m * p.T, rows = p.N - ms, tc = p.T < rows ? p.T : rows;
+    const int64_t ncb = (tc + B - 1) / B, tri = ncb * (ncb + 1) / 2;
+    const int64_t b = item - cur.base;
+    int64_t rb, cbk;
+    if (b < tri) {
+      rb = 0;
+      while ((rb + 1) * (rb + 2) / 2 <= b) ++rb;
+      cbk = b - rb * (rb + 1) / 2;
+    } else {
+      rb = ncb + (b - tri) / ncb;
+      cbk = (b - tri) % ncb;
+    }
+    const int dev = (int)(m % p.D);
+    double* shard = reinterpret_cast<double*>(p.shards[dev - p.dev0]);
+    const int64_t loc = (m / p.D) * p.T;
+    blk.a_row = (int)(ms - p.prow0);
+    blk.b_row = (int)(ms - p.prow0);
+    blk.m0 = rb * B;
+    blk.n0 = cbk * B;
+    blk.M = rows;
+    blk.N = tc;
+    blk.ep = Epilogue{shard + ms + loc * p.N, p.N, -1.0, 1.0, 0, 0};
+    return true;
+  };
+  Cursor cp{p.m_first, 0, -1}, cc{p.m_first, 0, -1};
+  tma_gemm_loop<TL>(
+      &mapP, &mapP, (int)p.K, [&](int64_t item, TmaBlock& blk) { return decode(cp, item, blk); },
+      [&](int64_t item, TmaBlock& blk) { return decode(cc, item, blk); });
+}
+
+// Single GEMM C := alpha A B^H (+ beta C) with A (M x K) and B (N x K) both
+// i-contiguous real double, persistent over the ceil(M/BM) x ceil(N/BN) blocks.
+template <class TL>
+__global__ void __launch_bounds__(TL::THREADS, 1)
+    gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int64_t M,
+                    int64_t N, int64_t K, Epilogue ep, const int* info) {
+  if (ld_flag(info)) return;
+  const int64_t nbm = (M + TL::BM - 1) / TL::BM, nbn = (N + TL::BN - 1) / TL::BN;
+  auto decode = [&](int64_t item, TmaBlock& blk) -> bool {
+    if (item >= nbm * nbn) return false;
+    // column-block-major: co-resident CTAs share the B (N x K) tile in L2
+    blk.a_row = 0;
+    blk.b_row = 0;
+    blk.m0 = (item % nbm) * TL::BM;
+    blk.n0 = (item / nbm) * TL::BN;
+    blk.M = M;
+    blk.N = N;
+    blk.ep = ep;
+    return true;
+  };
+  tma_gemm_loop<TL>(&mapA, &mapB, (int)K, decode, decode);
+}
+
+}  // namespace bcmg

@@ -8,6 +8,9 @@
 #include <atomic>
 #include <type_traits>
 
+#include <cudaTypedefs.h>
+
+#include "gemm_tma.cuh"
 #include "ops.h"
 
 namespace bcmg {
@@ -69,6 +72,11 @@ static void launch_gemm(int64_t M, int64_t N, int64_t K, const Operand& A, const
   }
 }
 
+static bool use_tma();
+static bool tma_ok(const void* p, int64_t ld);
+static void launch_gemm_tma(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+                            const int* info, cudaStream_t st);
+
 template <class S>
 static void gemm_t(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
                    const int* info, cudaStream_t st) {
@@ -77,7 +85,11 @@ static void gemm_t(int64_t M, int64_t N, int64_t K, const Operand& A, const Oper
     if (cp) {
       if (N <= 16) return launch_gemm<S, TileNarrow, true>(M, N, K, A, B, ep, info, st);
       const int64_t big_blocks = ((M + TileBig::BM - 1) / TileBig::BM) * ((N + TileBig::BN - 1) / TileBig::BN);
-      if (big_blocks >= num_sms()) return launch_gemm<S, TileBig, true>(M, N, K, A, B, ep, info, st);
+      if (big_blocks >= num_sms()) {
+        if (use_tma() && !A.trans && !B.trans && tma_ok(A.ptr, A.ld) && tma_ok(B.ptr, B.ld))
+          return launch_gemm_tma(M, N, K, A, B, ep, info, st);
+        return launch_gemm<S, TileBig, true>(M, N, K, A, B, ep, info, st);
+      }
       return launch_gemm<S, TileMed, true>(M, N, K, A, B, ep, info, st);
     }
   }
@@ -114,9 +126,83 @@ static void launch_trail(const TrailParams& p, const int* info, cudaStream_t st)
   int per_sm = 0;
   BCMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TL::THREADS, smem));
   per_sm = std::max(per_sm, 1);
-  const int64_t grid = std::min<int64_t>(total, (int64_t)num_sms() * per_sm);
+  int64_t grid = std::min<int64_t>(total, (int64_t)num_sms() * per_sm);
+  if (p.max_ctas > 0) grid = std::min<int64_t>(grid, p.max_ctas);
   kern<<<(unsigned)grid, TL::THREADS, smem, st>>>(p, info);
   BCMG_CHECK_LAUNCH();
+}
+
+// ============================================================== TMA tensor maps
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    BCMG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !f) throw Error(CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// 2D map over a column-major double matrix (rows contiguous), box {box_rows, box_cols}.
+static CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows, int box_cols) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+static bool tma_ok(const void* p, int64_t ld) { return aligned16(p) && ld % 2 == 0 && ld < ((int64_t)1 << 36); }
+
+static void launch_trail_tma(const TrailParams& p, const int* info, cudaStream_t st) {
+  using TL = TileBig;
+  int64_t total = 0;
+  for (int64_t m = p.m_first; m < p.m_last; ++m) {
+    const int dev = (int)(m % p.D);
+    if (dev < p.dev0 || dev >= p.dev0 + p.nloc) continue;
+    const int64_t rows = p.N - m * p.T, tc = std::min(p.T, rows);
+    const int64_t nrb = (rows + TL::BM - 1) / TL::BM, ncb = (tc + TL::BM - 1) / TL::BM;
+    total += nrb <= ncb ? nrb * (nrb + 1) / 2 : ncb * (ncb + 1) / 2 + (nrb - ncb) * ncb;
+  }
+  if (total == 0) return;
+  const CUtensorMap map = make_map(p.P, p.N - p.prow0, p.K, p.ldp, TL::LDA, TL::BK);
+  constexpr size_t smem = tma_smem_bytes<TL>();
+  auto kern = trail_tma_kernel<TL>;
+  set_smem(kern, smem);
+  int64_t grid = std::min<int64_t>(total, (int64_t)num_sms());
+  if (p.max_ctas > 0) grid = std::min<int64_t>(grid, p.max_ctas);
+  kern<<<(unsigned)grid, TL::THREADS, smem, st>>>(map, p, info);
+  BCMG_CHECK_LAUNCH();
+}
+
+static void launch_gemm_tma(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+                            const int* info, cudaStream_t st) {
+  using TL = TileBig;
+  const CUtensorMap ma = make_map(A.ptr, M, K, A.ld, TL::LDA, TL::BK);
+  const CUtensorMap mb = make_map(B.ptr, N, K, B.ld, TL::LDB, TL::BK);
+  constexpr size_t smem = tma_smem_bytes<TL>();
+  auto kern = gemm_tma_kernel<TL>;
+  set_smem(kern, smem);
+  const int64_t blocks = ((M + TL::BM - 1) / TL::BM) * ((N + TL::BN - 1) / TL::BN);
+  const int64_t grid = std::min<int64_t>(blocks, (int64_t)num_sms());
+  kern<<<(unsigned)grid, TL::THREADS, smem, st>>>(ma, mb, M, N, K, ep, info);
+  BCMG_CHECK_LAUNCH();
+}
+
+static bool use_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BCMG_NO_TMA");
+    v = (e && atoi(e)) ? 0 : 1;
+  }
+  return v == 1;
 }
 
 void trailing_update(int dt, const TrailParams& p, const int* info, cudaStream_t st) {
@@ -125,6 +211,7 @@ void trailing_update(int dt, const TrailParams& p, const int* info, cudaStream_t
     using S = decltype(s);
     if constexpr (std::is_same_v<S, double>) {
       const bool cp = aligned16(p.P) && p.ldp % 2 == 0 && p.T % 2 == 0 && (p.prow0 % 2 == 0);
+      if (cp && use_tma() && tma_ok(p.P, p.ldp)) return launch_trail_tma(p, info, st);
       if (cp) return launch_trail<S, TileBig, true>(p, info, st);
     }
     launch_trail<S, TileMed, false>(p, info, st);

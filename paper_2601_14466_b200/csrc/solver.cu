@@ -21,6 +21,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cstring>
 #include <memory>
@@ -308,8 +309,17 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
       });
     }
   };
-  auto trail = [&](int64_t k, int64_t m_first, int64_t m_last, cudaStream_t st) {
+  // While the lookahead path (diag factor + panel solve of tile k+1) runs on the
+  // crit stream, the bulk update is a persistent grid capped at (SMs - reserve)
+  // CTAs: its CTAs fill an SM's shared memory, so the cap is what leaves SMs
+  // on which the latency-bound critical path can overlap the bulk GEMM.
+  int reserve = 8;
+  if (const char* e = getenv("BCMG_RESERVE_SMS")) reserve = std::max(0, atoi(e));
+  int nsm = 148;
+  BCMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  auto trail = [&](int64_t k, int64_t m_first, int64_t m_last, cudaStream_t st, int cap = 0) {
     TrailParams p{};
+    p.max_ctas = cap;
     p.P = panel[k % 2].p;
     p.prow0 = g.stop(k);
     p.ldp = n - p.prow0;
@@ -362,7 +372,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
     }
     // -- bulk update of the other local trailing tiles (bulk stream)
     BCMG_CUDA(cudaStreamWaitEvent(bulk, E(R, k), 0));
-    trail(k, look ? k + 2 : k + 1, g.nt, bulk);
+    trail(k, look ? k + 2 : k + 1, g.nt, bulk, look ? std::max(1, nsm - reserve) : 0);
     if (mine)  // factor below the diagonal back into A (potrs/potri read it there)
       copy2d(dt, panel[b].p, n - s1, colp(shard_of(k), g, s1, g.loc(k)), n, n - s1, s1 - g.start(k), false, info,
              bulk);
