@@ -373,6 +373,26 @@ __global__ void __launch_bounds__(TL::THREADS) gemm_kernel(Operand A, Operand B,
                                 smem);
 }
 
+// Split-K GEMM: part z = blockIdx.z contracts k in [z*kchunk, (z+1)*kchunk)
+// into its own M x N slab of `parts` (ld M); a fixed-order reduction sums
+// the slabs afterwards, so the result does not depend on scheduling.
+template <class S, class TL, bool CP, bool TA, bool TB>
+__global__ void __launch_bounds__(TL::THREADS) gemm_splitk_kernel(Operand A, Operand B, int64_t M, int64_t N,
+                                                                   int64_t K, int64_t kchunk, S* parts) {
+  extern __shared__ __align__(16) double smem[];
+  const int64_t k0 = (int64_t)blockIdx.z * kchunk;
+  const int64_t kz = (K - k0 < kchunk) ? K - k0 : kchunk;
+  if (kz <= 0) return;
+  // advance both operands by k0 along their k dimension
+  A.ptr = reinterpret_cast<const S*>(A.ptr) + (A.trans ? k0 : k0 * A.ld);
+  B.ptr = reinterpret_cast<const S*>(B.ptr) + (B.trans ? k0 : k0 * B.ld);
+  A.mask_off += A.trans ? k0 : -k0;
+  B.mask_off += B.trans ? k0 : -k0;
+  Epilogue ep{parts + (int64_t)blockIdx.z * M * N, M, 1.0, 0.0, 0, 0};
+  gemm_block<S, TL, CP, TA, TB>(A, B, M, N, kz, (int64_t)blockIdx.x * TL::BM, (int64_t)blockIdx.y * TL::BN, ep,
+                                smem);
+}
+
 // Trailing update of potrf step k on this process's shards:
 //   for every local tile m in [m_first, m_last):
 //     A_m[ms:N, :] -= P[ms:N, :] * P[ms:ms+tc_m, :]^H

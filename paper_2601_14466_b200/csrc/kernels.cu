@@ -97,6 +97,54 @@ static void gemm_t(int64_t M, int64_t N, int64_t K, const Operand& A, const Oper
   return launch_gemm<S, TileMed, false>(M, N, K, A, B, ep, info, st);
 }
 
+template <class S, class TL, bool CP, bool TA, bool TB>
+static void launch_splitk_t(int64_t M, int64_t N, int64_t K, int64_t kchunk, int np, const Operand& A,
+                            const Operand& B, void* parts, cudaStream_t st) {
+  constexpr size_t smem = gemm_smem_bytes<TL, Traits<S>::cplx, CP>();
+  auto kern = gemm_splitk_kernel<S, TL, CP, TA, TB>;
+  set_smem(kern, smem);
+  dim3 grid((unsigned)((M + TL::BM - 1) / TL::BM), (unsigned)((N + TL::BN - 1) / TL::BN), (unsigned)np);
+  kern<<<grid, TL::THREADS, smem, st>>>(A, B, M, N, K, kchunk, static_cast<S*>(parts));
+  BCMG_CHECK_LAUNCH();
+}
+
+template <class S, class TL, bool CP>
+static int splitk_t(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, void* parts, int max_parts,
+                    cudaStream_t st) {
+  const int64_t ctas = ((M + TL::BM - 1) / TL::BM) * ((N + TL::BN - 1) / TL::BN);
+  int64_t np = (2 * num_sms() + ctas - 1) / ctas;
+  np = std::max<int64_t>(1, std::min<int64_t>({np, (int64_t)max_parts, (K + 255) / 256}));
+  int64_t kchunk = ((K + np - 1) / np + TL::BK - 1) / TL::BK * TL::BK;
+  np = (K + kchunk - 1) / kchunk;
+  if (A.trans) {
+    if (B.trans) launch_splitk_t<S, TL, CP, true, true>(M, N, K, kchunk, (int)np, A, B, parts, st);
+    else launch_splitk_t<S, TL, CP, true, false>(M, N, K, kchunk, (int)np, A, B, parts, st);
+  } else {
+    if (B.trans) launch_splitk_t<S, TL, CP, false, true>(M, N, K, kchunk, (int)np, A, B, parts, st);
+    else launch_splitk_t<S, TL, CP, false, false>(M, N, K, kchunk, (int)np, A, B, parts, st);
+  }
+  return (int)np;
+}
+
+int gemm_splitk(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, void* parts,
+                int max_parts, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  int np = 0;
+  dispatch_dtype(dt, [&](auto s) {
+    using S = decltype(s);
+    if constexpr (std::is_same_v<S, double>) {
+      if (cp_ok(A) && cp_ok(B)) {
+        np = N <= 16 ? splitk_t<S, TileNarrow, true>(M, N, K, A, B, parts, max_parts, st)
+                     : splitk_t<S, TileMed, true>(M, N, K, A, B, parts, max_parts, st);
+        return;
+      }
+    }
+    np = N <= 16 ? splitk_t<S, TileNarrow, false>(M, N, K, A, B, parts, max_parts, st)
+                 : splitk_t<S, TileMed, false>(M, N, K, A, B, parts, max_parts, st);
+  });
+  return np;
+}
+
 void gemm(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
           const int* info, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;

@@ -17,6 +17,11 @@ double measure_dmma_peak(cudaStream_t st);  // TFLOP/s
 void gemm(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
           const int* info, cudaStream_t st);
 
+// Split-K GEMM into `parts` (np slabs of M x N, ld M; np <= max_parts chosen
+// for >= 2 waves); returns np.  Sum the slabs with reduce_parts.
+int gemm_splitk(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, void* parts,
+                int max_parts, cudaStream_t st);
+
 // Trailing update for potrf step (see trail_kernel).
 void trailing_update(int dt, const TrailParams& p, const int* info, cudaStream_t st);
 

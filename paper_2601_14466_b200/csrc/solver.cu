@@ -313,7 +313,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
   // crit stream, the bulk update is a persistent grid capped at (SMs - reserve)
   // CTAs: its CTAs fill an SM's shared memory, so the cap is what leaves SMs
   // on which the latency-bound critical path can overlap the bulk GEMM.
-  int reserve = 8;
+  int reserve = 2;  // measured at N=32768, T=1024: 2 -> 28.9, 4 -> 27.7, 8 -> 28.2 TFLOP/s
   if (const char* e = getenv("BCMG_RESERVE_SMS")) reserve = std::max(0, atoi(e));
   int nsm = 148;
   BCMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
@@ -409,8 +409,7 @@ void Session::potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* 
   if (ldx < n) throw Error(CONFIG, "ldx < n");
   if (last_dinv_T != T || dinv.bytes < (size_t)g.nt * T * T * g.esz)
     throw Error(CONFIG, "potrs needs a potrf of the same tiling in this session");
-  constexpr int64_t KSPLIT = 8192;  // split-K chunk of the backward update
-  const int64_t max_parts = (n + KSPLIT - 1) / KSPLIT;
+  const int64_t max_parts = 64;  // split-K slabs of the backward update
   const size_t y_bytes = (size_t)T * nrhs * g.esz;
   const size_t parts_bytes = (size_t)max_parts * T * nrhs * g.esz;
   const size_t pack_bytes = world > 1 ? (size_t)n * nrhs * g.esz : 0;
@@ -446,13 +445,11 @@ void Session::potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* 
     if (g.owns(k)) {
       void* sh = shards[(k % g.D) - g.dev0];
       if (s1 < n) {
-        const int64_t K = n - s1, np = (K + KSPLIT - 1) / KSPLIT;
-        for (int64_t p = 0; p < np; ++p) {
-          const int64_t k0 = p * KSPLIT, kc = std::min(KSPLIT, K - k0);
-          gemm(dt, tc, nrhs, kc, opA(colp(sh, g, s1 + k0, g.loc(k)), n, OP_C), opB(xrow(s1 + k0), ldx, OP_N),
-               Epilogue{parts + (size_t)p * tc * nrhs * g.esz, tc, 1.0, 0.0, 0, 0}, nullptr, st);
-        }
-        reduce_parts(dt, parts, tc * nrhs, (int)np, xrow(s0), ldx, tc, nrhs, -1.0, st);
+        // split-K over the rows below the tile (fixed slabs, fixed-order sum:
+        // the bits depend on n and T only, not on the device count)
+        const int np = gemm_splitk(dt, tc, nrhs, n - s1, opA(colp(sh, g, s1, g.loc(k)), n, OP_C),
+                                   opB(xrow(s1), ldx, OP_N), parts, (int)max_parts, st);
+        reduce_parts(dt, parts, tc * nrhs, np, xrow(s0), ldx, tc, nrhs, -1.0, st);
       }
       gemm(dt, tc, nrhs, tc, opA(dinv_k(k), T, OP_C), opB(xrow(s0), ldx, OP_N), Epilogue{y, tc, 1.0, 0.0, 0, 0},
            nullptr, st);
