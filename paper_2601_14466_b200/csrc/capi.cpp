@@ -130,6 +130,25 @@ int bcmg_segment_plan_info(int64_t n_cols, int64_t tile, int ndev, int64_t* seg_
   });
 }
 
+int bcmg_schedule(int routine, int64_t n, int64_t tile, int ndev, int world, int rank, int64_t nrhs, int64_t* ops,
+                  int64_t cap, int64_t* count) {
+  return guarded([&] {
+    std::vector<bcmg::SchedOp> v;
+    if (routine == 0) v = bcmg::potrf_schedule(n, tile, ndev, world, rank);
+    else if (routine == 1) v = bcmg::potrs_schedule(n, tile, ndev, world, rank, nrhs);
+    else throw bcmg::Error(BCMG_ERR_CONFIG, "unknown routine");
+    *count = (int64_t)v.size();
+    if (ops) {
+      if ((int64_t)v.size() > cap) throw bcmg::Error(BCMG_ERR_CONFIG, "schedule buffer too small");
+      for (size_t i = 0; i < v.size(); ++i) {
+        const auto& o = v[i];
+        const int64_t row[7] = {o.kind, o.stream, o.k, o.a, o.b, o.root, o.elems};
+        std::memcpy(ops + 7 * i, row, sizeof(row));
+      }
+    }
+  });
+}
+
 int bcmg_nccl_unique_id(unsigned char* id) {
   return guarded([&] {
     ncclUniqueId u;

@@ -272,6 +272,65 @@ void Session::redistribute(int dt, int64_t n_rows, int64_t n_cols, int64_t T, in
   sync_streams(user, crit);
 }
 
+// ------------------------------------------------------------------ schedules
+// The per-process operation sequence of potrf / potrs.  The drivers below
+// execute it on CUDA streams; bcmg_schedule() exposes it so the multi-process
+// logic (ownership, broadcast roots / sizes / order, update ranges) is tested
+// on CPU ranks without GPUs (tests/test_multirank_schedule.py).
+static Geo geo_only(int64_t n, int64_t T, int ndev, int world, int rank) {
+  if (n < 1 || T < 1 || T > n) throw Error(CONFIG, "bad matrix order / tile width");
+  if (ndev < 1 || world < 1 || ndev % world || rank < 0 || rank >= world) throw Error(CONFIG, "bad device grid");
+  Geo g;
+  g.n = n;
+  g.T = T;
+  g.nt = (n + T - 1) / T;
+  g.D = ndev;
+  g.nloc = ndev / world;
+  g.dev0 = rank * g.nloc;
+  g.esz = 1;
+  return g;
+}
+
+std::vector<SchedOp> potrf_schedule(int64_t n, int64_t T, int ndev, int world, int rank) {
+  const Geo g = geo_only(n, T, ndev, world, rank);
+  std::vector<SchedOp> ops;
+  auto push = [&](int kind, int stream, int64_t k, int64_t a, int64_t b, int64_t root, int64_t elems) {
+    ops.push_back(SchedOp{kind, stream, k, a, b, root, elems});
+  };
+  if (g.owns(0)) push(S_FACTOR, STREAM_CRIT, 0, 0, 0, 0, 0);
+  for (int64_t k = 0; k < g.nt; ++k) {
+    const int64_t s0 = g.start(k), s1 = g.stop(k);
+    if (s1 >= n) break;  // last tile: nothing below it
+    // panel rows [stop_k, n) x tile width, from the owner of tile k
+    if (world > 1) push(S_BCAST, STREAM_COMM, k, 0, 0, g.owner_rank(k), (n - s1) * (s1 - s0));
+    const bool look = g.owns(k + 1);
+    if (look) push(S_UPDATE, STREAM_CRIT, k, k + 1, k + 2, 0, 0);
+    // bulk: root field = 1 when the grid is capped to leave SMs to the lookahead path
+    push(S_UPDATE, STREAM_BULK, k, look ? k + 2 : k + 1, g.nt, look ? 1 : 0, 0);
+    if (g.owns(k)) push(S_COPYBACK, STREAM_BULK, k, 0, 0, 0, 0);
+    push(S_STEP_END, STREAM_BULK, k, look ? 1 : 0, 0, 0, 0);
+    if (look) push(S_FACTOR, STREAM_CRIT, k + 1, 0, 0, 0, 0);
+  }
+  return ops;
+}
+
+std::vector<SchedOp> potrs_schedule(int64_t n, int64_t T, int ndev, int world, int rank, int64_t nrhs) {
+  const Geo g = geo_only(n, T, ndev, world, rank);
+  std::vector<SchedOp> ops;
+  for (int64_t k = 0; k < g.nt; ++k) {
+    if (g.owns(k)) ops.push_back(SchedOp{S_FWD, STREAM_CRIT, k, 0, 0, 0, 0});
+    if (world > 1)  // updated x[start_k:] from the owner
+      ops.push_back(SchedOp{S_SHARE, STREAM_CRIT, k, g.start(k), n, g.owner_rank(k), (n - g.start(k)) * nrhs});
+  }
+  for (int64_t k = g.nt - 1; k >= 0; --k) {
+    if (g.owns(k)) ops.push_back(SchedOp{S_BWD, STREAM_CRIT, k, 0, 0, 0, 0});
+    if (world > 1)  // solved x_k from the owner
+      ops.push_back(SchedOp{S_SHARE, STREAM_CRIT, k, g.start(k), g.stop(k), g.owner_rank(k),
+                            (g.stop(k) - g.start(k)) * nrhs});
+  }
+  return ops;
+}
+
 // ------------------------------------------------------------------ potrf
 // Panel k lives in panel[k % 2] with rows [stop_k, n) (ld = n - stop_k): only
 // the rows the trailing update reads (the reference copies the full-height
@@ -342,50 +401,53 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
     if (flops > 0) timed(K_TRAIL, st, flops, [&] { trailing_update(dt, p, info, st); });
   };
 
-  // Event slots: type*8 + k%8 (dependencies reach back at most two steps).
+  // Execute this process's schedule (potrf_schedule).  Event slots:
+  // type*8 + k%8 (dependencies reach back at most two steps).
+  //   R[k]    panel k usable on this process     C[k] broadcast of panel k done
+  //   B[k]    bulk update + copy-back of step k  U[k] lookahead update of step k
+  //   FREE[k] panel buffer k%2 reusable
   enum { R = 0, C = 1, B = 2, U = 3, FREE = 4 };
   auto E = [&](int type, int64_t k) { return ev(type * 8 + (int)(k % 8)); };
-  if (g.owns(0)) {
-    factor(0);
-    BCMG_CUDA(cudaEventRecord(E(R, 0), crit));
-  }
-  for (int64_t k = 0; k < g.nt; ++k) {
-    const int64_t s1 = g.stop(k);
-    if (s1 >= n) break;  // last tile: nothing below it
+  for (const SchedOp& op : potrf_schedule(n, T, ndev, world, rank)) {
+    const int64_t k = op.k, s1 = g.stop(k);
     const bool mine = g.owns(k);
     const int b = (int)(k % 2);
-    // -- panel k reaches every rank (R[k]: usable here; C[k]: broadcast done)
-    if (world > 1) {
-      if (mine) BCMG_CUDA(cudaStreamWaitEvent(comm, E(R, k), 0));
-      else if (k >= 2) BCMG_CUDA(cudaStreamWaitEvent(comm, E(FREE, k - 2), 0));
-      bcast(panel[b].p, (size_t)(n - s1) * (s1 - g.start(k)) * g.esz, g.owner_rank(k), comm);
-      BCMG_CUDA(cudaEventRecord(E(C, k), comm));
-      if (!mine) BCMG_CUDA(cudaEventRecord(E(R, k), comm));
-    }
-    // -- lookahead: the owner of tile k+1 applies update k to it first (crit stream)
-    const bool look = g.owns(k + 1);
-    if (look) {
-      if (!mine) BCMG_CUDA(cudaStreamWaitEvent(crit, E(R, k), 0));
-      if (k >= 1) BCMG_CUDA(cudaStreamWaitEvent(crit, E(B, k - 1), 0));
-      trail(k, k + 1, k + 2, crit);
-      BCMG_CUDA(cudaEventRecord(E(U, k), crit));
-    }
-    // -- bulk update of the other local trailing tiles (bulk stream)
-    BCMG_CUDA(cudaStreamWaitEvent(bulk, E(R, k), 0));
-    trail(k, look ? k + 2 : k + 1, g.nt, bulk, look ? std::max(1, nsm - reserve) : 0);
-    if (mine)  // factor below the diagonal back into A (potrs/potri read it there)
-      copy2d(dt, panel[b].p, n - s1, colp(shard_of(k), g, s1, g.loc(k)), n, n - s1, s1 - g.start(k), false, info,
-             bulk);
-    BCMG_CUDA(cudaEventRecord(E(B, k), bulk));
-    // -- panel buffer b is reusable once bulk(k), U(k) and the broadcast are done
-    if (look) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(U, k), 0));
-    if (world > 1) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(C, k), 0));
-    BCMG_CUDA(cudaEventRecord(E(FREE, k), bulk));
-    // -- F(k+1) overwrites panel buffer 1-b (last used by panel k-1)
-    if (look) {
-      if (k >= 1) BCMG_CUDA(cudaStreamWaitEvent(crit, E(FREE, k - 1), 0));
-      factor(k + 1);
-      BCMG_CUDA(cudaEventRecord(E(R, k + 1), crit));
+    switch (op.kind) {
+      case S_FACTOR:  // F(k) overwrites panel buffer k%2, last used by panel k-2
+        if (k >= 2) BCMG_CUDA(cudaStreamWaitEvent(crit, E(FREE, k - 2), 0));
+        factor(k);
+        BCMG_CUDA(cudaEventRecord(E(R, k), crit));
+        break;
+      case S_BCAST:  // panel k reaches every process
+        if (mine) BCMG_CUDA(cudaStreamWaitEvent(comm, E(R, k), 0));
+        else if (k >= 2) BCMG_CUDA(cudaStreamWaitEvent(comm, E(FREE, k - 2), 0));
+        bcast(panel[b].p, (size_t)op.elems * g.esz, (int)op.root, comm);
+        BCMG_CUDA(cudaEventRecord(E(C, k), comm));
+        if (!mine) BCMG_CUDA(cudaEventRecord(E(R, k), comm));
+        break;
+      case S_UPDATE:
+        if (op.stream == STREAM_CRIT) {  // lookahead: tile k+1 first, full grid
+          if (!mine) BCMG_CUDA(cudaStreamWaitEvent(crit, E(R, k), 0));
+          if (k >= 1) BCMG_CUDA(cudaStreamWaitEvent(crit, E(B, k - 1), 0));
+          trail(k, op.a, op.b, crit);
+          BCMG_CUDA(cudaEventRecord(E(U, k), crit));
+        } else {
+          BCMG_CUDA(cudaStreamWaitEvent(bulk, E(R, k), 0));
+          trail(k, op.a, op.b, bulk, op.root ? std::max(1, nsm - reserve) : 0);
+        }
+        break;
+      case S_COPYBACK:  // factor below the diagonal back into A (potrs/potri read it there)
+        copy2d(dt, panel[b].p, n - s1, colp(shard_of(k), g, s1, g.loc(k)), n, n - s1, s1 - g.start(k), false, info,
+               bulk);
+        break;
+      case S_STEP_END:  // panel buffer k%2 reusable once bulk(k), U(k) and the broadcast are done
+        BCMG_CUDA(cudaEventRecord(E(B, k), bulk));
+        if (op.a) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(U, k), 0));
+        if (world > 1) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(C, k), 0));
+        BCMG_CUDA(cudaEventRecord(E(FREE, k), bulk));
+        break;
+      default:
+        throw Error(CONFIG, "bad potrf schedule op");
     }
   }
   join();
@@ -427,23 +489,23 @@ void Session::potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* 
     bcast(pack, (size_t)rows * nrhs * g.esz, root, st);
     if (rank != root) copy2d(dt, pack, rows, xrow(r0), ldx, rows, nrhs, false, nullptr, st);
   };
-  for (int64_t k = 0; k < g.nt; ++k) {
-    const int64_t s0 = g.start(k), s1 = g.stop(k), tc = s1 - s0;
-    if (g.owns(k)) {
-      void* sh = shards[(k % g.D) - g.dev0];
+  for (const SchedOp& op : potrs_schedule(n, T, ndev, world, rank, nrhs)) {
+    const int64_t k = op.k, s0 = g.start(k), s1 = g.stop(k), tc = s1 - s0;
+    if (op.kind == S_SHARE) {
+      share(op.a, op.b - op.a, (int)op.root);
+      continue;
+    }
+    void* sh = shards[(k % g.D) - g.dev0];
+    if (op.kind == S_FWD) {
       gemm(dt, tc, nrhs, tc, opA(dinv_k(k), T, OP_N), opB(xrow(s0), ldx, OP_N), Epilogue{y, tc, 1.0, 0.0, 0, 0},
            nullptr, st);
       copy2d(dt, y, tc, xrow(s0), ldx, tc, nrhs, false, nullptr, st);
       if (s1 < n)
         gemm(dt, n - s1, nrhs, tc, opA(colp(sh, g, s1, g.loc(k)), n, OP_N), opB(xrow(s0), ldx, OP_N),
              Epilogue{xrow(s1), ldx, -1.0, 1.0, 0, 0}, nullptr, st);
+      continue;
     }
-    share(s0, n - s0, g.owner_rank(k));
-  }
-  for (int64_t k = g.nt - 1; k >= 0; --k) {
-    const int64_t s0 = g.start(k), s1 = g.stop(k), tc = s1 - s0;
-    if (g.owns(k)) {
-      void* sh = shards[(k % g.D) - g.dev0];
+    {
       if (s1 < n) {
         // split-K over the rows below the tile (fixed slabs, fixed-order sum:
         // the bits depend on n and T only, not on the device count)
@@ -455,7 +517,6 @@ void Session::potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* 
            nullptr, st);
       copy2d(dt, y, tc, xrow(s0), ldx, tc, nrhs, false, nullptr, st);
     }
-    share(s0, tc, g.owner_rank(k));
   }
   sync_streams(user, crit);
 }

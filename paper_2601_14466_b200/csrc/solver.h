@@ -18,6 +18,19 @@ struct DevBuf {
   void release();
 };
 
+// One operation of a process's potrf / potrs schedule (solver.cu).
+enum SchedKind : int { S_FACTOR = 1, S_BCAST = 2, S_UPDATE = 3, S_COPYBACK = 4, S_STEP_END = 5, S_FWD = 6,
+                       S_BWD = 7, S_SHARE = 8 };
+enum SchedStream : int { STREAM_CRIT = 0, STREAM_BULK = 1, STREAM_COMM = 2 };
+struct SchedOp {
+  int64_t kind, stream, k;
+  int64_t a, b;      // S_UPDATE: tile range [a, b); S_SHARE: row range [a, b); S_STEP_END: a = lookahead flag
+  int64_t root;      // S_BCAST / S_SHARE: source process; S_UPDATE (bulk): 1 = grid capped
+  int64_t elems;     // S_BCAST / S_SHARE: elements moved
+};
+std::vector<SchedOp> potrf_schedule(int64_t n, int64_t T, int ndev, int world, int rank);
+std::vector<SchedOp> potrs_schedule(int64_t n, int64_t T, int ndev, int world, int rank, int64_t nrhs);
+
 // Phase timing slots (CUDA events on the critical stream).
 enum Phase : int { T_BEGIN = 0, T_REDIST = 1, T_POTRF = 2, T_SOLVE = 3, T_END = 4 };
 
