@@ -107,6 +107,12 @@ int bcmg_segment_plan_info(int64_t n_cols, int64_t tile, int ndev, int64_t* seg_
 int bcmg_schedule(int routine, int64_t n, int64_t tile, int ndev, int world, int rank, int64_t nrhs, int64_t* ops,
                   int64_t cap, int64_t* count);
 
+/* Cross-process redistribution plan: every segment move {src_pos, dst_pos,
+   src_rank, dst_rank} (4 int64 each, segment = *seg_width columns) in the
+   global order both sides of a send/recv pair use.  Host only. */
+int bcmg_redistribute_plan(int64_t n_cols, int64_t tile, int ndev, int world, int direction, int64_t* seg_width,
+                           int64_t* moves, int64_t cap, int64_t* count);
+
 /* ---- sessions ---- */
 int bcmg_nccl_unique_id(unsigned char* id /* [128] */);
 int bcmg_open(int cuda_device, int rank, int world, const unsigned char* nccl_id /* NULL if world==1 */,

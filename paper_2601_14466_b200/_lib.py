@@ -45,6 +45,7 @@ SIGNATURES = {
     "bcmg_invert_cycles": (C.c_int, [_i64, _i64p, _i64p]),
     "bcmg_segment_plan_info": (C.c_int, [_i64, _i64, C.c_int, _i64p, _i64p, _i64p]),
     "bcmg_schedule": (C.c_int, [C.c_int, _i64, _i64, C.c_int, C.c_int, C.c_int, _i64, _i64p, _i64, _i64p]),
+    "bcmg_redistribute_plan": (C.c_int, [_i64, _i64, C.c_int, C.c_int, C.c_int, _i64p, _i64p, _i64, _i64p]),
     "bcmg_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "bcmg_open": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]),
     "bcmg_close": (C.c_int, [_vp]),

@@ -149,6 +149,26 @@ int bcmg_schedule(int routine, int64_t n, int64_t tile, int ndev, int world, int
   });
 }
 
+int bcmg_redistribute_plan(int64_t n_cols, int64_t tile, int ndev, int world, int direction, int64_t* seg_width,
+                           int64_t* moves, int64_t cap, int64_t* count) {
+  return guarded([&] {
+    if (direction != BCMG_TO_CYCLIC && direction != BCMG_TO_CONTIG)
+      throw bcmg::Error(BCMG_ERR_CONFIG, "unknown redistribution direction");
+    const auto rp = bcmg::redist_plan(n_cols, tile, ndev, world, direction == BCMG_TO_CONTIG);
+    *seg_width = rp.seg;
+    *count = (int64_t)rp.moves.size();
+    if (moves) {
+      if (*count > cap) throw bcmg::Error(BCMG_ERR_CONFIG, "move buffer too small");
+      for (size_t i = 0; i < rp.moves.size(); ++i) {
+        moves[4 * i + 0] = rp.moves[i].src_pos;
+        moves[4 * i + 1] = rp.moves[i].dst_pos;
+        moves[4 * i + 2] = rp.moves[i].src_rank;
+        moves[4 * i + 3] = rp.moves[i].dst_rank;
+      }
+    }
+  });
+}
+
 int bcmg_nccl_unique_id(unsigned char* id) {
   return guarded([&] {
     ncclUniqueId u;

@@ -667,6 +667,33 @@ void mirror_diag(int dt, void* a, int64_t lda, int64_t n, cudaStream_t st) {
   BCMG_CHECK_LAUNCH();
 }
 
+// ============================================================== chunk copies
+template <class W>
+__global__ void __launch_bounds__(256) chunk_copy_kernel(const uint64_t* __restrict__ src,
+                                                         const uint64_t* __restrict__ dst, int n, int64_t soff,
+                                                         int64_t doff, int64_t lanes) {
+  for (int i = blockIdx.y; i < n; i += gridDim.y) {
+    const W* s = reinterpret_cast<const W*>(__ldg(src + i) + soff);
+    W* d = reinterpret_cast<W*>(__ldg(dst + i) + doff);
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < lanes; l += (int64_t)gridDim.x * blockDim.x)
+      d[l] = s[l];
+  }
+}
+
+void chunk_copy(const uint64_t* src, const uint64_t* dst, int n, int64_t soff, int64_t doff, int64_t len, int vec,
+                cudaStream_t st) {
+  if (n <= 0 || len <= 0) return;
+  const int64_t lanes = len / vec;
+  const unsigned gy = (unsigned)std::min(n, 1024);
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((lanes + 255) / 256,
+                                                                       (int64_t)num_sms() * 8 / gy + 1));
+  dim3 grid(gx, gy);
+  if (vec == 16) chunk_copy_kernel<uint4><<<grid, 256, 0, st>>>(src, dst, n, soff, doff, lanes);
+  else if (vec == 8) chunk_copy_kernel<uint2><<<grid, 256, 0, st>>>(src, dst, n, soff, doff, lanes);
+  else chunk_copy_kernel<unsigned><<<grid, 256, 0, st>>>(src, dst, n, soff, doff, lanes);
+  BCMG_CHECK_LAUNCH();
+}
+
 // ============================================================== FP64 peak probe
 // Register-resident DMMA loop (8 independent accumulators per warp, 16 warps
 // per SM): the FP64 tensor roofline denominator, measured live by bench.py.

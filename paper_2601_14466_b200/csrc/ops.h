@@ -79,4 +79,9 @@ struct RotateJob {
 };
 void rotate_cycles(const RotateJob& j, cudaStream_t st);
 
+// n independent copies of len bytes: dst[i] + doff <- src[i] + soff (device
+// address tables), vec-byte lanes.
+void chunk_copy(const uint64_t* src, const uint64_t* dst, int n, int64_t soff, int64_t doff, int64_t len, int vec,
+                cudaStream_t st);
+
 }  // namespace bcmg

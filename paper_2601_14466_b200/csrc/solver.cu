@@ -223,7 +223,10 @@ void Session::redistribute(int dt, int64_t n_rows, int64_t n_cols, int64_t T, in
   if (ndev < 1) throw Error(CONFIG, "need at least one device");
   const int esz = dtype_size(dt);
   if (!esz) throw Error(CONFIG, "unknown element-type code");
-  if (world > 1) throw Error(CONFIG, "multi-process redistribution is not implemented in this build");
+  // BCMG_STAGED_REDIST=1 routes a single process through the staged
+  // (cross-process) algorithm too, so one GPU exercises its pack/unpack path.
+  const char* staged = getenv("BCMG_STAGED_REDIST");
+  if (world > 1 || (staged && atoi(staged))) return redistribute_multi(dt, n_rows, n_cols, T, ndev, shards, inverse);
   last_moved_bytes = 0;
   SegPlan plan = segment_plan(n_cols, T, ndev, inverse);
   const int64_t nc = (int64_t)plan.offsets.size() - 1;
@@ -269,6 +272,121 @@ void Session::redistribute(int dt, int64_t n_rows, int64_t n_cols, int64_t T, in
   timed(K_ROTATE, crit, 2.0 * (double)nm * plan.seg * col_bytes, [&] { rotate_cycles(j, crit); });
   // (cudaMemcpyAsync from pageable memory returns once the source is consumed)
   last_moved_bytes = 2 * (int64_t)nm * plan.seg * col_bytes;
+  sync_streams(user, crit);
+}
+
+// ------------------------------------------------------------------ cross-process redistribution
+// Same segment-level cycle plan on every process.  A move c_i -> c_{i+1}
+// between processes becomes an NCCL send/recv pair; a move inside a process a
+// device copy.  In place with bounded staging: the segments are processed in
+// byte chunks of CH; per chunk every process first PACKS (reads) the chunk of
+// each segment it owns that moves -- so every slot that is about to be
+// overwritten has already been read -- then exchanges (one ncclGroup of
+// sends/recvs, paired in the global move order on both sides), then UNPACKS
+// into the destination slots.  Algorithmic traffic is the reference's
+// (each moved segment read once and written once, layout.py:234-250).
+RedistPlan redist_plan(int64_t n_cols, int64_t T, int ndev, int world, bool inverse) {
+  if (world < 1 || ndev % world) throw Error(CONFIG, "logical devices must be a multiple of the processes");
+  const SegPlan sp = segment_plan(n_cols, T, ndev, inverse);
+  const auto counts = column_counts(n_cols, T, ndev);
+  std::vector<int64_t> off(ndev, 0);
+  for (int d = 1; d < ndev; ++d) off[d] = off[d - 1] + counts[d - 1];
+  const int nloc = ndev / world;
+  auto rank_of = [&](int64_t seg_pos) {
+    const int64_t col = seg_pos * sp.seg;
+    const int d = (int)(std::upper_bound(off.begin(), off.end(), col) - off.begin()) - 1;
+    return d / nloc;
+  };
+  RedistPlan rp;
+  rp.seg = sp.seg;
+  for (size_t c = 0; c + 1 < sp.offsets.size(); ++c) {
+    const int64_t b = sp.offsets[c], e = sp.offsets[c + 1], m = e - b;
+    for (int64_t i = 0; i < m; ++i) {
+      const int64_t src = sp.members[b + i], dst = sp.members[b + (i + 1) % m];
+      rp.moves.push_back(RedistMove{src, dst, rank_of(src), rank_of(dst)});
+    }
+  }
+  return rp;
+}
+
+void Session::redistribute_multi(int dt, int64_t n_rows, int64_t n_cols, int64_t T, int ndev, void* const* shards,
+                                 bool inverse) {
+  const int esz = dtype_size(dt);
+  const RedistPlan rp = redist_plan(n_cols, T, ndev, world, inverse);
+  const auto counts = column_counts(n_cols, T, ndev);
+  std::vector<int64_t> off(ndev, 0);
+  for (int d = 1; d < ndev; ++d) off[d] = off[d - 1] + counts[d - 1];
+  const int nloc = ndev / world, dev0 = rank * nloc;
+  const int64_t col_bytes = n_rows * esz, seg_bytes = rp.seg * col_bytes;
+  auto addr = [&](int64_t seg_pos) {
+    const int64_t col = seg_pos * rp.seg;
+    const int d = (int)(std::upper_bound(off.begin(), off.end(), col) - off.begin()) - 1;
+    return reinterpret_cast<uint64_t>(shards[d - dev0]) + (uint64_t)((col - off[d]) * col_bytes);
+  };
+  std::vector<const RedistMove*> sends, recvs, locals;
+  for (const auto& mv : rp.moves) {
+    if (mv.src_rank == rank && mv.dst_rank == rank) locals.push_back(&mv);
+    else if (mv.src_rank == rank) sends.push_back(&mv);
+    else if (mv.dst_rank == rank) recvs.push_back(&mv);
+  }
+  last_moved_bytes = 2 * (int64_t)rp.moves.size() * seg_bytes;  // whole-job algorithmic bytes
+  const int64_t slots = (int64_t)(sends.size() + locals.size() + recvs.size());
+  // every process takes part in the exchange rounds even with nothing to move,
+  // so all processes agree on the chunk size (it depends on global counts only)
+  int64_t max_slots = 0;
+  for (int r = 0; r < world; ++r) {
+    int64_t s = 0;
+    for (const auto& mv : rp.moves) s += (mv.src_rank == r) + (mv.dst_rank == r && mv.src_rank != r);
+    max_slots = std::max(max_slots, s);
+  }
+  if (max_slots == 0) return;
+  int64_t budget = (int64_t)1 << 30;
+  if (const char* e = getenv("BCMG_REDIST_STAGING")) budget = std::max<int64_t>(1 << 20, atoll(e));
+  int64_t CH = std::min<int64_t>(seg_bytes, std::max<int64_t>(1 << 20, budget / max_slots));
+  if (CH < seg_bytes) CH = std::max<int64_t>(256, CH / 256 * 256);
+  const int vec = (col_bytes % 16 == 0) ? 16 : (col_bytes % 8 == 0 ? 8 : 4);
+  // staging: [sends | locals] pack slots, then recv slots
+  stage_buf.ensure((size_t)std::max<int64_t>(slots, 1) * CH);
+  char* pack = static_cast<char*>(stage_buf.p);
+  char* recv = pack + (sends.size() + locals.size()) * CH;
+  // descriptor tables: pack (src = segment, dst = slot), unpack (src = slot, dst = segment)
+  const size_t npk = sends.size() + locals.size(), nup = locals.size() + recvs.size();
+  std::vector<uint64_t> h(2 * npk + 2 * nup);
+  for (size_t j = 0; j < sends.size(); ++j) {
+    h[j] = addr(sends[j]->src_pos);
+    h[npk + j] = reinterpret_cast<uint64_t>(pack + j * CH);
+  }
+  for (size_t j = 0; j < locals.size(); ++j) {
+    const size_t s = sends.size() + j;
+    h[s] = addr(locals[j]->src_pos);
+    h[npk + s] = reinterpret_cast<uint64_t>(pack + s * CH);
+    h[2 * npk + j] = reinterpret_cast<uint64_t>(pack + s * CH);
+    h[2 * npk + nup + j] = addr(locals[j]->dst_pos);
+  }
+  for (size_t j = 0; j < recvs.size(); ++j) {
+    const size_t u = locals.size() + j;
+    h[2 * npk + u] = reinterpret_cast<uint64_t>(recv + j * CH);
+    h[2 * npk + nup + u] = addr(recvs[j]->dst_pos);
+  }
+  desc_buf.ensure(std::max<size_t>(8, h.size() * 8));
+  const uint64_t* d = static_cast<const uint64_t*>(desc_buf.p);
+  if (!h.empty()) BCMG_CUDA(cudaMemcpyAsync(desc_buf.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, crit));
+  auto comm_ = static_cast<ncclComm_t>(nccl);
+  for (int64_t o = 0; o < seg_bytes; o += CH) {
+    const int64_t len = std::min(CH, seg_bytes - o);
+    timed(K_ROTATE, crit, 2.0 * (double)len * (npk), [&] {
+      chunk_copy(d, d + npk, (int)npk, o, 0, len, vec, crit);
+    });
+    if (world > 1) {
+      BCMG_NCCL(ncclGroupStart());
+      for (size_t j = 0; j < sends.size(); ++j)
+        BCMG_NCCL(ncclSend(pack + j * CH, (size_t)len, ncclUint8, sends[j]->dst_rank, comm_, crit));
+      for (size_t j = 0; j < recvs.size(); ++j)
+        BCMG_NCCL(ncclRecv(recv + j * CH, (size_t)len, ncclUint8, recvs[j]->src_rank, comm_, crit));
+      BCMG_NCCL(ncclGroupEnd());
+    }
+    chunk_copy(d + 2 * npk, d + 2 * npk + nup, (int)nup, 0, o, len, vec, crit);
+  }
   sync_streams(user, crit);
 }
 

@@ -31,6 +31,19 @@ struct SchedOp {
 std::vector<SchedOp> potrf_schedule(int64_t n, int64_t T, int ndev, int world, int rank);
 std::vector<SchedOp> potrs_schedule(int64_t n, int64_t T, int ndev, int world, int rank, int64_t nrhs);
 
+// Cross-process redistribution: every segment move of the cycle plan
+// (cycles in order, c_i -> c_{i+1} within a cycle) with the processes that
+// own its source and destination segments.
+struct RedistMove {
+  int64_t src_pos, dst_pos;  // segment indices (column = index * seg)
+  int src_rank, dst_rank;
+};
+struct RedistPlan {
+  int64_t seg = 1;
+  std::vector<RedistMove> moves;
+};
+RedistPlan redist_plan(int64_t n_cols, int64_t T, int ndev, int world, bool inverse);
+
 // Phase timing slots (CUDA events on the critical stream).
 enum Phase : int { T_BEGIN = 0, T_REDIST = 1, T_POTRF = 2, T_SOLVE = 3, T_END = 4 };
 
@@ -88,6 +101,9 @@ struct Session {
 
   // drivers (see solver.cu); shards are this process's logical-device shards
   void redistribute(int dt, int64_t n_rows, int64_t n_cols, int64_t T, int ndev, void* const* shards, bool inverse);
+  void redistribute_multi(int dt, int64_t n_rows, int64_t n_cols, int64_t T, int ndev, void* const* shards,
+                          bool inverse);
+  DevBuf stage_buf, desc_buf;
   int potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards);
   void potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* const* shards, void* x, int64_t ldx);
   void potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards);

@@ -180,3 +180,98 @@ def test_two_rank_gloo_execution_matches_oracle(n, t, ndev, nrhs, dtype):
         assert p.exitcode == 0, "rank failed or deadlocked"
     for r in range(2):
         assert out[r] <= 1e3 * n * O.eps_of(dtype), out[r]
+
+
+# ----------------------------------------------------------------- cross-process redistribution
+
+
+def redist_plan(n, t, ndev, world, direction):
+    lib = _lib.load()
+    seg, cnt = C.c_int64(), C.c_int64()
+    _lib.check(lib.bcmg_redistribute_plan(n, t, ndev, world, direction, C.byref(seg), None, 0, C.byref(cnt)))
+    buf = np.zeros((max(cnt.value, 1), 4), dtype=np.int64)
+    _lib.check(lib.bcmg_redistribute_plan(n, t, ndev, world, direction, C.byref(seg),
+                                          buf.ctypes.data_as(_lib._i64p), cnt.value, C.byref(cnt)))
+    return seg.value, [tuple(int(v) for v in r) for r in buf[: cnt.value]]
+
+
+def _redist_rank(rank, world, port, n_rows, n, t, ndev, chunk, out):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a = np.asfortranarray(np.arange(n_rows * n, dtype=np.float64).reshape(n_rows, n, order="F"))
+        counts = O.column_counts(n, t, ndev)
+        offs = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(int)
+        nloc = ndev // world
+        mine = range(rank * nloc, (rank + 1) * nloc)
+        shards = {d: a[:, offs[d]:offs[d] + counts[d]].copy(order="F") for d in mine}
+        colb = n_rows * 8
+
+        def run(direction):
+            seg, moves = redist_plan(n, t, ndev, world, direction)
+            segb = seg * colb
+
+            def view(pos):  # byte view of segment `pos` in its (local) shard
+                col = pos * seg
+                d = int(np.searchsorted(offs, col, side="right") - 1)
+                flat = shards[d].reshape(-1, order="F").view(np.uint8)
+                return flat[(col - offs[d]) * colb:(col - offs[d]) * colb + segb]
+
+            sends = [m for m in moves if m[2] == rank and m[3] != rank]
+            locs = [m for m in moves if m[2] == rank and m[3] == rank]
+            recvs = [m for m in moves if m[3] == rank and m[2] != rank]
+            for o in range(0, segb, chunk):
+                ln = min(chunk, segb - o)
+                pack = [view(m[0])[o:o + ln].copy() for m in sends + locs]  # all reads first
+                reqs = [dist.isend(torch.from_numpy(pack[j]), dst=m[3]) for j, m in enumerate(sends)]
+                rbuf = [torch.empty(ln, dtype=torch.uint8) for _ in recvs]
+                reqs += [dist.irecv(rbuf[j], src=m[2]) for j, m in enumerate(recvs)]
+                for r in reqs:
+                    r.wait()
+                for j, m in enumerate(locs):
+                    view(m[1])[o:o + ln] = pack[len(sends) + j]
+                for j, m in enumerate(recvs):
+                    view(m[1])[o:o + ln] = rbuf[j].numpy()
+
+        def gathered():
+            parts = [None] * world
+            dist.all_gather_object(parts, [shards[d] for d in mine])
+            return np.hstack([s for p in parts for s in p])
+
+        run(0)
+        fwd = gathered()
+        run(1)
+        back = gathered()
+        out[rank] = (fwd.tobytes(order="F") == O.deal_columns(a, t, ndev).tobytes(order="F"),
+                     back.tobytes(order="F") == a.tobytes(order="F"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_rows,n,t,ndev,chunk", [(3, 32, 4, 2, 8), (5, 40, 3, 4, 16), (2, 24, 5, 2, 1000),
+                                                    (4, 64, 8, 4, 24)])
+def test_two_rank_gloo_redistribution_bit_exact(n_rows, n, t, ndev, chunk):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_redist_rank, args=(r, 2, port, n_rows, n, t, ndev, chunk, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0, "rank failed or deadlocked"
+    assert out[0] == (True, True) and out[1] == (True, True)
+
+
+def test_redistribution_plan_covers_every_moved_segment():
+    for n, t, ndev, world in [(2048, 256, 2, 2), (131072, 1024, 8, 8), (100, 7, 4, 2), (10, 3, 3, 1)]:
+        seg, moves = redist_plan(n, t, ndev, world, 0)
+        moved = sum(len(c) for c in O.cycles_of(O.dest_positions(n, t, ndev)))
+        assert len(moves) * seg == moved
+        dests = [m[1] for m in moves]
+        assert len(set(dests)) == len(dests) and sorted(dests) == sorted(m[0] for m in moves)
