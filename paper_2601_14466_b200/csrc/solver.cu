@@ -117,10 +117,14 @@ void Session::kernel_stats(int kind, double* out) {
   if (kind < 0 || kind >= K_KINDS) throw Error(CONFIG, "unknown kernel kind");
   KStat& k = kstat[kind];
   double tot = 0, mx = 0;
-  for (auto& pr : k.ev) {
+  FILE* dump = nullptr;
+  if (const char* path = getenv("BCMG_PROFILE_DUMP")) dump = fopen(path, "a");
+  for (size_t i = 0; i < k.ev.size(); ++i) {
+    auto& pr = k.ev[i];
     BCMG_CUDA(cudaEventSynchronize(pr.second));
     float ms = 0;
     BCMG_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+    if (dump) fprintf(dump, "%d %zu %.6f %.6e\n", kind, i, ms, i < k.works.size() ? k.works[i] : 0.0);
     tot += ms;
     mx = std::max(mx, (double)ms);
     ev_spare.push_back(pr.first);
@@ -130,7 +134,9 @@ void Session::kernel_stats(int kind, double* out) {
   out[1] = tot;
   out[2] = k.work;
   out[3] = mx;
+  if (dump) fclose(dump);
   k.ev.clear();
+  k.works.clear();
   k.work = 0;
 }
 
@@ -341,8 +347,8 @@ void Session::redistribute_multi(int dt, int64_t n_rows, int64_t n_cols, int64_t
   }
   if (max_slots == 0) return;
   int64_t budget = (int64_t)1 << 30;
-  if (const char* e = getenv("BCMG_REDIST_STAGING")) budget = std::max<int64_t>(1 << 20, atoll(e));
-  int64_t CH = std::min<int64_t>(seg_bytes, std::max<int64_t>(1 << 20, budget / max_slots));
+  if (const char* e = getenv("BCMG_REDIST_STAGING")) budget = std::max<int64_t>(4096, atoll(e));
+  int64_t CH = std::min<int64_t>(seg_bytes, std::max<int64_t>(budget < (1 << 20) ? 256 : (1 << 20), budget / max_slots));
   if (CH < seg_bytes) CH = std::max<int64_t>(256, CH / 256 * 256);
   const int vec = (col_bytes % 16 == 0) ? 16 : (col_bytes % 8 == 0 ? 8 : 4);
   // staging: [sends | locals] pack slots, then recv slots

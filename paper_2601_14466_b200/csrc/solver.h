@@ -69,6 +69,7 @@ struct Session {
   struct KStat {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
     double work = 0;
+    std::vector<double> works;  // per launch
   } kstat[K_KINDS];
   std::vector<cudaEvent_t> ev_spare;
   cudaEvent_t take_event();
@@ -84,6 +85,7 @@ struct Session {
     BCMG_CUDA(cudaEventRecord(b, st));
     kstat[kind].ev.emplace_back(a, b);
     kstat[kind].work += work;
+    kstat[kind].works.push_back(work);
   }
   // launches, total ms, work (flops or bytes), max ms; clears the record
   void kernel_stats(int kind, double* out);

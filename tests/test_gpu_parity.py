@@ -289,7 +289,7 @@ def test_dropin_potri_row_sharded(meshes):
     assert O.inverse_residual(a, inv) <= 100 * n * O.eps_of(np.complex128)
 
 
-@pytest.mark.parametrize("n,t,d,rows,chunk", [(2048, 256, 2, 64, 1 << 20), (1000, 37, 3, 33, 1 << 20),
+@pytest.mark.parametrize("n,t,d,rows,chunk", [(2048, 256, 2, 64, 8192), (1000, 37, 3, 33, 1 << 20),
                                               (96, 8, 4, 5, 1 << 20)])
 def test_staged_redistribution_path(meshes, monkeypatch, n, t, d, rows, chunk):
     """The cross-process (pack / exchange / unpack) redistribution algorithm,
