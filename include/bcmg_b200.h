@@ -139,6 +139,12 @@ int bcmg_potrs_factored(bcmg_session* s, void* stream, int dtype, int64_t n, int
 int bcmg_potri_factored(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev,
                         void* const* shards);
 
+/* The DMMA GEMM every contraction of the path runs on:
+   C := alpha * op(A) * op(B) + beta * C, column-major, op 0 = N, 1 = C (conj-
+   transpose); op(A) is m x k, op(B) is k x n.  No session needed. */
+int bcmg_gemm(void* stream, int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void* a, int64_t lda,
+              int op_a, const void* b, int64_t ldb, int op_b, double beta, void* c, int64_t ldc);
+
 /* ---- measurement ---- */
 /* milliseconds of the last pipeline call: [0] redistribute_in, [1] potrf,
    [2] potrs/potri(+redistribute_out), [3] total (CUDA events on `stream`) */

@@ -55,6 +55,8 @@ SIGNATURES = {
     "bcmg_potrf": (C.c_int, [_vp, _vp, C.c_int, _i64, _i64, C.c_int, _vpp, _ip]),
     "bcmg_potrs_factored": (C.c_int, [_vp, _vp, C.c_int, _i64, _i64, _i64, C.c_int, _vpp, _vp, _i64]),
     "bcmg_potri_factored": (C.c_int, [_vp, _vp, C.c_int, _i64, _i64, C.c_int, _vpp]),
+    "bcmg_gemm": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, C.c_double, _vp, _i64, C.c_int, _vp, _i64, C.c_int,
+                            C.c_double, _vp, _i64]),
     "bcmg_last_timings": (C.c_int, [_vp, C.POINTER(C.c_float)]),
     "bcmg_last_moved_bytes": (C.c_int64, [_vp]),
     "bcmg_set_profiling": (C.c_int, [_vp, C.c_int]),

@@ -305,6 +305,17 @@ int bcmg_potri(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile
   });
 }
 
+int bcmg_gemm(void* stream, int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void* a, int64_t lda,
+              int op_a, const void* b, int64_t ldb, int op_b, double beta, void* c, int64_t ldc) {
+  return guarded([&] {
+    if (bcmg::dtype_size(dtype) == 0) throw bcmg::Error(BCMG_ERR_CONFIG, "unknown element-type code");
+    if ((op_a != 0 && op_a != 1) || (op_b != 0 && op_b != 1)) throw bcmg::Error(BCMG_ERR_CONFIG, "op must be 0 or 1");
+    if (m < 0 || n < 0 || k < 0) throw bcmg::Error(BCMG_ERR_CONFIG, "negative dimension");
+    bcmg::gemm(dtype, m, n, k, bcmg::opA(a, lda, op_a), bcmg::opB(b, ldb, op_b),
+               bcmg::Epilogue{c, ldc, alpha, beta, 0, 0}, nullptr, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int bcmg_last_timings(bcmg_session* s, float* ms) {
   return guarded([&] {
     auto* S = live(s);

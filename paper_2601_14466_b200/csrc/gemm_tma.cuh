@@ -119,10 +119,25 @@ __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUt
 
   uint32_t g = 0;
   TmaBlock cb;
+  // C tile prefetch into L2 a few slices before the epilogue: all CTAs reach
+  // their epilogues at nearly the same time (uniform items), and without it
+  // the read-modify-write of 128 KB per CTA would stall every SM on HBM.
+  constexpr int PREFETCH_AHEAD = 6;
+  auto prefetch_c = [&](const TmaBlock& blk) {
+    if (blk.ep.beta == 0.0) return;
+    const double* C = reinterpret_cast<const double*>(blk.ep.C);
+    constexpr int SEGS = TL::BM * 8 / 128;  // 128-byte lines per column of the tile
+    for (int i = tid; i < TL::BN * SEGS; i += TL::THREADS) {
+      const int64_t col = blk.n0 + i / SEGS, row = blk.m0 + (i % SEGS) * 16;
+      if (col < blk.N && row < blk.M)
+        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(C + row + col * blk.ep.ldc));
+    }
+  };
   for (int64_t item = blockIdx.x; next_c(item, cb); item += gridDim.x) {
     Acc<TL, false> acc;
     acc.zero();
     for (int kt = 0; kt < KT; ++kt) {
+      if (kt == (KT > PREFETCH_AHEAD ? KT - PREFETCH_AHEAD : 0)) prefetch_c(cb);
       if (tid == 0) produce_one();
       const int s = g % TL::STAGES;
       mbar_wait(&full[s], (g / TL::STAGES) & 1);
