@@ -266,27 +266,40 @@ template <class S, class TL, bool CPLX>
 __device__ __forceinline__ void store_block(const Acc<TL, CPLX>& acc, const Epilogue& ep, int64_t M, int64_t N,
                                             int64_t m0, int64_t n0, int wm0, int wn0, int lane) {
   const int r = lane >> 2, q = lane & 3;
-  S* C = reinterpret_cast<S*>(ep.C);
+  S* __restrict__ C = reinterpret_cast<S*>(ep.C);
+  // One fragment row at a time: issue all of its C loads before any store, so
+  // the read-modify-write pays one memory latency per row group instead of one
+  // per element (the compiler cannot reorder loads across the stores itself).
 #pragma unroll
-  for (int fm = 0; fm < TL::FM; ++fm)
+  for (int fm = 0; fm < TL::FM; ++fm) {
+    const int64_t row = m0 + wm0 + frag_row<TL>(fm, r);
+    bool ok[TL::FN][2];
+    S old[TL::FN][2];
 #pragma unroll
     for (int fn = 0; fn < TL::FN; ++fn)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const int64_t row = m0 + wm0 + frag_row<TL>(fm, r);
         const int64_t col = n0 + wn0 + (TL::PAIR ? 16 * (fn >> 1) + 2 * (2 * q + j) + (fn & 1) : fn * 8 + 2 * q + j);
-        if (row < M && col < N && (!ep.lower_only || row - col >= ep.lower_off)) {
-          S* c = C + row + col * ep.ldc;
-          double2 v = make_double2(ep.alpha * acc.re[fm][fn][j], 0.0);
-          if constexpr (CPLX) v.y = ep.alpha * acc.im[fm][fn][j];
-          if (ep.beta != 0.0) {
-            double2 o = to_c(*c);
-            v.x += ep.beta * o.x;
-            v.y += ep.beta * o.y;
-          }
-          *c = from_c<S>(v);
-        }
+        ok[fn][j] = row < M && col < N && (!ep.lower_only || row - col >= ep.lower_off);
+        old[fn][j] = from_c<S>(make_double2(0.0, 0.0));
+        if (ok[fn][j] && ep.beta != 0.0) old[fn][j] = C[row + col * ep.ldc];
       }
+#pragma unroll
+    for (int fn = 0; fn < TL::FN; ++fn)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (!ok[fn][j]) continue;
+        const int64_t col = n0 + wn0 + (TL::PAIR ? 16 * (fn >> 1) + 2 * (2 * q + j) + (fn & 1) : fn * 8 + 2 * q + j);
+        double2 v = make_double2(ep.alpha * acc.re[fm][fn][j], 0.0);
+        if constexpr (CPLX) v.y = ep.alpha * acc.im[fm][fn][j];
+        if (ep.beta != 0.0) {
+          const double2 o = to_c(old[fn][j]);
+          v.x += ep.beta * o.x;
+          v.y += ep.beta * o.y;
+        }
+        C[row + col * ep.ldc] = from_c<S>(v);
+      }
+  }
 }
 
 // ----------------------------------------------------------------- block GEMM

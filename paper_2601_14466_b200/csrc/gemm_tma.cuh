@@ -151,12 +151,41 @@ __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUt
   }
 }
 
+// Lower-trapezoid enumeration of one trailing tile (rows x tc, row blocks of
+// BM, column blocks of BN, BM a multiple of BN): row block rb keeps the
+// column blocks that reach the diagonal, min(ncb, (rb+1)*BM/BN) of them.
+template <int BM, int BN>
+struct Trap {
+  static_assert(BM % BN == 0, "BM must be a multiple of BN");
+  static constexpr int64_t R = BM / BN;
+  __host__ __device__ static int64_t count(int64_t rows, int64_t tc) {
+    const int64_t nrb = (rows + BM - 1) / BM, ncb = (tc + BN - 1) / BN;
+    const int64_t r0 = (ncb + R - 1) / R - 1;  // rows [0, r0) have fewer than ncb blocks
+    const int64_t t = nrb < r0 ? nrb : r0;
+    return R * t * (t + 1) / 2 + (nrb > r0 ? (nrb - r0) * ncb : 0);
+  }
+  __host__ __device__ static void decode(int64_t b, int64_t tc, int64_t& rb, int64_t& cb) {
+    const int64_t ncb = (tc + BN - 1) / BN, r0 = (ncb + R - 1) / R - 1, tri = R * r0 * (r0 + 1) / 2;
+    if (b < tri) {
+      rb = 0;
+      while (R * (rb + 1) * (rb + 2) / 2 <= b) ++rb;
+      cb = b - R * rb * (rb + 1) / 2;
+    } else {
+      rb = r0 + (b - tri) / ncb;
+      cb = (b - tri) % ncb;
+    }
+  }
+};
+
+template <class TL>
+constexpr int min_blocks() { return 65536 / (TL::THREADS * 128) > 0 ? 65536 / (TL::THREADS * 128) : 1; }
+
 // Trailing update (see trail_kernel in gemm.cuh) over one panel tensor map.
 template <class TL>
-__global__ void __launch_bounds__(TL::THREADS, 1)
-    trail_tma_kernel(const __grid_constant__ CUtensorMap mapP, TrailParams p, const int* info) {
-  static_assert(TL::BM == TL::BN, "square blocks");
-  constexpr int B = TL::BM;
+__global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
+    trail_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TrailParams p,
+                     const int* info) {
+  using TZ = Trap<TL::BM, TL::BN>;
   if (ld_flag(info)) return;
   // tile cursor: items only grow for a given caller, so the walk over tiles is
   // amortised O(1); producer and consumer each own one
@@ -171,7 +200,7 @@ __global__ void __launch_bounds__(TL::THREADS, 1)
       if (local) {
         if (cur.cnt < 0) {
           const int64_t ms = cur.m * p.T;
-          cur.cnt = trail_blocks<B>(p.N - ms, (p.T < p.N - ms ? p.T : p.N - ms));
+          cur.cnt = TZ::count(p.N - ms, (p.T < p.N - ms ? p.T : p.N - ms));
         }
         if (item < cur.base + cur.cnt) break;
         cur.base += cur.cnt;
@@ -180,24 +209,15 @@ __global__ void __launch_bounds__(TL::THREADS, 1)
       cur.cnt = -1;
     }
     const int64_t m = cur.m, ms = m * p.T, rows = p.N - ms, tc = p.T < rows ? p.T : rows;
-    const int64_t ncb = (tc + B - 1) / B, tri = ncb * (ncb + 1) / 2;
-    const int64_t b = item - cur.base;
     int64_t rb, cbk;
-    if (b < tri) {
-      rb = 0;
-      while ((rb + 1) * (rb + 2) / 2 <= b) ++rb;
-      cbk = b - rb * (rb + 1) / 2;
-    } else {
-      rb = ncb + (b - tri) / ncb;
-      cbk = (b - tri) % ncb;
-    }
+    TZ::decode(item - cur.base, tc, rb, cbk);
     const int dev = (int)(m % p.D);
     double* shard = reinterpret_cast<double*>(p.shards[dev - p.dev0]);
     const int64_t loc = (m / p.D) * p.T;
     blk.a_row = (int)(ms - p.prow0);
     blk.b_row = (int)(ms - p.prow0);
-    blk.m0 = rb * B;
-    blk.n0 = cbk * B;
+    blk.m0 = rb * TL::BM;
+    blk.n0 = cbk * TL::BN;
     blk.M = rows;
     blk.N = tc;
     blk.ep = Epilogue{shard + ms + loc * p.N, p.N, -1.0, 1.0, 0, 0};
@@ -205,7 +225,7 @@ __global__ void __launch_bounds__(TL::THREADS, 1)
   };
   Cursor cp{p.m_first, 0, -1}, cc{p.m_first, 0, -1};
   tma_gemm_loop<TL>(
-      &mapP, &mapP, (int)p.K, [&](int64_t item, TmaBlock& blk) { return decode(cp, item, blk); },
+      &mapA, &mapB, (int)p.K, [&](int64_t item, TmaBlock& blk) { return decode(cp, item, blk); },
       [&](int64_t item, TmaBlock& blk) { return decode(cc, item, blk); });
 }
 

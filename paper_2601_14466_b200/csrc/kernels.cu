@@ -209,25 +209,46 @@ static CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int64_
 
 static bool tma_ok(const void* p, int64_t ld) { return aligned16(p) && ld % 2 == 0 && ld < ((int64_t)1 << 36); }
 
-static void launch_trail_tma(const TrailParams& p, const int* info, cudaStream_t st) {
-  using TL = TileBig;
+// 128x64 tiles, 8 warps, 2-stage ring, two CTAs per SM: the two co-resident
+// CTAs drift apart, so one CTA's epilogue overlaps the other's DMMAs.
+using TileTrail2 = Tile<128, 64, 32, 32, 32, 2, true>;
+
+template <class TL>
+static void launch_trail_tma_t(const TrailParams& p, const int* info, cudaStream_t st) {
   int64_t total = 0;
   for (int64_t m = p.m_first; m < p.m_last; ++m) {
     const int dev = (int)(m % p.D);
     if (dev < p.dev0 || dev >= p.dev0 + p.nloc) continue;
     const int64_t rows = p.N - m * p.T, tc = std::min(p.T, rows);
-    const int64_t nrb = (rows + TL::BM - 1) / TL::BM, ncb = (tc + TL::BM - 1) / TL::BM;
-    total += nrb <= ncb ? nrb * (nrb + 1) / 2 : ncb * (ncb + 1) / 2 + (nrb - ncb) * ncb;
+    total += Trap<TL::BM, TL::BN>::count(rows, tc);
   }
   if (total == 0) return;
-  const CUtensorMap map = make_map(p.P, p.N - p.prow0, p.K, p.ldp, TL::LDA, TL::BK);
+  const CUtensorMap mapA = make_map(p.P, p.N - p.prow0, p.K, p.ldp, TL::LDA, TL::BK);
+  const CUtensorMap mapB = make_map(p.P, p.N - p.prow0, p.K, p.ldp, TL::LDB, TL::BK);
   constexpr size_t smem = tma_smem_bytes<TL>();
   auto kern = trail_tma_kernel<TL>;
   set_smem(kern, smem);
-  int64_t grid = std::min<int64_t>(total, (int64_t)num_sms());
-  if (p.max_ctas > 0) grid = std::min<int64_t>(grid, p.max_ctas);
-  kern<<<(unsigned)grid, TL::THREADS, smem, st>>>(map, p, info);
+  int per_sm = 1;
+  BCMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TL::THREADS, smem));
+  per_sm = std::max(per_sm, 1);
+  const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, num_sms()) : num_sms();
+  const int64_t grid = std::min<int64_t>(total, (int64_t)sms * per_sm);
+  kern<<<(unsigned)grid, TL::THREADS, smem, st>>>(mapA, mapB, p, info);
   BCMG_CHECK_LAUNCH();
+}
+
+static int trail_tile_choice() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BCMG_TRAIL_TILE");
+    v = e ? atoi(e) : 2;
+  }
+  return v;
+}
+
+static void launch_trail_tma(const TrailParams& p, const int* info, cudaStream_t st) {
+  if (trail_tile_choice() == 1) return launch_trail_tma_t<TileBig>(p, info, st);
+  launch_trail_tma_t<TileTrail2>(p, info, st);
 }
 
 static void launch_gemm_tma(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
