@@ -421,6 +421,7 @@ struct TrailParams {
   void* shards[MAX_LOCAL_DEV];
   int64_t m_first, m_last;
   int max_ctas;       // host-side: persistent grid cap (0 = all SMs)
+  long long stagger_ns;  // delay of the second half of the grid (two CTAs per SM)
 };
 
 template <int B>

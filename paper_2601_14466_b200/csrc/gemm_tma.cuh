@@ -54,8 +54,19 @@ template <class TL>
 constexpr int tma_box_rows_b() { return TL::LDB; }
 template <class TL>
 constexpr unsigned tma_stage_bytes() { return (unsigned)(TL::BK * (TL::LDA + TL::LDB) * 8); }
+// Dynamic shared memory: STAGES operand stages | 2*STAGES mbarriers | 256-byte
+// aux area (producer state [0,128), caller state [128,256)) -- the producer's
+// bookkeeping lives here, not in registers every consumer thread would pay for.
+constexpr int TMA_AUX_BYTES = 256;
 template <class TL>
-constexpr size_t tma_smem_bytes() { return (size_t)TL::STAGES * tma_stage_bytes<TL>() + 2 * TL::STAGES * 8 + 64; }
+constexpr size_t tma_smem_bytes() {
+  return (size_t)TL::STAGES * tma_stage_bytes<TL>() + 2 * TL::STAGES * 8 + TMA_AUX_BYTES;
+}
+extern __shared__ __align__(1024) unsigned char tma_dyn_smem[];
+template <class TL>
+__device__ __forceinline__ unsigned char* tma_aux() {
+  return tma_dyn_smem + (size_t)TL::STAGES * tma_stage_bytes<TL>() + 2 * TL::STAGES * 8;
+}
 
 // One output block: rows [a_row + m0 ...) of A's map, [b_row + n0 ...) of B's map.
 struct TmaBlock {
@@ -70,8 +81,8 @@ struct TmaBlock {
 // stateful cursors stay monotone) and return false when there is none.
 template <class TL, class NextP, class NextC>
 __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUtensorMap* mapB, int K, NextP&& next_p,
-                                              NextC&& next_c) {
-  extern __shared__ __align__(128) double smem[];
+                                              NextC&& next_c, long long stagger_ns = 0) {
+  double* smem = reinterpret_cast<double*>(tma_dyn_smem);
   constexpr int NW = TL::THREADS / 32;
   constexpr unsigned STAGE_BYTES = tma_stage_bytes<TL>();
   constexpr int STAGE_WORDS = TL::BK * (TL::LDA + TL::LDB);
@@ -91,29 +102,39 @@ __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUt
   }
   __syncthreads();
 
-  // producer state (thread 0 only): slice counter gp over (item, kt)
-  int64_t p_item = blockIdx.x;
-  int p_kt = 0;
-  TmaBlock pb;
-  bool p_live = false;
-  uint32_t gp = 0;
+  // producer state (thread 0 only) lives in shared memory so it costs the
+  // consumer warps no registers: slice counter gp over (item, kt)
+  struct Prod {
+    int64_t item;
+    TmaBlock blk;
+    uint32_t gp;
+    int kt, live;
+  };
+  static_assert(sizeof(Prod) <= 128, "producer state must fit its aux slot");
+  Prod& ps = *reinterpret_cast<Prod*>(tma_aux<TL>());
   auto produce_one = [&]() {
-    if (!p_live) return;
-    const int s = gp % TL::STAGES;
+    if (!ps.live) return;
+    const uint32_t gp = ps.gp;
+    const int s = gp % TL::STAGES, kt = ps.kt;
     mbar_wait(&empty[s], ((gp / TL::STAGES) & 1) ^ 1);
     double* st = smem + s * STAGE_WORDS;
     mbar_expect_tx(&full[s], STAGE_BYTES);
-    tma_load_2d(st, mapA, pb.a_row + (int)pb.m0, p_kt * TL::BK, &full[s]);
-    tma_load_2d(st + TL::BK * TL::LDA, mapB, pb.b_row + (int)pb.n0, p_kt * TL::BK, &full[s]);
-    ++gp;
-    if (++p_kt == KT) {
-      p_kt = 0;
-      p_item += gridDim.x;
-      p_live = next_p(p_item, pb);
+    tma_load_2d(st, mapA, ps.blk.a_row + (int)ps.blk.m0, kt * TL::BK, &full[s]);
+    tma_load_2d(st + TL::BK * TL::LDA, mapB, ps.blk.b_row + (int)ps.blk.n0, kt * TL::BK, &full[s]);
+    ps.gp = gp + 1;
+    if (kt + 1 == KT) {
+      ps.kt = 0;
+      ps.item += gridDim.x;
+      ps.live = next_p(ps.item, ps.blk);
+    } else {
+      ps.kt = kt + 1;
     }
   };
   if (tid == 0) {
-    p_live = next_p(p_item, pb);
+    ps.item = blockIdx.x;
+    ps.gp = 0;
+    ps.kt = 0;
+    ps.live = next_p(ps.item, ps.blk);
     for (int i = 0; i < TL::STAGES - 1; ++i) produce_one();
   }
 
@@ -133,6 +154,13 @@ __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUt
         asm volatile("prefetch.global.L2 [%0];\n" ::"l"(C + row + col * blk.ep.ldc));
     }
   };
+  // Two co-resident CTAs per SM start in lockstep and, with uniform items,
+  // would hit their epilogues together; delaying the second half of the grid
+  // by about half an item makes one CTA's epilogue overlap the other's DMMAs.
+  if (stagger_ns > 0 && blockIdx.x >= gridDim.x / 2) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < stagger_ns * 2) __nanosleep(1000);  // ~2 cycles per ns at ~2 GHz
+  }
   for (int64_t item = blockIdx.x; next_c(item, cb); item += gridDim.x) {
     Acc<TL, false> acc;
     acc.zero();
@@ -223,16 +251,19 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
     blk.ep = Epilogue{shard + ms + loc * p.N, p.N, -1.0, 1.0, 0, 0};
     return true;
   };
-  Cursor cp{p.m_first, 0, -1}, cc{p.m_first, 0, -1};
+  // producer's cursor (thread 0 only) in the caller aux slot: no registers in the consumers
+  Cursor& cp = *reinterpret_cast<Cursor*>(tma_aux<TL>() + 128);
+  if (threadIdx.x == 0) cp = Cursor{p.m_first, 0, -1};
+  Cursor cc{p.m_first, 0, -1};
   tma_gemm_loop<TL>(
       &mapA, &mapB, (int)p.K, [&](int64_t item, TmaBlock& blk) { return decode(cp, item, blk); },
-      [&](int64_t item, TmaBlock& blk) { return decode(cc, item, blk); });
+      [&](int64_t item, TmaBlock& blk) { return decode(cc, item, blk); }, p.stagger_ns);
 }
 
 // Single GEMM C := alpha A B^H (+ beta C) with A (M x K) and B (N x K) both
 // i-contiguous real double, persistent over the ceil(M/BM) x ceil(N/BN) blocks.
 template <class TL>
-__global__ void __launch_bounds__(TL::THREADS, 1)
+__global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
     gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int64_t M,
                     int64_t N, int64_t K, Epilogue ep, const int* info) {
   if (ld_flag(info)) return;

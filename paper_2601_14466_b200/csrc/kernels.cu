@@ -233,7 +233,15 @@ static void launch_trail_tma_t(const TrailParams& p, const int* info, cudaStream
   per_sm = std::max(per_sm, 1);
   const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, num_sms()) : num_sms();
   const int64_t grid = std::min<int64_t>(total, (int64_t)sms * per_sm);
-  kern<<<(unsigned)grid, TL::THREADS, smem, st>>>(mapA, mapB, p, info);
+  TrailParams q = p;
+  q.stagger_ns = 0;
+  if (per_sm >= 2 && total >= 8 * grid) {
+    // half an item at ~85% of the per-CTA DMMA rate (37 TF/s over 2 CTAs per SM)
+    const double item_flops = 2.0 * TL::BM * TL::BN * (double)p.K;
+    q.stagger_ns = (long long)(0.5 * item_flops / (0.85 * 37e12 / (num_sms() * per_sm)) * 1e9);
+    if (const char* e = getenv("BCMG_STAGGER")) q.stagger_ns = atoi(e) ? q.stagger_ns : 0;
+  }
+  kern<<<(unsigned)grid, TL::THREADS, smem, st>>>(mapA, mapB, q, info);
   BCMG_CHECK_LAUNCH();
 }
 
@@ -251,18 +259,29 @@ static void launch_trail_tma(const TrailParams& p, const int* info, cudaStream_t
   launch_trail_tma_t<TileTrail2>(p, info, st);
 }
 
-static void launch_gemm_tma(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
-                            const int* info, cudaStream_t st) {
-  using TL = TileBig;
+template <class TL>
+static void launch_gemm_tma_t(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B,
+                              const Epilogue& ep, const int* info, cudaStream_t st) {
   const CUtensorMap ma = make_map(A.ptr, M, K, A.ld, TL::LDA, TL::BK);
   const CUtensorMap mb = make_map(B.ptr, N, K, B.ld, TL::LDB, TL::BK);
   constexpr size_t smem = tma_smem_bytes<TL>();
   auto kern = gemm_tma_kernel<TL>;
   set_smem(kern, smem);
+  int per_sm = 1;
+  BCMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TL::THREADS, smem));
   const int64_t blocks = ((M + TL::BM - 1) / TL::BM) * ((N + TL::BN - 1) / TL::BN);
-  const int64_t grid = std::min<int64_t>(blocks, (int64_t)num_sms());
+  const int64_t grid = std::min<int64_t>(blocks, (int64_t)num_sms() * std::max(per_sm, 1));
   kern<<<(unsigned)grid, TL::THREADS, smem, st>>>(ma, mb, M, N, K, ep, info);
   BCMG_CHECK_LAUNCH();
+}
+
+static int trail_tile_choice();
+using TileTrail2 = Tile<128, 64, 32, 32, 32, 2, true>;
+
+static void launch_gemm_tma(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+                            const int* info, cudaStream_t st) {
+  if (trail_tile_choice() == 1) return launch_gemm_tma_t<TileBig>(M, N, K, A, B, ep, info, st);
+  launch_gemm_tma_t<TileTrail2>(M, N, K, A, B, ep, info, st);
 }
 
 static bool use_tma() {

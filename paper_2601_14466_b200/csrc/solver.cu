@@ -557,6 +557,10 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
           BCMG_CUDA(cudaEventRecord(E(U, k), crit));
         } else {
           BCMG_CUDA(cudaStreamWaitEvent(bulk, E(R, k), 0));
+          // with a lookahead this step, the full-grid update of tile k+1 goes
+          // first; otherwise both persistent grids would race for the SMs and
+          // the critical path could be queued behind the whole bulk update
+          if (op.root) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(U, k), 0));
           trail(k, op.a, op.b, bulk, op.root ? std::max(1, nsm - reserve) : 0);
         }
         break;
