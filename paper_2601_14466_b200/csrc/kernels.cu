@@ -375,9 +375,9 @@ __global__ void __launch_bounds__(256) leaf_kernel(S* A, int64_t lda, S* X, int6
         if (!(d > 0.0) || !isfinite(d)) {
           s_bad = j;
         } else {
-          const double lv = sqrt(d);
-          l[jo][jo] = v_from<V>(make_double2(lv, 0.0));
-          s_inv[buf] = 1.0 / lv;
+          const double r = rsqrt(d);  // one MUFU + Newton steps on the serial chain (not sqrt + div)
+          l[jo][jo] = v_from<V>(make_double2(d * r, 0.0));
+          s_inv[buf] = r;
         }
       }
       __syncthreads();
@@ -409,16 +409,29 @@ __global__ void __launch_bounds__(256) leaf_kernel(S* A, int64_t lda, S* X, int6
         }
       }
       __syncthreads();
+      {
+        // branch-free rank-1 update: all broadcast operands are loaded up front
+        // (stale entries are loaded but never selected), then predicated FMAs,
+        // so the shared-memory latency is paid once per column, not per element
+        V li[4], lc[4], xc[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int i = ty + 16 * a;
-        if (i > j && i < n) {
-          const V lij = colL[buf][i];
+        for (int a = 0; a < 4; ++a) li[a] = colL[buf][ty + 16 * a];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          lc[b] = colL[buf][tx + 16 * b];
+          xc[b] = rowX[buf][tx + 16 * b];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int i = ty + 16 * a;
+          const bool row = i > j && i < n;
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             const int c = tx + 16 * b;
-            if (c <= j) x[a][b] = v_fnms(x[a][b], lij, rowX[buf][c]);
-            else if (c <= i) l[a][b] = v_fnmsc(l[a][b], lij, colL[buf][c]);
+            const V nx = v_fnms(x[a][b], li[a], xc[b]);
+            const V nl = v_fnmsc(l[a][b], li[a], lc[b]);
+            x[a][b] = (row && c <= j) ? nx : x[a][b];
+            l[a][b] = (row && c > j && c <= i) ? nl : l[a][b];
           }
         }
       }
