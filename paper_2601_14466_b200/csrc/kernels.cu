@@ -11,6 +11,7 @@
 #include <cudaTypedefs.h>
 
 #include "gemm_tma.cuh"
+#include "tc_gemm.cuh"
 #include "ops.h"
 
 namespace bcmg {
@@ -73,6 +74,10 @@ static void launch_gemm(int64_t M, int64_t N, int64_t K, const Operand& A, const
 }
 
 static bool use_tma();
+static bool use_tc();
+static bool tc_ok(const void* p, int64_t ld);
+static void launch_tc3_gemm(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+                            const int* info, cudaStream_t st);
 static bool tma_ok(const void* p, int64_t ld);
 static void launch_gemm_tma(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
                             const int* info, cudaStream_t st);
@@ -92,6 +97,11 @@ static void gemm_t(int64_t M, int64_t N, int64_t K, const Operand& A, const Oper
       }
       return launch_gemm<S, TileMed, true>(M, N, K, A, B, ep, info, st);
     }
+  }
+  if constexpr (std::is_same_v<S, float>) {
+    if (use_tc() && !A.trans && !B.trans && !A.mask && !B.mask && tc_ok(A.ptr, A.ld) && tc_ok(B.ptr, B.ld) &&
+        tc_ok(ep.C, 4) && M >= 256 && N >= 64 && K >= 32)
+      return launch_tc3_gemm(M, N, K, A, B, ep, info, st);
   }
   if (N <= 16) return launch_gemm<S, TileNarrow, false>(M, N, K, A, B, ep, info, st);
   return launch_gemm<S, TileMed, false>(M, N, K, A, B, ep, info, st);
@@ -293,10 +303,68 @@ static bool use_tma() {
   return v == 1;
 }
 
+// ============================================================== tcgen05 3xTF32 (float32)
+static CUtensorMap make_map_f32_sw128(const void* base, int64_t rows, int64_t cols, int64_t ld) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32, (cuuint32_t)tc::BK};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(CUDA, "cuTensorMapEncodeTiled (f32 sw128) failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+static bool tc_ok(const void* p, int64_t ld) { return aligned16(p) && ld % 4 == 0; }
+
+static bool use_tc() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BCMG_NO_TCGEN05");
+    v = (e && atoi(e)) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static void launch_tc3_gemm(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+                            const int* info, cudaStream_t st) {
+  const CUtensorMap ma = make_map_f32_sw128(A.ptr, M, K, A.ld);
+  const CUtensorMap mb = make_map_f32_sw128(B.ptr, N, K, B.ld);
+  set_smem(tc3_gemm_kernel, tc::SMEM_BYTES);
+  const int64_t blocks = ((M + tc::BM - 1) / tc::BM) * ((N + tc::BN - 1) / tc::BN);
+  const int64_t grid = std::min<int64_t>(blocks, (int64_t)num_sms());
+  tc3_gemm_kernel<<<(unsigned)grid, tc::THREADS, tc::SMEM_BYTES, st>>>(
+      ma, mb, M, N, K, static_cast<float*>(ep.C), ep.ldc, (float)ep.alpha, (float)ep.beta, info);
+  BCMG_CHECK_LAUNCH();
+}
+
+static void launch_tc3_trail(const TrailParams& p, const int* info, cudaStream_t st) {
+  int64_t total = 0;
+  for (int64_t m = p.m_first; m < p.m_last; ++m) {
+    const int dev = (int)(m % p.D);
+    if (dev < p.dev0 || dev >= p.dev0 + p.nloc) continue;
+    const int64_t rows = p.N - m * p.T;
+    total += Trap<tc::BM, tc::BN>::count(rows, std::min(p.T, rows));
+  }
+  if (total == 0) return;
+  const CUtensorMap map = make_map_f32_sw128(p.P, p.N - p.prow0, p.K, p.ldp);
+  set_smem(tc3_trail_kernel, tc::SMEM_BYTES);
+  const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, num_sms()) : num_sms();
+  const int64_t grid = std::min<int64_t>(total, sms);
+  tc3_trail_kernel<<<(unsigned)grid, tc::THREADS, tc::SMEM_BYTES, st>>>(map, p, info);
+  BCMG_CHECK_LAUNCH();
+}
+
 void trailing_update(int dt, const TrailParams& p, const int* info, cudaStream_t st) {
   if (p.m_first >= p.m_last || p.K <= 0) return;
   dispatch_dtype(dt, [&](auto s) {
     using S = decltype(s);
+    if constexpr (std::is_same_v<S, float>) {
+      if (use_tc() && tc_ok(p.P, p.ldp) && p.T % 4 == 0 && p.prow0 % 4 == 0 && p.N % 4 == 0)
+        return launch_tc3_trail(p, info, st);
+    }
     if constexpr (std::is_same_v<S, double>) {
       const bool cp = aligned16(p.P) && p.ldp % 2 == 0 && p.T % 2 == 0 && (p.prow0 % 2 == 0);
       if (cp && use_tma() && tma_ok(p.P, p.ldp)) return launch_trail_tma(p, info, st);

@@ -1,0 +1,335 @@
+// float32 contractions on the 5th-gen tensor cores: tcgen05.mma kind::tf32
+// with a 3xTF32 split (a = a_hi + a_lo, a*b ~= a_hi*b_hi + a_hi*b_lo +
+// a_lo*b_hi, FP32 accumulation in TMEM) -- FP32-level accuracy at tensor-core
+// rate, as the north star asks for float32 / complex64.
+//
+// Warp-specialised persistent kernel, 12 warps:
+//   warp 0        TMA producer: fp32 boxes {32 rows, BK} (SWIZZLE_128B) of
+//                 the operands as stored (rows contiguous) into a raw ring
+//   warp 1        TMEM allocator + single-thread MMA issuer
+//   warps 2,3,8-11 splitters: raw -> K-major SW128 "hi" = rna_tf32(x) and
+//                 "lo" = x - hi planes (kind::tf32 takes K-major operands
+//                 only), then fence.proxy.async for the tensor core
+//   warps 4-7     epilogue warpgroup: tcgen05.ld 32x32b accumulator rows,
+//                 C := alpha*acc + beta*C, coalesced along the column
+// Pipelines: raw stages (TMA tx -> split), split stages (split -> MMA commit),
+// two TMEM accumulators (commit -> epilogue), so TMA, splitting, MMA and the
+// epilogue of the previous tile all overlap.
+#pragma once
+
+#include "gemm_tma.cuh"
+
+namespace bcmg {
+
+namespace tc {
+
+constexpr int BM = 128, BN = 128, BK = 32;
+constexpr int RAW_STAGES = 2, SPL_STAGES = 2;
+constexpr int THREADS = 384;                         // 12 warps (see the role map above)
+constexpr int SPLIT_WARPS = 6;                       // warps 2, 3, 8, 9, 10, 11
+constexpr int ATOM_BYTES = 32 * 4 * BK;              // raw: one 32-row MN chunk x BK k-rows
+constexpr int PLANE_A = BM * BK * 4, PLANE_B = BN * BK * 4;  // 16 KB each
+constexpr int RAW_BYTES = PLANE_A + PLANE_B;         // raw stage (TMA, MN-major)
+constexpr int SPL_BYTES = 2 * (PLANE_A + PLANE_B);   // split stage: A hi, A lo, B hi, B lo (K-major)
+constexpr int TMEM_COLS = 2 * BN;                    // two accumulators
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + (size_t)RAW_STAGES * RAW_BYTES + (size_t)SPL_STAGES * SPL_BYTES + 256;
+
+// UMMA instruction descriptor: D f32, A/B tf32, both K-major (kind::tf32 on
+// sm_100a accepts only K-major operands -- measured: MN-major writes nothing),
+// M=128, N=128.
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+// Shared-memory matrix descriptor, K-major SWIZZLE_128B: rows of 128 B (32 k),
+// 8-row 1 KB atoms stacked along M/N (SBO = 1 KB), LBO unused (16 B).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)((1024 >> 4) & 0x3FFF) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+
+// raw (TMA, MN-major SW128) byte offset of element (i, k) of a 128 x BK tile
+__device__ __forceinline__ int raw_off(int i, int k) {
+  return (i >> 5) * ATOM_BYTES + k * 128 + ((((i & 31) >> 2) ^ (k & 7)) << 4) + ((i & 3) << 2);
+}
+// K-major SW128 byte offset of the 16-byte chunk holding (i, 4c .. 4c+3)
+__device__ __forceinline__ int kmaj_off(int i, int c) { return (i >> 3) * 1024 + (i & 7) * 128 + ((c ^ (i & 7)) << 4); }
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(IDESC), "r"(accumulate));
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// Block of work: output rows [m0, m0+BM) x cols [n0, n0+BN); TMA row
+// coordinates of its A and B panels; epilogue target.
+struct Blk {
+  int a_row, b_row;
+  int64_t m0, n0, M, N;
+  float* C;
+  int64_t ldc;
+  float alpha, beta;
+};
+
+template <class Next>
+__device__ __forceinline__ void tc3_loop(const CUtensorMap* mapA, const CUtensorMap* mapB, int K, Next&& next) {
+  extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
+  // 1024-byte aligned base for the SWIZZLE_128B atoms
+  unsigned char* base = tc_smem_raw + ((1024 - (smem_u32(tc_smem_raw) & 1023)) & 1023);
+  unsigned char* raw = base;                                       // RAW_STAGES x RAW_BYTES
+  unsigned char* spl = base + (size_t)RAW_STAGES * RAW_BYTES;      // SPL_STAGES x SPL_BYTES
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(spl + (size_t)SPL_STAGES * SPL_BYTES);
+  uint64_t* raw_free = raw_full + RAW_STAGES;
+  uint64_t* spl_ready = raw_free + RAW_STAGES;
+  uint64_t* spl_empty = spl_ready + SPL_STAGES;
+  uint64_t* tfull = spl_empty + SPL_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int KT = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RAW_STAGES; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&raw_free[s], SPLIT_WARPS);
+    }
+    for (int s = 0; s < SPL_STAGES; ++s) {
+      mbar_init(&spl_ready[s], SPLIT_WARPS);
+      mbar_init(&spl_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      uint32_t g = 0;
+      Blk blk;
+      for (int64_t item = blockIdx.x; next(item, blk); item += gridDim.x) {
+        for (int kt = 0; kt < KT; ++kt, ++g) {
+          const int s = g % RAW_STAGES;
+          mbar_wait(&raw_free[s], ((g / RAW_STAGES) & 1) ^ 1);
+          unsigned char* st = raw + (size_t)s * RAW_BYTES;
+          mbar_expect_tx(&raw_full[s], RAW_BYTES);
+#pragma unroll
+          for (int c = 0; c < BM / 32; ++c)
+            tma_load_2d(st + c * ATOM_BYTES, mapA, blk.a_row + (int)blk.m0 + 32 * c, kt * BK, &raw_full[s]);
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c)
+            tma_load_2d(st + PLANE_A + c * ATOM_BYTES, mapB, blk.b_row + (int)blk.n0 + 32 * c, kt * BK,
+                        &raw_full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      uint32_t g = 0, t = 0;
+      Blk blk;
+      for (int64_t item = blockIdx.x; next(item, blk); item += gridDim.x, ++t) {
+        const int b = t & 1;
+        mbar_wait(&tempty[b], ((t >> 1) & 1) ^ 1);
+        fence_after();
+        const uint32_t d = tmem + b * BN;
+        for (int kt = 0; kt < KT; ++kt, ++g) {
+          const int s = g % SPL_STAGES;
+          mbar_wait(&spl_ready[s], (g / SPL_STAGES) & 1);
+          fence_after();
+          const uint32_t st = smem_u32(spl + (size_t)s * SPL_BYTES);
+          const uint32_t ahi = st, alo = st + PLANE_A, bhi = st + 2 * PLANE_A, blo = bhi + PLANE_B;
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint32_t off = ks * 32;  // 8 tf32 k = 32 bytes along the 128-byte K-major row
+            // small terms first, then the dominant hi*hi product
+            mma_tf32(d, sdesc(alo + off), sdesc(bhi + off), (kt | ks) != 0);
+            mma_tf32(d, sdesc(ahi + off), sdesc(blo + off), 1);
+            mma_tf32(d, sdesc(ahi + off), sdesc(bhi + off), 1);
+          }
+          commit(&spl_empty[s]);  // split stage reusable once these MMAs have read it
+        }
+        commit(&tfull[b]);  // accumulator b complete
+      }
+    }
+  } else if (warp < 4 || warp >= 8) {
+    // ---------------------------------------------------------- splitters
+    // raw MN-major (TMA) -> K-major SW128 hi / lo planes.  A warp takes 32
+    // consecutive rows i of one 4-wide k chunk: the four scalar raw loads and
+    // the 16-byte hi / lo stores are all bank-conflict free.
+    const int sw = warp < 4 ? warp - 2 : warp - 6;  // 0..5
+    uint32_t g = 0;
+    Blk blk;
+    for (int64_t item = blockIdx.x; next(item, blk); item += gridDim.x) {
+      for (int kt = 0; kt < KT; ++kt, ++g) {
+        const int rs = g % RAW_STAGES, ss = g % SPL_STAGES;
+        mbar_wait(&raw_full[rs], (g / RAW_STAGES) & 1);
+        mbar_wait(&spl_empty[ss], ((g / SPL_STAGES) & 1) ^ 1);
+        const unsigned char* rst = raw + (size_t)rs * RAW_BYTES;
+        unsigned char* sst = spl + (size_t)ss * SPL_BYTES;
+        // units: (operand, 32-row group, k chunk) = 2 x 4 x 8 = 64, warp-strided
+        for (int u = sw; u < 64; u += SPLIT_WARPS) {
+          const int op = u >> 5, grp = (u >> 3) & 3, c = u & 7;
+          const int i = grp * 32 + lane;
+          const unsigned char* rsrc = rst + op * PLANE_A;
+          float x[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) x[e] = *reinterpret_cast<const float*>(rsrc + raw_off(i, 4 * c + e));
+          const float4 h = make_float4(tf32_rna(x[0]), tf32_rna(x[1]), tf32_rna(x[2]), tf32_rna(x[3]));
+          const float4 l = make_float4(x[0] - h.x, x[1] - h.y, x[2] - h.z, x[3] - h.w);
+          unsigned char* dst = sst + op * 2 * PLANE_A + kmaj_off(i, c);
+          *reinterpret_cast<float4*>(dst) = h;
+          *reinterpret_cast<float4*>(dst + PLANE_A) = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&spl_ready[ss]);
+          mbar_arrive(&raw_free[rs]);
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    const int q = warp - 4;  // TMEM lane quarter
+    const int row = 32 * q + lane;
+    uint32_t t = 0;
+    Blk blk;
+    for (int64_t item = blockIdx.x; next(item, blk); item += gridDim.x, ++t) {
+      const int b = t & 1;
+      mbar_wait(&tfull[b], (t >> 1) & 1);
+      fence_after();
+      const int64_t r = blk.m0 + row;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + b * BN + c0, v);
+        if (r < blk.M) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int64_t col = blk.n0 + c0 + j;
+            if (col < blk.N) {
+              float* cp = blk.C + r + col * blk.ldc;
+              *cp = blk.alpha * v[j] + (blk.beta != 0.f ? blk.beta * *cp : 0.f);
+            }
+          }
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace tc
+
+// C := alpha * A * B^T + beta * C, A (M x K) and B (N x K) M-/N-contiguous fp32.
+__global__ void __launch_bounds__(tc::THREADS, 1)
+    tc3_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int64_t M,
+                    int64_t N, int64_t K, float* C, int64_t ldc, float alpha, float beta, const int* info) {
+  if (ld_flag(info)) return;
+  const int64_t nbm = (M + tc::BM - 1) / tc::BM, nbn = (N + tc::BN - 1) / tc::BN;
+  tc::tc3_loop(&mapA, &mapB, (int)K, [&](int64_t item, tc::Blk& blk) -> bool {
+    if (item >= nbm * nbn) return false;
+    blk.a_row = 0;
+    blk.b_row = 0;
+    blk.m0 = (item % nbm) * tc::BM;
+    blk.n0 = (item / nbm) * tc::BN;
+    blk.M = M;
+    blk.N = N;
+    blk.C = C;
+    blk.ldc = ldc;
+    blk.alpha = alpha;
+    blk.beta = beta;
+    return true;
+  });
+}
+
+// potrf trailing update for float32 shards (see trail_kernel): stateless
+// decode (every role walks the same item sequence independently).
+__global__ void __launch_bounds__(tc::THREADS, 1)
+    tc3_trail_kernel(const __grid_constant__ CUtensorMap mapP, TrailParams p, const int* info) {
+  using TZ = Trap<tc::BM, tc::BN>;
+  if (ld_flag(info)) return;
+  int64_t cm = p.m_first, cbase = 0, ccnt = -1;  // per-thread monotone cursor
+  tc::tc3_loop(&mapP, &mapP, (int)p.K, [&](int64_t item, tc::Blk& blk) -> bool {
+    for (;;) {
+      if (cm >= p.m_last) return false;
+      const int dev = (int)(cm % p.D);
+      if (dev >= p.dev0 && dev < p.dev0 + p.nloc) {
+        if (ccnt < 0) {
+          const int64_t ms = cm * p.T;
+          ccnt = TZ::count(p.N - ms, (p.T < p.N - ms ? p.T : p.N - ms));
+        }
+        if (item < cbase + ccnt) break;
+        cbase += ccnt;
+      }
+      ++cm;
+      ccnt = -1;
+    }
+    const int64_t ms = cm * p.T, rows = p.N - ms, tcw = p.T < rows ? p.T : rows;
+    int64_t rb, cb;
+    TZ::decode(item - cbase, tcw, rb, cb);
+    const int dev = (int)(cm % p.D);
+    float* shard = reinterpret_cast<float*>(p.shards[dev - p.dev0]);
+    const int64_t loc = (cm / p.D) * p.T;
+    blk.a_row = (int)(ms - p.prow0);
+    blk.b_row = (int)(ms - p.prow0);
+    blk.m0 = rb * tc::BM;
+    blk.n0 = cb * tc::BN;
+    blk.M = rows;
+    blk.N = tcw;
+    blk.C = shard + ms + loc * p.N;
+    blk.ldc = p.N;
+    blk.alpha = -1.f;
+    blk.beta = 1.f;
+    return true;
+  });
+}
+
+}  // namespace bcmg

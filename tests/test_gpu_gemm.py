@@ -64,3 +64,14 @@ def test_gemm_large_tma_path(cuda, m, n, k):
 
     for op_b in (0, 1):
         assert _run(torch, 1, m, n, k, 0, op_b, -1.0, 1.0) <= 0
+
+
+@pytest.mark.parametrize("m,n,k", [(512, 256, 96), (4096, 2048, 1024), (1000, 300, 77), (256, 64, 32)])
+def test_gemm_f32_tcgen05_3xtf32(cuda, m, n, k):
+    """float32 natural-layout shapes take the tcgen05 kind::tf32 3xTF32 kernel
+    (TMEM accumulators); FP32-level accuracy against a float64 torch reference."""
+    import torch
+
+    pad = (-m) % 4
+    assert _run(torch, 0, m, n, k, 0, 1, -1.0, 1.0, lda_pad=pad) <= 0
+    assert _run(torch, 0, m, n, k, 0, 1, 1.0, 0.0, lda_pad=pad, seed=3) <= 0
