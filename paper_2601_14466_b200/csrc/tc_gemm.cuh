@@ -239,18 +239,24 @@ __device__ __forceinline__ void tc3_loop(const CUtensorMap* mapA, const CUtensor
       mbar_wait(&tfull[b], (t >> 1) & 1);
       fence_after();
       const int64_t r = blk.m0 + row;
+      float* __restrict__ crow = blk.C + r;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
+        // issue this chunk's 32 C loads before touching TMEM or storing:
+        // one memory latency per chunk instead of one per element
+        float old[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int64_t col = blk.n0 + c0 + j;
+          old[j] = (blk.beta != 0.f && r < blk.M && col < blk.N) ? crow[col * blk.ldc] : 0.f;
+        }
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + b * BN + c0, v);
         if (r < blk.M) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int64_t col = blk.n0 + c0 + j;
-            if (col < blk.N) {
-              float* cp = blk.C + r + col * blk.ldc;
-              *cp = blk.alpha * v[j] + (blk.beta != 0.f ? blk.beta * *cp : 0.f);
-            }
+            if (col < blk.N) crow[col * blk.ldc] = blk.alpha * v[j] + blk.beta * old[j];
           }
         }
       }
