@@ -123,7 +123,7 @@ static int splitk_t(int64_t M, int64_t N, int64_t K, const Operand& A, const Ope
                     cudaStream_t st) {
   const int64_t ctas = ((M + TL::BM - 1) / TL::BM) * ((N + TL::BN - 1) / TL::BN);
   int64_t np = (2 * num_sms() + ctas - 1) / ctas;
-  np = std::max<int64_t>(1, std::min<int64_t>({np, (int64_t)max_parts, (K + 255) / 256}));
+  np = std::max<int64_t>(1, std::min<int64_t>({np, (int64_t)max_parts, (K + 127) / 128}));
   int64_t kchunk = ((K + np - 1) / np + TL::BK - 1) / TL::BK * TL::BK;
   np = (K + kchunk - 1) / kchunk;
   if (A.trans) {
@@ -683,7 +683,7 @@ void realify_diag(int dt, void* a, int64_t lda, int64_t n, cudaStream_t st) {
 
 template <class S>
 __global__ void reduce_parts_kernel(const S* __restrict__ parts, int64_t pstride, int nparts, S* dst, int64_t ldd,
-                                    int64_t rows, int64_t cols, double alpha) {
+                                    int64_t rows, int64_t cols, double alpha, double beta) {
   const int64_t total = rows * cols;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -694,18 +694,18 @@ __global__ void reduce_parts_kernel(const S* __restrict__ parts, int64_t pstride
       acc.x += v.x;
       acc.y += v.y;
     }
-    double2 o = to_c(dst[r + c * ldd]);
-    dst[r + c * ldd] = from_c<S>(make_double2(o.x + alpha * acc.x, o.y + alpha * acc.y));
+    double2 o = beta != 0.0 ? to_c(dst[r + c * ldd]) : make_double2(0, 0);
+    dst[r + c * ldd] = from_c<S>(make_double2(beta * o.x + alpha * acc.x, beta * o.y + alpha * acc.y));
   }
 }
 
 void reduce_parts(int dt, const void* parts, int64_t part_stride, int nparts, void* dst, int64_t ldd, int64_t rows,
-                  int64_t cols, double alpha, cudaStream_t st) {
+                  int64_t cols, double alpha, cudaStream_t st, double beta) {
   if (rows <= 0 || cols <= 0) return;
   dispatch_dtype(dt, [&](auto s) {
     using S = decltype(s);
     reduce_parts_kernel<S><<<ew_grid(rows * cols), 256, 0, st>>>(static_cast<const S*>(parts), part_stride, nparts,
-                                                                 static_cast<S*>(dst), ldd, rows, cols, alpha);
+                                                                 static_cast<S*>(dst), ldd, rows, cols, alpha, beta);
   });
   BCMG_CHECK_LAUNCH();
 }

@@ -48,9 +48,9 @@ void conj_transpose(int dt, const void* src, int64_t lds, void* dst, int64_t ldd
 void realify_diag(int dt, void* a, int64_t lda, int64_t n, cudaStream_t st);
 void mirror_diag(int dt, void* a, int64_t lda, int64_t n, cudaStream_t st);
 
-// Split-K deterministic reduction: dst += sum_s part[s] (fixed order).
+// Split-K deterministic reduction: dst = beta*dst + alpha*sum_s part[s] (fixed order).
 void reduce_parts(int dt, const void* parts, int64_t part_stride, int nparts, void* dst, int64_t ldd, int64_t rows,
-                  int64_t cols, double alpha, cudaStream_t st);
+                  int64_t cols, double alpha, cudaStream_t st, double beta = 1.0);
 
 // ----------------------------------------------------------------- redistribution
 // Segment-level plan of the contiguous <-> cyclic permutation (layout.py:126-256).

@@ -599,13 +599,12 @@ void Session::potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* 
   if (ldx < n) throw Error(CONFIG, "ldx < n");
   if (last_dinv_T != T || dinv.bytes < (size_t)g.nt * T * T * g.esz)
     throw Error(CONFIG, "potrs needs a potrf of the same tiling in this session");
-  const int64_t max_parts = 64;  // split-K slabs of the backward update
-  const size_t y_bytes = (size_t)T * nrhs * g.esz;
+  // split-K slabs (fixed count per shape: bits independent of the device count)
+  const int64_t max_parts = 64;
   const size_t parts_bytes = (size_t)max_parts * T * nrhs * g.esz;
   const size_t pack_bytes = world > 1 ? (size_t)n * nrhs * g.esz : 0;
-  tmp.ensure(std::max<size_t>(4096, y_bytes + parts_bytes + pack_bytes));
-  char* y = static_cast<char*>(tmp.p);
-  char* parts = y + y_bytes;
+  tmp.ensure(std::max<size_t>(4096, parts_bytes + pack_bytes));
+  char* parts = static_cast<char*>(tmp.p);
   char* pack = parts + parts_bytes;
   char* xb = static_cast<char*>(x);
   auto xrow = [&](int64_t r) { return xb + r * g.esz; };
@@ -625,12 +624,22 @@ void Session::potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* 
     }
     void* sh = shards[(k % g.D) - g.dev0];
     if (op.kind == S_FWD) {
-      gemm(dt, tc, nrhs, tc, opA(dinv_k(k), T, OP_N), opB(xrow(s0), ldx, OP_N), Epilogue{y, tc, 1.0, 0.0, 0, 0},
-           nullptr, st);
-      copy2d(dt, y, tc, xrow(s0), ldx, tc, nrhs, false, nullptr, st);
-      if (s1 < n)
-        gemm(dt, n - s1, nrhs, tc, opA(colp(sh, g, s1, g.loc(k)), n, OP_N), opB(xrow(s0), ldx, OP_N),
-             Epilogue{xrow(s1), ldx, -1.0, 1.0, 0, 0}, nullptr, st);
+      // x_k <- X_kk x_k: split-K straight into x_k (the slabs hold the product)
+      const int npd = gemm_splitk(dt, tc, nrhs, tc, opA(dinv_k(k), T, OP_N), opB(xrow(s0), ldx, OP_N), parts,
+                                  (int)max_parts, st);
+      reduce_parts(dt, parts, tc * nrhs, npd, xrow(s0), ldx, tc, nrhs, 1.0, st, 0.0);
+      if (s1 < n) {
+        // x[stop:] -= L[stop:, k] x_k, split-K when the row blocks alone are under two waves
+        const int64_t cap = (int64_t)(parts_bytes / ((size_t)(n - s1) * nrhs * g.esz));
+        if (cap >= 2) {
+          const int np = gemm_splitk(dt, n - s1, nrhs, tc, opA(colp(sh, g, s1, g.loc(k)), n, OP_N),
+                                     opB(xrow(s0), ldx, OP_N), parts, (int)std::min(cap, max_parts), st);
+          reduce_parts(dt, parts, (n - s1) * nrhs, np, xrow(s1), ldx, n - s1, nrhs, -1.0, st);
+        } else {
+          gemm(dt, n - s1, nrhs, tc, opA(colp(sh, g, s1, g.loc(k)), n, OP_N), opB(xrow(s0), ldx, OP_N),
+               Epilogue{xrow(s1), ldx, -1.0, 1.0, 0, 0}, nullptr, st);
+        }
+      }
       continue;
     }
     {
@@ -641,9 +650,9 @@ void Session::potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* 
                                    opB(xrow(s1), ldx, OP_N), parts, (int)max_parts, st);
         reduce_parts(dt, parts, tc * nrhs, np, xrow(s0), ldx, tc, nrhs, -1.0, st);
       }
-      gemm(dt, tc, nrhs, tc, opA(dinv_k(k), T, OP_C), opB(xrow(s0), ldx, OP_N), Epilogue{y, tc, 1.0, 0.0, 0, 0},
-           nullptr, st);
-      copy2d(dt, y, tc, xrow(s0), ldx, tc, nrhs, false, nullptr, st);
+      const int npd = gemm_splitk(dt, tc, nrhs, tc, opA(dinv_k(k), T, OP_C), opB(xrow(s0), ldx, OP_N), parts,
+                                  (int)max_parts, st);
+      reduce_parts(dt, parts, tc * nrhs, npd, xrow(s0), ldx, tc, nrhs, 1.0, st, 0.0);
     }
   }
   sync_streams(user, crit);
