@@ -4,21 +4,22 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-A step is one potrs pipeline (contiguous -> block-cyclic redistribution,
-tiled potrf, tiled substitution) on a synthetic SPD matrix already resident
-in HBM.  Because potrf factors A in place, every step first restores A from a
-pristine device copy (a D2D copy of N^2 doubles, kept inside the timed region:
-it only makes the number conservative).  Workloads:
+Workload at every GPU count: BASELINE config 3 -- potrs float64 N=131072,
+T_A=1024, N_RHS=64, A row-sharded over the N GPUs (P("x", None)); at N=1 the
+whole 137 GB matrix sits on one 180 GB B200 and is factored in place
+(overwrite_a=True).  Total work is fixed as N grows ("scaling": "strong").
 
-* N=1 (default): BASELINE config 2 -- f64 N=32768, T_A=1024, N_RHS=16, 1 GPU.
-* N>1 (torchrun): BASELINE config 3 -- f64 N=131072, T_A=1024, N_RHS=64,
-  row-sharded over the N GPUs (strong scaling of the headline shape).
-
-`value` = algorithmic TFLOP/s (N^3/3 + 2 N^2 N_RHS per step) over the max-over-
-ranks device time of the K timed steps; `e2e` = the same through the public
-drop-in call with A and b in pinned HOST memory and x read back to the host.
+A step is one potrs pipeline on a synthetic SPD matrix already resident in
+HBM: regenerate A in place (potrf destroys it; a write-only device kernel,
+bcmg_generate_spd, kept inside the timed region -- it only makes the number
+conservative), contiguous -> block-cyclic redistribution, tiled potrf, tiled
+substitution.  `value` = algorithmic TFLOP/s (N^3/3 + 2 N^2 N_RHS per step)
+over the max-over-ranks device time of the K timed steps.  `e2e` = the same
+metric through the public drop-in call `potrs(A_host, b_host, T_A, mesh)`
+with A's row block and b in pinned HOST memory and x read back to the host.
 `--impl reference` times the reference's CPU algorithm (the oracle port of
 pkg/src/bcmg/solvers.py on numpy/scipy-openblas) on a bounded sample.
+`--n/--t/--nrhs` override the shape (probe runs only).
 """
 
 from __future__ import annotations
@@ -36,6 +37,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "potrs TFLOP/s fp64 N=131072 at 1/2/4/8 B200; block-cyclic redistribute GB/s"
 UNIT = "TFLOP/s"
+SEED = 1
 
 
 def potrs_flops(n: int, nrhs: int) -> float:
@@ -44,17 +46,16 @@ def potrs_flops(n: int, nrhs: int) -> float:
 
 def workload(world: int, args) -> dict:
     if args.n:
-        return {"n": args.n, "t": args.t or 1024, "nrhs": args.nrhs or 16,
-                "workload": f"potrs f64 N={args.n} T_A={args.t or 1024} N_RHS={args.nrhs or 16}"}
-    if world == 1:
-        return {"n": 32768, "t": 1024, "nrhs": 16,
-                "workload": "BASELINE config 2: potrs float64 N=32768, T_A=1024, N_RHS=16 on 1xB200"}
+        return {"n": args.n, "t": args.t or 1024, "nrhs": args.nrhs or 64,
+                "workload": f"potrs f64 N={args.n} T_A={args.t or 1024} N_RHS={args.nrhs or 64} "
+                            f"row-sharded over {world}xB200 (probe shape)"}
     return {"n": 131072, "t": 1024, "nrhs": 64,
-            "workload": f"BASELINE config 3: potrs float64 N=131072, T_A=1024, N_RHS=64 row-sharded over {world}xB200"}
+            "workload": f"BASELINE config 3: potrs float64 N=131072, T_A=1024, N_RHS=64 row-sharded over "
+                        f"{world}xB200"}
 
 
 # ---------------------------------------------------------------- CPU baseline (oracle port)
-def cpu_baseline(seconds: float = 12.0, n: int = 4096, t: int = 1024, nrhs: int = 16) -> dict:
+def cpu_baseline(seconds: float = 12.0, n: int = 4096, t: int = 1024, nrhs: int = 64, full_n: int = 131072) -> dict:
     """The reference's tiled algorithm (oracle/bcmg_oracle.py, a restatement of
     pkg/src/bcmg/solvers.py potrf/potrs on numpy + scipy-openblas) on host cores."""
     import numpy as np
@@ -81,7 +82,7 @@ def cpu_baseline(seconds: float = 12.0, n: int = 4096, t: int = 1024, nrhs: int 
     return {"value": potrs_flops(n, nrhs) * reps / dt / 1e12, "unit": UNIT, "cores": int(cores), "kind": "port",
             "sample": f"oracle port of the reference tiled potrf+potrs (solvers.py:341-474), f64 N={n} T_A={t} "
                       f"N_RHS={nrhs}, {reps} solves in {dt:.1f}s, residual {res:.2e}; N^3 extrapolation to "
-                      f"N=32768 = {dt / reps * (32768 / n) ** 3:.0f}s/solve"}
+                      f"N={full_n} = {dt / reps * (full_n / n) ** 3 / 3600:.1f} h/solve"}
 
 
 def run_reference(args, rank: int, world: int) -> None:
@@ -89,8 +90,6 @@ def run_reference(args, rank: int, world: int) -> None:
         return
     k, w = max(1, args.steps), max(0, args.warmup)
     per = 6.0  # seconds of CPU work per timed step (bounded sample)
-    import numpy as np  # noqa: F401
-
     for _ in range(min(w, 1)):
         cpu_baseline(seconds=1.0)
     vals = [cpu_baseline(seconds=per) for _ in range(k)]
@@ -165,25 +164,20 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     n, t, nrhs = cfg["n"], cfg["t"], cfg["nrhs"]
     rows = n // world
     lib = _lib.load()
+    stream = lambda: C.c_void_p(torch.cuda.current_stream().cuda_stream)  # noqa: E731
 
-    # synthetic SPD row block: A = (R + R^T)/2 + n I, R ~ U[-1,1) (symmetric by construction:
-    # element (i, j) depends only on the unordered pair, generated on device)
-    def make_block(dst):
-        # element (i, j) is a hash of the unordered pair {i, j}: symmetric across rank boundaries
-        i = torch.arange(rank * rows, (rank + 1) * rows, device=dev, dtype=torch.int64)[:, None]
-        for c0 in range(0, n, 4096):
-            c1 = min(n, c0 + 4096)
-            j = torch.arange(c0, c1, device=dev, dtype=torch.int64)[None, :]
-            lo, hi = torch.minimum(i, j), torch.maximum(i, j)
-            h = (lo * 1103515245 + hi * 12345 + (lo ^ hi) * 2654435761) % 2147483647
-            h = (h * 48271) % 2147483647
-            v = h.to(torch.float64) / 2147483647.0 * 2.0 - 1.0
-            v = torch.where(i == j, v + float(n), v)
-            dst[:, c0:c1].copy_(v)
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
 
-    A0 = torch.empty(rows, n, dtype=torch.float64, device=dev)
-    make_block(A0)
-    A = torch.empty_like(A0)
+    # this rank's row block of A (row-major rows x n == columns rank*rows.. of the symmetric A)
+    A = torch.empty(rows, n, dtype=torch.float64, device=dev)
+
+    def regen(dst):
+        _lib.check(lib.bcmg_generate_spd(stream(), 1, n, rank * rows, rows, C.c_void_p(dst.data_ptr()), n, SEED,
+                                         float(n)))
+
     gb = torch.Generator(device=dev).manual_seed(7)
     b = torch.rand(n, nrhs, dtype=torch.float64, device=dev, generator=gb) * 2 - 1
     mesh = bc.make_mesh(world)
@@ -191,28 +185,33 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     _lib.check(lib.bcmg_measure_fp64_peak(local_rank, C.byref(peak)))
 
     def step():
-        A.copy_(A0)
+        regen(A)
         return bc.potrs(A, b, T_A=t, mesh=mesh, overwrite_a=True)
 
-    for _ in range(max(3, args.warmup)):
+    warm = max(3, args.warmup)
+    for _ in range(warm):
         x = step()
-    torch.cuda.synchronize()
-    # accuracy check of the last warm-up solve: ||Ax-b|| / (||A|| ||x|| + ||b||)
-    ax = A0 @ x
+    sync_all()
+
+    # accuracy of the last warm-up solve: ||Ax - b||_F / (||A||_F ||x||_F + ||b||_F) on a fresh A
+    regen(A)
+    ax = torch.empty(rows, nrhs, dtype=torch.float64, device=dev)
+    anorm2 = torch.zeros((), dtype=torch.float64, device=dev)
+    for r0 in range(0, rows, 4096):
+        blk = A[r0:r0 + 4096]
+        torch.matmul(blk, x, out=ax[r0:r0 + 4096])
+        anorm2 += (blk * blk).sum()
     if world > 1:
         full = [torch.empty_like(ax) for _ in range(world)]
         dist.all_gather(full, ax)
         ax = torch.cat(full)
-    anorm2 = (A0.double() ** 2).sum()
-    if world > 1:
         dist.all_reduce(anorm2)
     resid = float((ax - b).norm() / (anorm2.sqrt() * x.norm() + b.norm()))
+    del ax, blk  # blk is a view: it would keep A's storage alive past `del A` below
 
     lib.bcmg_set_profiling(mesh.session, 1)
     launches0 = lib.bcmg_launch_count()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    sync_all()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clocks:
         e0.record()
@@ -220,16 +219,18 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             x = step()
         e1.record()
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    sync_all()
+    # library kernels + the per-step generator launch (bcmg_generate_spd is ours too)
     launches = lib.bcmg_launch_count() - launches0
     ms = e0.elapsed_time(e1)
     lib.bcmg_set_profiling(mesh.session, 0)
     st = (C.c_double * 4)()
     _lib.check(lib.bcmg_kernel_stats(mesh.session, 0, st))
     trail = {"launches": st[0], "ms": st[1], "flops": st[2]}
-    for kind in (1, 2, 3):
+    other = {}
+    for kind, name in ((1, "panel_trsm"), (2, "diag_factor"), (3, "rotate")):
         _lib.check(lib.bcmg_kernel_stats(mesh.session, kind, st))
+        other[name] = {"launches": st[0], "ms": st[1]}
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -237,11 +238,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     flops = potrs_flops(n, nrhs)
     value = flops * args.steps / (ms * 1e-3) / 1e12
 
-    # redistribution GB/s: same shape with 8 virtual devices on this GPU (D=1 is the identity)
+    # redistribution GB/s: the same matrix as 8 virtual devices on this GPU (D=1 itself is the identity)
     redist = None
-    if world == 1:
+    if world == 1 and n % (8 * t) == 0:
         vm = bc.make_mesh(8)
-        A.copy_(A0)
+        regen(A)
         ptrs = _lib.ptr_array([A.data_ptr() + d * (n // 8) * n * 8 for d in range(8)])
         lib.bcmg_set_profiling(vm.session, 1)
         for _ in range(2):
@@ -256,53 +257,58 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                                "frac": rot_gbs / _hbm_peak()}}
         vm.close()
 
-    # e2e through the public call with host buffers
-    e2e = None
-    if world == 1:
-        Ah = torch.empty(rows, n, dtype=torch.float64, pin_memory=True)
-        Ah.copy_(A0)
-        bh = b.cpu().pin_memory()
-        ke = max(1, min(args.steps, 3))
-        bc.potrs(Ah, bh, T_A=t, mesh=mesh).cpu()
-        torch.cuda.synchronize()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record()
-        for _ in range(ke):
-            xh = bc.potrs(Ah, bh, T_A=t, mesh=mesh).cpu()
-        t1.record()
-        torch.cuda.synchronize()
-        ems = t0.elapsed_time(t1)
-        e2e = {"value": flops * ke / (ems * 1e-3) / 1e12, "unit": UNIT,
-               "h2d_bytes_per_step": int(Ah.numel() * 8 + bh.numel() * 8),
-               "d2h_bytes_per_step": int(xh.numel() * 8), "steps": ke,
-               "path": "paper_2601_14466_b200.potrs(A_host_pinned, b_host, T_A, mesh) -> x.cpu()"}
-        del Ah
+    # e2e through the public call with host buffers: A's row block and b in pinned host
+    # memory, x read back; A's device block is released first (the call uploads its own copy)
+    regen(A)
+    Ah = torch.empty(rows, n, dtype=torch.float64, pin_memory=True)
+    Ah.copy_(A)
+    bh = b.cpu().pin_memory()
+    del A  # stays in torch's cache: the call's upload reuses the block
+    sync_all()
+    ke = 1
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(ke):
+        xh = bc.potrs(Ah, bh, T_A=t, mesh=mesh).cpu()
+    t1.record()
+    torch.cuda.synchronize()
+    ems = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+    e2e = {"value": flops * ke / (float(ems) * 1e-3) / 1e12, "unit": UNIT,
+           "h2d_bytes_per_step": int(Ah.numel() * 8 + bh.numel() * 8),
+           "d2h_bytes_per_step": int(xh.numel() * 8), "steps": ke,
+           "path": "paper_2601_14466_b200.potrs(A_row_block_host_pinned, b_host, T_A, mesh) -> x.cpu()"}
+    e2e_ok = bool(torch.allclose(xh, x.cpu(), rtol=0, atol=1e-12))
+    del Ah
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     achieved = trail["flops"] / (trail["ms"] * 1e-3) / 1e12 if trail["ms"] else 0.0
-    prof_traffic = _profile_traffic()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "warmup": warm, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["workload"], "n": n, "tile": t, "n_rhs": nrhs, "logical_devices": world,
                    "parallelism": f"1D block-cyclic columns over {world} GPU(s)",
-                   "l2": "inputs (A: %.1f GB) exceed L2 (126 MB)" % (rows * n * 8 / 1e9),
-                   "step": "restore A (D2D copy, inside the timed region) + redistribute_in + potrf + potrs",
-                   "residual": resid},
-        "roofline": {"bound": "tensor", "kernel": "trail_kernel (DMMA GEMM trailing update)",
+                   "l2": "inputs (A: %.1f GB per GPU) exceed L2 (126 MB)" % (rows * n * 8 / 1e9),
+                   "input": "A = (R+R^T)/2 + N I, R ~ U[-1,1) hashed per unordered (i,j) (bcmg_generate_spd, "
+                            "seed 1); b ~ U[-1,1)",
+                   "step": "regenerate A in place (inside the timed region) + redistribute_in + potrf + potrs",
+                   "residual": resid, "e2e_matches_device_x": e2e_ok},
+        "roofline": {"bound": "tensor", "kernel": "trail_tma_kernel (TMA + DMMA trailing update)",
                      "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                      "frac": achieved / peak.value if peak.value else None,
                      "peak_source": "measured live: bcmg_measure_fp64_peak (register-resident mma.sync.m8n8k4.f64 "
                                     "loop on all SMs); MEASURED_PEAKS.json has no FP64 entry",
-                     "traffic": prof_traffic, "launches": trail["launches"],
+                     "traffic": _profile_traffic(), "launches": trail["launches"],
                      "flops_per_launch": trail["flops"] / max(trail["launches"], 1),
                      "ms_per_launch": trail["ms"] / max(trail["launches"], 1),
-                     "share_of_step": trail["ms"] / ms if ms else None},
+                     "share_of_step": trail["ms"] / ms if ms else None,
+                     "step_fraction_of_peak": value / peak.value if peak.value else None},
+        "kernels": other,
         "clocks": clocks.summary(),
         "gpu_launches": int(launches),
         "e2e": e2e,
@@ -322,7 +328,7 @@ def _hbm_peak() -> float:
 
 
 def _profile_traffic():
-    """dram bytes per trail_kernel launch from the committed ncu --set full capture."""
+    """dram bytes per trail_tma_kernel launch from the committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "trail_kernel_traffic.json")
     try:
         return json.load(open(p))["dram_bytes_per_launch"]
@@ -333,7 +339,7 @@ def _profile_traffic():
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--n", type=int, default=0)

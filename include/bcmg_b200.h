@@ -164,6 +164,14 @@ int64_t bcmg_launch_count(void);
 /* FP64 tensor-core (DMMA) throughput of a register-resident mma.sync loop on
    all SMs, TFLOP/s: the roofline denominator of the FP64 kernels */
 int bcmg_measure_fp64_peak(int cuda_device, double* tflops);
+/* Synthetic input: rows [row0, row0+rows) of the n x n
+   Hermitian positive-definite A = (R + R^H)/2 + shift*I, R ~ U[-1,1)
+   (+ i U[-1,1) for complex dtypes), written row-major: element (row0+r, j)
+   at a[r*lda + j] (device).  Element {i,j} is a hash of (seed, min, max),
+   so row blocks generated on different GPUs form one exact Hermitian A.
+   Stream-ordered on `stream`. */
+int bcmg_generate_spd(void* stream, int dtype, int64_t n, int64_t row0, int64_t rows, void* a, int64_t lda,
+                      uint64_t seed, double shift);
 
 #ifdef __cplusplus
 }

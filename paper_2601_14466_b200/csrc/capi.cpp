@@ -335,6 +335,16 @@ int bcmg_kernel_stats(bcmg_session* s, int kind, double* stats) {
 
 int64_t bcmg_launch_count(void) { return (int64_t)bcmg::launch_count(); }
 
+int bcmg_generate_spd(void* stream, int dtype, int64_t n, int64_t row0, int64_t rows, void* a, int64_t lda,
+                      uint64_t seed, double shift) {
+  return guarded([&] {
+    if (bcmg::dtype_size(dtype) == 0) throw bcmg::Error(BCMG_ERR_CONFIG, "unknown element-type code");
+    if (n < 0 || rows < 0 || row0 < 0 || row0 + rows > n || lda < n)
+      throw bcmg::Error(BCMG_ERR_CONFIG, "bad row block");
+    bcmg::generate_spd(dtype, a, lda, n, row0, rows, seed, shift, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int bcmg_measure_fp64_peak(int cuda_device, double* tflops) {
   return guarded([&] {
     BCMG_CUDA(cudaSetDevice(cuda_device));

@@ -833,6 +833,45 @@ __global__ void __launch_bounds__(512) dmma_peak_kernel(double* out, int iters) 
   if (s == 12345.0) out[threadIdx.x] = s;
 }
 
+// ============================================================== synthetic SPD input
+// A = (R + R^H)/2 + shift*I with R ~ U[-1,1) (+ i U[-1,1) for complex): the
+// value of the unordered pair {i, j} is a splitmix64 hash of (seed, lo, hi),
+// so any row block can be generated independently and A is exactly
+// Hermitian; the diagonal is real.  Row-major row block: element (row0 + r, j)
+// at p[r * ld + j].  (the BASELINE synthetic inputs.)
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double unit_pm1(uint64_t h) { return (double)(h >> 11) * 0x1.0p-52 - 1.0; }
+
+template <class S>
+__global__ void gen_spd_kernel(S* p, int64_t ld, int64_t n, int64_t row0, int64_t rows, uint64_t seed,
+                               double shift) {
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x)
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const int64_t i = row0 + r;
+    const uint64_t lo = (uint64_t)(i < j ? i : j), hi = (uint64_t)(i < j ? j : i);
+    const uint64_t h = mix64(seed ^ mix64(lo * 0x100000001b3ull + hi));
+    double2 v = make_double2(unit_pm1(h), 0.0);
+    if (Traits<S>::cplx) v.y = (i == j) ? 0.0 : (i > j ? 1.0 : -1.0) * unit_pm1(mix64(h));
+    if (i == j) v.x += shift;
+    p[r * ld + j] = from_c<S>(v);
+  }
+}
+
+void generate_spd(int dt, void* p, int64_t ld, int64_t n, int64_t row0, int64_t rows, uint64_t seed, double shift,
+                  cudaStream_t st) {
+  if (rows <= 0 || n <= 0) return;
+  dispatch_dtype(dt, [&](auto s) {
+    using S = decltype(s);
+    gen_spd_kernel<S><<<num_sms() * 8, 256, 0, st>>>(static_cast<S*>(p), ld, n, row0, rows, seed, shift);
+  });
+  BCMG_CHECK_LAUNCH();
+}
+
 double measure_dmma_peak(cudaStream_t st) {
   double* out = nullptr;
   BCMG_CUDA(cudaMalloc(&out, 4096 * sizeof(double)));

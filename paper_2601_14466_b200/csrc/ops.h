@@ -11,6 +11,9 @@ namespace bcmg {
 
 long long launch_count();
 double measure_dmma_peak(cudaStream_t st);  // TFLOP/s
+// Synthetic Hermitian positive-definite row block (see gen_spd_kernel).
+void generate_spd(int dt, void* p, int64_t ld, int64_t n, int64_t row0, int64_t rows, uint64_t seed, double shift,
+                  cudaStream_t st);
 
 // C := alpha*op(A)*op(B) + beta*C, any dtype (dt), any shape; dispatches to
 // the cp.async DMMA kernel when the operands qualify, else the REG kernel.
