@@ -756,8 +756,76 @@ __global__ void __launch_bounds__(256) rotate_kernel(RotateJob j) {
   }
 }
 
+// Bulk-copy rotation (16-byte aligned segments): work item = (cycle, chunk of
+// RB_CH bytes at the same offset in every member).  One thread per CTA drives
+// the copy engine: cp.async.bulk loads of up to RB_G members into shared
+// memory (one mbarrier transaction), then cp.async.bulk stores of each member
+// into its successor.  Cycles longer than RB_G are walked in groups with the
+// last member's chunk carried in a spare slot; every address is read (load
+// completed) before it is written, and items touch disjoint bytes.  Three
+// CTAs per SM keep ~200 KB per SM in flight.
+constexpr int RB_CH = 8192, RB_G = 8;
+constexpr size_t RB_SMEM = (size_t)(RB_G + 1) * RB_CH;
+
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, unsigned src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(src), "r"(bytes)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(32) rotate_bulk_kernel(RotateJob j) {
+  extern __shared__ __align__(128) unsigned char rb_smem[];
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x != 0) return;
+  mbar_init(&bar, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  const unsigned base = smem_u32(rb_smem);
+  unsigned phase = 0;
+  for (int64_t item = blockIdx.x; item < j.total_lanes; item += gridDim.x) {
+    int64_t lo = 0, hi = j.n_cycles;  // chunk prefix: lane_pref[lo] <= item < lane_pref[hi]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(j.lane_pref + mid) <= item) lo = mid; else hi = mid;
+    }
+    const int64_t c = lo;
+    const int64_t off = (item - __ldg(j.lane_pref + c)) * RB_CH;
+    const unsigned len = (unsigned)min((int64_t)RB_CH, __ldg(j.seg_bytes + c) - off);
+    const int64_t b = __ldg(j.offsets + c), m = __ldg(j.offsets + c + 1) - b;
+    auto at = [&](int64_t i) { return reinterpret_cast<char*>(__ldg(j.addr + b + i)) + off; };
+    int carry = -1;  // slot holding old[c_{i0-1}]
+    for (int64_t i0 = 0; i0 < m; i0 += RB_G) {
+      const int g = (int)min((int64_t)RB_G, m - i0);
+      auto slot = [&](int k) { return (carry >= 0 && k >= carry) ? k + 1 : k; };
+      mbar_expect_tx(&bar, (unsigned)g * len);
+      for (int k = 0; k < g; ++k) bulk_g2s(base + slot(k) * RB_CH, at(i0 + k), len, &bar);
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+      if (carry >= 0) bulk_s2g(at(i0), base + carry * RB_CH, len);
+      for (int k = 0; k + 1 < g; ++k) bulk_s2g(at(i0 + k + 1), base + slot(k) * RB_CH, len);
+      carry = slot(g - 1);
+      if (i0 + g == m) bulk_s2g(at(0), base + carry * RB_CH, len);
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // slots reusable
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+int64_t rotate_bulk_chunk() { return RB_CH; }
+
 void rotate_cycles(const RotateJob& j, cudaStream_t st) {
   if (j.total_lanes <= 0) return;
+  if (j.bulk) {
+    set_smem(rotate_bulk_kernel, RB_SMEM);
+    const unsigned grid = (unsigned)std::min<int64_t>(j.total_lanes, (int64_t)num_sms() * 3);
+    rotate_bulk_kernel<<<grid, 32, RB_SMEM, st>>>(j);
+    BCMG_CHECK_LAUNCH();
+    return;
+  }
   const unsigned grid = (unsigned)std::min<int64_t>((j.total_lanes + 255) / 256, (int64_t)num_sms() * 8);
   if (j.vec == 16) rotate_kernel<uint4, 4><<<grid, 256, 0, st>>>(j);
   else if (j.vec == 8) rotate_kernel<uint2, 4><<<grid, 256, 0, st>>>(j);

@@ -75,12 +75,14 @@ std::vector<int64_t> column_counts(int64_t n_cols, int64_t tile, int ndev);
 struct RotateJob {
   const uint64_t* addr;      // device: member addresses, cycles concatenated
   const int64_t* offsets;    // device: CSR, n_cycles + 1
-  const int64_t* lane_pref;  // device: prefix sum of lanes per cycle, n_cycles + 1
+  const int64_t* lane_pref;  // device: prefix sum of lanes (bulk: chunks) per cycle, n_cycles + 1
   const int64_t* seg_bytes;  // device: bytes per segment of each cycle
   int64_t n_cycles, total_lanes;
   int vec;                   // 16, 8 or 4
+  int bulk;                  // 1: cp.async.bulk chunks of rotate_bulk_chunk() bytes (vec == 16)
 };
 void rotate_cycles(const RotateJob& j, cudaStream_t st);
+int64_t rotate_bulk_chunk();
 
 // n independent copies of len bytes: dst[i] + doff <- src[i] + soff (device
 // address tables), vec-byte lanes.

@@ -252,10 +252,14 @@ void Session::redistribute(int dt, int64_t n_rows, int64_t n_cols, int64_t T, in
     int d = (int)(std::upper_bound(off.begin(), off.end(), pos) - off.begin()) - 1;
     addr[i] = reinterpret_cast<uint64_t>(shards[d]) + (uint64_t)((pos - off[d]) * col_bytes);
   }
+  // 16-byte aligned segments go through the bulk-copy engine in chunks
+  const char* lanes_env = getenv("BCMG_ROTATE_LANES");
+  const bool bulk = vec == 16 && !(lanes_env && atoi(lanes_env));
+  const int64_t unit = bulk ? rotate_bulk_chunk() : vec;
   std::vector<int64_t> lane_pref(nc + 1, 0), seg_bytes(nc);
   for (int64_t c = 0; c < nc; ++c) {
     seg_bytes[c] = plan.seg_cols[c] * col_bytes;
-    lane_pref[c + 1] = lane_pref[c] + seg_bytes[c] / vec;
+    lane_pref[c + 1] = lane_pref[c] + (seg_bytes[c] + unit - 1) / unit;
   }
   const size_t bytes = nm * 8 + (nc + 1) * 8 * 2 + nc * 8;
   plan_host.resize(bytes);
@@ -275,6 +279,7 @@ void Session::redistribute(int dt, int64_t n_rows, int64_t n_cols, int64_t T, in
   j.n_cycles = nc;
   j.total_lanes = lane_pref[nc];
   j.vec = vec;
+  j.bulk = bulk ? 1 : 0;
   timed(K_ROTATE, crit, 2.0 * (double)nm * plan.seg * col_bytes, [&] { rotate_cycles(j, crit); });
   // (cudaMemcpyAsync from pageable memory returns once the source is consumed)
   last_moved_bytes = 2 * (int64_t)nm * plan.seg * col_bytes;
