@@ -96,14 +96,18 @@ int bcmg_invert_cycles(int64_t n_cycles, const int64_t* offsets, int64_t* member
 int bcmg_segment_plan_info(int64_t n_cols, int64_t tile, int ndev, int64_t* seg_width, int64_t* n_cycles,
                            int64_t* moved_columns);
 
-/* Per-process operation schedule of potrf (routine 0) or potrs (routine 1)
-   for `world` processes holding ndev logical devices -- exactly the sequence
-   the drivers execute.  Each op is 7 int64: {kind, stream, k, a, b, root,
-   elems}; kinds: 1 factor tile k, 2 broadcast panel k (root process, elems),
-   3 trailing update with panel k of tiles [a, b), 4 copy panel k back,
-   5 end of step k, 6 forward step k, 7 backward step k, 8 broadcast solution
-   rows [a, b) (root, elems); streams: 0 crit, 1 bulk, 2 comm.  Host only.
-   Pass ops = NULL to query *count. */
+/* Per-process operation schedule of potrf (routine 0), potrs (routine 1) or
+   potri (routine 2) for `world` processes holding ndev logical devices --
+   exactly the sequence the drivers execute.  Each op is 7 int64: {kind,
+   stream, k, a, b, root, elems}; kinds: 1 factor tile k, 2 broadcast panel k
+   (root process, elems), 3 trailing update with panel k of tiles [a, b),
+   4 copy panel k back, 5 end of step k, 6 forward step k, 7 backward step k,
+   8 broadcast solution rows [a, b) (root, elems); potri: 9 finalise W_k
+   (owner), 10 broadcast tile k rows [start_k, n) (root, elems), 11 add
+   W_k's contribution to the local tiles < k, 12 product blocks (k, j <= k)
+   of the local tiles, 13 gather those blocks on the owner of k (root; elems
+   this process sends) and mirror them into tile k; streams: 0 crit, 1 bulk,
+   2 comm.  Host only.  Pass ops = NULL to query *count. */
 int bcmg_schedule(int routine, int64_t n, int64_t tile, int ndev, int world, int rank, int64_t nrhs, int64_t* ops,
                   int64_t cap, int64_t* count);
 

@@ -136,6 +136,7 @@ int bcmg_schedule(int routine, int64_t n, int64_t tile, int ndev, int world, int
     std::vector<bcmg::SchedOp> v;
     if (routine == 0) v = bcmg::potrf_schedule(n, tile, ndev, world, rank);
     else if (routine == 1) v = bcmg::potrs_schedule(n, tile, ndev, world, rank, nrhs);
+    else if (routine == 2) v = bcmg::potri_schedule(n, tile, ndev, world, rank);
     else throw bcmg::Error(BCMG_ERR_CONFIG, "unknown routine");
     *count = (int64_t)v.size();
     if (ops) {

@@ -664,6 +664,40 @@ void conj_transpose(int dt, const void* src, int64_t lds, void* dst, int64_t ldd
   BCMG_CHECK_LAUNCH();
 }
 
+// Mirror scatter of potri's product blocks: src (rows x cols, lds) holds
+// columns of logical device d's shard (local column c = global column
+// ((c / T) * D + d) * T + c % T); dst(global column of c, i) = conj(src(i, c)).
+template <class S>
+__global__ void ct_scatter_kernel(const S* __restrict__ src, int64_t lds, int64_t rows, int64_t cols, S* dst,
+                                  int64_t ldd, int64_t T, int D, int d) {
+  __shared__ double2 t[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t i = i0 + threadIdx.x, c = c0 + y;
+    if (i < rows && c < cols) t[y][threadIdx.x] = to_c(src[i + c * lds]);
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t c = c0 + threadIdx.x, i = i0 + y;
+    if (i < rows && c < cols) {
+      const int64_t g = ((c / T) * D + d) * T + c % T;
+      dst[g + i * ldd] = from_c<S>(cconj(t[threadIdx.x][y]));
+    }
+  }
+}
+
+void ct_scatter(int dt, const void* src, int64_t lds, int64_t rows, int64_t cols, void* dst, int64_t ldd, int64_t T,
+                int D, int d, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32)), block(32, 8);
+  dispatch_dtype(dt, [&](auto s) {
+    using S = decltype(s);
+    ct_scatter_kernel<S><<<grid, block, 0, st>>>(static_cast<const S*>(src), lds, rows, cols, static_cast<S*>(dst),
+                                                 ldd, T, D, d);
+  });
+  BCMG_CHECK_LAUNCH();
+}
+
 template <class S>
 __global__ void realify_diag_kernel(S* a, int64_t lda, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {

@@ -48,6 +48,9 @@ void zero_upper(int dt, void* a, int64_t lda, int64_t rows, int64_t cols, int64_
 // Mirror: a(r, c) = conj(src(c, r)) for the block; diagonal forced real when diag.
 void conj_transpose(int dt, const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
                     cudaStream_t st);
+// potri mirror: dst(global column of local column c of device d, i) = conj(src(i, c))
+void ct_scatter(int dt, const void* src, int64_t lds, int64_t rows, int64_t cols, void* dst, int64_t ldd, int64_t T,
+                int D, int d, cudaStream_t st);
 void realify_diag(int dt, void* a, int64_t lda, int64_t n, cudaStream_t st);
 void mirror_diag(int dt, void* a, int64_t lda, int64_t n, cudaStream_t st);
 

@@ -664,60 +664,167 @@ void Session::potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* 
 }
 
 // ------------------------------------------------------------------ potri
-// In place on the cyclic shards (solvers.py:487-594):
-//   W sweep (last tile first):  acc = sum_{s>k} tril(W_s)[stop:] L21[s rows];
-//                               W21 = -acc X_kk;  W_kk = X_kk
-//   product sweep (first tile first): tile j <- sum_{s>=j} tril(W_s)^H tril(W_j)
-//   mirror: upper := conj-transpose of lower, diagonal exactly real.
+// In place on the cyclic shards, restructured so that every W tile crosses
+// the processes exactly once per sweep (the reference fetches W_s once per
+// (k, s) pair, solvers.py:513-571):
+//
+//   W sweep (s = nt-1 .. 0), W = L^-1:
+//     WFINAL(s)  owner: W21_s = -acc_s X_ss (acc_s accumulated in tile s rows
+//                [stop_s, n) -- those rows of L21_s are dead by then); W_ss = X_ss
+//     BCAST(s)   W_s rows [start_s, n) to every process
+//     WACC(s)    every process, for all its tiles k < s at once (contiguous
+//                local columns): acc_k[start_s:] += W_s L21_k[start_s:stop_s]
+//                (the L21 rows are staged first: acc and L21 share storage)
+//   product sweep (s = 0 .. nt-1), A^-1 = W^H W:
+//     BCAST(s)   W_s rows [start_s, n)
+//     PGEMM(s)   every process: block (s, j) = W_s^H W_j[start_s:] for all its
+//                tiles j <= s in one GEMM; written to tile j rows [start_s, stop_s)
+//     PGATHER(s) blocks gathered on the owner of s and mirrored (conjugate
+//                transpose) into tile s rows [start_j, stop_j); diagonal block
+//                made exactly Hermitian with a real diagonal (solvers.py:577-583)
+//
+// acc_k receives W_s in descending s on every process and each product block
+// is one GEMM, so the bits do not depend on the device or process count.
+static int64_t cols_below(const Geo& g, int d, int64_t s) {  // local columns of device d's tiles < s
+  return s > d ? ((s - d + g.D - 1) / g.D) * g.T : 0;
+}
+static int64_t cols_upto(const Geo& g, int d, int64_t s) {  // ... tiles <= s
+  return cols_below(g, d, s) + (s % g.D == d ? g.stop(s) - g.start(s) : 0);
+}
+
+std::vector<SchedOp> potri_schedule(int64_t n, int64_t T, int ndev, int world, int rank) {
+  const Geo g = geo_only(n, T, ndev, world, rank);
+  std::vector<SchedOp> ops;
+  auto tile_elems = [&](int64_t s) { return (n - g.start(s)) * (g.stop(s) - g.start(s)); };
+  for (int64_t s = g.nt - 1; s >= 0; --s) {
+    if (g.owns(s)) ops.push_back(SchedOp{S_WFINAL, STREAM_CRIT, s, 0, 0, 0, 0});
+    if (s == 0) break;  // nothing below tile 0 accumulates
+    ops.push_back(SchedOp{S_TILE_BCAST, STREAM_CRIT, s, 0, 0, g.owner_rank(s), tile_elems(s)});
+    ops.push_back(SchedOp{S_WACC, STREAM_CRIT, s, 0, 0, 0, 0});
+  }
+  for (int64_t s = 0; s < g.nt; ++s) {
+    const int64_t tcs = g.stop(s) - g.start(s);
+    int64_t mine = 0;
+    for (int d = g.dev0; d < g.dev0 + g.nloc; ++d) mine += cols_upto(g, d, s);
+    ops.push_back(SchedOp{S_TILE_BCAST, STREAM_CRIT, s, 0, 0, g.owner_rank(s), tile_elems(s)});
+    ops.push_back(SchedOp{S_PGEMM, STREAM_CRIT, s, 0, 0, 0, 0});
+    ops.push_back(SchedOp{S_PGATHER, STREAM_CRIT, s, 0, 0, g.owner_rank(s), tcs * mine});
+  }
+  return ops;
+}
+
 void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards) {
   const Geo g = make_geo(*this, dt, n, T, ndev);
-  if (world > 1) throw Error(CONFIG, "multi-process potri is not implemented in this build");
   if (last_dinv_T != T || dinv.bytes < (size_t)g.nt * T * T * g.esz)
     throw Error(CONFIG, "potri needs a potrf of the same tiling in this session");
-  acc.ensure((size_t)n * T * g.esz);
-  char* accp = static_cast<char*>(acc.p);
+  const size_t nt_bytes = (size_t)n * T * g.esz;
+  panel[0].ensure(nt_bytes);  // broadcast W tile
+  panel[1].ensure(nt_bytes);  // staged L21 rows / finalisation product
+  acc.ensure(nt_bytes);       // product blocks of every device (gather buffer)
   cudaStream_t st = crit;
-  auto sh = [&](int64_t k) { return shards[(k % g.D) - g.dev0]; };
+  char* pan = static_cast<char*>(panel[0].p);
+  char* stage = static_cast<char*>(panel[1].p);
+  char* blocks = static_cast<char*>(acc.p);
+  auto shard_of = [&](int64_t k) { return shards[(k % g.D) - g.dev0]; };
   auto dinv_k = [&](int64_t k) { return static_cast<char*>(dinv.p) + (size_t)k * T * T * g.esz; };
-  for (int64_t k = g.nt - 1; k >= 0; --k) {
-    const int64_t s0 = g.start(k), s1 = g.stop(k), tc = s1 - s0;
-    if (s1 < n) {
-      const int64_t lda = n - s1;
-      for (int64_t s = k + 1; s < g.nt; ++s) {
-        const int64_t ss = g.start(s), tcs = g.stop(s) - ss;
-        Operand Ws = opA(colp(sh(s), g, ss, g.loc(s)), n, OP_N);
-        Ws.mask = 1;  // tril in global coordinates: row ss+i >= col ss+kk
-        gemm(dt, n - ss, tc, tcs, Ws, opB(colp(sh(k), g, ss, g.loc(k)), n, OP_N),
-             Epilogue{accp + (ss - s1) * g.esz, lda, 1.0, s == k + 1 ? 0.0 : 1.0, 0, 0}, nullptr, st);
-      }
-      gemm(dt, n - s1, tc, tc, opA(accp, lda, OP_N), opB(dinv_k(k), T, OP_N),
-           Epilogue{colp(sh(k), g, s1, g.loc(k)), n, -1.0, 0.0, 0, 0}, nullptr, st);
+  // W_s rows [start_s, n): the owner's tile itself in one process, else the broadcast copy
+  auto w_of = [&](int64_t s, int64_t* ld) -> const void* {
+    if (world == 1) {
+      *ld = n;
+      return colp(shard_of(s), g, g.start(s), g.loc(s));
     }
-    copy2d(dt, dinv_k(k), T, colp(sh(k), g, s0, g.loc(k)), n, tc, tc, false, nullptr, st);
-  }
-  for (int64_t j = 0; j < g.nt; ++j) {
-    const int64_t js = g.start(j), tcj = g.stop(j) - js, lda = n - js;
-    for (int64_t s = j; s < g.nt; ++s) {
-      const int64_t ss = g.start(s), tcs = g.stop(s) - ss;
-      Operand Ws = opA(colp(sh(s), g, ss, g.loc(s)), n, OP_C);
-      Ws.mask = 1;  // storage row ss+kk >= storage col ss+i
-      Operand Wj = opB(colp(sh(j), g, ss, g.loc(j)), n, OP_N);
-      Wj.mask = 1;
-      Wj.mask_off = ss - js;  // storage row ss+kk >= col js+nn
-      gemm(dt, tcs, tcj, n - ss, Ws, Wj, Epilogue{accp + (ss - js) * g.esz, lda, 1.0, 0.0, 0, 0}, nullptr, st);
-    }
-    copy2d(dt, accp, lda, colp(sh(j), g, js, g.loc(j)), n, n - js, tcj, false, nullptr, st);
-    zero_upper(dt, colp(sh(j), g, 0, g.loc(j)), n, js, tcj, js + 1, st);  // rows above the tile: 0
-  }
-  for (int64_t j = 0; j < g.nt; ++j) {
-    const int64_t js = g.start(j), tcj = g.stop(j) - js;
-    for (int64_t i = j; i < g.nt; ++i) {
-      const int64_t is = g.start(i), tci = g.stop(i) - is;
-      if (i == j) {
-        mirror_diag(dt, colp(sh(j), g, js, g.loc(j)), n, tcj, st);
-      } else {
-        conj_transpose(dt, colp(sh(j), g, is, g.loc(j)), n, colp(sh(i), g, js, g.loc(i)), n, tcj, tci, st);
+    *ld = n - g.start(s);
+    return pan;
+  };
+  // offset (elements) of device d's product block in the gather buffer
+  auto block_off = [&](int64_t s, int d) {
+    int64_t o = 0;
+    for (int e = 0; e < d; ++e) o += cols_upto(g, e, s);
+    return o * (g.stop(s) - g.start(s));
+  };
+  auto comm_ = static_cast<ncclComm_t>(nccl);
+  for (const SchedOp& op : potri_schedule(n, T, ndev, world, rank)) {
+    const int64_t s = op.k, ss = g.start(s), se = g.stop(s), tcs = se - ss;
+    switch (op.kind) {
+      case S_WFINAL: {
+        char* Ws = colp(shard_of(s), g, 0, g.loc(s));
+        if (se < n) {  // W21 = -acc X_ss, through the staging buffer (in place otherwise)
+          gemm(dt, n - se, tcs, tcs, opA(Ws + se * g.esz, n, OP_N), opB(dinv_k(s), T, OP_N),
+               Epilogue{stage, n - se, -1.0, 0.0, 0, 0}, nullptr, st);
+          copy2d(dt, stage, n - se, Ws + se * g.esz, n, n - se, tcs, false, nullptr, st);
+        }
+        copy2d(dt, dinv_k(s), T, Ws + ss * g.esz, n, tcs, tcs, false, nullptr, st);
+        break;
       }
+      case S_TILE_BCAST:
+        if (world == 1) break;
+        if (rank == op.root) copy2d(dt, colp(shard_of(s), g, ss, g.loc(s)), n, pan, n - ss, n - ss, tcs, false,
+                                    nullptr, st);
+        bcast(pan, (size_t)op.elems * g.esz, (int)op.root, st);
+        break;
+      case S_WACC: {
+        int64_t ldw = 0;
+        const void* W = w_of(s, &ldw);
+        for (int d = g.dev0; d < g.dev0 + g.nloc; ++d) {
+          const int64_t c = cols_below(g, d, s);
+          if (c == 0) continue;
+          char* sh = colp(shards[d - g.dev0], g, ss, 0);
+          // L21_k rows [ss, se) of all k < s, staged as (L21 rows)^H (c x tcs) so that the
+          // GEMM's B operand is in natural orientation (TMA-eligible)
+          conj_transpose(dt, sh, n, stage, c, c, tcs, st);
+          BCMG_CUDA(cudaMemset2DAsync(sh, n * g.esz, 0, tcs * g.esz, c, st));  // first touch of acc rows [ss, se)
+          gemm(dt, n - ss, c, tcs, opA(W, ldw, OP_N), opB(stage, c, OP_C), Epilogue{sh, n, 1.0, 1.0, 0, 0},
+               nullptr, st);
+        }
+        break;
+      }
+      case S_PGEMM: {
+        int64_t ldw = 0;
+        const void* W = w_of(s, &ldw);
+        for (int d = g.dev0; d < g.dev0 + g.nloc; ++d) {
+          const int64_t c = cols_upto(g, d, s);
+          if (c == 0) continue;
+          gemm(dt, tcs, c, n - ss, opA(W, ldw, OP_C), opB(colp(shards[d - g.dev0], g, ss, 0), n, OP_N),
+               Epilogue{blocks + block_off(s, d) * g.esz, tcs, 1.0, 0.0, 0, 0}, nullptr, st);
+        }
+        // written back only after every GEMM: with one process W_s is read from tile s itself
+        for (int d = g.dev0; d < g.dev0 + g.nloc; ++d) {
+          const int64_t c = cols_upto(g, d, s);
+          if (c) copy2d(dt, blocks + block_off(s, d) * g.esz, tcs, colp(shards[d - g.dev0], g, ss, 0), n, tcs, c,
+                        false, nullptr, st);
+        }
+        break;
+      }
+      case S_PGATHER: {
+        const int root = (int)op.root;
+        if (world > 1) {
+          const size_t off = (size_t)block_off(s, g.dev0) * g.esz;
+          BCMG_NCCL(ncclGroupStart());
+          if (rank != root) {
+            if (op.elems) BCMG_NCCL(ncclSend(blocks + off, (size_t)op.elems * g.esz, ncclUint8, root, comm_, st));
+          } else {
+            for (int r = 0; r < world; ++r) {
+              if (r == root) continue;
+              const int d0 = r * g.nloc;
+              const size_t bytes = (size_t)(block_off(s, d0 + g.nloc) - block_off(s, d0)) * g.esz;
+              if (bytes)
+                BCMG_NCCL(ncclRecv(blocks + (size_t)block_off(s, d0) * g.esz, bytes, ncclUint8, r, comm_, st));
+            }
+          }
+          BCMG_NCCL(ncclGroupEnd());
+        }
+        if (rank != root) break;
+        // mirror: tile s rows [start_j, stop_j) = (block (s, j))^H for every j < s, any device
+        char* Ts = colp(shard_of(s), g, 0, g.loc(s));
+        for (int d = 0; d < g.D; ++d) {
+          const int64_t c = cols_below(g, d, s);
+          if (c) ct_scatter(dt, blocks + block_off(s, d) * g.esz, tcs, tcs, c, Ts, n, T, g.D, d, st);
+        }
+        mirror_diag(dt, Ts + ss * g.esz, n, tcs, st);
+        break;
+      }
+      default:
+        throw Error(CONFIG, "bad potri schedule op");
     }
   }
   sync_streams(user, crit);

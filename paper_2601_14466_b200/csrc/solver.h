@@ -20,16 +20,20 @@ struct DevBuf {
 
 // One operation of a process's potrf / potrs schedule (solver.cu).
 enum SchedKind : int { S_FACTOR = 1, S_BCAST = 2, S_UPDATE = 3, S_COPYBACK = 4, S_STEP_END = 5, S_FWD = 6,
-                       S_BWD = 7, S_SHARE = 8 };
+                       S_BWD = 7, S_SHARE = 8,
+                       // potri
+                       S_WFINAL = 9, S_TILE_BCAST = 10, S_WACC = 11, S_PGEMM = 12, S_PGATHER = 13 };
 enum SchedStream : int { STREAM_CRIT = 0, STREAM_BULK = 1, STREAM_COMM = 2 };
 struct SchedOp {
   int64_t kind, stream, k;
   int64_t a, b;      // S_UPDATE: tile range [a, b); S_SHARE: row range [a, b); S_STEP_END: a = lookahead flag
-  int64_t root;      // S_BCAST / S_SHARE: source process; S_UPDATE (bulk): 1 = grid capped
-  int64_t elems;     // S_BCAST / S_SHARE: elements moved
+  int64_t root;      // S_BCAST / S_SHARE / S_TILE_BCAST / S_PGATHER: source (gather: destination) process;
+                     // S_UPDATE (bulk): 1 = grid capped
+  int64_t elems;     // S_BCAST / S_SHARE / S_TILE_BCAST: elements moved; S_PGATHER: elements this process sends
 };
 std::vector<SchedOp> potrf_schedule(int64_t n, int64_t T, int ndev, int world, int rank);
 std::vector<SchedOp> potrs_schedule(int64_t n, int64_t T, int ndev, int world, int rank, int64_t nrhs);
+std::vector<SchedOp> potri_schedule(int64_t n, int64_t T, int ndev, int world, int rank);
 
 // Cross-process redistribution: every segment move of the cycle plan
 // (cycles in order, c_i -> c_{i+1} within a cycle) with the processes that

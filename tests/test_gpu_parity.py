@@ -201,6 +201,23 @@ def test_device_count_bit_exact(meshes):
     for d in (2, 4):
         inv, _ = bc.invert_positive_definite(meshes(d), a, bc.TileSpec(16))
         assert np.array_equal(inv, base), d
+    a = O.make_matrix("random_spd", 200, np.complex128, 13)
+    base, _ = bc.invert_positive_definite(meshes(1), a, bc.TileSpec(24))
+    for d in (3, 4):
+        inv, _ = bc.invert_positive_definite(meshes(d), a, bc.TileSpec(24))
+        assert np.array_equal(inv, base), d
+
+
+def test_potri_large_device_count_bit_exact(meshes):
+    """potri at a size where the W-sweep GEMMs take the TMA kernel on one
+    device and the cp.async kernels on two: same bits, inverse within tolerance."""
+    n, t = 4096, 512
+    a = O.make_matrix("random_spd", n, np.float64, 3)
+    base, _ = bc.invert_positive_definite(meshes(1), a, bc.TileSpec(t))
+    assert np.array_equal(base, base.T)
+    assert O.inverse_residual(a, base) <= 100 * n * O.eps_of(np.float64)
+    inv, _ = bc.invert_positive_definite(meshes(2), a, bc.TileSpec(t))
+    assert np.array_equal(inv, base)
 
 
 def test_paper_benchmark_fixture(meshes):

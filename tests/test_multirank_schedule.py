@@ -1,7 +1,7 @@
 """CPU, world_size 2 (gloo): the multi-process logic of the native drivers.
 
 `bcmg_schedule` returns exactly the per-process operation sequence the CUDA
-drivers execute (solver.cu potrf_schedule / potrs_schedule).  Here each rank
+drivers execute (solver.cu potrf/potrs/potri_schedule).  Here each rank
 executes its own sequence with numpy on its logical devices' shards and real
 `torch.distributed` broadcasts (gloo) in place of NCCL, and the result must
 equal the oracle: this checks tile ownership, broadcast roots / sizes / order
@@ -21,6 +21,7 @@ from paper_2601_14466_b200 import _lib  # noqa: E402
 from oracle import bcmg_oracle as O  # noqa: E402
 
 S_FACTOR, S_BCAST, S_UPDATE, S_COPYBACK, S_STEP_END, S_FWD, S_BWD, S_SHARE = range(1, 9)
+S_WFINAL, S_TILE_BCAST, S_WACC, S_PGEMM, S_PGATHER = range(9, 14)
 
 
 def schedule(routine, n, t, ndev, world, rank, nrhs=1):
@@ -160,6 +161,69 @@ def _rank_main(rank, world, port, n, t, ndev, nrhs, dtype, out):
         xr = O.solve_unblocked(a, b)
         err = float(np.abs(x - xr).max())
         out[rank] = err
+
+        # potri on the factored tiles (solver.cu potri_schedule): W sweep, product sweep, mirror
+        def cols_below(d, s):
+            return ((s - d + ndev - 1) // ndev) * t if s > d else 0
+
+        def cols_upto(d, s):
+            return cols_below(d, s) + (min(n, (s + 1) * t) - s * t if s % ndev == d else 0)
+
+        pan = np.zeros(n * t, dtype=dtype)
+        W = None
+        for kind, _, s, lo, hi, root, elems in schedule(2, n, t, ndev, world, rank):
+            ss, se = s * t, min(n, (s + 1) * t)
+            tcs = se - ss
+            if kind == S_WFINAL:
+                assert owns(s)
+                T_ = tile(s)
+                if se < n:
+                    T_[se:, :] = -(T_[se:, :] @ xinv[s])
+                T_[ss:se, :] = xinv[s]
+            elif kind == S_TILE_BCAST:
+                assert elems == (n - ss) * tcs and root == (s % ndev) // nloc
+                if owns(s):
+                    pan[:elems] = np.asfortranarray(tile(s)[ss:, :]).ravel(order="F")
+                bcast(pan, elems, root)
+                W = pan[:elems].reshape((n - ss, tcs), order="F").copy()
+            elif kind == S_WACC:
+                for d in shards:
+                    c = cols_below(d, s)
+                    if c:
+                        stage = shards[d][ss:se, :c].copy()
+                        shards[d][ss:se, :c] = 0
+                        shards[d][ss:, :c] += W @ stage
+            elif kind == S_PGEMM:
+                blocks = {}
+                for d in shards:
+                    c = cols_upto(d, s)
+                    if c:
+                        blocks[d] = W.conj().T @ shards[d][ss:, :c]
+                for d, blk in blocks.items():
+                    shards[d][ss:se, :blk.shape[1]] = blk
+            elif kind == S_PGATHER:
+                assert elems == tcs * sum(cols_upto(d, s) for d in shards)
+                flat = np.concatenate([blocks[d].ravel(order="F") for d in sorted(blocks)] or
+                                      [np.zeros(0, dtype=dtype)])
+                assert flat.size == elems
+                gathered = [None] * world
+                dist.all_gather_object(gathered, {d: blocks[d] for d in blocks})  # stands in for send/recv
+                if rank == root:
+                    T_ = tile(s)
+                    for part in gathered:
+                        for d, blk in part.items():
+                            for cl in range(cols_below(d, s)):
+                                T_[((cl // t) * ndev + d) * t + cl % t, :] = blk[:, cl].conj()
+                    B = T_[ss:se, :].copy()
+                    T_[ss:se, :] = np.tril(B, -1) + np.triu(B.conj().T, 1)
+                    T_[np.arange(ss, se), np.arange(tcs)] = B.diagonal().real
+        inv_ref = np.linalg.inv(a)
+        inv_err = 0.0
+        for k in range(nt):
+            if owns(k):
+                s0, s1 = k * t, min(n, (k + 1) * t)
+                inv_err = max(inv_err, float(np.abs(tile(k) - inv_ref[:, s0:s1]).max()))
+        out[(rank, "inv")] = inv_err / float(np.abs(inv_ref).max())
     finally:
         dist.destroy_process_group()
 
@@ -180,6 +244,7 @@ def test_two_rank_gloo_execution_matches_oracle(n, t, ndev, nrhs, dtype):
         assert p.exitcode == 0, "rank failed or deadlocked"
     for r in range(2):
         assert out[r] <= 1e3 * n * O.eps_of(dtype), out[r]
+        assert out[(r, "inv")] <= 1e3 * n * O.eps_of(dtype), out[(r, "inv")]
 
 
 # ----------------------------------------------------------------- cross-process redistribution
