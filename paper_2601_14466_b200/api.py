@@ -121,7 +121,9 @@ def potrs(A, b, T_A: int, mesh: DeviceMesh | None = None, in_specs=None, *, over
         raise DescriptorError("dimension-mismatch", f"right-hand side shape {tuple(b.shape)} does not match n={n}")
     nrhs = int(b2.shape[1])
     # column-major RHS on the device (n x nrhs, ld n)
-    x = b2.to(device=mesh.torch_device, dtype=et.torch_dtype).t().contiguous()
+    # a fresh buffer: b2.t().contiguous() would alias the caller's b when N_RHS == 1
+    x = torch.empty((nrhs, n), dtype=et.torch_dtype, device=mesh.torch_device)
+    x.copy_(b2.t())
     info = C.c_int(0)
     with mesh.coordinated():
         rc = _lib.load().bcmg_potrs(mesh.session, mesh.stream_handle(), et.code, n, nrhs, int(T_A), mesh.num_devices,

@@ -296,6 +296,22 @@ def test_dropin_potrs_row_sharded(meshes, dtype):
     assert np.array_equal(A.cpu().numpy(), np.ascontiguousarray(a)), "caller's A must be untouched"
 
 
+@pytest.mark.parametrize("shape", [(256, 1), (256,)])
+def test_dropin_potrs_leaves_b_untouched(meshes, shape):
+    """Caller inputs are never mutated (reference SPEC.md:556), including a
+    single right-hand side already on the device in the solve dtype."""
+    import torch
+
+    n = shape[0]
+    a = O.make_matrix("random_spd", n, np.float64, 9)
+    b = torch.ones(shape, dtype=torch.float64, device="cuda")
+    x = bc.potrs(torch.from_numpy(np.ascontiguousarray(a)).cuda(), b, T_A=32, mesh=meshes(2))
+    assert torch.equal(b, torch.ones_like(b))
+    assert x.shape == b.shape and x.data_ptr() != b.data_ptr()
+    xr = O.solve_unblocked(a, np.ones((n, 1)))
+    assert np.abs(x.cpu().numpy().reshape(n, 1) - xr).max() <= 10 * n * O.eps_of(np.float64)
+
+
 def test_dropin_potri_row_sharded(meshes):
     import torch
 
