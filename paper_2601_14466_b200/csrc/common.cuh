@@ -57,11 +57,12 @@ struct Error : std::runtime_error {
 
 // Every kernel launch of the library goes through BCMG_CHECK_LAUNCH, which
 // also counts it (bcmg_launch_count(): evidence that the native path ran).
-void note_launch();
-#define BCMG_CHECK_LAUNCH()            \
-  do {                                 \
-    BCMG_CUDA(cudaGetLastError());     \
-    ::bcmg::note_launch();             \
+// BCMG_DEBUG_SYNC=1 synchronises after every launch and names the failing one.
+void note_launch(const char* file, int line);
+#define BCMG_CHECK_LAUNCH()                      \
+  do {                                           \
+    BCMG_CUDA(cudaGetLastError());               \
+    ::bcmg::note_launch(__FILE__, __LINE__);     \
   } while (0)
 
 // ---------------------------------------------------------------- storage traits

@@ -415,6 +415,11 @@ __global__ void __launch_bounds__(TL::THREADS) gemm_splitk_kernel(Operand A, Ope
 constexpr int MAX_LOCAL_DEV = 16;
 struct TrailParams {
   const void* P;      // panel, element (r, c) at P[r + c*ldp], r = global row - prow0
+  // complex128 through the real FP64 TMA kernel (cplx = 1): P holds [P | -iP]
+  // (ld = ldp = panel rows) and PB the planar [Re P | Im P] (real, ld ldp);
+  // the update is then one real GEMM with interleaved re/im output rows
+  const void* PB;
+  int cplx;
   int64_t ldp, prow0;
   int64_t N, T, K;    // matrix order, tile width, panel width
   int D, dev0, nloc;  // logical devices; this launch owns dev0 .. dev0+nloc-1

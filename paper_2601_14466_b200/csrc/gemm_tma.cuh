@@ -214,6 +214,9 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
     trail_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TrailParams p,
                      const int* info) {
   using TZ = Trap<TL::BM, TL::BN>;
+  // complex embedding: real rows 2r, 2r+1 = re, im of complex row r, so a block
+  // of BM real rows covers BM/2 complex rows of the lower trapezoid
+  using TZC = Trap<(TL::BM / 2 >= TL::BN ? TL::BM / 2 : TL::BN), TL::BN>;
   if (ld_flag(info)) return;
   // tile cursor: items only grow for a given caller, so the walk over tiles is
   // amortised O(1); producer and consumer each own one
@@ -227,8 +230,8 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
       const bool local = dev >= p.dev0 && dev < p.dev0 + p.nloc;
       if (local) {
         if (cur.cnt < 0) {
-          const int64_t ms = cur.m * p.T;
-          cur.cnt = TZ::count(p.N - ms, (p.T < p.N - ms ? p.T : p.N - ms));
+          const int64_t ms = cur.m * p.T, tcm = p.T < p.N - ms ? p.T : p.N - ms;
+          cur.cnt = p.cplx ? TZC::count(p.N - ms, tcm) : TZ::count(p.N - ms, tcm);
         }
         if (item < cur.base + cur.cnt) break;
         cur.base += cur.cnt;
@@ -238,10 +241,21 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
     }
     const int64_t m = cur.m, ms = m * p.T, rows = p.N - ms, tc = p.T < rows ? p.T : rows;
     int64_t rb, cbk;
-    TZ::decode(item - cur.base, tc, rb, cbk);
     const int dev = (int)(m % p.D);
     double* shard = reinterpret_cast<double*>(p.shards[dev - p.dev0]);
     const int64_t loc = (m / p.D) * p.T;
+    if (p.cplx) {
+      TZC::decode(item - cur.base, tc, rb, cbk);
+      blk.a_row = (int)(2 * (ms - p.prow0));
+      blk.b_row = (int)(ms - p.prow0);
+      blk.m0 = rb * TL::BM;
+      blk.n0 = cbk * TL::BN;
+      blk.M = 2 * rows;
+      blk.N = tc;
+      blk.ep = Epilogue{shard + 2 * (ms + loc * p.N), 2 * p.N, -1.0, 1.0, 0, 0};
+      return true;
+    }
+    TZ::decode(item - cur.base, tc, rb, cbk);
     blk.a_row = (int)(ms - p.prow0);
     blk.b_row = (int)(ms - p.prow0);
     blk.m0 = rb * TL::BM;
@@ -256,7 +270,7 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
   if (threadIdx.x == 0) cp = Cursor{p.m_first, 0, -1};
   Cursor cc{p.m_first, 0, -1};
   tma_gemm_loop<TL>(
-      &mapA, &mapB, (int)p.K, [&](int64_t item, TmaBlock& blk) { return decode(cp, item, blk); },
+      &mapA, &mapB, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, TmaBlock& blk) { return decode(cp, item, blk); },
       [&](int64_t item, TmaBlock& blk) { return decode(cc, item, blk); }, p.stagger_ns);
 }
 

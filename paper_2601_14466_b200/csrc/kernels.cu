@@ -17,7 +17,19 @@
 namespace bcmg {
 
 static std::atomic<long long> g_launches{0};
-void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void note_launch(const char* file, int line) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  static const bool debug = [] {
+    const char* e = getenv("BCMG_DEBUG_SYNC");
+    return e && atoi(e);
+  }();
+  if (debug) {
+    const cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess)
+      throw Error(CUDA, std::string("kernel launched at ") + file + ":" + std::to_string(line) + ": " +
+                            cudaGetErrorString(e));
+  }
+}
 long long launch_count() { return g_launches.load(); }
 
 // ============================================================== GEMM dispatch
@@ -74,6 +86,7 @@ static void launch_gemm(int64_t M, int64_t N, int64_t K, const Operand& A, const
 }
 
 static bool use_tma();
+static unsigned ew_grid(int64_t total);
 static bool use_tc();
 static bool tc_ok(const void* p, int64_t ld);
 static void launch_tc3_gemm(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
@@ -225,16 +238,22 @@ using TileTrail2 = Tile<128, 64, 32, 32, 32, 2, true>;
 
 template <class TL>
 static void launch_trail_tma_t(const TrailParams& p, const int* info, cudaStream_t st) {
+  static_assert(TL::BM / 2 >= TL::BN || !std::is_same_v<TL, TileTrail2>, "complex embedding needs BM/2 >= BN");
+  using TZC = Trap<(TL::BM / 2 >= TL::BN ? TL::BM / 2 : TL::BN), TL::BN>;
   int64_t total = 0;
   for (int64_t m = p.m_first; m < p.m_last; ++m) {
     const int dev = (int)(m % p.D);
     if (dev < p.dev0 || dev >= p.dev0 + p.nloc) continue;
     const int64_t rows = p.N - m * p.T, tc = std::min(p.T, rows);
-    total += Trap<TL::BM, TL::BN>::count(rows, tc);
+    total += p.cplx ? TZC::count(rows, tc) : Trap<TL::BM, TL::BN>::count(rows, tc);
   }
   if (total == 0) return;
-  const CUtensorMap mapA = make_map(p.P, p.N - p.prow0, p.K, p.ldp, TL::LDA, TL::BK);
-  const CUtensorMap mapB = make_map(p.P, p.N - p.prow0, p.K, p.ldp, TL::LDB, TL::BK);
+  const int64_t prow = p.N - p.prow0;
+  // complex: A = [P | -iP] read as a (2 rows) x (2K) real matrix, B = planar [Re P | Im P]
+  const CUtensorMap mapA = p.cplx ? make_map(p.P, 2 * prow, 2 * p.K, 2 * p.ldp, TL::LDA, TL::BK)
+                                  : make_map(p.P, prow, p.K, p.ldp, TL::LDA, TL::BK);
+  const CUtensorMap mapB = p.cplx ? make_map(p.PB, prow, 2 * p.K, p.ldp, TL::LDB, TL::BK)
+                                  : make_map(p.P, prow, p.K, p.ldp, TL::LDB, TL::BK);
   constexpr size_t smem = tma_smem_bytes<TL>();
   auto kern = trail_tma_kernel<TL>;
   set_smem(kern, smem);
@@ -247,7 +266,7 @@ static void launch_trail_tma_t(const TrailParams& p, const int* info, cudaStream
   q.stagger_ns = 0;
   if (per_sm >= 2 && total >= 8 * grid) {
     // half an item at ~85% of the per-CTA DMMA rate (37 TF/s over 2 CTAs per SM)
-    const double item_flops = 2.0 * TL::BM * TL::BN * (double)p.K;
+    const double item_flops = 2.0 * TL::BM * TL::BN * (double)p.K * (p.cplx ? 2 : 1);
     q.stagger_ns = (long long)(0.5 * item_flops / (0.85 * 37e12 / (num_sms() * per_sm)) * 1e9);
     if (const char* e = getenv("BCMG_STAGGER")) q.stagger_ns = atoi(e) ? q.stagger_ns : 0;
   }
@@ -265,8 +284,35 @@ static int trail_tile_choice() {
 }
 
 static void launch_trail_tma(const TrailParams& p, const int* info, cudaStream_t st) {
-  if (trail_tile_choice() == 1) return launch_trail_tma_t<TileBig>(p, info, st);
+  if (trail_tile_choice() == 1 && !p.cplx) return launch_trail_tma_t<TileBig>(p, info, st);
   launch_trail_tma_t<TileTrail2>(p, info, st);
+}
+
+// complex128 trailing updates through the real TMA kernel (TrailParams::cplx).
+// TMA box starts must be 16-byte aligned: the planar operand's row offsets are
+// multiples of T (even T), and its ld (= panel rows) must be even.
+bool complex_embed_ok(int dt, int64_t panel_rows, int64_t T) {
+  return dt == C128 && use_tma() && panel_rows % 2 == 0 && T % 2 == 0 && !getenv("BCMG_NO_CPLX_EMBED");
+}
+
+// [P | -iP] and planar [Re P | Im P] from the complex128 panel P (rows x K, ld rows)
+__global__ void expand_panel_kernel(double2* P, double* PB, int64_t rows, int64_t K) {
+  const int64_t total = rows * K;
+  double2* Q = P + total;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = P[idx];
+    Q[idx] = make_double2(v.y, -v.x);
+    PB[idx] = v.x;
+    PB[idx + total] = v.y;
+  }
+}
+
+void expand_panel(void* P, void* PB, int64_t rows, int64_t K, cudaStream_t st) {
+  if (rows <= 0 || K <= 0) return;
+  expand_panel_kernel<<<ew_grid(rows * K), 256, 0, st>>>(static_cast<double2*>(P), static_cast<double*>(PB), rows,
+                                                         K);
+  BCMG_CHECK_LAUNCH();
 }
 
 template <class TL>
@@ -369,6 +415,9 @@ void trailing_update(int dt, const TrailParams& p, const int* info, cudaStream_t
       const bool cp = aligned16(p.P) && p.ldp % 2 == 0 && p.T % 2 == 0 && (p.prow0 % 2 == 0);
       if (cp && use_tma() && tma_ok(p.P, p.ldp)) return launch_trail_tma(p, info, st);
       if (cp) return launch_trail<S, TileBig, true>(p, info, st);
+    }
+    if constexpr (std::is_same_v<S, double2>) {
+      if (p.cplx) return launch_trail_tma(p, info, st);
     }
     launch_trail<S, TileMed, false>(p, info, st);
   });

@@ -27,6 +27,12 @@ int gemm_splitk(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const
 
 // Trailing update for potrf step (see trail_kernel).
 void trailing_update(int dt, const TrailParams& p, const int* info, cudaStream_t st);
+// complex128 trailing update through the real FP64 TMA kernel: usable for this
+// dtype / panel height?  The panel must then be expanded with expand_panel:
+// P (rows x K complex, ld rows) is followed in memory by -iP, and PB receives
+// the planar [Re P | Im P] (rows x 2K real, ld rows).
+bool complex_embed_ok(int dt, int64_t panel_rows, int64_t T);
+void expand_panel(void* P, void* PB, int64_t rows, int64_t K, cudaStream_t st);
 
 // Diagonal tile: in-place lower Cholesky of the n x n block at A (lda) and
 // X := L^-1 (n x n, ldx, zero upper).  goff = global column of the block's

@@ -85,7 +85,9 @@ Session::~Session() {
   cudaSetDevice(device);
   cudaDeviceSynchronize();
   if (nccl) ncclCommDestroy(static_cast<ncclComm_t>(nccl));
-  for (auto* b : {&panel[0], &panel[1], &dinv, &wdiag, &info_dev, &tmp, &acc, &plan_buf}) b->release();
+  for (auto* b : {&panel[0], &panel[1], &panel_pb[0], &panel_pb[1], &dinv, &wdiag, &info_dev, &tmp, &acc, &plan_buf,
+                  &stage_buf, &desc_buf})
+    b->release();
   for (auto& e : ev_pool) cudaEventDestroy(e);
   for (auto& e : ev_time) cudaEventDestroy(e);
   for (auto& k : kstat)
@@ -467,8 +469,15 @@ std::vector<SchedOp> potrs_schedule(int64_t n, int64_t T, int ndev, int world, i
 int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) {
   const Geo g = make_geo(*this, dt, n, T, ndev);
   const size_t panel_bytes = (size_t)n * T * g.esz;
-  panel[0].ensure(panel_bytes);
-  panel[1].ensure(panel_bytes);
+  // complex128: the panel is followed by -iP, plus a planar copy (TrailParams::cplx)
+  const bool embed = complex_embed_ok(dt, 0, T);
+  panel[0].ensure(embed ? 2 * panel_bytes : panel_bytes);
+  panel[1].ensure(embed ? 2 * panel_bytes : panel_bytes);
+  if (embed) {
+    panel_pb[0].ensure(panel_bytes);
+    panel_pb[1].ensure(panel_bytes);
+  }
+  auto embed_k = [&](int64_t k) { return embed && complex_embed_ok(dt, n - g.stop(k), T); };
   dinv.ensure((size_t)g.nt * T * T * g.esz);
   wdiag.ensure((size_t)T * T * g.esz);
   info_dev.ensure(sizeof(int));
@@ -495,6 +504,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
         gemm(dt, n - s1, tc, tc, opA(colp(sh, g, s1, g.loc(k)), n, OP_N), opB(dinv_k(k), T, OP_C),
              Epilogue{panel[k % 2].p, n - s1, 1.0, 0.0, 0, 0}, info, crit);
       });
+      if (embed_k(k)) expand_panel(panel[k % 2].p, panel_pb[k % 2].p, n - s1, tc, crit);
     }
   };
   // While the lookahead path (diag factor + panel solve of tile k+1) runs on the
@@ -509,6 +519,10 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
     TrailParams p{};
     p.max_ctas = cap;
     p.P = panel[k % 2].p;
+    if (embed_k(k)) {
+      p.cplx = 1;
+      p.PB = panel_pb[k % 2].p;
+    }
     p.prow0 = g.stop(k);
     p.ldp = n - p.prow0;
     p.N = n;
@@ -552,6 +566,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
         else if (k >= 2) BCMG_CUDA(cudaStreamWaitEvent(comm, E(FREE, k - 2), 0));
         bcast(panel[b].p, (size_t)op.elems * g.esz, (int)op.root, comm);
         BCMG_CUDA(cudaEventRecord(E(C, k), comm));
+        if (!mine && embed_k(k)) expand_panel(panel[b].p, panel_pb[b].p, n - s1, s1 - g.start(k), comm);
         if (!mine) BCMG_CUDA(cudaEventRecord(E(R, k), comm));
         break;
       case S_UPDATE:
