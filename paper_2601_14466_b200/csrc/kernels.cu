@@ -340,6 +340,75 @@ static void launch_gemm_tma(int64_t M, int64_t N, int64_t K, const Operand& A, c
   launch_gemm_tma_t<TileTrail2>(M, N, K, A, B, ep, info, st);
 }
 
+// ---------------------------------------------------------------- complex128 by real embedding
+// C = alpha*Ahat*Bhat^T + beta*C (complex) as ONE real FP64 TMA GEMM:
+//   Atilde = [Ahat | -i Ahat]          (M x 2K complex = 2M x 2K real, re/im interleaved rows)
+//   X      = [Re Bhat | -Im Bhat]      (N x 2K real, planar)
+//   Ctilde (2M x N real, interleaved re/im rows = C's storage) = Atilde X^T:
+//     row 2r:   sum Re A Re B - Im A Im B = Re (A B)_rc
+//     row 2r+1: sum Im A Re B + Re A Im B = Im (A B)_rc
+// The gather kernel materialises either operand from any Operand view
+// (transposed / conjugated) through a 32x32 shared-memory tile.
+__global__ void embed_gather_kernel(Operand X, int64_t I, int64_t K, int64_t k0, int64_t kn, double2* outc,
+                                    double* outp, int64_t ldo) {
+  // logical element (i, k0 + kk) of X, kk < kn; outc: complex Atilde (ld ldo, cols kk and kn + kk),
+  // outp: planar X (ld ldo, cols kk and kn + kk)
+  __shared__ double2 t[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  const double2* base = static_cast<const double2*>(X.ptr);
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    // coalesced along the storage-contiguous index
+    const int64_t i = X.trans ? i0 + y : i0 + threadIdx.x, kk = X.trans ? c0 + threadIdx.x : c0 + y;
+    double2 v = make_double2(0.0, 0.0);
+    if (i < I && kk < kn) {
+      const int64_t k = k0 + kk;
+      v = X.trans ? base[k + i * X.ld] : base[i + k * X.ld];
+      if (X.conj) v.y = -v.y;
+    }
+    if (X.trans) t[threadIdx.x][y] = v; else t[y][threadIdx.x] = v;  // t[kk][i]
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t i = i0 + threadIdx.x, kk = c0 + y;
+    if (i >= I || kk >= kn) continue;
+    const double2 v = t[y][threadIdx.x];
+    if (outc) {
+      outc[i + kk * ldo] = v;
+      outc[i + (kn + kk) * ldo] = make_double2(v.y, -v.x);
+    } else {
+      outp[i + kk * ldo] = v.x;
+      outp[i + (kn + kk) * ldo] = -v.y;
+    }
+  }
+}
+
+static void embed_gather(const Operand& X, int64_t I, int64_t k0, int64_t kn, double2* outc, double* outp,
+                         int64_t ldo, cudaStream_t st) {
+  dim3 grid((unsigned)((I + 31) / 32), (unsigned)((kn + 31) / 32)), block(32, 8);
+  embed_gather_kernel<<<grid, block, 0, st>>>(X, I, 0, k0, kn, outc, outp, ldo);
+  BCMG_CHECK_LAUNCH();
+}
+
+size_t gemm_c128_embed_bytes(int64_t M, int64_t N, int64_t K) { return (size_t)(2 * M + N) * K * 16; }
+
+bool gemm_c128_embed(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+                     void* scratch, size_t scratch_bytes, const int* info, cudaStream_t st, bool always) {
+  if (!use_tma() || getenv("BCMG_NO_CPLX_EMBED") || A.mask || B.mask || ep.lower_only) return false;
+  if (M <= 0 || N <= 0 || K <= 0 || N % 2 || !aligned16(ep.C) || !aligned16(scratch)) return false;
+  if (scratch_bytes < gemm_c128_embed_bytes(M, N, K)) return false;
+  // enough real blocks to fill the GPU (smaller GEMMs stay on the complex kernels), unless
+  // the caller needs a shape-independent choice (bit-identical results across device counts)
+  const int64_t blocks = ((2 * M + TileTrail2::BM - 1) / TileTrail2::BM) * ((N + TileTrail2::BN - 1) / TileTrail2::BN);
+  if (!always && blocks < num_sms()) return false;
+  double2* at = static_cast<double2*>(scratch);              // M x 2K complex, ld M
+  double* xp = reinterpret_cast<double*>(at + 2 * M * K);    // N x 2K real, ld N
+  embed_gather(A, M, 0, K, at, nullptr, M, st);
+  embed_gather(B, N, 0, K, nullptr, xp, N, st);
+  launch_gemm_tma_t<TileTrail2>(2 * M, N, 2 * K, Operand{at, 2 * M, 0, 0, 0, 0}, Operand{xp, N, 0, 0, 0, 0},
+                                Epilogue{ep.C, 2 * ep.ldc, ep.alpha, ep.beta, 0, 0}, info, st);
+  return true;
+}
+
 static bool use_tma() {
   static int v = -1;
   if (v < 0) {

@@ -86,7 +86,7 @@ Session::~Session() {
   cudaDeviceSynchronize();
   if (nccl) ncclCommDestroy(static_cast<ncclComm_t>(nccl));
   for (auto* b : {&panel[0], &panel[1], &panel_pb[0], &panel_pb[1], &dinv, &wdiag, &info_dev, &tmp, &acc, &plan_buf,
-                  &stage_buf, &desc_buf})
+                  &stage_buf, &desc_buf, &embed_buf})
     b->release();
   for (auto& e : ev_pool) cudaEventDestroy(e);
   for (auto& e : ev_time) cudaEventDestroy(e);
@@ -477,6 +477,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
     panel_pb[0].ensure(panel_bytes);
     panel_pb[1].ensure(panel_bytes);
   }
+  if (dt == C128) embed_buf.ensure(gemm_c128_embed_bytes(n, T, T));  // panel solve by real embedding
   auto embed_k = [&](int64_t k) { return embed && complex_embed_ok(dt, n - g.stop(k), T); };
   dinv.ensure((size_t)g.nt * T * T * g.esz);
   wdiag.ensure((size_t)T * T * g.esz);
@@ -501,8 +502,10 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
           [&] { diag_factor(dt, Akk, n, dinv_k(k), T, wdiag.p, tc, s0, info, crit); });
     if (s1 < n) {
       timed(K_TRSM, crit, cf * 2.0 * (double)(n - s1) * tc * tc, [&] {
-        gemm(dt, n - s1, tc, tc, opA(colp(sh, g, s1, g.loc(k)), n, OP_N), opB(dinv_k(k), T, OP_C),
-             Epilogue{panel[k % 2].p, n - s1, 1.0, 0.0, 0, 0}, info, crit);
+        const Operand a21 = opA(colp(sh, g, s1, g.loc(k)), n, OP_N), xh = opB(dinv_k(k), T, OP_C);
+        const Epilogue ep{panel[k % 2].p, n - s1, 1.0, 0.0, 0, 0};
+        if (!(dt == C128 && gemm_c128_embed(n - s1, tc, tc, a21, xh, ep, embed_buf.p, embed_buf.bytes, info, crit)))
+          gemm(dt, n - s1, tc, tc, a21, xh, ep, info, crit);
       });
       if (embed_k(k)) expand_panel(panel[k % 2].p, panel_pb[k % 2].p, n - s1, tc, crit);
     }
@@ -736,6 +739,11 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
   panel[0].ensure(nt_bytes);  // broadcast W tile
   panel[1].ensure(nt_bytes);  // staged L21 rows / finalisation product
   acc.ensure(nt_bytes);       // product blocks of every device (gather buffer)
+  // complex128: scratch of the real-embedding GEMMs (W sweep: (2(n-s)+c) x T; product
+  // sweep: column chunks of (2T + chunk) x (n-s))
+  // (T and n even: every column count is even, so the choice is the same for any device count)
+  const bool emb = dt == C128 && T % 2 == 0 && n % 2 == 0 && !getenv("BCMG_NO_CPLX_EMBED");
+  if (emb) embed_buf.ensure(std::max(gemm_c128_embed_bytes(n, n, T), (size_t)(2 * T + 2048) * n * 16));
   cudaStream_t st = crit;
   char* pan = static_cast<char*>(panel[0].p);
   char* stage = static_cast<char*>(panel[1].p);
@@ -788,8 +796,10 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
           // GEMM's B operand is in natural orientation (TMA-eligible)
           conj_transpose(dt, sh, n, stage, c, c, tcs, st);
           BCMG_CUDA(cudaMemset2DAsync(sh, n * g.esz, 0, tcs * g.esz, c, st));  // first touch of acc rows [ss, se)
-          gemm(dt, n - ss, c, tcs, opA(W, ldw, OP_N), opB(stage, c, OP_C), Epilogue{sh, n, 1.0, 1.0, 0, 0},
-               nullptr, st);
+          const Operand wa = opA(W, ldw, OP_N), lb = opB(stage, c, OP_C);
+          const Epilogue ep{sh, n, 1.0, 1.0, 0, 0};
+          if (!(emb && gemm_c128_embed(n - ss, c, tcs, wa, lb, ep, embed_buf.p, embed_buf.bytes, nullptr, st, true)))
+            gemm(dt, n - ss, c, tcs, wa, lb, ep, nullptr, st);
         }
         break;
       }
@@ -799,8 +809,29 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
         for (int d = g.dev0; d < g.dev0 + g.nloc; ++d) {
           const int64_t c = cols_upto(g, d, s);
           if (c == 0) continue;
-          gemm(dt, tcs, c, n - ss, opA(W, ldw, OP_C), opB(colp(shards[d - g.dev0], g, ss, 0), n, OP_N),
-               Epilogue{blocks + block_off(s, d) * g.esz, tcs, 1.0, 0.0, 0, 0}, nullptr, st);
+          const Operand wh = opA(W, ldw, OP_C);
+          char* sh = colp(shards[d - g.dev0], g, ss, 0);
+          char* blk = blocks + block_off(s, d) * g.esz;
+          if (emb) {
+            // real embedding in column chunks sized to the scratch (both operands are gathered)
+            int64_t nc = (int64_t)(embed_buf.bytes / ((size_t)(n - ss) * 16)) - 2 * tcs;
+            nc = nc / 64 * 64;
+            bool done = nc >= 64;
+            for (int64_t c0 = 0; done && c0 < c; c0 += nc) {
+              const int64_t cn = std::min(nc, c - c0);
+              done = gemm_c128_embed(tcs, cn, n - ss, wh, opB(sh + c0 * n * g.esz, n, OP_N),
+                                     Epilogue{blk + c0 * tcs * g.esz, tcs, 1.0, 0.0, 0, 0}, embed_buf.p,
+                                     embed_buf.bytes, nullptr, st, true);
+              if (!done && c0 > 0) {  // finish the remaining columns on the complex kernels
+                gemm(dt, tcs, c - c0, n - ss, wh, opB(sh + c0 * n * g.esz, n, OP_N),
+                     Epilogue{blk + c0 * tcs * g.esz, tcs, 1.0, 0.0, 0, 0}, nullptr, st);
+                done = true;
+                break;
+              }
+            }
+            if (done) continue;
+          }
+          gemm(dt, tcs, c, n - ss, wh, opB(sh, n, OP_N), Epilogue{blk, tcs, 1.0, 0.0, 0, 0}, nullptr, st);
         }
         // written back only after every GEMM: with one process W_s is read from tile s itself
         for (int d = g.dev0; d < g.dev0 + g.nloc; ++d) {
