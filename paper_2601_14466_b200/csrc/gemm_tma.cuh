@@ -205,6 +205,35 @@ struct Trap {
   }
 };
 
+// Same enumeration with column blocks twice as wide as row blocks (BN = 2 BM):
+// row block rb keeps min(ncb, rb/2 + 1) column blocks (complex embedding on
+// the 128x128 tcgen05 tile: 128 real rows = 64 complex rows).
+template <int BM, int BN>
+struct TrapH {
+  static_assert(BN == 2 * BM, "TrapH is for BN == 2 BM");
+  __host__ __device__ static int64_t tri(int64_t t) {  // sum_{rb < t} (rb/2 + 1)
+    const int64_t p = t / 2;
+    return p * (p + 1) + (t & 1) * (p + 1);
+  }
+  __host__ __device__ static int64_t count(int64_t rows, int64_t tc) {
+    const int64_t nrb = (rows + BM - 1) / BM, ncb = (tc + BN - 1) / BN, r0 = 2 * (ncb - 1);
+    return nrb <= r0 ? tri(nrb) : tri(r0) + (nrb - r0) * ncb;
+  }
+  __host__ __device__ static void decode(int64_t b, int64_t tc, int64_t& rb, int64_t& cb) {
+    const int64_t ncb = (tc + BN - 1) / BN, r0 = 2 * (ncb - 1), t0 = tri(r0);
+    if (b < t0) {  // pair g of row blocks (2g, 2g+1) holds 2(g+1) items, g(g+1) before it
+      int64_t g = 0;
+      while ((g + 1) * (g + 2) <= b) ++g;
+      const int64_t o = b - g * (g + 1);
+      rb = 2 * g + o / (g + 1);
+      cb = o % (g + 1);
+    } else {
+      rb = r0 + (b - t0) / ncb;
+      cb = (b - t0) % ncb;
+    }
+  }
+};
+
 template <class TL>
 constexpr int min_blocks() { return 65536 / (TL::THREADS * 128) > 0 ? 65536 / (TL::THREADS * 128) : 1; }
 

@@ -291,27 +291,39 @@ static void launch_trail_tma(const TrailParams& p, const int* info, cudaStream_t
 // complex128 trailing updates through the real TMA kernel (TrailParams::cplx).
 // TMA box starts must be 16-byte aligned: the planar operand's row offsets are
 // multiples of T (even T), and its ld (= panel rows) must be even.
+// complex64 uses the tcgen05 3xTF32 kernel the same way (16-byte box starts: T and
+// the panel height multiples of 4 floats).
 bool complex_embed_ok(int dt, int64_t panel_rows, int64_t T) {
-  return dt == C128 && use_tma() && panel_rows % 2 == 0 && T % 2 == 0 && !getenv("BCMG_NO_CPLX_EMBED");
+  if (getenv("BCMG_NO_CPLX_EMBED")) return false;
+  if (dt == C128) return use_tma() && panel_rows % 2 == 0 && T % 2 == 0;
+  if (dt == C64) return use_tc() && panel_rows % 4 == 0 && T % 4 == 0;
+  return false;
 }
 
-// [P | -iP] and planar [Re P | Im P] from the complex128 panel P (rows x K, ld rows)
-__global__ void expand_panel_kernel(double2* P, double* PB, int64_t rows, int64_t K) {
+// [P | -iP] and planar [Re P | Im P] from the complex panel P (rows x K, ld rows)
+template <class C, class R>
+__global__ void expand_panel_kernel(C* P, R* PB, int64_t rows, int64_t K) {
   const int64_t total = rows * K;
-  double2* Q = P + total;
+  C* Q = P + total;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const double2 v = P[idx];
-    Q[idx] = make_double2(v.y, -v.x);
+    const C v = P[idx];
+    C q;
+    q.x = v.y;
+    q.y = -v.x;
+    Q[idx] = q;
     PB[idx] = v.x;
     PB[idx + total] = v.y;
   }
 }
 
-void expand_panel(void* P, void* PB, int64_t rows, int64_t K, cudaStream_t st) {
+void expand_panel(int dt, void* P, void* PB, int64_t rows, int64_t K, cudaStream_t st) {
   if (rows <= 0 || K <= 0) return;
-  expand_panel_kernel<<<ew_grid(rows * K), 256, 0, st>>>(static_cast<double2*>(P), static_cast<double*>(PB), rows,
-                                                         K);
+  if (dt == C128)
+    expand_panel_kernel<<<ew_grid(rows * K), 256, 0, st>>>(static_cast<double2*>(P), static_cast<double*>(PB), rows,
+                                                           K);
+  else
+    expand_panel_kernel<<<ew_grid(rows * K), 256, 0, st>>>(static_cast<float2*>(P), static_cast<float*>(PB), rows, K);
   BCMG_CHECK_LAUNCH();
 }
 
@@ -340,8 +352,9 @@ static void launch_gemm_tma(int64_t M, int64_t N, int64_t K, const Operand& A, c
   launch_gemm_tma_t<TileTrail2>(M, N, K, A, B, ep, info, st);
 }
 
-// ---------------------------------------------------------------- complex128 by real embedding
-// C = alpha*Ahat*Bhat^T + beta*C (complex) as ONE real FP64 TMA GEMM:
+// ---------------------------------------------------------------- complex GEMM by real embedding
+// C = alpha*Ahat*Bhat^T + beta*C (complex) as ONE real GEMM on the tensor-core
+// kernels (FP64 TMA + DMMA for complex128, tcgen05 3xTF32 for complex64):
 //   Atilde = [Ahat | -i Ahat]          (M x 2K complex = 2M x 2K real, re/im interleaved rows)
 //   X      = [Re Bhat | -Im Bhat]      (N x 2K real, planar)
 //   Ctilde (2M x N real, interleaved re/im rows = C's storage) = Atilde X^T:
@@ -349,20 +362,21 @@ static void launch_gemm_tma(int64_t M, int64_t N, int64_t K, const Operand& A, c
 //     row 2r+1: sum Im A Re B + Re A Im B = Im (A B)_rc
 // The gather kernel materialises either operand from any Operand view
 // (transposed / conjugated) through a 32x32 shared-memory tile.
-__global__ void embed_gather_kernel(Operand X, int64_t I, int64_t K, int64_t k0, int64_t kn, double2* outc,
-                                    double* outp, int64_t ldo) {
-  // logical element (i, k0 + kk) of X, kk < kn; outc: complex Atilde (ld ldo, cols kk and kn + kk),
+template <class C, class R>
+__global__ void embed_gather_kernel(Operand X, int64_t I, int64_t kn, C* outc, R* outp, int64_t ldo) {
+  // logical element (i, kk) of X, kk < kn; outc: complex Atilde (ld ldo, cols kk and kn + kk),
   // outp: planar X (ld ldo, cols kk and kn + kk)
-  __shared__ double2 t[32][33];
+  __shared__ C t[32][33];
   const int64_t i0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
-  const double2* base = static_cast<const double2*>(X.ptr);
+  const C* base = static_cast<const C*>(X.ptr);
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
     // coalesced along the storage-contiguous index
     const int64_t i = X.trans ? i0 + y : i0 + threadIdx.x, kk = X.trans ? c0 + threadIdx.x : c0 + y;
-    double2 v = make_double2(0.0, 0.0);
+    C v;
+    v.x = 0;
+    v.y = 0;
     if (i < I && kk < kn) {
-      const int64_t k = k0 + kk;
-      v = X.trans ? base[k + i * X.ld] : base[i + k * X.ld];
+      v = X.trans ? base[kk + i * X.ld] : base[i + kk * X.ld];
       if (X.conj) v.y = -v.y;
     }
     if (X.trans) t[threadIdx.x][y] = v; else t[y][threadIdx.x] = v;  // t[kk][i]
@@ -371,10 +385,13 @@ __global__ void embed_gather_kernel(Operand X, int64_t I, int64_t K, int64_t k0,
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
     const int64_t i = i0 + threadIdx.x, kk = c0 + y;
     if (i >= I || kk >= kn) continue;
-    const double2 v = t[y][threadIdx.x];
+    const C v = t[y][threadIdx.x];
     if (outc) {
+      C q;
+      q.x = v.y;
+      q.y = -v.x;
       outc[i + kk * ldo] = v;
-      outc[i + (kn + kk) * ldo] = make_double2(v.y, -v.x);
+      outc[i + (kn + kk) * ldo] = q;
     } else {
       outp[i + kk * ldo] = v.x;
       outp[i + (kn + kk) * ldo] = -v.y;
@@ -382,30 +399,46 @@ __global__ void embed_gather_kernel(Operand X, int64_t I, int64_t K, int64_t k0,
   }
 }
 
-static void embed_gather(const Operand& X, int64_t I, int64_t k0, int64_t kn, double2* outc, double* outp,
-                         int64_t ldo, cudaStream_t st) {
+template <class C, class R>
+static void embed_gather(const Operand& X, int64_t I, int64_t kn, C* outc, R* outp, int64_t ldo, cudaStream_t st) {
   dim3 grid((unsigned)((I + 31) / 32), (unsigned)((kn + 31) / 32)), block(32, 8);
-  embed_gather_kernel<<<grid, block, 0, st>>>(X, I, 0, k0, kn, outc, outp, ldo);
+  embed_gather_kernel<C, R><<<grid, block, 0, st>>>(X, I, kn, outc, outp, ldo);
   BCMG_CHECK_LAUNCH();
 }
 
-size_t gemm_c128_embed_bytes(int64_t M, int64_t N, int64_t K) { return (size_t)(2 * M + N) * K * 16; }
+size_t gemm_cplx_embed_bytes(int dt, int64_t M, int64_t N, int64_t K) {
+  return (size_t)(2 * M + N) * K * (dt == C64 ? 8 : 16);
+}
 
-bool gemm_c128_embed(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
                      void* scratch, size_t scratch_bytes, const int* info, cudaStream_t st, bool always) {
-  if (!use_tma() || getenv("BCMG_NO_CPLX_EMBED") || A.mask || B.mask || ep.lower_only) return false;
-  if (M <= 0 || N <= 0 || K <= 0 || N % 2 || !aligned16(ep.C) || !aligned16(scratch)) return false;
-  if (scratch_bytes < gemm_c128_embed_bytes(M, N, K)) return false;
+  if (getenv("BCMG_NO_CPLX_EMBED") || A.mask || B.mask || ep.lower_only) return false;
+  if (dt != C128 && dt != C64) return false;
+  if (dt == C128 ? !use_tma() : !use_tc()) return false;
+  const int64_t align = dt == C128 ? 2 : 4;  // real ld and box starts: 16 bytes
+  if (M <= 0 || N <= 0 || K <= 0 || N % align || (2 * M) % align || !aligned16(ep.C) || !aligned16(scratch))
+    return false;
+  if (scratch_bytes < gemm_cplx_embed_bytes(dt, M, N, K)) return false;
+  if (dt == C64 && (2 * M < 256 || N < 64)) return false;  // the tcgen05 tile's minimum shape
   // enough real blocks to fill the GPU (smaller GEMMs stay on the complex kernels), unless
   // the caller needs a shape-independent choice (bit-identical results across device counts)
   const int64_t blocks = ((2 * M + TileTrail2::BM - 1) / TileTrail2::BM) * ((N + TileTrail2::BN - 1) / TileTrail2::BN);
   if (!always && blocks < num_sms()) return false;
-  double2* at = static_cast<double2*>(scratch);              // M x 2K complex, ld M
-  double* xp = reinterpret_cast<double*>(at + 2 * M * K);    // N x 2K real, ld N
-  embed_gather(A, M, 0, K, at, nullptr, M, st);
-  embed_gather(B, N, 0, K, nullptr, xp, N, st);
-  launch_gemm_tma_t<TileTrail2>(2 * M, N, 2 * K, Operand{at, 2 * M, 0, 0, 0, 0}, Operand{xp, N, 0, 0, 0, 0},
-                                Epilogue{ep.C, 2 * ep.ldc, ep.alpha, ep.beta, 0, 0}, info, st);
+  if (dt == C128) {
+    double2* at = static_cast<double2*>(scratch);              // M x 2K complex, ld M
+    double* xp = reinterpret_cast<double*>(at + 2 * M * K);    // N x 2K real, ld N
+    embed_gather<double2, double>(A, M, K, at, nullptr, M, st);
+    embed_gather<double2, double>(B, N, K, nullptr, xp, N, st);
+    launch_gemm_tma_t<TileTrail2>(2 * M, N, 2 * K, Operand{at, 2 * M, 0, 0, 0, 0}, Operand{xp, N, 0, 0, 0, 0},
+                                  Epilogue{ep.C, 2 * ep.ldc, ep.alpha, ep.beta, 0, 0}, info, st);
+  } else {
+    float2* at = static_cast<float2*>(scratch);
+    float* xp = reinterpret_cast<float*>(at + 2 * M * K);
+    embed_gather<float2, float>(A, M, K, at, nullptr, M, st);
+    embed_gather<float2, float>(B, N, K, nullptr, xp, N, st);
+    launch_tc3_gemm(2 * M, N, 2 * K, Operand{at, 2 * M, 0, 0, 0, 0}, Operand{xp, N, 0, 0, 0, 0},
+                    Epilogue{ep.C, 2 * ep.ldc, ep.alpha, ep.beta, 0, 0}, info, st);
+  }
   return true;
 }
 
@@ -460,15 +493,19 @@ static void launch_tc3_trail(const TrailParams& p, const int* info, cudaStream_t
   for (int64_t m = p.m_first; m < p.m_last; ++m) {
     const int dev = (int)(m % p.D);
     if (dev < p.dev0 || dev >= p.dev0 + p.nloc) continue;
-    const int64_t rows = p.N - m * p.T;
-    total += Trap<tc::BM, tc::BN>::count(rows, std::min(p.T, rows));
+    const int64_t rows = p.N - m * p.T, tcm = std::min(p.T, rows);
+    total += p.cplx ? TrapH<tc::BM / 2, tc::BN>::count(rows, tcm) : Trap<tc::BM, tc::BN>::count(rows, tcm);
   }
   if (total == 0) return;
-  const CUtensorMap map = make_map_f32_sw128(p.P, p.N - p.prow0, p.K, p.ldp);
+  const int64_t prow = p.N - p.prow0;
+  // complex64: A = [P | -iP] as a (2 rows) x (2K) float matrix, B = planar [Re P | Im P]
+  const CUtensorMap ma = p.cplx ? make_map_f32_sw128(p.P, 2 * prow, 2 * p.K, 2 * p.ldp)
+                                : make_map_f32_sw128(p.P, prow, p.K, p.ldp);
+  const CUtensorMap mb = p.cplx ? make_map_f32_sw128(p.PB, prow, 2 * p.K, p.ldp) : ma;
   set_smem(tc3_trail_kernel, tc::SMEM_BYTES);
   const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, num_sms()) : num_sms();
   const int64_t grid = std::min<int64_t>(total, sms);
-  tc3_trail_kernel<<<(unsigned)grid, tc::THREADS, tc::SMEM_BYTES, st>>>(map, p, info);
+  tc3_trail_kernel<<<(unsigned)grid, tc::THREADS, tc::SMEM_BYTES, st>>>(ma, mb, p, info);
   BCMG_CHECK_LAUNCH();
 }
 
@@ -487,6 +524,9 @@ void trailing_update(int dt, const TrailParams& p, const int* info, cudaStream_t
     }
     if constexpr (std::is_same_v<S, double2>) {
       if (p.cplx) return launch_trail_tma(p, info, st);
+    }
+    if constexpr (std::is_same_v<S, float2>) {
+      if (p.cplx) return launch_tc3_trail(p, info, st);
     }
     launch_trail<S, TileMed, false>(p, info, st);
   });

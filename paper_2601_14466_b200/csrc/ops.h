@@ -27,20 +27,21 @@ int gemm_splitk(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const
 
 // Trailing update for potrf step (see trail_kernel).
 void trailing_update(int dt, const TrailParams& p, const int* info, cudaStream_t st);
-// complex128 trailing update through the real FP64 TMA kernel: usable for this
+// complex trailing update through the real tensor-core kernels: usable for this
 // dtype / panel height?  The panel must then be expanded with expand_panel:
 // P (rows x K complex, ld rows) is followed in memory by -iP, and PB receives
 // the planar [Re P | Im P] (rows x 2K real, ld rows).
 bool complex_embed_ok(int dt, int64_t panel_rows, int64_t T);
-void expand_panel(void* P, void* PB, int64_t rows, int64_t K, cudaStream_t st);
-// complex128 GEMM (gemm() semantics) as one real FP64 TMA GEMM on the embedded
-// operands [Ahat | -i Ahat] and [Re Bhat | -Im Bhat], materialised in `scratch`
-// (gemm_c128_embed_bytes).  Returns false (nothing launched) when the shape or
-// the operands do not qualify; the caller then uses gemm().
-size_t gemm_c128_embed_bytes(int64_t M, int64_t N, int64_t K);
-// always: skip the fill-the-GPU size heuristic (callers whose N depends on the
-// device count need the same arithmetic for every shape).
-bool gemm_c128_embed(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+void expand_panel(int dt, void* P, void* PB, int64_t rows, int64_t K, cudaStream_t st);
+// complex GEMM (gemm() semantics) as one real tensor-core GEMM (FP64 TMA for
+// complex128, tcgen05 3xTF32 for complex64) on the embedded operands
+// [Ahat | -i Ahat] and [Re Bhat | -Im Bhat], materialised in `scratch`
+// (gemm_cplx_embed_bytes).  Returns false (nothing launched) when the shape or
+// the operands do not qualify; the caller then uses gemm().  always: skip the
+// fill-the-GPU size heuristic (callers whose N depends on the device count
+// need the same arithmetic for every shape).
+size_t gemm_cplx_embed_bytes(int dt, int64_t M, int64_t N, int64_t K);
+bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
                      void* scratch, size_t scratch_bytes, const int* info, cudaStream_t st, bool always = false);
 
 // Diagonal tile: in-place lower Cholesky of the n x n block at A (lda) and

@@ -477,7 +477,8 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
     panel_pb[0].ensure(panel_bytes);
     panel_pb[1].ensure(panel_bytes);
   }
-  if (dt == C128) embed_buf.ensure(gemm_c128_embed_bytes(n, T, T));  // panel solve by real embedding
+  const bool cplx_dt = dt == C128 || dt == C64;
+  if (cplx_dt) embed_buf.ensure(gemm_cplx_embed_bytes(dt, n, T, T));  // panel solve by real embedding
   auto embed_k = [&](int64_t k) { return embed && complex_embed_ok(dt, n - g.stop(k), T); };
   dinv.ensure((size_t)g.nt * T * T * g.esz);
   wdiag.ensure((size_t)T * T * g.esz);
@@ -504,10 +505,10 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
       timed(K_TRSM, crit, cf * 2.0 * (double)(n - s1) * tc * tc, [&] {
         const Operand a21 = opA(colp(sh, g, s1, g.loc(k)), n, OP_N), xh = opB(dinv_k(k), T, OP_C);
         const Epilogue ep{panel[k % 2].p, n - s1, 1.0, 0.0, 0, 0};
-        if (!(dt == C128 && gemm_c128_embed(n - s1, tc, tc, a21, xh, ep, embed_buf.p, embed_buf.bytes, info, crit)))
+        if (!(cplx_dt && gemm_cplx_embed(dt, n - s1, tc, tc, a21, xh, ep, embed_buf.p, embed_buf.bytes, info, crit)))
           gemm(dt, n - s1, tc, tc, a21, xh, ep, info, crit);
       });
-      if (embed_k(k)) expand_panel(panel[k % 2].p, panel_pb[k % 2].p, n - s1, tc, crit);
+      if (embed_k(k)) expand_panel(dt, panel[k % 2].p, panel_pb[k % 2].p, n - s1, tc, crit);
     }
   };
   // While the lookahead path (diag factor + panel solve of tile k+1) runs on the
@@ -569,7 +570,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
         else if (k >= 2) BCMG_CUDA(cudaStreamWaitEvent(comm, E(FREE, k - 2), 0));
         bcast(panel[b].p, (size_t)op.elems * g.esz, (int)op.root, comm);
         BCMG_CUDA(cudaEventRecord(E(C, k), comm));
-        if (!mine && embed_k(k)) expand_panel(panel[b].p, panel_pb[b].p, n - s1, s1 - g.start(k), comm);
+        if (!mine && embed_k(k)) expand_panel(dt, panel[b].p, panel_pb[b].p, n - s1, s1 - g.start(k), comm);
         if (!mine) BCMG_CUDA(cudaEventRecord(E(R, k), comm));
         break;
       case S_UPDATE:
@@ -742,8 +743,9 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
   // complex128: scratch of the real-embedding GEMMs (W sweep: (2(n-s)+c) x T; product
   // sweep: column chunks of (2T + chunk) x (n-s))
   // (T and n even: every column count is even, so the choice is the same for any device count)
-  const bool emb = dt == C128 && T % 2 == 0 && n % 2 == 0 && !getenv("BCMG_NO_CPLX_EMBED");
-  if (emb) embed_buf.ensure(std::max(gemm_c128_embed_bytes(n, n, T), (size_t)(2 * T + 2048) * n * 16));
+  const bool emb = (dt == C128 && T % 2 == 0 && n % 2 == 0) || (dt == C64 && T % 64 == 0 && n % 4 == 0);  // c64: tcgen05 tile minimums hold for every D
+  if (emb && !getenv("BCMG_NO_CPLX_EMBED"))
+    embed_buf.ensure(std::max(gemm_cplx_embed_bytes(dt, n, n, T), (size_t)(2 * T + 2048) * n * g.esz));
   cudaStream_t st = crit;
   char* pan = static_cast<char*>(panel[0].p);
   char* stage = static_cast<char*>(panel[1].p);
@@ -798,7 +800,7 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
           BCMG_CUDA(cudaMemset2DAsync(sh, n * g.esz, 0, tcs * g.esz, c, st));  // first touch of acc rows [ss, se)
           const Operand wa = opA(W, ldw, OP_N), lb = opB(stage, c, OP_C);
           const Epilogue ep{sh, n, 1.0, 1.0, 0, 0};
-          if (!(emb && gemm_c128_embed(n - ss, c, tcs, wa, lb, ep, embed_buf.p, embed_buf.bytes, nullptr, st, true)))
+          if (!(emb && gemm_cplx_embed(dt, n - ss, c, tcs, wa, lb, ep, embed_buf.p, embed_buf.bytes, nullptr, st, true)))
             gemm(dt, n - ss, c, tcs, wa, lb, ep, nullptr, st);
         }
         break;
@@ -814,12 +816,12 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
           char* blk = blocks + block_off(s, d) * g.esz;
           if (emb) {
             // real embedding in column chunks sized to the scratch (both operands are gathered)
-            int64_t nc = (int64_t)(embed_buf.bytes / ((size_t)(n - ss) * 16)) - 2 * tcs;
+            int64_t nc = (int64_t)(embed_buf.bytes / ((size_t)(n - ss) * g.esz)) - 2 * tcs;
             nc = nc / 64 * 64;
             bool done = nc >= 64;
             for (int64_t c0 = 0; done && c0 < c; c0 += nc) {
               const int64_t cn = std::min(nc, c - c0);
-              done = gemm_c128_embed(tcs, cn, n - ss, wh, opB(sh + c0 * n * g.esz, n, OP_N),
+              done = gemm_cplx_embed(dt, tcs, cn, n - ss, wh, opB(sh + c0 * n * g.esz, n, OP_N),
                                      Epilogue{blk + c0 * tcs * g.esz, tcs, 1.0, 0.0, 0, 0}, embed_buf.p,
                                      embed_buf.bytes, nullptr, st, true);
               if (!done && c0 > 0) {  // finish the remaining columns on the complex kernels

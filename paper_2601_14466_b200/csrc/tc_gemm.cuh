@@ -298,19 +298,24 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 
 // potrf trailing update for float32 shards (see trail_kernel): stateless
 // decode (every role walks the same item sequence independently).
+// complex64 (p.cplx): the real embedding of TrailParams (A = [P | -iP] as a
+// (2 rows) x (2K) float matrix, B = planar [Re P | Im P]); a 128-row tile then
+// covers 64 complex rows (TrapH enumeration) and C is addressed as floats.
 __global__ void __launch_bounds__(tc::THREADS, 1)
-    tc3_trail_kernel(const __grid_constant__ CUtensorMap mapP, TrailParams p, const int* info) {
+    tc3_trail_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                     TrailParams p, const int* info) {
   using TZ = Trap<tc::BM, tc::BN>;
+  using TZC = TrapH<tc::BM / 2, tc::BN>;
   if (ld_flag(info)) return;
   int64_t cm = p.m_first, cbase = 0, ccnt = -1;  // per-thread monotone cursor
-  tc::tc3_loop(&mapP, &mapP, (int)p.K, [&](int64_t item, tc::Blk& blk) -> bool {
+  tc::tc3_loop(&mapA, &mapB, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, tc::Blk& blk) -> bool {
     for (;;) {
       if (cm >= p.m_last) return false;
       const int dev = (int)(cm % p.D);
       if (dev >= p.dev0 && dev < p.dev0 + p.nloc) {
         if (ccnt < 0) {
-          const int64_t ms = cm * p.T;
-          ccnt = TZ::count(p.N - ms, (p.T < p.N - ms ? p.T : p.N - ms));
+          const int64_t ms = cm * p.T, tcm = p.T < p.N - ms ? p.T : p.N - ms;
+          ccnt = p.cplx ? TZC::count(p.N - ms, tcm) : TZ::count(p.N - ms, tcm);
         }
         if (item < cbase + ccnt) break;
         cbase += ccnt;
@@ -320,10 +325,24 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     }
     const int64_t ms = cm * p.T, rows = p.N - ms, tcw = p.T < rows ? p.T : rows;
     int64_t rb, cb;
-    TZ::decode(item - cbase, tcw, rb, cb);
     const int dev = (int)(cm % p.D);
     float* shard = reinterpret_cast<float*>(p.shards[dev - p.dev0]);
     const int64_t loc = (cm / p.D) * p.T;
+    if (p.cplx) {
+      TZC::decode(item - cbase, tcw, rb, cb);
+      blk.a_row = (int)(2 * (ms - p.prow0));
+      blk.b_row = (int)(ms - p.prow0);
+      blk.m0 = rb * tc::BM;
+      blk.n0 = cb * tc::BN;
+      blk.M = 2 * rows;
+      blk.N = tcw;
+      blk.C = shard + 2 * (ms + loc * p.N);
+      blk.ldc = 2 * p.N;
+      blk.alpha = -1.f;
+      blk.beta = 1.f;
+      return true;
+    }
+    TZ::decode(item - cbase, tcw, rb, cb);
     blk.a_row = (int)(ms - p.prow0);
     blk.b_row = (int)(ms - p.prow0);
     blk.m0 = rb * tc::BM;
