@@ -236,20 +236,33 @@ __device__ __forceinline__ void tc3_loop(const CUtensorMap* mapA, const CUtensor
     Blk blk;
     for (int64_t item = blockIdx.x; next(item, blk); item += gridDim.x, ++t) {
       const int b = t & 1;
-      mbar_wait(&tfull[b], (t >> 1) & 1);
-      fence_after();
       const int64_t r = blk.m0 + row;
       float* __restrict__ crow = blk.C + r;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        // issue this chunk's 32 C loads before touching TMEM or storing:
-        // one memory latency per chunk instead of one per element
-        float old[32];
+      auto load_chunk = [&](int c0, float* dst) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int64_t col = blk.n0 + c0 + j;
-          old[j] = (blk.beta != 0.f && r < blk.M && col < blk.N) ? crow[col * blk.ldc] : 0.f;
+          dst[j] = (blk.beta != 0.f && r < blk.M && col < blk.N) ? crow[col * blk.ldc] : 0.f;
         }
+      };
+      // C does not depend on this tile's MMAs: pull the warp's 32 x 128 block into
+      // L2 and load its first chunk while they run (short K leaves little MMA time
+      // to hide the read-modify-write behind)
+      if (blk.beta != 0.f) {
+#pragma unroll
+        for (int j = 0; j < BN / 32; ++j) {
+          const int64_t col = blk.n0 + 4 * lane + j, r0 = blk.m0 + 32 * q;
+          if (col < blk.N && r0 < blk.M) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(blk.C + r0 + col * blk.ldc));
+        }
+      }
+      float old[32], nxt[32];
+      load_chunk(0, old);
+      mbar_wait(&tfull[b], (t >> 1) & 1);
+      fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        // next chunk's C loads are in flight while this chunk is read from TMEM and stored
+        if (c0 + 32 < BN) load_chunk(c0 + 32, nxt);
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + b * BN + c0, v);
         if (r < blk.M) {
@@ -259,6 +272,8 @@ __device__ __forceinline__ void tc3_loop(const CUtensorMap* mapA, const CUtensor
             if (col < blk.N) crow[col * blk.ldc] = blk.alpha * v[j] + blk.beta * old[j];
           }
         }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) old[j] = nxt[j];
       }
       fence_before();
       __syncwarp();

@@ -4,7 +4,10 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_14466_b200 import _lib
 lib = _lib.load()
-for (m, n, k) in [(8192, 8192, 1024), (16384, 16384, 1024), (16384, 16384, 4096)]:
+SHAPES = [(8192, 8192, 1024), (16384, 16384, 1024), (16384, 16384, 4096)]
+if len(sys.argv) > 1:
+    SHAPES = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]]
+for (m, n, k) in SHAPES:
     A = torch.rand(k, m, dtype=torch.float32, device="cuda")
     B = torch.rand(k, n, dtype=torch.float32, device="cuda")
     Cm = torch.rand(n, m, dtype=torch.float32, device="cuda")
