@@ -197,6 +197,11 @@ __device__ __forceinline__ void tc3_loop(const CUtensorMap* mapA, const CUtensor
     // consecutive rows i of one 4-wide k chunk: the four scalar raw loads and
     // the 16-byte hi / lo stores are all bank-conflict free.
     const int sw = warp < 4 ? warp - 2 : warp - 6;  // 0..5
+    // A warp owns whole 32-row groups (operand x 4 groups = 8 per k-step): the
+    // lane's row is fixed, so the swizzle terms of its raw reads and K-major
+    // writes are computed once (xo / wo) and every access in the fully
+    // unrolled k loop is a register base plus an immediate.
+    const int xr = (lane >> 2) & 7;  // raw swizzle row phase ((i & 31) >> 2)
     uint32_t g = 0;
     Blk blk;
     for (int64_t item = blockIdx.x; next(item, blk); item += gridDim.x) {
@@ -206,19 +211,28 @@ __device__ __forceinline__ void tc3_loop(const CUtensorMap* mapA, const CUtensor
         mbar_wait(&spl_empty[ss], ((g / SPL_STAGES) & 1) ^ 1);
         const unsigned char* rst = raw + (size_t)rs * RAW_BYTES;
         unsigned char* sst = spl + (size_t)ss * SPL_BYTES;
-        // units: (operand, 32-row group, k chunk) = 2 x 4 x 8 = 64, warp-strided
-        for (int u = sw; u < 64; u += SPLIT_WARPS) {
-          const int op = u >> 5, grp = (u >> 3) & 3, c = u & 7;
-          const int i = grp * 32 + lane;
-          const unsigned char* rsrc = rst + op * PLANE_A;
-          float x[4];
+        for (int rg = sw; rg < 8; rg += SPLIT_WARPS) {
+          const int op = rg >> 2, grp = rg & 3;
+          const int i = grp * 32 + lane, xw = i & 7;
+          const unsigned char* rsrc = rst + op * PLANE_A + grp * ATOM_BYTES + ((lane & 3) << 2);
+          unsigned char* dst = sst + op * 2 * PLANE_A + (i >> 3) * 1024 + (i & 7) * 128;
+          const unsigned char* rb[8];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) x[e] = *reinterpret_cast<const float*>(rsrc + raw_off(i, 4 * c + e));
-          const float4 h = make_float4(tf32_rna(x[0]), tf32_rna(x[1]), tf32_rna(x[2]), tf32_rna(x[3]));
-          const float4 l = make_float4(x[0] - h.x, x[1] - h.y, x[2] - h.z, x[3] - h.w);
-          unsigned char* dst = sst + op * 2 * PLANE_A + kmaj_off(i, c);
-          *reinterpret_cast<float4*>(dst) = h;
-          *reinterpret_cast<float4*>(dst + PLANE_A) = l;
+          for (int j = 0; j < 8; ++j) rb[j] = rsrc + ((xr ^ j) << 4);
+#pragma unroll
+          for (int c = 0; c < BK / 4; ++c) {
+            float x[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int k = 4 * c + e;
+              x[e] = *reinterpret_cast<const float*>(rb[k & 7] + k * 128);
+            }
+            const float4 h = make_float4(tf32_rna(x[0]), tf32_rna(x[1]), tf32_rna(x[2]), tf32_rna(x[3]));
+            const float4 l = make_float4(x[0] - h.x, x[1] - h.y, x[2] - h.z, x[3] - h.w);
+            unsigned char* d = dst + ((c ^ xw) << 4);
+            *reinterpret_cast<float4*>(d) = h;
+            *reinterpret_cast<float4*>(d + PLANE_A) = l;
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();
