@@ -119,6 +119,11 @@ int bcmg_redistribute_plan(int64_t n_cols, int64_t tile, int ndev, int world, in
 
 /* ---- sessions ---- */
 int bcmg_nccl_unique_id(unsigned char* id /* [128] */);
+/* In-process loopback transport id: sessions opened with the same id in ONE
+   process (one host thread per rank, each with its own streams, normally all
+   on one GPU) exchange data by event-ordered device-to-device copies instead
+   of NCCL -- runs the multi-process drivers on a single GPU (tests). */
+int bcmg_loopback_id(unsigned char* id /* [128] */);
 int bcmg_open(int cuda_device, int rank, int world, const unsigned char* nccl_id /* NULL if world==1 */,
               bcmg_session** out);
 int bcmg_close(bcmg_session* s);

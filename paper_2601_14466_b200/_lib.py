@@ -63,6 +63,7 @@ SIGNATURES = {
     "bcmg_kernel_stats": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_double)]),
     "bcmg_launch_count": (C.c_int64, []),
     "bcmg_measure_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
+    "bcmg_loopback_id": (C.c_int, [C.c_char_p]),
     "bcmg_generate_spd": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _vp, _i64, C.c_uint64, C.c_double]),
 }
 

@@ -8,6 +8,7 @@
 
 #include "../../include/bcmg_b200.h"
 #include "ops.h"
+#include "comm.h"
 #include "solver.h"
 
 struct bcmg_session {
@@ -177,6 +178,13 @@ int bcmg_nccl_unique_id(unsigned char* id) {
     if (r != ncclSuccess) throw bcmg::Error(BCMG_ERR_CUDA, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
     static_assert(sizeof(u) == 128, "NCCL unique id is 128 bytes");
     std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+int bcmg_loopback_id(unsigned char* id) {
+  return guarded([&] {
+    if (!id) throw bcmg::Error(BCMG_ERR_CONFIG, "null id");
+    bcmg::make_loopback_id(id);
   });
 }
 

@@ -1,0 +1,259 @@
+// Transports of comm.h.
+#include "comm.h"
+
+#include <nccl.h>
+
+#include <atomic>
+#include <climits>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace bcmg {
+
+#define BCMG_NCCL_CALL(call)                                                                          \
+  do {                                                                                                \
+    ncclResult_t r_ = (call);                                                                         \
+    if (r_ != ncclSuccess) throw Error(CUDA, std::string(#call) + ": " + ncclGetErrorString(r_));     \
+  } while (0)
+
+// ------------------------------------------------------------------ NCCL
+class NcclComm final : public Comm {
+ public:
+  NcclComm(int rank, int world, const unsigned char* id) {
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    BCMG_NCCL_CALL(ncclCommInitRank(&c_, world, u, rank));
+  }
+  ~NcclComm() override {
+    if (c_) ncclCommDestroy(c_);
+  }
+  void bcast(void* buf, size_t bytes, int root, cudaStream_t st) override {
+    BCMG_NCCL_CALL(ncclBroadcast(buf, buf, bytes, ncclUint8, root, c_, st));
+  }
+  void group_start() override { BCMG_NCCL_CALL(ncclGroupStart()); }
+  void send(const void* buf, size_t bytes, int peer, cudaStream_t st) override {
+    BCMG_NCCL_CALL(ncclSend(buf, bytes, ncclUint8, peer, c_, st));
+  }
+  void recv(void* buf, size_t bytes, int peer, cudaStream_t st) override {
+    BCMG_NCCL_CALL(ncclRecv(buf, bytes, ncclUint8, peer, c_, st));
+  }
+  void group_end() override { BCMG_NCCL_CALL(ncclGroupEnd()); }
+  int allreduce_min(int v, void* scratch, cudaStream_t st) override {
+    int* d = static_cast<int*>(scratch);
+    BCMG_CUDA(cudaMemcpyAsync(d, &v, sizeof(int), cudaMemcpyHostToDevice, st));
+    BCMG_NCCL_CALL(ncclAllReduce(d, d, 1, ncclInt32, ncclMin, c_, st));
+    int out = 0;
+    BCMG_CUDA(cudaMemcpyAsync(&out, d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    BCMG_CUDA(cudaStreamSynchronize(st));
+    return out;
+  }
+
+ private:
+  ncclComm_t c_ = nullptr;
+};
+
+// ------------------------------------------------------------------ loopback
+namespace {
+
+cudaEvent_t new_event() {
+  cudaEvent_t e;
+  BCMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return e;
+}
+
+struct Hub {
+  explicit Hub(int w) : world(w) {}
+  const int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  struct Bcast {
+    const void* src = nullptr;
+    cudaEvent_t ready = nullptr;
+    std::vector<cudaEvent_t> done;
+    bool posted = false;
+  };
+  std::map<uint64_t, Bcast> bcasts;  // by collective sequence number
+  struct Msg {
+    const void* src;
+    size_t bytes;
+    cudaEvent_t ready;
+    cudaEvent_t done = nullptr;
+    bool acked = false;
+  };
+  std::map<std::pair<int, int>, std::deque<std::shared_ptr<Msg>>> queues;  // (sender, receiver) FIFO
+  struct Reduce {
+    int count = 0, value = INT_MAX, reads = 0;
+  };
+  std::map<uint64_t, Reduce> reduces;
+};
+
+std::mutex g_hubs_mu;
+std::map<uint64_t, std::weak_ptr<Hub>> g_hubs;
+std::atomic<uint64_t> g_next_key{1};
+constexpr char kMagic[] = "bcmg-loopback-v1";
+
+std::shared_ptr<Hub> join_hub(uint64_t key, int world) {
+  std::lock_guard<std::mutex> lk(g_hubs_mu);
+  auto it = g_hubs.find(key);
+  if (it != g_hubs.end())
+    if (auto h = it->second.lock()) {
+      if (h->world != world) throw Error(CONFIG, "loopback id reused with a different world size");
+      return h;
+    }
+  auto h = std::make_shared<Hub>(world);
+  g_hubs[key] = h;
+  return h;
+}
+
+}  // namespace
+
+class LoopbackComm final : public Comm {
+ public:
+  LoopbackComm(int rank, int world, uint64_t key) : rank_(rank), hub_(join_hub(key, world)) {}
+
+  void bcast(void* buf, size_t bytes, int root, cudaStream_t st) override {
+    const uint64_t seq = bc_seq_++;
+    std::unique_lock<std::mutex> lk(hub_->mu);
+    auto& b = hub_->bcasts[seq];
+    if (rank_ == root) {
+      cudaEvent_t ready = new_event();
+      BCMG_CUDA(cudaEventRecord(ready, st));
+      b.src = buf;
+      b.ready = ready;
+      b.posted = true;
+      hub_->cv.notify_all();
+      // the source buffer stays untouched until every receiver's copy has run
+      hub_->cv.wait(lk, [&] { return (int)hub_->bcasts[seq].done.size() == hub_->world - 1; });
+      auto& bb = hub_->bcasts[seq];
+      for (cudaEvent_t e : bb.done) {
+        BCMG_CUDA(cudaStreamWaitEvent(st, e, 0));
+        cudaEventDestroy(e);
+      }
+      cudaEventDestroy(bb.ready);
+      hub_->bcasts.erase(seq);
+      return;
+    }
+    hub_->cv.wait(lk, [&] { return hub_->bcasts[seq].posted; });
+    const void* src = hub_->bcasts[seq].src;
+    cudaEvent_t ready = hub_->bcasts[seq].ready;
+    lk.unlock();
+    BCMG_CUDA(cudaStreamWaitEvent(st, ready, 0));
+    if (bytes) BCMG_CUDA(cudaMemcpyAsync(buf, src, bytes, cudaMemcpyDeviceToDevice, st));
+    cudaEvent_t done = new_event();
+    BCMG_CUDA(cudaEventRecord(done, st));
+    lk.lock();
+    hub_->bcasts[seq].done.push_back(done);
+    hub_->cv.notify_all();
+  }
+
+  void group_start() override {
+    sends_.clear();
+    recvs_.clear();
+  }
+  void send(const void* buf, size_t bytes, int peer, cudaStream_t st) override {
+    auto m = std::make_shared<Hub::Msg>();
+    m->src = buf;
+    m->bytes = bytes;
+    m->ready = new_event();
+    BCMG_CUDA(cudaEventRecord(m->ready, st));
+    {
+      std::lock_guard<std::mutex> lk(hub_->mu);
+      hub_->queues[{rank_, peer}].push_back(m);
+    }
+    hub_->cv.notify_all();
+    sends_.push_back({m, st});
+  }
+  void recv(void* buf, size_t bytes, int peer, cudaStream_t st) override { recvs_.push_back({buf, bytes, peer, st}); }
+  void group_end() override {
+    // receives first (every send of the group is already posted), then wait for
+    // the receivers of our sends so that the send buffers can be reused
+    for (const auto& r : recvs_) {
+      std::shared_ptr<Hub::Msg> m;
+      {
+        std::unique_lock<std::mutex> lk(hub_->mu);
+        auto& q = hub_->queues[{r.peer, rank_}];
+        hub_->cv.wait(lk, [&] { return !q.empty(); });
+        m = q.front();
+        q.pop_front();
+      }
+      if (m->bytes != r.bytes) throw Error(CONFIG, "loopback: send/recv size mismatch");
+      BCMG_CUDA(cudaStreamWaitEvent(r.st, m->ready, 0));
+      if (r.bytes) BCMG_CUDA(cudaMemcpyAsync(r.buf, m->src, r.bytes, cudaMemcpyDeviceToDevice, r.st));
+      cudaEvent_t done = new_event();
+      BCMG_CUDA(cudaEventRecord(done, r.st));
+      {
+        std::lock_guard<std::mutex> lk(hub_->mu);
+        m->done = done;
+        m->acked = true;
+      }
+      hub_->cv.notify_all();
+    }
+    for (auto& s : sends_) {
+      std::unique_lock<std::mutex> lk(hub_->mu);
+      hub_->cv.wait(lk, [&] { return s.m->acked; });
+      lk.unlock();
+      BCMG_CUDA(cudaStreamWaitEvent(s.st, s.m->done, 0));
+      cudaEventDestroy(s.m->done);
+      cudaEventDestroy(s.m->ready);
+    }
+    sends_.clear();
+    recvs_.clear();
+  }
+
+  int allreduce_min(int v, void*, cudaStream_t) override {
+    const uint64_t seq = red_seq_++;
+    std::unique_lock<std::mutex> lk(hub_->mu);
+    auto& r = hub_->reduces[seq];
+    r.count++;
+    r.value = std::min(r.value, v);
+    hub_->cv.notify_all();
+    hub_->cv.wait(lk, [&] { return hub_->reduces[seq].count == hub_->world; });
+    auto& rr = hub_->reduces[seq];
+    const int out = rr.value;
+    if (++rr.reads == hub_->world) hub_->reduces.erase(seq);
+    return out;
+  }
+
+ private:
+  struct PendingSend {
+    std::shared_ptr<Hub::Msg> m;
+    cudaStream_t st;
+  };
+  struct PendingRecv {
+    void* buf;
+    size_t bytes;
+    int peer;
+    cudaStream_t st;
+  };
+  const int rank_;
+  std::shared_ptr<Hub> hub_;
+  uint64_t bc_seq_ = 0, red_seq_ = 0;
+  std::vector<PendingSend> sends_;
+  std::vector<PendingRecv> recvs_;
+};
+
+void make_loopback_id(unsigned char* id) {
+  std::memset(id, 0, kCommIdBytes);
+  std::memcpy(id, kMagic, sizeof(kMagic));
+  const uint64_t key = g_next_key.fetch_add(1);
+  std::memcpy(id + 32, &key, sizeof(key));
+}
+
+std::unique_ptr<Comm> make_comm(int rank, int world, const unsigned char* id) {
+  if (!id) throw Error(CONFIG, "world > 1 needs a communicator id (bcmg_nccl_unique_id / bcmg_loopback_id)");
+  if (std::memcmp(id, kMagic, sizeof(kMagic)) == 0) {
+    uint64_t key;
+    std::memcpy(&key, id + 32, sizeof(key));
+    return std::make_unique<LoopbackComm>(rank, world, key);
+  }
+  return std::make_unique<NcclComm>(rank, world, id);
+}
+
+}  // namespace bcmg

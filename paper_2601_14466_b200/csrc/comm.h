@@ -1,0 +1,43 @@
+// Transport between the processes ("ranks") of a session.
+//
+//   * NcclComm     -- one process per GPU: ncclBroadcast / grouped
+//                     ncclSend+ncclRecv / ncclAllReduce on the caller's stream.
+//   * LoopbackComm -- several sessions of ONE process act as the ranks, each on
+//                     its own host thread and streams (normally on one GPU):
+//                     every transfer is a device-to-device copy ordered by
+//                     CUDA events, matched on the host exactly as NCCL matches
+//                     collectives (same call order on every rank) and
+//                     point-to-point messages (FIFO per sender/receiver pair).
+//                     No kernel ever waits on another rank, so ranks sharing
+//                     one GPU cannot deadlock it.  This runs the multi-process
+//                     drivers (schedules, events, buffers) on a single GPU.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <memory>
+
+namespace bcmg {
+
+class Comm {
+ public:
+  virtual ~Comm() = default;
+  // bytes of buf from `root` to every rank (stream-ordered on st)
+  virtual void bcast(void* buf, size_t bytes, int root, cudaStream_t st) = 0;
+  // grouped point-to-point exchange: sends and receives between group_start
+  // and group_end are matched per (sender, receiver) pair in issue order
+  virtual void group_start() = 0;
+  virtual void send(const void* buf, size_t bytes, int peer, cudaStream_t st) = 0;
+  virtual void recv(void* buf, size_t bytes, int peer, cudaStream_t st) = 0;
+  virtual void group_end() = 0;
+  // host value in, minimum over ranks out (synchronous); scratch: 4 device bytes
+  virtual int allreduce_min(int v, void* scratch, cudaStream_t st) = 0;
+};
+
+constexpr size_t kCommIdBytes = 128;
+// id: kCommIdBytes from bcmg_nccl_unique_id (NCCL) or bcmg_loopback_id (loopback)
+std::unique_ptr<Comm> make_comm(int rank, int world, const unsigned char* id);
+void make_loopback_id(unsigned char* id);
+
+}  // namespace bcmg

@@ -18,8 +18,6 @@
 //                  diagonal-block inverses kept by potrf (solvers.py:430-474)
 //   potri        : W = L^-1 sweep, A^-1 = W^H W sweep, Hermitian mirror
 //                  (solvers.py:487-594)
-#include <nccl.h>
-
 #include <algorithm>
 #include <cstdlib>
 #include <atomic>
@@ -53,12 +51,6 @@ void DevBuf::release() {
   bytes = 0;
 }
 
-#define BCMG_NCCL(call)                                                                  \
-  do {                                                                                   \
-    ncclResult_t r_ = (call);                                                            \
-    if (r_ != ncclSuccess) throw Error(CUDA, std::string(#call) + ": " + ncclGetErrorString(r_)); \
-  } while (0)
-
 // ------------------------------------------------------------------ session
 Session::Session(int device_, int rank_, int world_, const unsigned char* nccl_id) : device(device_), rank(rank_), world(world_) {
   if (world < 1 || rank < 0 || rank >= world) throw Error(CONFIG, "bad rank/world");
@@ -71,20 +63,13 @@ Session::Session(int device_, int rank_, int world_, const unsigned char* nccl_i
   for (auto& e : ev_pool) BCMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : ev_time) BCMG_CUDA(cudaEventCreate(&e));
   BCMG_CUDA(cudaMallocHost(&info_host, sizeof(int)));
-  if (world > 1) {
-    if (!nccl_id) throw Error(CONFIG, "world > 1 needs an NCCL unique id");
-    ncclUniqueId id;
-    std::memcpy(&id, nccl_id, sizeof(id));
-    ncclComm_t c;
-    BCMG_NCCL(ncclCommInitRank(&c, world, id, rank));
-    nccl = c;
-  }
+  if (world > 1) net = make_comm(rank, world, nccl_id);
 }
 
 Session::~Session() {
   cudaSetDevice(device);
   cudaDeviceSynchronize();
-  if (nccl) ncclCommDestroy(static_cast<ncclComm_t>(nccl));
+  net.reset();
   for (auto* b : {&panel[0], &panel[1], &panel_pb[0], &panel_pb[1], &dinv, &wdiag, &info_dev, &tmp, &acc, &plan_buf,
                   &stage_buf, &desc_buf, &embed_buf})
     b->release();
@@ -170,19 +155,13 @@ void Session::mark(int phase) {
 
 void Session::bcast(void* buf, size_t bytes, int root, cudaStream_t st) {
   if (world == 1 || bytes == 0) return;
-  BCMG_NCCL(ncclBroadcast(buf, buf, bytes, ncclUint8, root, static_cast<ncclComm_t>(nccl), st));
+  net->bcast(buf, bytes, root, st);
 }
 
 int Session::reduce_info(int local) {
   if (world == 1) return local;
   // smallest nonzero pivot over ranks (later tiles can only fail at larger pivots)
-  int* d = static_cast<int*>(tmp.p);
-  const int v = local ? local : 0x7fffffff;
-  BCMG_CUDA(cudaMemcpyAsync(d, &v, sizeof(int), cudaMemcpyHostToDevice, comm));
-  BCMG_NCCL(ncclAllReduce(d, d, 1, ncclInt32, ncclMin, static_cast<ncclComm_t>(nccl), comm));
-  int out = 0;
-  BCMG_CUDA(cudaMemcpyAsync(&out, d, sizeof(int), cudaMemcpyDeviceToHost, comm));
-  BCMG_CUDA(cudaStreamSynchronize(comm));
+  const int out = net->allreduce_min(local ? local : 0x7fffffff, tmp.p, comm);
   return out == 0x7fffffff ? 0 : out;
 }
 
@@ -384,19 +363,16 @@ void Session::redistribute_multi(int dt, int64_t n_rows, int64_t n_cols, int64_t
   desc_buf.ensure(std::max<size_t>(8, h.size() * 8));
   const uint64_t* d = static_cast<const uint64_t*>(desc_buf.p);
   if (!h.empty()) BCMG_CUDA(cudaMemcpyAsync(desc_buf.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, crit));
-  auto comm_ = static_cast<ncclComm_t>(nccl);
   for (int64_t o = 0; o < seg_bytes; o += CH) {
     const int64_t len = std::min(CH, seg_bytes - o);
     timed(K_ROTATE, crit, 2.0 * (double)len * (npk), [&] {
       chunk_copy(d, d + npk, (int)npk, o, 0, len, vec, crit);
     });
     if (world > 1) {
-      BCMG_NCCL(ncclGroupStart());
-      for (size_t j = 0; j < sends.size(); ++j)
-        BCMG_NCCL(ncclSend(pack + j * CH, (size_t)len, ncclUint8, sends[j]->dst_rank, comm_, crit));
-      for (size_t j = 0; j < recvs.size(); ++j)
-        BCMG_NCCL(ncclRecv(recv + j * CH, (size_t)len, ncclUint8, recvs[j]->src_rank, comm_, crit));
-      BCMG_NCCL(ncclGroupEnd());
+      net->group_start();
+      for (size_t j = 0; j < sends.size(); ++j) net->send(pack + j * CH, (size_t)len, sends[j]->dst_rank, crit);
+      for (size_t j = 0; j < recvs.size(); ++j) net->recv(recv + j * CH, (size_t)len, recvs[j]->src_rank, crit);
+      net->group_end();
     }
     chunk_copy(d + 2 * npk, d + 2 * npk + nup, (int)nup, 0, o, len, vec, crit);
   }
@@ -767,7 +743,6 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
     for (int e = 0; e < d; ++e) o += cols_upto(g, e, s);
     return o * (g.stop(s) - g.start(s));
   };
-  auto comm_ = static_cast<ncclComm_t>(nccl);
   for (const SchedOp& op : potri_schedule(n, T, ndev, world, rank)) {
     const int64_t s = op.k, ss = g.start(s), se = g.stop(s), tcs = se - ss;
     switch (op.kind) {
@@ -847,19 +822,19 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
         const int root = (int)op.root;
         if (world > 1) {
           const size_t off = (size_t)block_off(s, g.dev0) * g.esz;
-          BCMG_NCCL(ncclGroupStart());
+          net->group_start();
           if (rank != root) {
-            if (op.elems) BCMG_NCCL(ncclSend(blocks + off, (size_t)op.elems * g.esz, ncclUint8, root, comm_, st));
+            if (op.elems) net->send(blocks + off, (size_t)op.elems * g.esz, root, st);
           } else {
             for (int r = 0; r < world; ++r) {
               if (r == root) continue;
               const int d0 = r * g.nloc;
               const size_t bytes = (size_t)(block_off(s, d0 + g.nloc) - block_off(s, d0)) * g.esz;
               if (bytes)
-                BCMG_NCCL(ncclRecv(blocks + (size_t)block_off(s, d0) * g.esz, bytes, ncclUint8, r, comm_, st));
+                net->recv(blocks + (size_t)block_off(s, d0) * g.esz, bytes, r, st);
             }
           }
-          BCMG_NCCL(ncclGroupEnd());
+          net->group_end();
         }
         if (rank != root) break;
         // mirror: tile s rows [start_j, stop_j) = (block (s, j))^H for every j < s, any device

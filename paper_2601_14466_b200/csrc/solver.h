@@ -4,9 +4,11 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <memory>
 #include <cstdint>
 #include <vector>
 
+#include "comm.h"
 #include "common.cuh"
 
 namespace bcmg {
@@ -53,7 +55,7 @@ enum Phase : int { T_BEGIN = 0, T_REDIST = 1, T_POTRF = 2, T_SOLVE = 3, T_END = 
 
 struct Session {
   int device, rank, world;
-  void* nccl = nullptr;  // ncclComm_t when world > 1
+  std::unique_ptr<Comm> net;  // world > 1: NCCL or in-process loopback transport
   cudaStream_t crit = nullptr, bulk = nullptr, comm = nullptr, user = nullptr;
   static constexpr int kEvents = 64, kJoin = 56, kTimeEvents = 5;
   cudaEvent_t ev_pool[kEvents];

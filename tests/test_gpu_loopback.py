@@ -1,0 +1,151 @@
+"""The multi-process drivers on ONE GPU: `world` sessions of this process act
+as the ranks (one host thread each, own streams), joined by the in-process
+loopback transport (bcmg_loopback_id) instead of NCCL.  This runs the exact
+world > 1 code of solver.cu -- cross-process redistribution (pack / grouped
+send+recv / unpack), per-step panel broadcasts, substitution hand-offs, potri's
+W-tile broadcasts and block gathers, the info all-reduce -- on the device, and
+the result must be bit-identical to the single-process run (the reference's
+bit-exactness across device counts, test_solvers.py:172-179)."""
+
+import ctypes as C
+import threading
+
+import numpy as np
+import pytest
+
+
+bc = pytest.importorskip("paper_2601_14466_b200")
+from paper_2601_14466_b200 import _lib  # noqa: E402
+from oracle import bcmg_oracle as O  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+CODES = {np.float32: 0, np.float64: 1, np.complex64: 2, np.complex128: 3}
+
+
+def _run_ranks(world, body):
+    """body(rank, session, stream) on `world` threads with loopback sessions."""
+    import torch
+
+    lib = _lib.load()
+    idbuf = C.create_string_buffer(128)
+    _lib.check(lib.bcmg_loopback_id(idbuf))
+    sessions = []
+    for r in range(world):
+        s = C.c_void_p()
+        _lib.check(lib.bcmg_open(torch.cuda.current_device(), r, world, idbuf.raw, C.byref(s)))
+        sessions.append(s)
+    results, errors = [None] * world, []
+
+    def work(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                results[r] = body(r, sessions[r], st)
+            st.synchronize()
+        except Exception as exc:  # noqa: BLE001
+            errors.append((r, exc))
+
+    threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in threads), "a rank hung"
+    torch.cuda.synchronize()
+    for s in sessions:
+        _lib.check(lib.bcmg_close(s))
+    assert not errors, errors
+    return results
+
+
+def _local_shards(a, n, t, ndev, world, r, device):
+    """This rank's logical devices' shards (contiguous layout), back to back."""
+    import torch
+
+    counts = [0] * ndev
+    arr = (C.c_int64 * ndev)()
+    _lib.check(_lib.load().bcmg_column_counts(n, t, ndev, arr))
+    counts = list(arr)
+    nloc = ndev // world
+    c0 = sum(counts[: r * nloc])
+    c1 = c0 + sum(counts[r * nloc:(r + 1) * nloc])
+    block = torch.from_numpy(np.ascontiguousarray(a[:, c0:c1].T)).to(device)  # column-major n x (c1 - c0)
+    ptrs, off = [], 0
+    for d in range(r * nloc, (r + 1) * nloc):
+        ptrs.append(block.data_ptr() + off * n * block.element_size())
+        off += counts[d]
+    return block, _lib.ptr_array(ptrs), (c0, c1)
+
+
+@pytest.mark.parametrize("dtype,n,t,ndev,world", [
+    (np.float64, 300, 32, 2, 2), (np.float64, 512, 64, 4, 2), (np.complex128, 260, 24, 4, 2),
+    (np.float32, 384, 64, 4, 4), (np.complex64, 200, 40, 2, 2), (np.float64, 2048, 256, 4, 2),
+])
+def test_loopback_potrs_matches_single_process(dtype, n, t, ndev, world):
+    import torch
+
+    lib = _lib.load()
+    a = O.make_matrix("random_spd", n, dtype, 11)
+    b = np.asfortranarray(np.random.default_rng(2).standard_normal((n, 3)).astype(dtype))
+    base, _ = bc.solve_positive_definite(bc.make_mesh(ndev), a, b, bc.TileSpec(t))
+
+    def body(r, sess, st):
+        block, ptrs, _ = _local_shards(a, n, t, ndev, world, r, "cuda")
+        x = torch.from_numpy(np.ascontiguousarray(b.T)).to("cuda")  # column-major replica
+        info = C.c_int(0)
+        _lib.check(lib.bcmg_potrs(sess, C.c_void_p(st.cuda_stream), CODES[dtype], n, 3, t, ndev, ptrs,
+                                  C.c_void_p(x.data_ptr()), n, 0, C.byref(info)))
+        assert info.value == 0
+        st.synchronize()
+        return x.cpu().numpy().T
+
+    xs = _run_ranks(world, body)
+    for x in xs:
+        assert np.array_equal(x, base), "replicated solution differs from the single-process bits"
+    eps = O.eps_of(dtype)
+    assert O.solve_residual(a, xs[0], b) <= 100 * n * eps
+
+
+@pytest.mark.parametrize("dtype,n,t,ndev,world", [
+    (np.float64, 256, 32, 2, 2), (np.complex128, 192, 24, 4, 2), (np.float64, 1024, 128, 4, 4),
+])
+def test_loopback_potri_matches_single_process(dtype, n, t, ndev, world):
+    lib = _lib.load()
+    a = O.make_matrix("random_spd", n, dtype, 12)
+    base, _ = bc.invert_positive_definite(bc.make_mesh(ndev), a, bc.TileSpec(t))
+
+    def body(r, sess, st):
+        block, ptrs, cols = _local_shards(a, n, t, ndev, world, r, "cuda")
+        info = C.c_int(0)
+        _lib.check(lib.bcmg_potri(sess, C.c_void_p(st.cuda_stream), CODES[dtype], n, t, ndev, ptrs, 0,
+                                  C.byref(info)))
+        assert info.value == 0
+        st.synchronize()
+        return cols, block.cpu().numpy().T
+
+    parts = _run_ranks(world, body)
+    inv = np.zeros((n, n), dtype=dtype, order="F")
+    for (c0, c1), blk in parts:
+        inv[:, c0:c1] = blk
+    assert np.array_equal(inv, base)
+
+
+def test_loopback_not_positive_definite_info_on_every_rank():
+    """The pivot found on one rank reaches every rank (the info all-reduce)."""
+    import torch
+
+    lib = _lib.load()
+    n, t, ndev, world = 96, 16, 2, 2
+    a = np.asfortranarray(np.diag(np.arange(1.0, n + 1)))
+    a[70, 70] = -1.0  # tile 4 -> logical device 0 -> rank 0; the pivot is global column 71
+
+    def body(r, sess, st):
+        block, ptrs, _ = _local_shards(a, n, t, ndev, world, r, "cuda")
+        x = torch.ones(n, dtype=torch.float64, device="cuda")
+        info = C.c_int(0)
+        rc = lib.bcmg_potrs(sess, C.c_void_p(st.cuda_stream), 1, n, 1, t, ndev, ptrs, C.c_void_p(x.data_ptr()), n,
+                            0, C.byref(info))
+        return rc, info.value
+
+    for rc, info in _run_ranks(world, body):
+        assert rc == _lib.BCMG_ERR_NOT_POSITIVE_DEFINITE and info == 71
