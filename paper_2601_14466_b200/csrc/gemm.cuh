@@ -420,6 +420,11 @@ struct TrailParams {
   // the update is then one real GEMM with interleaved re/im output rows
   const void* PB;
   int cplx;
+  // float32 / complex64 on tcgen05: the panel pre-split into tf32 hi / lo
+  // planes, K-major (row-major rows x ld): A hi, A lo, B hi, B lo (A == B for
+  // real input; complex64: A = [P | -iP] with 2x the rows, B = [Re P | Im P])
+  const float* split[4];
+  int64_t split_ld[2];
   int64_t ldp, prow0;
   int64_t N, T, K;    // matrix order, tile width, panel width
   int D, dev0, nloc;  // logical devices; this launch owns dev0 .. dev0+nloc-1

@@ -12,6 +12,7 @@
 
 #include "gemm_tma.cuh"
 #include "tc_gemm.cuh"
+#include "tc_gemm_k.cuh"
 #include "ops.h"
 
 namespace bcmg {
@@ -88,6 +89,9 @@ static void launch_gemm(int64_t M, int64_t N, int64_t K, const Operand& A, const
 static bool use_tma();
 static unsigned ew_grid(int64_t total);
 static bool use_tc();
+static bool use_presplit();
+static void gemm_tck_generic(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+                             const int* info, cudaStream_t st);
 static bool tc_ok(const void* p, int64_t ld);
 static void launch_tc3_gemm(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
                             const int* info, cudaStream_t st);
@@ -112,6 +116,8 @@ static void gemm_t(int64_t M, int64_t N, int64_t K, const Operand& A, const Oper
     }
   }
   if constexpr (std::is_same_v<S, float>) {
+    if (use_tc() && use_presplit() && !A.mask && !B.mask && aligned16(ep.C) && M >= 256 && N >= 64 && K >= 32)
+      return gemm_tck_generic(M, N, K, A, B, ep, info, st);
     if (use_tc() && !A.trans && !B.trans && !A.mask && !B.mask && tc_ok(A.ptr, A.ld) && tc_ok(B.ptr, B.ld) &&
         tc_ok(ep.C, 4) && M >= 256 && N >= 64 && K >= 32)
       return launch_tc3_gemm(M, N, K, A, B, ep, info, st);
@@ -488,7 +494,168 @@ static void launch_tc3_gemm(int64_t M, int64_t N, int64_t K, const Operand& A, c
   BCMG_CHECK_LAUNCH();
 }
 
+// ---------------------------------------------------------------- pre-split tf32 planes
+// X (rows x Kx, logical) -> hi = rna_tf32(x), lo = x - hi, stored K-major
+// (row-major, ld kp >= Kx, columns [Kx, kp) zero) for tck_* kernels.
+//   mode 0: real float, X(m, k) = src[m + k*ld] (column-major)
+//   mode 1: complex64 embedding A = [P | -iP] as a (2R) x (2Kc) real matrix
+//           (re / im interleaved rows), P complex R x Kc, ld ld (complex)
+//   mode 2: complex64 planar B = [Re P | Im P] (R x 2Kc)
+template <int MODE>
+__global__ void split_tf32_kernel(const float* __restrict__ src, int64_t ld, int64_t rows, int64_t Kx, int64_t kc,
+                                  float* __restrict__ hi, float* __restrict__ lo, int64_t kp) {
+  __shared__ float t[32][33];
+  const int64_t m0 = (int64_t)blockIdx.x * 32, k0 = (int64_t)blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t m = m0 + threadIdx.x, k = k0 + y;  // coalesced along m (column-major source)
+    float v = 0.f;
+    if (m < rows && k < Kx) {
+      if (MODE == 0) {
+        v = src[m + k * ld];
+      } else if (MODE == 3) {
+        v = src[k + m * ld];  // transposed view (k contiguous)
+      } else if (MODE == 1) {
+        const int64_t kk = k < kc ? k : k - kc, r = m >> 1;
+        const float* e = src + 2 * (r + kk * ld);
+        if (k < kc) v = e[m & 1];
+        else v = (m & 1) ? -e[0] : e[1];  // -i P = (im, -re)
+      } else {
+        const int64_t kk = k < kc ? k : k - kc;
+        v = src[2 * (m + kk * ld) + (k < kc ? 0 : 1)];
+      }
+    }
+    t[y][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t m = m0 + y, k = k0 + threadIdx.x;  // coalesced along k (row-major planes)
+    if (m >= rows || k >= kp) continue;
+    const float x = t[threadIdx.x][y];
+    const float h = tc::tf32_rna(x);
+    hi[m * kp + k] = h;
+    lo[m * kp + k] = x - h;
+  }
+}
+
+int64_t split_ld(int64_t kx) { return (kx + 3) / 4 * 4; }
+
+void split_tf32(int mode, const void* src, int64_t ld, int64_t rows, int64_t Kx, int64_t kc, float* hi, float* lo,
+                int64_t kp, cudaStream_t st) {
+  if (rows <= 0 || kp <= 0) return;
+  dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((kp + 31) / 32)), block(32, 8);
+  const float* s = static_cast<const float*>(src);
+  if (mode == 0) split_tf32_kernel<0><<<grid, block, 0, st>>>(s, ld, rows, Kx, kc, hi, lo, kp);
+  else if (mode == 1) split_tf32_kernel<1><<<grid, block, 0, st>>>(s, ld, rows, Kx, kc, hi, lo, kp);
+  else if (mode == 2) split_tf32_kernel<2><<<grid, block, 0, st>>>(s, ld, rows, Kx, kc, hi, lo, kp);
+  else split_tf32_kernel<3><<<grid, block, 0, st>>>(s, ld, rows, Kx, kc, hi, lo, kp);
+  BCMG_CHECK_LAUNCH();
+}
+
+// K-major plane map: dims {kp, rows}, box {32 k, 128 rows}, SWIZZLE_128B (the
+// canonical K-major layout of the UMMA descriptors).
+static CUtensorMap make_map_kmajor(const float* base, int64_t rows, int64_t kp) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kp * 4};
+  cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)tc::BM};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(CUDA, "cuTensorMapEncodeTiled (k-major) failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+bool tc_presplit_enabled();
+static bool use_presplit() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BCMG_TC_INLINE_SPLIT");
+    v = (e && atoi(e)) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+bool tc_presplit_enabled() { return use_tc() && use_presplit(); }
+
+static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t st) {
+  int64_t total = 0;
+  for (int64_t m = p.m_first; m < p.m_last; ++m) {
+    const int dev = (int)(m % p.D);
+    if (dev < p.dev0 || dev >= p.dev0 + p.nloc) continue;
+    const int64_t rows = p.N - m * p.T, tcm = std::min(p.T, rows);
+    total += p.cplx ? TrapH<tc::BM / 2, tc::BN>::count(rows, tcm) : Trap<tc::BM, tc::BN>::count(rows, tcm);
+  }
+  if (total == 0) return;
+  const int64_t prow = p.N - p.prow0, arows = p.cplx ? 2 * prow : prow;
+  const CUtensorMap ah = make_map_kmajor(p.split[0], arows, p.split_ld[0]);
+  const CUtensorMap al = make_map_kmajor(p.split[1], arows, p.split_ld[0]);
+  const CUtensorMap bh = make_map_kmajor(p.split[2], prow, p.split_ld[1]);
+  const CUtensorMap bl = make_map_kmajor(p.split[3], prow, p.split_ld[1]);
+  set_smem(tck_trail_kernel, tck::SMEM_BYTES);
+  const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, num_sms()) : num_sms();
+  const int64_t grid = std::min<int64_t>(total, sms);
+  tck_trail_kernel<<<(unsigned)grid, tck::THREADS, tck::SMEM_BYTES, st>>>(ah, al, bh, bl, p, info);
+  BCMG_CHECK_LAUNCH();
+}
+
+// C = alpha*A*B^T + beta*C (float32) on pre-split planes Ah/Al (M x kp) and Bh/Bl (N x kp).
+void tck_gemm(int64_t M, int64_t N, int64_t K, const float* ah, const float* al, const float* bh, const float* bl,
+              int64_t kp, float* C, int64_t ldc, float alpha, float beta, const int* info, cudaStream_t st) {
+  const CUtensorMap mah = make_map_kmajor(ah, M, kp), mal = make_map_kmajor(al, M, kp);
+  const CUtensorMap mbh = make_map_kmajor(bh, N, kp), mbl = make_map_kmajor(bl, N, kp);
+  set_smem(tck_gemm_kernel, tck::SMEM_BYTES);
+  const int64_t blocks = ((M + tc::BM - 1) / tc::BM) * ((N + tc::BN - 1) / tc::BN);
+  const int64_t grid = std::min<int64_t>(blocks, (int64_t)num_sms());
+  tck_gemm_kernel<<<(unsigned)grid, tck::THREADS, tck::SMEM_BYTES, st>>>(mah, mal, mbh, mbl, M, N, K, C, ldc, alpha,
+                                                                         beta, info);
+  BCMG_CHECK_LAUNCH();
+}
+
+// gemm() for float32 on tcgen05: both operands split into a scratch owned by
+// the calling thread and stream (grow-only; stream order makes reuse safe).
+static float* split_scratch(cudaStream_t st, size_t bytes) {
+  struct Buf {
+    void* p = nullptr;
+    size_t n = 0;
+  };
+  thread_local std::vector<std::pair<cudaStream_t, Buf>> bufs;
+  Buf* b = nullptr;
+  for (auto& e : bufs)
+    if (e.first == st) b = &e.second;
+  if (!b) {
+    bufs.emplace_back(st, Buf{});
+    b = &bufs.back().second;
+  }
+  if (b->n < bytes) {
+    if (b->p) {
+      BCMG_CUDA(cudaStreamSynchronize(st));
+      cudaFree(b->p);
+      b->p = nullptr;
+      b->n = 0;
+    }
+    cudaError_t e = cudaMalloc(&b->p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(OUT_OF_MEMORY, "tf32 split scratch: " + std::string(cudaGetErrorString(e)));
+    }
+    b->n = bytes;
+  }
+  return static_cast<float*>(b->p);
+}
+
+static void gemm_tck_generic(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+                             const int* info, cudaStream_t st) {
+  const int64_t kp = split_ld(K);
+  float* s = split_scratch(st, (size_t)2 * (M + N) * kp * 4);
+  float *ah = s, *al = s + M * kp, *bh = al + M * kp, *bl = bh + N * kp;
+  split_tf32(A.trans ? 3 : 0, A.ptr, A.ld, M, K, K, ah, al, kp, st);
+  split_tf32(B.trans ? 3 : 0, B.ptr, B.ld, N, K, K, bh, bl, kp, st);
+  tck_gemm(M, N, K, ah, al, bh, bl, kp, static_cast<float*>(ep.C), ep.ldc, (float)ep.alpha, (float)ep.beta, info, st);
+}
+
 static void launch_tc3_trail(const TrailParams& p, const int* info, cudaStream_t st) {
+  if (p.split[0]) return launch_tck_trail(p, info, st);
   int64_t total = 0;
   for (int64_t m = p.m_first; m < p.m_last; ++m) {
     const int dev = (int)(m % p.D);
@@ -513,6 +680,9 @@ void trailing_update(int dt, const TrailParams& p, const int* info, cudaStream_t
   if (p.m_first >= p.m_last || p.K <= 0) return;
   dispatch_dtype(dt, [&](auto s) {
     using S = decltype(s);
+    if constexpr (std::is_same_v<S, float> || std::is_same_v<S, float2>) {
+      if (p.split[0]) return launch_tck_trail(p, info, st);  // pre-split panel (any T)
+    }
     if constexpr (std::is_same_v<S, float>) {
       if (use_tc() && tc_ok(p.P, p.ldp) && p.T % 4 == 0 && p.prow0 % 4 == 0 && p.N % 4 == 0)
         return launch_tc3_trail(p, info, st);

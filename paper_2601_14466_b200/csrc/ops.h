@@ -44,6 +44,15 @@ size_t gemm_cplx_embed_bytes(int dt, int64_t M, int64_t N, int64_t K);
 bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
                      void* scratch, size_t scratch_bytes, const int* info, cudaStream_t st, bool always = false);
 
+// tf32 hi / lo pre-split (see split_tf32_kernel) and the tcgen05 GEMM on the
+// split planes.  split_ld: the K-major leading dimension for Kx columns.
+int64_t split_ld(int64_t kx);
+void split_tf32(int mode, const void* src, int64_t ld, int64_t rows, int64_t Kx, int64_t kc, float* hi, float* lo,
+                int64_t kp, cudaStream_t st);
+void tck_gemm(int64_t M, int64_t N, int64_t K, const float* ah, const float* al, const float* bh, const float* bl,
+              int64_t kp, float* C, int64_t ldc, float alpha, float beta, const int* info, cudaStream_t st);
+bool tc_presplit_enabled();
+
 // Diagonal tile: in-place lower Cholesky of the n x n block at A (lda) and
 // X := L^-1 (n x n, ldx, zero upper).  goff = global column of the block's
 // first column; on a non-positive pivot writes the 1-based global pivot to

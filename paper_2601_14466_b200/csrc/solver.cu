@@ -71,7 +71,7 @@ Session::~Session() {
   cudaDeviceSynchronize();
   net.reset();
   for (auto* b : {&panel[0], &panel[1], &panel_pb[0], &panel_pb[1], &dinv, &wdiag, &info_dev, &tmp, &acc, &plan_buf,
-                  &stage_buf, &desc_buf, &embed_buf})
+                  &stage_buf, &desc_buf, &embed_buf, &split_buf[0], &split_buf[1]})
     b->release();
   for (auto& e : ev_pool) cudaEventDestroy(e);
   for (auto& e : ev_time) cudaEventDestroy(e);
@@ -446,7 +446,30 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
   const Geo g = make_geo(*this, dt, n, T, ndev);
   const size_t panel_bytes = (size_t)n * T * g.esz;
   // complex128: the panel is followed by -iP, plus a planar copy (TrailParams::cplx)
-  const bool embed = complex_embed_ok(dt, 0, T);
+  // float32 / complex64 on tcgen05: the panel is split once per step into tf32
+  // hi / lo K-major planes (split_buf[k % 2]) that every trailing tile reads
+  const bool presplit = (dt == R32 || dt == C64) && tc_presplit_enabled();
+  const int64_t kx = dt == C64 ? 2 * T : T, kp = split_ld(kx);
+  if (presplit) {
+    const size_t plane = (size_t)n * kp * 4;  // rows x kp floats (A rows: 2n for complex64)
+    const size_t bytes = dt == C64 ? 2 * (2 * plane) + 2 * plane : 2 * plane;
+    split_buf[0].ensure(bytes);
+    split_buf[1].ensure(bytes);
+  }
+  auto split_panel = [&](int64_t k, cudaStream_t st) {
+    const int64_t rows = n - g.stop(k), tck = g.stop(k) - g.start(k);
+    if (!presplit || rows <= 0) return;
+    float* b = static_cast<float*>(split_buf[k % 2].p);
+    const int64_t kpk = split_ld(dt == C64 ? 2 * tck : tck);
+    if (dt == R32) {
+      split_tf32(0, panel[k % 2].p, rows, rows, tck, tck, b, b + rows * kpk, kpk, st);
+    } else {
+      float* bb = b + 2 * (2 * rows) * kpk;  // B planes after the two A planes
+      split_tf32(1, panel[k % 2].p, rows, 2 * rows, 2 * tck, tck, b, b + 2 * rows * kpk, kpk, st);
+      split_tf32(2, panel[k % 2].p, rows, rows, 2 * tck, tck, bb, bb + rows * kpk, kpk, st);
+    }
+  };
+  const bool embed = !presplit && complex_embed_ok(dt, 0, T);
   panel[0].ensure(embed ? 2 * panel_bytes : panel_bytes);
   panel[1].ensure(embed ? 2 * panel_bytes : panel_bytes);
   if (embed) {
@@ -485,6 +508,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
           gemm(dt, n - s1, tc, tc, a21, xh, ep, info, crit);
       });
       if (embed_k(k)) expand_panel(dt, panel[k % 2].p, panel_pb[k % 2].p, n - s1, tc, crit);
+      split_panel(k, crit);
     }
   };
   // While the lookahead path (diag factor + panel solve of tile k+1) runs on the
@@ -502,6 +526,21 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
     if (embed_k(k)) {
       p.cplx = 1;
       p.PB = panel_pb[k % 2].p;
+    }
+    if (presplit) {
+      const int64_t rows = n - g.stop(k), kpk = split_ld(dt == C64 ? 2 * (g.stop(k) - g.start(k)) : g.stop(k) - g.start(k));
+      float* b = static_cast<float*>(split_buf[k % 2].p);
+      if (dt == R32) {
+        p.split[0] = p.split[2] = b;
+        p.split[1] = p.split[3] = b + rows * kpk;
+      } else {
+        p.cplx = 1;
+        p.split[0] = b;
+        p.split[1] = b + 2 * rows * kpk;
+        p.split[2] = b + 4 * rows * kpk;
+        p.split[3] = b + 5 * rows * kpk;
+      }
+      p.split_ld[0] = p.split_ld[1] = kpk;
     }
     p.prow0 = g.stop(k);
     p.ldp = n - p.prow0;
@@ -547,6 +586,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
         bcast(panel[b].p, (size_t)op.elems * g.esz, (int)op.root, comm);
         BCMG_CUDA(cudaEventRecord(E(C, k), comm));
         if (!mine && embed_k(k)) expand_panel(dt, panel[b].p, panel_pb[b].p, n - s1, s1 - g.start(k), comm);
+        if (!mine) split_panel(k, comm);
         if (!mine) BCMG_CUDA(cudaEventRecord(E(R, k), comm));
         break;
       case S_UPDATE:

@@ -1,0 +1,259 @@
+// 3xTF32 tcgen05 GEMM on PRE-SPLIT operands.
+//
+// tc_gemm.cuh splits every operand tile into tf32 hi / lo planes inside the
+// CTA, and that splitting (raw read + two plane writes per element, every
+// time a tile is used) plus the tensor core's own operand reads saturate the
+// SM's shared-memory bandwidth at ~1/3 of the tf32 MMA rate.  Here each
+// operand is split ONCE in global memory (split_tf32 kernel, K-major rows:
+// hi = rna_tf32(x), lo = x - hi) and TMA delivers the hi / lo tiles straight
+// into the canonical K-major SWIZZLE_128B layout the UMMA descriptors
+// describe; no splitter warps remain:
+//   warp 0        TMA producer: A hi, A lo, B hi, B lo boxes {32 k, 128 rows}
+//   warp 1        TMEM allocator + single-thread MMA issuer (3 MMAs per k8:
+//                 lo*hi, hi*lo, hi*hi into an FP32 accumulator)
+//   warps 4-11    epilogue: two warpgroups, each owns half of the accumulator
+//                 columns (TMEM lane quarter = warp % 4)
+// Stages: 3 x 64 KB operand ring (TMA tx -> MMA commit), two TMEM
+// accumulators (MMA commit -> epilogue).
+#pragma once
+
+#include "tc_gemm.cuh"
+
+namespace bcmg {
+namespace tck {
+
+using tc::BM;
+using tc::BN;
+using tc::BK;
+constexpr int STAGES = 3;
+constexpr int THREADS = 384;
+constexpr int PLANE = BM * BK * 4;            // 16 KB (BM == BN)
+constexpr int STAGE_BYTES = 4 * PLANE;        // A hi, A lo, B hi, B lo
+constexpr int TMEM_COLS = 2 * BN;
+constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+static_assert(BM == BN, "square tiles");
+
+template <class Next>
+__device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorMap* mAl, const CUtensorMap* mBh,
+                                         const CUtensorMap* mBl, int K, Next&& next) {
+  extern __shared__ __align__(1024) unsigned char tck_smem_raw[];
+  unsigned char* base = tck_smem_raw + ((1024 - (smem_u32(tck_smem_raw) & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int KT = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);  // 8 epilogue warps
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(mAh) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(mAl) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(mBh) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(mBl) : "memory");
+      uint32_t g = 0;
+      tc::Blk blk;
+      for (int64_t item = blockIdx.x; next(item, blk); item += gridDim.x) {
+        for (int kt = 0; kt < KT; ++kt, ++g) {
+          const int s = g % STAGES;
+          mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+          unsigned char* st = base + (size_t)s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          // box {32 k, 128 rows}: coordinates (k, row)
+          tma_load_2d(st, mAh, kt * BK, blk.a_row + (int)blk.m0, &full[s]);
+          tma_load_2d(st + PLANE, mAl, kt * BK, blk.a_row + (int)blk.m0, &full[s]);
+          tma_load_2d(st + 2 * PLANE, mBh, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
+          tma_load_2d(st + 3 * PLANE, mBl, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      uint32_t g = 0, t = 0;
+      tc::Blk blk;
+      for (int64_t item = blockIdx.x; next(item, blk); item += gridDim.x, ++t) {
+        const int b = t & 1;
+        mbar_wait(&tempty[b], ((t >> 1) & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t d = tmem + b * BN;
+        for (int kt = 0; kt < KT; ++kt, ++g) {
+          const int s = g % STAGES;
+          mbar_wait(&full[s], (g / STAGES) & 1);
+          tc::fence_after();
+          const uint32_t st = smem_u32(base + (size_t)s * STAGE_BYTES);
+          const uint32_t ahi = st, alo = st + PLANE, bhi = st + 2 * PLANE, blo = st + 3 * PLANE;
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint32_t off = ks * 32;  // 8 tf32 k = 32 bytes along the 128-byte K-major row
+            tc::mma_tf32(d, tc::sdesc(alo + off), tc::sdesc(bhi + off), (kt | ks) != 0);
+            tc::mma_tf32(d, tc::sdesc(ahi + off), tc::sdesc(blo + off), 1);
+            tc::mma_tf32(d, tc::sdesc(ahi + off), tc::sdesc(bhi + off), 1);
+          }
+          tc::commit(&empty[s]);  // stage reusable once these MMAs have read it
+        }
+        tc::commit(&tfull[b]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------- epilogue (8 warps)
+    const int q = warp & 3;             // TMEM lane quarter
+    const int ch = (warp - 4) >> 2;     // column half
+    const int row = 32 * q + lane;
+    uint32_t t = 0;
+    tc::Blk blk;
+    for (int64_t item = blockIdx.x; next(item, blk); item += gridDim.x, ++t) {
+      const int b = t & 1;
+      const int64_t r = blk.m0 + row;
+      float* __restrict__ crow = blk.C + r;
+      auto load_chunk = [&](int c0, float* dst) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int64_t col = blk.n0 + c0 + j;
+          dst[j] = (blk.beta != 0.f && r < blk.M && col < blk.N) ? crow[col * blk.ldc] : 0.f;
+        }
+      };
+      const int cbeg = ch * (BN / 2), cend = cbeg + BN / 2;
+      if (blk.beta != 0.f) {  // pull this warp's 32 x 64 block into L2 during the MMAs
+        const int64_t col = blk.n0 + cbeg + 2 * lane, r0 = blk.m0 + 32 * q;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          if (col + j < blk.N && r0 < blk.M) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(blk.C + r0 + (col + j) * blk.ldc));
+      }
+      float old[32], nxt[32];
+      load_chunk(cbeg, old);
+      mbar_wait(&tfull[b], (t >> 1) & 1);
+      tc::fence_after();
+#pragma unroll 1
+      for (int c0 = cbeg; c0 < cend; c0 += 32) {
+        if (c0 + 32 < cend) load_chunk(c0 + 32, nxt);
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + b * BN + c0, v);
+        if (r < blk.M) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int64_t col = blk.n0 + c0 + j;
+            if (col < blk.N) crow[col * blk.ldc] = blk.alpha * v[j] + blk.beta * old[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) old[j] = nxt[j];
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace tck
+
+// C := alpha * A * B^T + beta * C on pre-split K-major planes (rows x Kp).
+__global__ void __launch_bounds__(tck::THREADS, 1)
+    tck_gemm_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+                    const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, int64_t M,
+                    int64_t N, int64_t K, float* C, int64_t ldc, float alpha, float beta, const int* info) {
+  if (ld_flag(info)) return;
+  const int64_t nbm = (M + tc::BM - 1) / tc::BM, nbn = (N + tc::BN - 1) / tc::BN;
+  tck::tck_loop(&mAh, &mAl, &mBh, &mBl, (int)K, [&](int64_t item, tc::Blk& blk) -> bool {
+    if (item >= nbm * nbn) return false;
+    blk.a_row = 0;
+    blk.b_row = 0;
+    blk.m0 = (item % nbm) * tc::BM;
+    blk.n0 = (item / nbm) * tc::BN;
+    blk.M = M;
+    blk.N = N;
+    blk.C = C;
+    blk.ldc = ldc;
+    blk.alpha = alpha;
+    blk.beta = beta;
+    return true;
+  });
+}
+
+// potrf trailing update on the pre-split panel (TrailParams::split_*): same
+// item decode as tc3_trail_kernel (real, or the complex64 embedding).
+__global__ void __launch_bounds__(tck::THREADS, 1)
+    tck_trail_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+                     const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, TrailParams p,
+                     const int* info) {
+  using TZ = Trap<tc::BM, tc::BN>;
+  using TZC = TrapH<tc::BM / 2, tc::BN>;
+  if (ld_flag(info)) return;
+  int64_t cm = p.m_first, cbase = 0, ccnt = -1;
+  tck::tck_loop(&mAh, &mAl, &mBh, &mBl, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, tc::Blk& blk) -> bool {
+    for (;;) {
+      if (cm >= p.m_last) return false;
+      const int dev = (int)(cm % p.D);
+      if (dev >= p.dev0 && dev < p.dev0 + p.nloc) {
+        if (ccnt < 0) {
+          const int64_t ms = cm * p.T, tcm = p.T < p.N - ms ? p.T : p.N - ms;
+          ccnt = p.cplx ? TZC::count(p.N - ms, tcm) : TZ::count(p.N - ms, tcm);
+        }
+        if (item < cbase + ccnt) break;
+        cbase += ccnt;
+      }
+      ++cm;
+      ccnt = -1;
+    }
+    const int64_t ms = cm * p.T, rows = p.N - ms, tcw = p.T < rows ? p.T : rows;
+    int64_t rb, cb;
+    const int dev = (int)(cm % p.D);
+    float* shard = reinterpret_cast<float*>(p.shards[dev - p.dev0]);
+    const int64_t loc = (cm / p.D) * p.T;
+    if (p.cplx) {
+      TZC::decode(item - cbase, tcw, rb, cb);
+      blk.a_row = (int)(2 * (ms - p.prow0));
+      blk.b_row = (int)(ms - p.prow0);
+      blk.m0 = rb * tc::BM;
+      blk.n0 = cb * tc::BN;
+      blk.M = 2 * rows;
+      blk.N = tcw;
+      blk.C = shard + 2 * (ms + loc * p.N);
+      blk.ldc = 2 * p.N;
+    } else {
+      TZ::decode(item - cbase, tcw, rb, cb);
+      blk.a_row = (int)(ms - p.prow0);
+      blk.b_row = (int)(ms - p.prow0);
+      blk.m0 = rb * tc::BM;
+      blk.n0 = cb * tc::BN;
+      blk.M = rows;
+      blk.N = tcw;
+      blk.C = shard + ms + loc * p.N;
+      blk.ldc = p.N;
+    }
+    blk.alpha = -1.f;
+    blk.beta = 1.f;
+    return true;
+  });
+}
+
+}  // namespace bcmg
