@@ -90,6 +90,7 @@ static bool use_tma();
 static unsigned ew_grid(int64_t total);
 static bool use_tc();
 static bool use_presplit();
+static float* split_scratch(cudaStream_t st, size_t bytes);
 static void gemm_tck_generic(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
                              const int* info, cudaStream_t st);
 static bool tc_ok(const void* p, int64_t ld);
@@ -442,8 +443,18 @@ bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, 
     float* xp = reinterpret_cast<float*>(at + 2 * M * K);
     embed_gather<float2, float>(A, M, K, at, nullptr, M, st);
     embed_gather<float2, float>(B, N, K, nullptr, xp, N, st);
-    launch_tc3_gemm(2 * M, N, 2 * K, Operand{at, 2 * M, 0, 0, 0, 0}, Operand{xp, N, 0, 0, 0, 0},
-                    Epilogue{ep.C, 2 * ep.ldc, ep.alpha, ep.beta, 0, 0}, info, st);
+    if (use_presplit()) {  // tf32 hi / lo planes of both embedded operands, then the pre-split kernel
+      const int64_t kp = split_ld(2 * K);
+      float* s = split_scratch(st, (size_t)2 * (2 * M + N) * kp * 4);
+      float *ah = s, *al = s + 2 * M * kp, *bh = al + 2 * M * kp, *bl = bh + N * kp;
+      split_tf32(0, at, 2 * M, 2 * M, 2 * K, 2 * K, ah, al, kp, st);
+      split_tf32(0, xp, N, N, 2 * K, 2 * K, bh, bl, kp, st);
+      tck_gemm(2 * M, N, 2 * K, ah, al, bh, bl, kp, static_cast<float*>(ep.C), 2 * ep.ldc, (float)ep.alpha,
+               (float)ep.beta, info, st);
+    } else {
+      launch_tc3_gemm(2 * M, N, 2 * K, Operand{at, 2 * M, 0, 0, 0, 0}, Operand{xp, N, 0, 0, 0, 0},
+                      Epilogue{ep.C, 2 * ep.ldc, ep.alpha, ep.beta, 0, 0}, info, st);
+    }
   }
   return true;
 }
