@@ -820,25 +820,32 @@ __global__ void __launch_bounds__(256) leaf_kernel(S* A, int64_t lda, S* X, int6
         // branch-free rank-1 update: all broadcast operands are loaded up front
         // (stale entries are loaded but never selected), then predicated FMAs,
         // so the shared-memory latency is paid once per column, not per element
+        // (jo is a compile-time index here: row blocks a < jo lie above the
+        // pivot, L column blocks b < jo left of it and X column blocks b > jo
+        // right of it, so those are never touched -- the triangle shrinks)
         V li[4], lc[4], xc[4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) li[a] = colL[buf][ty + 16 * a];
+        for (int a = jo; a < 4; ++a) li[a] = colL[buf][ty + 16 * a];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          lc[b] = colL[buf][tx + 16 * b];
-          xc[b] = rowX[buf][tx + 16 * b];
+          if (b >= jo) lc[b] = colL[buf][tx + 16 * b];
+          if (b <= jo) xc[b] = rowX[buf][tx + 16 * b];
         }
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
+        for (int a = jo; a < 4; ++a) {
           const int i = ty + 16 * a;
           const bool row = i > j && i < n;
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             const int c = tx + 16 * b;
-            const V nx = v_fnms(x[a][b], li[a], xc[b]);
-            const V nl = v_fnmsc(l[a][b], li[a], lc[b]);
-            x[a][b] = (row && c <= j) ? nx : x[a][b];
-            l[a][b] = (row && c > j && c <= i) ? nl : l[a][b];
+            if (b <= jo) {
+              const V nx = v_fnms(x[a][b], li[a], xc[b]);
+              x[a][b] = (row && c <= j) ? nx : x[a][b];
+            }
+            if (b >= jo && b <= a) {
+              const V nl = v_fnmsc(l[a][b], li[a], lc[b]);
+              l[a][b] = (row && c > j && c <= i) ? nl : l[a][b];
+            }
           }
         }
       }
