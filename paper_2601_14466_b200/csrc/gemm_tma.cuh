@@ -234,6 +234,35 @@ struct TrapH {
   }
 };
 
+// General form for column blocks R = BN / BM times as wide as row blocks:
+// row block rb keeps min(ncb, rb / R + 1) column blocks.
+template <int BM, int BN>
+struct TrapR {
+  static_assert(BN % BM == 0, "BN must be a multiple of BM");
+  static constexpr int64_t R = BN / BM;
+  __host__ __device__ static int64_t tri(int64_t t) {  // sum_{rb < t} (rb / R + 1)
+    const int64_t p = t / R;
+    return R * p * (p + 1) / 2 + (t % R) * (p + 1);
+  }
+  __host__ __device__ static int64_t count(int64_t rows, int64_t tc) {
+    const int64_t nrb = (rows + BM - 1) / BM, ncb = (tc + BN - 1) / BN, r0 = R * (ncb - 1);
+    return nrb <= r0 ? tri(nrb) : tri(r0) + (nrb - r0) * ncb;
+  }
+  __host__ __device__ static void decode(int64_t b, int64_t tc, int64_t& rb, int64_t& cb) {
+    const int64_t ncb = (tc + BN - 1) / BN, r0 = R * (ncb - 1), t0 = tri(r0);
+    if (b < t0) {  // group g of R row blocks holds R(g+1) items, R g(g+1)/2 before it
+      int64_t g = 0;
+      while (R * (g + 1) * (g + 2) / 2 <= b) ++g;
+      const int64_t o = b - R * g * (g + 1) / 2;
+      rb = R * g + o / (g + 1);
+      cb = o % (g + 1);
+    } else {
+      rb = r0 + (b - t0) / ncb;
+      cb = (b - t0) % ncb;
+    }
+  }
+};
+
 template <class TL>
 constexpr int min_blocks() { return 65536 / (TL::THREADS * 128) > 0 ? 65536 / (TL::THREADS * 128) : 1; }
 

@@ -564,11 +564,11 @@ void split_tf32(int mode, const void* src, int64_t ld, int64_t rows, int64_t Kx,
 
 // K-major plane map: dims {kp, rows}, box {32 k, 128 rows}, SWIZZLE_128B (the
 // canonical K-major layout of the UMMA descriptors).
-static CUtensorMap make_map_kmajor(const float* base, int64_t rows, int64_t kp) {
+static CUtensorMap make_map_kmajor(const float* base, int64_t rows, int64_t kp, int box_rows = tc::BM) {
   CUtensorMap m;
   cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)kp * 4};
-  cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)tc::BM};
+  cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -589,38 +589,66 @@ static bool use_presplit() {
 
 bool tc_presplit_enabled() { return use_tc() && use_presplit(); }
 
-static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t st) {
+static int tck_width(int64_t n) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("BCMG_TCK_N");
+    forced = e ? atoi(e) : 0;
+  }
+  if (forced == 128 || forced == 256) return forced;
+  return n >= 256 ? 256 : 128;
+}
+
+template <int BNT>
+static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream_t st) {
+  using TZ = TrapR<tc::BM, BNT>;
+  using TZC = TrapR<tc::BM / 2, BNT>;
   int64_t total = 0;
   for (int64_t m = p.m_first; m < p.m_last; ++m) {
     const int dev = (int)(m % p.D);
     if (dev < p.dev0 || dev >= p.dev0 + p.nloc) continue;
     const int64_t rows = p.N - m * p.T, tcm = std::min(p.T, rows);
-    total += p.cplx ? TrapH<tc::BM / 2, tc::BN>::count(rows, tcm) : Trap<tc::BM, tc::BN>::count(rows, tcm);
+    total += p.cplx ? TZC::count(rows, tcm) : TZ::count(rows, tcm);
   }
   if (total == 0) return;
   const int64_t prow = p.N - p.prow0, arows = p.cplx ? 2 * prow : prow;
   const CUtensorMap ah = make_map_kmajor(p.split[0], arows, p.split_ld[0]);
   const CUtensorMap al = make_map_kmajor(p.split[1], arows, p.split_ld[0]);
-  const CUtensorMap bh = make_map_kmajor(p.split[2], prow, p.split_ld[1]);
-  const CUtensorMap bl = make_map_kmajor(p.split[3], prow, p.split_ld[1]);
-  set_smem(tck_trail_kernel, tck::SMEM_BYTES);
+  const CUtensorMap bh = make_map_kmajor(p.split[2], prow, p.split_ld[1], BNT);
+  const CUtensorMap bl = make_map_kmajor(p.split[3], prow, p.split_ld[1], BNT);
+  constexpr size_t smem = tck::Cfg<BNT>::SMEM_BYTES;
+  set_smem(tck_trail_kernel<BNT>, smem);
   const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, num_sms()) : num_sms();
   const int64_t grid = std::min<int64_t>(total, sms);
-  tck_trail_kernel<<<(unsigned)grid, tck::THREADS, tck::SMEM_BYTES, st>>>(ah, al, bh, bl, p, info);
+  tck_trail_kernel<BNT><<<(unsigned)grid, tck::THREADS, smem, st>>>(ah, al, bh, bl, p, info);
   BCMG_CHECK_LAUNCH();
 }
 
+static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t st) {
+  if (tck_width(p.T) == 256) return launch_tck_trail_t<256>(p, info, st);
+  launch_tck_trail_t<128>(p, info, st);
+}
+
 // C = alpha*A*B^T + beta*C (float32) on pre-split planes Ah/Al (M x kp) and Bh/Bl (N x kp).
+template <int BNT>
+static void tck_gemm_t(int64_t M, int64_t N, int64_t K, const float* ah, const float* al, const float* bh,
+                       const float* bl, int64_t kp, float* C, int64_t ldc, float alpha, float beta, const int* info,
+                       cudaStream_t st) {
+  const CUtensorMap mah = make_map_kmajor(ah, M, kp), mal = make_map_kmajor(al, M, kp);
+  const CUtensorMap mbh = make_map_kmajor(bh, N, kp, BNT), mbl = make_map_kmajor(bl, N, kp, BNT);
+  constexpr size_t smem = tck::Cfg<BNT>::SMEM_BYTES;
+  set_smem(tck_gemm_kernel<BNT>, smem);
+  const int64_t blocks = ((M + tc::BM - 1) / tc::BM) * ((N + BNT - 1) / BNT);
+  const int64_t grid = std::min<int64_t>(blocks, (int64_t)num_sms());
+  tck_gemm_kernel<BNT><<<(unsigned)grid, tck::THREADS, smem, st>>>(mah, mal, mbh, mbl, M, N, K, C, ldc, alpha, beta,
+                                                                    info);
+  BCMG_CHECK_LAUNCH();
+}
+
 void tck_gemm(int64_t M, int64_t N, int64_t K, const float* ah, const float* al, const float* bh, const float* bl,
               int64_t kp, float* C, int64_t ldc, float alpha, float beta, const int* info, cudaStream_t st) {
-  const CUtensorMap mah = make_map_kmajor(ah, M, kp), mal = make_map_kmajor(al, M, kp);
-  const CUtensorMap mbh = make_map_kmajor(bh, N, kp), mbl = make_map_kmajor(bl, N, kp);
-  set_smem(tck_gemm_kernel, tck::SMEM_BYTES);
-  const int64_t blocks = ((M + tc::BM - 1) / tc::BM) * ((N + tc::BN - 1) / tc::BN);
-  const int64_t grid = std::min<int64_t>(blocks, (int64_t)num_sms());
-  tck_gemm_kernel<<<(unsigned)grid, tck::THREADS, tck::SMEM_BYTES, st>>>(mah, mal, mbh, mbl, M, N, K, C, ldc, alpha,
-                                                                         beta, info);
-  BCMG_CHECK_LAUNCH();
+  if (tck_width(N) == 256) return tck_gemm_t<256>(M, N, K, ah, al, bh, bl, kp, C, ldc, alpha, beta, info, st);
+  tck_gemm_t<128>(M, N, K, ah, al, bh, bl, kp, C, ldc, alpha, beta, info, st);
 }
 
 // gemm() for float32 on tcgen05: both operands split into a scratch owned by

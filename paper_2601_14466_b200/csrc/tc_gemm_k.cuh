@@ -23,19 +23,36 @@ namespace bcmg {
 namespace tck {
 
 using tc::BM;
-using tc::BN;
 using tc::BK;
-constexpr int STAGES = 3;
+// BNT: 128 or 256 output columns per tile (UMMA M=128, N=BNT).  N=256 halves
+// the A-operand traffic (TMA and tensor-core shared-memory reads) per flop.
+template <int BNT>
+struct Cfg {
+  static_assert(BNT == 128 || BNT == 256, "tile width");
+  static constexpr int PLANE_A = BM * BK * 4, PLANE_B = BNT * BK * 4;
+  static constexpr int STAGE_BYTES = 2 * (PLANE_A + PLANE_B);   // A hi, A lo, B hi, B lo
+  static constexpr int STAGES = BNT == 256 ? 2 : 3;
+  static constexpr int TMEM_COLS = 2 * BNT;
+  static constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BNT >> 3) << 17) |
+                                    ((uint32_t)(BM >> 4) << 24);
+};
 constexpr int THREADS = 384;
-constexpr int PLANE = BM * BK * 4;            // 16 KB (BM == BN)
-constexpr int STAGE_BYTES = 4 * PLANE;        // A hi, A lo, B hi, B lo
-constexpr int TMEM_COLS = 2 * BN;
-constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
-static_assert(BM == BN, "square tiles");
 
-template <class Next>
+__device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+template <int BNT, class Next>
 __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorMap* mAl, const CUtensorMap* mBh,
                                          const CUtensorMap* mBl, int K, Next&& next) {
+  using CF = Cfg<BNT>;
+  constexpr int STAGES = CF::STAGES, STAGE_BYTES = CF::STAGE_BYTES, PLANE_A = CF::PLANE_A, PLANE_B = CF::PLANE_B;
+  constexpr int BN = BNT;
   extern __shared__ __align__(1024) unsigned char tck_smem_raw[];
   unsigned char* base = tck_smem_raw + ((1024 - (smem_u32(tck_smem_raw) & 1023)) & 1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)STAGES * STAGE_BYTES);
@@ -59,7 +76,7 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
+                 "r"(CF::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   tc::fence_before();
@@ -84,9 +101,9 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
           mbar_expect_tx(&full[s], STAGE_BYTES);
           // box {32 k, 128 rows}: coordinates (k, row)
           tma_load_2d(st, mAh, kt * BK, blk.a_row + (int)blk.m0, &full[s]);
-          tma_load_2d(st + PLANE, mAl, kt * BK, blk.a_row + (int)blk.m0, &full[s]);
-          tma_load_2d(st + 2 * PLANE, mBh, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
-          tma_load_2d(st + 3 * PLANE, mBl, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
+          tma_load_2d(st + PLANE_A, mAl, kt * BK, blk.a_row + (int)blk.m0, &full[s]);
+          tma_load_2d(st + 2 * PLANE_A, mBh, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
+          tma_load_2d(st + 2 * PLANE_A + PLANE_B, mBl, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
         }
       }
     }
@@ -105,13 +122,13 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
           mbar_wait(&full[s], (g / STAGES) & 1);
           tc::fence_after();
           const uint32_t st = smem_u32(base + (size_t)s * STAGE_BYTES);
-          const uint32_t ahi = st, alo = st + PLANE, bhi = st + 2 * PLANE, blo = st + 3 * PLANE;
+          const uint32_t ahi = st, alo = st + PLANE_A, bhi = st + 2 * PLANE_A, blo = bhi + PLANE_B;
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {
             const uint32_t off = ks * 32;  // 8 tf32 k = 32 bytes along the 128-byte K-major row
-            tc::mma_tf32(d, tc::sdesc(alo + off), tc::sdesc(bhi + off), (kt | ks) != 0);
-            tc::mma_tf32(d, tc::sdesc(ahi + off), tc::sdesc(blo + off), 1);
-            tc::mma_tf32(d, tc::sdesc(ahi + off), tc::sdesc(bhi + off), 1);
+            mma(d, tc::sdesc(alo + off), tc::sdesc(bhi + off), CF::IDESC, (kt | ks) != 0);
+            mma(d, tc::sdesc(ahi + off), tc::sdesc(blo + off), CF::IDESC, 1);
+            mma(d, tc::sdesc(ahi + off), tc::sdesc(bhi + off), CF::IDESC, 1);
           }
           tc::commit(&empty[s]);  // stage reusable once these MMAs have read it
         }
@@ -137,10 +154,11 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
         }
       };
       const int cbeg = ch * (BN / 2), cend = cbeg + BN / 2;
-      if (blk.beta != 0.f) {  // pull this warp's 32 x 64 block into L2 during the MMAs
-        const int64_t col = blk.n0 + cbeg + 2 * lane, r0 = blk.m0 + 32 * q;
+      if (blk.beta != 0.f) {  // pull this warp's 32-row block into L2 during the MMAs
+        constexpr int PER = BN / 2 / 32;
+        const int64_t col = blk.n0 + cbeg + PER * lane, r0 = blk.m0 + 32 * q;
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < PER; ++j)
           if (col + j < blk.N && r0 < blk.M) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(blk.C + r0 + (col + j) * blk.ldc));
       }
       float old[32], nxt[32];
@@ -170,25 +188,26 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
   __syncthreads();
   if (warp == 1) {
     tc::fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(CF::TMEM_COLS));
   }
 }
 
 }  // namespace tck
 
 // C := alpha * A * B^T + beta * C on pre-split K-major planes (rows x Kp).
+template <int BNT>
 __global__ void __launch_bounds__(tck::THREADS, 1)
     tck_gemm_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                     const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, int64_t M,
                     int64_t N, int64_t K, float* C, int64_t ldc, float alpha, float beta, const int* info) {
   if (ld_flag(info)) return;
-  const int64_t nbm = (M + tc::BM - 1) / tc::BM, nbn = (N + tc::BN - 1) / tc::BN;
-  tck::tck_loop(&mAh, &mAl, &mBh, &mBl, (int)K, [&](int64_t item, tc::Blk& blk) -> bool {
+  const int64_t nbm = (M + tc::BM - 1) / tc::BM, nbn = (N + BNT - 1) / BNT;
+  tck::tck_loop<BNT>(&mAh, &mAl, &mBh, &mBl, (int)K, [&](int64_t item, tc::Blk& blk) -> bool {
     if (item >= nbm * nbn) return false;
     blk.a_row = 0;
     blk.b_row = 0;
     blk.m0 = (item % nbm) * tc::BM;
-    blk.n0 = (item / nbm) * tc::BN;
+    blk.n0 = (item / nbm) * BNT;
     blk.M = M;
     blk.N = N;
     blk.C = C;
@@ -201,15 +220,16 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
 
 // potrf trailing update on the pre-split panel (TrailParams::split_*): same
 // item decode as tc3_trail_kernel (real, or the complex64 embedding).
+template <int BNT>
 __global__ void __launch_bounds__(tck::THREADS, 1)
     tck_trail_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                      const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, TrailParams p,
                      const int* info) {
-  using TZ = Trap<tc::BM, tc::BN>;
-  using TZC = TrapH<tc::BM / 2, tc::BN>;
+  using TZ = TrapR<tc::BM, BNT>;
+  using TZC = TrapR<tc::BM / 2, BNT>;
   if (ld_flag(info)) return;
   int64_t cm = p.m_first, cbase = 0, ccnt = -1;
-  tck::tck_loop(&mAh, &mAl, &mBh, &mBl, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, tc::Blk& blk) -> bool {
+  tck::tck_loop<BNT>(&mAh, &mAl, &mBh, &mBl, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, tc::Blk& blk) -> bool {
     for (;;) {
       if (cm >= p.m_last) return false;
       const int dev = (int)(cm % p.D);
@@ -234,7 +254,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
       blk.a_row = (int)(2 * (ms - p.prow0));
       blk.b_row = (int)(ms - p.prow0);
       blk.m0 = rb * tc::BM;
-      blk.n0 = cb * tc::BN;
+      blk.n0 = cb * BNT;
       blk.M = 2 * rows;
       blk.N = tcw;
       blk.C = shard + 2 * (ms + loc * p.N);
@@ -244,7 +264,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
       blk.a_row = (int)(ms - p.prow0);
       blk.b_row = (int)(ms - p.prow0);
       blk.m0 = rb * tc::BM;
-      blk.n0 = cb * tc::BN;
+      blk.n0 = cb * BNT;
       blk.M = rows;
       blk.N = tcw;
       blk.C = shard + ms + loc * p.N;
