@@ -777,8 +777,7 @@ __device__ __forceinline__ double2 v_to(double2 a) { return a; }
 // Right-looking: step j takes the pivot d = Re a_jj after all earlier
 // updates -- the reference's test, failing unless d > 0 and finite.
 template <class S>
-__global__ void __launch_bounds__(256) leaf_kernel(S* A, int64_t lda, S* X, int64_t ldx, int n, int64_t goff,
-                                                   int* info) {
+__device__ __forceinline__ void leaf_body(S* A, int64_t lda, S* X, int64_t ldx, int n, int64_t goff, int* info) {
   using V = typename V_<Traits<S>::cplx>::type;
   if (*(volatile int*)info) return;
   __shared__ V colL[2][LEAF];
@@ -893,8 +892,164 @@ finished:
 }
 
 template <class S>
+__global__ void __launch_bounds__(256) leaf_kernel(S* A, int64_t lda, S* X, int64_t ldx, int n, int64_t goff,
+                                                   int* info) {
+  leaf_body<S>(A, lda, X, ldx, n, goff, info);
+}
+
+template <class S>
 static void launch_leaf(S* A, int64_t lda, S* X, int64_t ldx, int n, int64_t goff, int* info, cudaStream_t st) {
   leaf_kernel<S><<<1, 256, 0, st>>>(A, lda, X, ldx, n, goff, info);
+  BCMG_CHECK_LAUNCH();
+}
+
+// One recursion node of size 64 < n <= 128 in ONE CTA (the bottom level of
+// diag_factor, which otherwise costs two leaf launches, four 64^3 GEMM
+// launches and three copies):
+//   leaf(A11) -> L11, X11;  L21 = A21 X11^H;  A22 -= L21 L21^H (lower);
+//   leaf(A22) -> L22, X22;  X21 = -X22 (L21 X11);  X12 = 0
+// The 64x64 operands of the small products live in shared memory (row
+// stride 65); thread (ty, tx) computes rows ty + 16a, columns tx + 16b.
+template <class S>
+__global__ void __launch_bounds__(256) node_kernel(S* A, int64_t lda, S* X, int64_t ldx, int n, int64_t goff,
+                                                   int* info) {
+  using V = typename V_<Traits<S>::cplx>::type;
+  constexpr int LD = LEAF + 1;
+  extern __shared__ __align__(16) unsigned char node_smem[];
+  V* X11 = reinterpret_cast<V*>(node_smem);  // X11[r * LD + c]
+  V* B1 = X11 + LEAF * LD;                   // A21, then T1 = L21 X11
+  V* B2 = B1 + LEAF * LD;                    // L21, then X22
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int n1 = LEAF, n2 = n - LEAF;
+  auto ld = [](const S* p, int64_t ld_, int r, int c) { return v_from<V>(to_c(p[r + (int64_t)c * ld_])); };
+  auto st = [](S* p, int64_t ld_, int r, int c, V v) { p[r + (int64_t)c * ld_] = from_c<S>(v_to(v)); };
+  auto zero = [] { return v_from<V>(make_double2(0.0, 0.0)); };
+  auto fma_ = [](V acc, V a, V b) { return v_fnms(acc, v_scale(a, -1.0), b); };         // acc + a*b
+  auto fmac_ = [](V acc, V a, V b) { return v_fnmsc(acc, v_scale(a, -1.0), b); };       // acc + a*conj(b)
+
+  leaf_body<S>(A, lda, X, ldx, n1, goff, info);
+  __syncthreads();
+  if (*(volatile int*)info) return;
+  for (int e = tid; e < LEAF * LEAF; e += 256) {
+    const int r = e % LEAF, c = e / LEAF;
+    X11[r * LD + c] = ld(X, ldx, r, c);
+    B1[r * LD + c] = r < n2 ? ld(A, lda, n1 + r, c) : zero();
+  }
+  __syncthreads();
+  // L21 = A21 X11^H  (X11 lower: k <= c)
+  V acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = zero();
+  for (int kk = 0; kk < LEAF; ++kk) {
+    V av[4], bv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) av[a] = B1[(ty + 16 * a) * LD + kk];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) bv[b] = X11[(tx + 16 * b) * LD + kk];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fmac_(acc[a][b], av[a], bv[b]);
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, c = tx + 16 * b;
+      B2[i * LD + c] = i < n2 ? acc[a][b] : zero();
+      if (i < n2) st(A, lda, n1 + i, c, acc[a][b]);
+    }
+  __syncthreads();
+  // A22 -= L21 L21^H on the lower triangle
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = zero();
+  for (int kk = 0; kk < LEAF; ++kk) {
+    V av[4], bv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) av[a] = B2[(ty + 16 * a) * LD + kk];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) bv[b] = B2[(tx + 16 * b) * LD + kk];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fmac_(acc[a][b], av[a], bv[b]);
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, c = tx + 16 * b;
+      if (i < n2 && c <= i) {
+        const V old = ld(A, lda, n1 + i, n1 + c);
+        st(A, lda, n1 + i, n1 + c, v_fnms(old, acc[a][b], v_from<V>(make_double2(1.0, 0.0))));
+      }
+    }
+  __syncthreads();
+  leaf_body<S>(A + n1 + (int64_t)n1 * lda, lda, X + n1 + (int64_t)n1 * ldx, ldx, n2, goff + n1, info);
+  __syncthreads();
+  if (*(volatile int*)info) return;
+  // T1 = L21 X11 -> B1
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = zero();
+  for (int kk = 0; kk < LEAF; ++kk) {
+    V av[4], bv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) av[a] = B2[(ty + 16 * a) * LD + kk];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) bv[b] = X11[kk * LD + tx + 16 * b];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fma_(acc[a][b], av[a], bv[b]);
+  }
+  __syncthreads();  // every read of B2 (L21) done before X22 overwrites it
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) B1[(ty + 16 * a) * LD + tx + 16 * b] = acc[a][b];
+  for (int e = tid; e < LEAF * LEAF; e += 256) {
+    const int r = e % LEAF, c = e / LEAF;
+    B2[r * LD + c] = (r < n2 && c < n2) ? ld(X, ldx, n1 + r, n1 + c) : zero();
+  }
+  __syncthreads();
+  // X21 = -X22 T1 ; X12 = 0
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = zero();
+  for (int kk = 0; kk < LEAF; ++kk) {
+    V av[4], bv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) av[a] = B2[(ty + 16 * a) * LD + kk];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) bv[b] = B1[kk * LD + tx + 16 * b];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fma_(acc[a][b], av[a], bv[b]);
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, c = tx + 16 * b;
+      if (i < n2) st(X, ldx, n1 + i, c, v_scale(acc[a][b], -1.0));
+      if (c < n2) st(X, ldx, i, n1 + c, zero());
+    }
+}
+
+template <class S>
+static void launch_node(S* A, int64_t lda, S* X, int64_t ldx, int n, int64_t goff, int* info, cudaStream_t st) {
+  using V = typename V_<Traits<S>::cplx>::type;
+  constexpr size_t smem = (size_t)3 * LEAF * (LEAF + 1) * sizeof(V);
+  set_smem(node_kernel<S>, smem);
+  node_kernel<S><<<1, 256, smem, st>>>(A, lda, X, ldx, n, goff, info);
   BCMG_CHECK_LAUNCH();
 }
 
@@ -911,6 +1066,13 @@ void diag_factor(int dt, void* A, int64_t lda, void* X, int64_t ldx, void* W, in
     dispatch_dtype(dt, [&](auto s) {
       using S = decltype(s);
       launch_leaf<S>(static_cast<S*>(A), lda, static_cast<S*>(X), ldx, (int)n, goff, info, st);
+    });
+    return;
+  }
+  if (n <= 2 * LEAF && !getenv("BCMG_NO_NODE_KERNEL")) {
+    dispatch_dtype(dt, [&](auto s) {
+      using S = decltype(s);
+      launch_node<S>(static_cast<S*>(A), lda, static_cast<S*>(X), ldx, (int)n, goff, info, st);
     });
     return;
   }
