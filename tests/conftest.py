@@ -37,3 +37,20 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="module")
+def meshes(cuda):
+    """Cached DeviceMesh per logical-device count (virtual devices on GPU 0)."""
+    import paper_2601_14466_b200 as bc
+
+    cache = {}
+
+    def get(d):
+        if d not in cache:
+            cache[d] = bc.DeviceMesh(d, device=0)
+        return cache[d]
+
+    yield get
+    for m in cache.values():
+        m.close()
