@@ -1,9 +1,11 @@
 // Transports of comm.h.
 #include "comm.h"
 
+#include <cuda.h>
 #include <nccl.h>
 
 #include <atomic>
+#include <chrono>
 #include <climits>
 #include <condition_variable>
 #include <cstring>
@@ -45,6 +47,41 @@ class NcclComm final : public Comm {
     BCMG_NCCL_CALL(ncclRecv(buf, bytes, ncclUint8, peer, c_, st));
   }
   void group_end() override { BCMG_NCCL_CALL(ncclGroupEnd()); }
+  std::vector<void*> exchange_pointers(void* local) override {
+    // CUDA IPC handles of every rank's allocation, all-gathered over NCCL
+    int world = 0, me = 0;
+    BCMG_NCCL_CALL(ncclCommCount(c_, &world));
+    BCMG_NCCL_CALL(ncclCommUserRank(c_, &me));
+    cudaIpcMemHandle_t h;
+    BCMG_CUDA(cudaIpcGetMemHandle(&h, local));
+    void* dev = nullptr;
+    BCMG_CUDA(cudaMalloc(&dev, sizeof(h) * (size_t)(world + 1)));
+    std::vector<cudaIpcMemHandle_t> all(world);
+    cudaStream_t st;
+    BCMG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    BCMG_CUDA(cudaMemcpyAsync(static_cast<char*>(dev) + sizeof(h) * world, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+    BCMG_NCCL_CALL(ncclAllGather(static_cast<char*>(dev) + sizeof(h) * world, dev, sizeof(h), ncclUint8, c_, st));
+    BCMG_CUDA(cudaMemcpyAsync(all.data(), dev, sizeof(h) * world, cudaMemcpyDeviceToHost, st));
+    BCMG_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    cudaFree(dev);
+    std::vector<void*> out(world, nullptr);
+    for (int r = 0; r < world; ++r) {
+      if (r == me) {
+        out[r] = local;
+        continue;
+      }
+      BCMG_CUDA(cudaIpcOpenMemHandle(&out[r], all[r], cudaIpcMemLazyEnablePeerAccess));
+    }
+    me_ = me;
+    return out;
+  }
+  void release_pointers(std::vector<void*>& ptrs) override {
+    for (int r = 0; r < (int)ptrs.size(); ++r)
+      if (r != me_ && ptrs[r]) cudaIpcCloseMemHandle(ptrs[r]);
+    ptrs.clear();
+  }
+  bool peer_default() const override { return true; }
   int allreduce_min(int v, void* scratch, cudaStream_t st) override {
     int* d = static_cast<int*>(scratch);
     BCMG_CUDA(cudaMemcpyAsync(d, &v, sizeof(int), cudaMemcpyHostToDevice, st));
@@ -55,8 +92,10 @@ class NcclComm final : public Comm {
     return out;
   }
 
+
  private:
   ncclComm_t c_ = nullptr;
+  int me_ = 0;
 };
 
 // ------------------------------------------------------------------ loopback
@@ -92,6 +131,11 @@ struct Hub {
     int count = 0, value = INT_MAX, reads = 0;
   };
   std::map<uint64_t, Reduce> reduces;
+  struct Gather {
+    std::vector<void*> ptrs;
+    int count = 0, reads = 0;
+  };
+  std::map<uint64_t, Gather> gathers;
 };
 
 std::mutex g_hubs_mu;
@@ -115,6 +159,14 @@ std::shared_ptr<Hub> join_hub(uint64_t key, int world) {
 }  // namespace
 
 class LoopbackComm final : public Comm {
+  // a rank that never arrives (a schedule mismatch or a crashed peer thread)
+  // becomes an error instead of a hang
+  template <class Pred>
+  void hub_wait(std::unique_lock<std::mutex>& lk, Pred pred) {
+    if (!hub_->cv.wait_for(lk, std::chrono::seconds(300), pred))
+      throw Error(CUDA, "loopback transport: peer rank did not arrive within 300 s");
+  }
+
  public:
   LoopbackComm(int rank, int world, uint64_t key) : rank_(rank), hub_(join_hub(key, world)) {}
 
@@ -130,7 +182,7 @@ class LoopbackComm final : public Comm {
       b.posted = true;
       hub_->cv.notify_all();
       // the source buffer stays untouched until every receiver's copy has run
-      hub_->cv.wait(lk, [&] { return (int)hub_->bcasts[seq].done.size() == hub_->world - 1; });
+      hub_wait(lk, [&] { return (int)hub_->bcasts[seq].done.size() == hub_->world - 1; });
       auto& bb = hub_->bcasts[seq];
       for (cudaEvent_t e : bb.done) {
         BCMG_CUDA(cudaStreamWaitEvent(st, e, 0));
@@ -140,7 +192,7 @@ class LoopbackComm final : public Comm {
       hub_->bcasts.erase(seq);
       return;
     }
-    hub_->cv.wait(lk, [&] { return hub_->bcasts[seq].posted; });
+    hub_wait(lk, [&] { return hub_->bcasts[seq].posted; });
     const void* src = hub_->bcasts[seq].src;
     cudaEvent_t ready = hub_->bcasts[seq].ready;
     lk.unlock();
@@ -179,7 +231,7 @@ class LoopbackComm final : public Comm {
       {
         std::unique_lock<std::mutex> lk(hub_->mu);
         auto& q = hub_->queues[{r.peer, rank_}];
-        hub_->cv.wait(lk, [&] { return !q.empty(); });
+        hub_wait(lk, [&] { return !q.empty(); });
         m = q.front();
         q.pop_front();
       }
@@ -197,7 +249,7 @@ class LoopbackComm final : public Comm {
     }
     for (auto& s : sends_) {
       std::unique_lock<std::mutex> lk(hub_->mu);
-      hub_->cv.wait(lk, [&] { return s.m->acked; });
+      hub_wait(lk, [&] { return s.m->acked; });
       lk.unlock();
       BCMG_CUDA(cudaStreamWaitEvent(s.st, s.m->done, 0));
       cudaEventDestroy(s.m->done);
@@ -207,6 +259,24 @@ class LoopbackComm final : public Comm {
     recvs_.clear();
   }
 
+  std::vector<void*> exchange_pointers(void* local) override {
+    // one address space: the other ranks' allocations are directly usable
+    const uint64_t seq = gather_seq_++;
+    std::unique_lock<std::mutex> lk(hub_->mu);
+    auto& gth = hub_->gathers[seq];
+    if (gth.ptrs.empty()) gth.ptrs.assign(hub_->world, nullptr);
+    gth.ptrs[rank_] = local;
+    gth.count++;
+    hub_->cv.notify_all();
+    hub_wait(lk, [&] { return hub_->gathers[seq].count == hub_->world; });
+    auto& g2 = hub_->gathers[seq];
+    std::vector<void*> out = g2.ptrs;
+    if (++g2.reads == hub_->world) hub_->gathers.erase(seq);
+    return out;
+  }
+  void release_pointers(std::vector<void*>& ptrs) override { ptrs.clear(); }
+  bool peer_default() const override { return false; }
+
   int allreduce_min(int v, void*, cudaStream_t) override {
     const uint64_t seq = red_seq_++;
     std::unique_lock<std::mutex> lk(hub_->mu);
@@ -214,7 +284,7 @@ class LoopbackComm final : public Comm {
     r.count++;
     r.value = std::min(r.value, v);
     hub_->cv.notify_all();
-    hub_->cv.wait(lk, [&] { return hub_->reduces[seq].count == hub_->world; });
+    hub_wait(lk, [&] { return hub_->reduces[seq].count == hub_->world; });
     auto& rr = hub_->reduces[seq];
     const int out = rr.value;
     if (++rr.reads == hub_->world) hub_->reduces.erase(seq);
@@ -234,10 +304,36 @@ class LoopbackComm final : public Comm {
   };
   const int rank_;
   std::shared_ptr<Hub> hub_;
-  uint64_t bc_seq_ = 0, red_seq_ = 0;
+  uint64_t bc_seq_ = 0, red_seq_ = 0, gather_seq_ = 0;
   std::vector<PendingSend> sends_;
   std::vector<PendingRecv> recvs_;
 };
+
+// ------------------------------------------------------------------ stream flags
+namespace {
+typedef CUresult (*WaitValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValueFn wait_fn() {
+  static WaitValueFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (WaitValueFn) nullptr;
+    }
+    return reinterpret_cast<WaitValueFn>(f);
+  }();
+  return fn;
+}
+}  // namespace
+
+bool stream_wait_supported() { return wait_fn() != nullptr; }
+
+void stream_wait_geq(cudaStream_t st, const void* addr, unsigned v) {
+  const CUresult r = wait_fn()(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), v,
+                               CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) throw Error(CUDA, "cuStreamWaitValue32 failed (" + std::to_string((int)r) + ")");
+}
 
 void make_loopback_id(unsigned char* id) {
   std::memset(id, 0, kCommIdBytes);

@@ -17,6 +17,7 @@
 
 #include <cstddef>
 #include <memory>
+#include <vector>
 
 namespace bcmg {
 
@@ -33,7 +34,25 @@ class Comm {
   virtual void group_end() = 0;
   // host value in, minimum over ranks out (synchronous); scratch: 4 device bytes
   virtual int allreduce_min(int v, void* scratch, cudaStream_t st) = 0;
+  // Peer memory (NVLink P2P through CUDA IPC handles; the shared address space
+  // of loopback ranks): every rank contributes the base of one cudaMalloc
+  // allocation and gets all ranks' bases mapped into its own address space
+  // (collective, same call order on every rank).  Empty if unsupported.
+  virtual std::vector<void*> exchange_pointers(void* local) = 0;
+  virtual void release_pointers(std::vector<void*>& ptrs) = 0;
+  // peer-memory hand-offs by default?  Across GPUs yes; for loopback ranks
+  // sharing one context only on request (BCMG_P2P=1): a context-wide
+  // synchronisation there (lazy kernel loading, cudaFree) waits for streams
+  // parked on flags that the synchronising rank has yet to raise.
+  virtual bool peer_default() const = 0;
 };
+
+// Stream-ordered flags for peer-memory hand-offs: `signal` stores v to a
+// (possibly peer) 32-bit word from a one-thread kernel; `wait_geq` blocks the
+// stream until a LOCAL word reaches v (no kernel waits on another rank).
+bool stream_wait_supported();
+void stream_wait_geq(cudaStream_t st, const void* addr, unsigned v);
+void stream_signal(cudaStream_t st, void* const* addrs, int n, unsigned v);
 
 constexpr size_t kCommIdBytes = 128;
 // id: kCommIdBytes from bcmg_nccl_unique_id (NCCL) or bcmg_loopback_id (loopback)

@@ -60,12 +60,18 @@ inline Operand opB(const void* p, int64_t ld, int op) {
   return Operand{p, ld, op == OP_N ? 1 : 0, op == OP_C ? 1 : 0, 0, 0};
 }
 
+constexpr int MAX_FAN = 7;  // peers of an 8-GPU node
 struct Epilogue {
   void* C;
   int64_t ldc;
   double alpha, beta;
   int lower_only;      // store only where row - col >= lower_off
   int64_t lower_off;
+  // fan-out: every stored element is also written at the same offset from
+  // each fan[e] (peer GPUs' copies of C over NVLink: a GEMM fused with its
+  // broadcast, see Session::potrf's peer-memory mode)
+  void* fan[MAX_FAN];
+  int nfan;
 };
 
 // PAIR: fragment f covers rows {16(f/2) + 2r + f%2 : r = 0..7} instead of
@@ -297,7 +303,9 @@ __device__ __forceinline__ void store_block(const Acc<TL, CPLX>& acc, const Epil
           v.x += ep.beta * o.x;
           v.y += ep.beta * o.y;
         }
-        C[row + col * ep.ldc] = from_c<S>(v);
+        const S out = from_c<S>(v);
+        C[row + col * ep.ldc] = out;
+        for (int e = 0; e < ep.nfan; ++e) reinterpret_cast<S*>(ep.fan[e])[row + col * ep.ldc] = out;
       }
   }
 }

@@ -54,10 +54,10 @@ template <class TL>
 constexpr int tma_box_rows_b() { return TL::LDB; }
 template <class TL>
 constexpr unsigned tma_stage_bytes() { return (unsigned)(TL::BK * (TL::LDA + TL::LDB) * 8); }
-// Dynamic shared memory: STAGES operand stages | 2*STAGES mbarriers | 256-byte
-// aux area (producer state [0,128), caller state [128,256)) -- the producer's
+// Dynamic shared memory: STAGES operand stages | 2*STAGES mbarriers | 512-byte
+// aux area (producer state [0,384), caller state [384,512)) -- the producer's
 // bookkeeping lives here, not in registers every consumer thread would pay for.
-constexpr int TMA_AUX_BYTES = 256;
+constexpr int TMA_AUX_BYTES = 512;
 template <class TL>
 constexpr size_t tma_smem_bytes() {
   return (size_t)TL::STAGES * tma_stage_bytes<TL>() + 2 * TL::STAGES * 8 + TMA_AUX_BYTES;
@@ -110,7 +110,7 @@ __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUt
     uint32_t gp;
     int kt, live;
   };
-  static_assert(sizeof(Prod) <= 128, "producer state must fit its aux slot");
+  static_assert(sizeof(Prod) <= 384, "producer state must fit its aux slot");
   Prod& ps = *reinterpret_cast<Prod*>(tma_aux<TL>());
   auto produce_one = [&]() {
     if (!ps.live) return;
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
     return true;
   };
   // producer's cursor (thread 0 only) in the caller aux slot: no registers in the consumers
-  Cursor& cp = *reinterpret_cast<Cursor*>(tma_aux<TL>() + 128);
+  Cursor& cp = *reinterpret_cast<Cursor*>(tma_aux<TL>() + 384);
   if (threadIdx.x == 0) cp = Cursor{p.m_first, 0, -1};
   Cursor cc{p.m_first, 0, -1};
   tma_gemm_loop<TL>(

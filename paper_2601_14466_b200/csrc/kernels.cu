@@ -6,6 +6,7 @@
 //   * small copy / conjugate / mirror helpers.
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <type_traits>
 
 #include <cudaTypedefs.h>
@@ -14,6 +15,7 @@
 #include "tc_gemm.cuh"
 #include "tc_gemm_k.cuh"
 #include "ops.h"
+#include "comm.h"
 
 namespace bcmg {
 
@@ -49,11 +51,15 @@ static int num_sms() {
   return sms;
 }
 
+// once per kernel and process (the attribute is per function, not per
+// thread; a first cudaFuncSetAttribute can load the function's module, which
+// must not happen in the middle of another rank's flag hand-off)
+static std::mutex g_smem_mu;
 template <class K>
 static void set_smem(K kernel, size_t bytes) {
-  // idempotent; cheap enough to call per launch but cache per kernel anyway
-  static thread_local std::vector<const void*> done;
+  static std::vector<const void*> done;
   const void* key = reinterpret_cast<const void*>(kernel);
+  std::lock_guard<std::mutex> lk(g_smem_mu);
   if (std::find(done.begin(), done.end(), key) != done.end()) return;
   BCMG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   done.push_back(key);
@@ -119,8 +125,8 @@ static void gemm_t(int64_t M, int64_t N, int64_t K, const Operand& A, const Oper
   if constexpr (std::is_same_v<S, float>) {
     if (use_tc() && use_presplit() && !A.mask && !B.mask && aligned16(ep.C) && M >= 256 && N >= 64 && K >= 32)
       return gemm_tck_generic(M, N, K, A, B, ep, info, st);
-    if (use_tc() && !A.trans && !B.trans && !A.mask && !B.mask && tc_ok(A.ptr, A.ld) && tc_ok(B.ptr, B.ld) &&
-        tc_ok(ep.C, 4) && M >= 256 && N >= 64 && K >= 32)
+    if (use_tc() && ep.nfan == 0 && !A.trans && !B.trans && !A.mask && !B.mask && tc_ok(A.ptr, A.ld) &&
+        tc_ok(B.ptr, B.ld) && tc_ok(ep.C, 4) && M >= 256 && N >= 64 && K >= 32)
       return launch_tc3_gemm(M, N, K, A, B, ep, info, st);
   }
   if (N <= 16) return launch_gemm<S, TileNarrow, false>(M, N, K, A, B, ep, info, st);
@@ -427,6 +433,7 @@ bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, 
     return false;
   if (scratch_bytes < gemm_cplx_embed_bytes(dt, M, N, K)) return false;
   if (dt == C64 && (2 * M < 256 || N < 64)) return false;  // the tcgen05 tile's minimum shape
+  if (dt == C64 && ep.nfan && !use_presplit()) return false;  // the inline-split kernel has no fan-out
   // enough real blocks to fill the GPU (smaller GEMMs stay on the complex kernels), unless
   // the caller needs a shape-independent choice (bit-identical results across device counts)
   const int64_t blocks = ((2 * M + TileTrail2::BM - 1) / TileTrail2::BM) * ((N + TileTrail2::BN - 1) / TileTrail2::BN);
@@ -436,8 +443,10 @@ bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, 
     double* xp = reinterpret_cast<double*>(at + 2 * M * K);    // N x 2K real, ld N
     embed_gather<double2, double>(A, M, K, at, nullptr, M, st);
     embed_gather<double2, double>(B, N, K, nullptr, xp, N, st);
-    launch_gemm_tma_t<TileTrail2>(2 * M, N, 2 * K, Operand{at, 2 * M, 0, 0, 0, 0}, Operand{xp, N, 0, 0, 0, 0},
-                                  Epilogue{ep.C, 2 * ep.ldc, ep.alpha, ep.beta, 0, 0}, info, st);
+    Epilogue er = ep;  // real view of C (and of its fan-out copies)
+    er.ldc = 2 * ep.ldc;
+    launch_gemm_tma_t<TileTrail2>(2 * M, N, 2 * K, Operand{at, 2 * M, 0, 0, 0, 0}, Operand{xp, N, 0, 0, 0, 0}, er,
+                                  info, st);
   } else {
     float2* at = static_cast<float2*>(scratch);
     float* xp = reinterpret_cast<float*>(at + 2 * M * K);
@@ -450,7 +459,7 @@ bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, 
       split_tf32(0, at, 2 * M, 2 * M, 2 * K, 2 * K, ah, al, kp, st);
       split_tf32(0, xp, N, N, 2 * K, 2 * K, bh, bl, kp, st);
       tck_gemm(2 * M, N, 2 * K, ah, al, bh, bl, kp, static_cast<float*>(ep.C), 2 * ep.ldc, (float)ep.alpha,
-               (float)ep.beta, info, st);
+               (float)ep.beta, info, st, &ep);
     } else {
       launch_tc3_gemm(2 * M, N, 2 * K, Operand{at, 2 * M, 0, 0, 0, 0}, Operand{xp, N, 0, 0, 0, 0},
                       Epilogue{ep.C, 2 * ep.ldc, ep.alpha, ep.beta, 0, 0}, info, st);
@@ -633,7 +642,7 @@ static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t
 template <int BNT>
 static void tck_gemm_t(int64_t M, int64_t N, int64_t K, const float* ah, const float* al, const float* bh,
                        const float* bl, int64_t kp, float* C, int64_t ldc, float alpha, float beta, const int* info,
-                       cudaStream_t st) {
+                       cudaStream_t st, const FloatFan& fan) {
   const CUtensorMap mah = make_map_kmajor(ah, M, kp), mal = make_map_kmajor(al, M, kp);
   const CUtensorMap mbh = make_map_kmajor(bh, N, kp, BNT), mbl = make_map_kmajor(bl, N, kp, BNT);
   constexpr size_t smem = tck::Cfg<BNT>::SMEM_BYTES;
@@ -641,14 +650,23 @@ static void tck_gemm_t(int64_t M, int64_t N, int64_t K, const float* ah, const f
   const int64_t blocks = ((M + tc::BM - 1) / tc::BM) * ((N + BNT - 1) / BNT);
   const int64_t grid = std::min<int64_t>(blocks, (int64_t)num_sms());
   tck_gemm_kernel<BNT><<<(unsigned)grid, tck::THREADS, smem, st>>>(mah, mal, mbh, mbl, M, N, K, C, ldc, alpha, beta,
-                                                                    info);
+                                                                    info, fan);
   BCMG_CHECK_LAUNCH();
 }
 
+static FloatFan float_fan(const Epilogue& ep) {
+  FloatFan f{};
+  f.n = ep.nfan;
+  for (int e = 0; e < ep.nfan; ++e) f.p[e] = static_cast<float*>(ep.fan[e]);
+  return f;
+}
+
 void tck_gemm(int64_t M, int64_t N, int64_t K, const float* ah, const float* al, const float* bh, const float* bl,
-              int64_t kp, float* C, int64_t ldc, float alpha, float beta, const int* info, cudaStream_t st) {
-  if (tck_width(N) == 256) return tck_gemm_t<256>(M, N, K, ah, al, bh, bl, kp, C, ldc, alpha, beta, info, st);
-  tck_gemm_t<128>(M, N, K, ah, al, bh, bl, kp, C, ldc, alpha, beta, info, st);
+              int64_t kp, float* C, int64_t ldc, float alpha, float beta, const int* info, cudaStream_t st,
+              const Epilogue* fan_src) {
+  const FloatFan fan = fan_src ? float_fan(*fan_src) : FloatFan{};
+  if (tck_width(N) == 256) return tck_gemm_t<256>(M, N, K, ah, al, bh, bl, kp, C, ldc, alpha, beta, info, st, fan);
+  tck_gemm_t<128>(M, N, K, ah, al, bh, bl, kp, C, ldc, alpha, beta, info, st, fan);
 }
 
 // gemm() for float32 on tcgen05: both operands split into a scratch owned by
@@ -683,6 +701,15 @@ static float* split_scratch(cudaStream_t st, size_t bytes) {
   return static_cast<float*>(b->p);
 }
 
+// Grow the calling thread's split scratch for `st` ahead of a schedule loop:
+// growth frees the old buffer (cudaFree synchronises the device), which must
+// not happen while another rank's stream waits for a flag this thread has yet
+// to raise (peer-memory mode).
+void reserve_split_scratch(cudaStream_t st, size_t bytes) { split_scratch(st, bytes); }
+size_t split_scratch_bytes(int dt, int64_t M, int64_t N, int64_t K) {
+  return dt == C64 ? (size_t)2 * (2 * M + N) * split_ld(2 * K) * 4 : (size_t)2 * (M + N) * split_ld(K) * 4;
+}
+
 static void gemm_tck_generic(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
                              const int* info, cudaStream_t st) {
   const int64_t kp = split_ld(K);
@@ -690,7 +717,8 @@ static void gemm_tck_generic(int64_t M, int64_t N, int64_t K, const Operand& A, 
   float *ah = s, *al = s + M * kp, *bh = al + M * kp, *bl = bh + N * kp;
   split_tf32(A.trans ? 3 : 0, A.ptr, A.ld, M, K, K, ah, al, kp, st);
   split_tf32(B.trans ? 3 : 0, B.ptr, B.ld, N, K, K, bh, bl, kp, st);
-  tck_gemm(M, N, K, ah, al, bh, bl, kp, static_cast<float*>(ep.C), ep.ldc, (float)ep.alpha, (float)ep.beta, info, st);
+  tck_gemm(M, N, K, ah, al, bh, bl, kp, static_cast<float*>(ep.C), ep.ldc, (float)ep.alpha, (float)ep.beta, info, st,
+           &ep);
 }
 
 static void launch_tc3_trail(const TrailParams& p, const int* info, cudaStream_t st) {
@@ -1469,6 +1497,25 @@ __global__ void __launch_bounds__(512) dmma_peak_kernel(double* out, int iters) 
 #pragma unroll
   for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
   if (s == 12345.0) out[threadIdx.x] = s;
+}
+
+// ============================================================== peer-memory flags
+// One thread stores v to n (possibly peer, over NVLink) 32-bit words after
+// everything earlier on the stream; the fence makes the stream's earlier
+// peer-memory writes (fused GEMM fan-out) visible before the flag.
+__global__ void signal_kernel(PtrList addrs, unsigned v) {
+  __threadfence_system();
+  for (int i = 0; i < addrs.n; ++i) *reinterpret_cast<volatile unsigned*>(addrs.p[i]) = v;
+  __threadfence_system();
+}
+
+void stream_signal(cudaStream_t st, void* const* addrs, int n, unsigned v) {
+  if (n <= 0) return;
+  PtrList l{};
+  l.n = std::min(n, (int)(sizeof(l.p) / sizeof(l.p[0])));
+  for (int i = 0; i < l.n; ++i) l.p[i] = addrs[i];
+  signal_kernel<<<1, 1, 0, st>>>(l, v);
+  BCMG_CHECK_LAUNCH();
 }
 
 // ============================================================== synthetic SPD input

@@ -9,6 +9,10 @@
 
 namespace bcmg {
 
+struct PtrList {  // kernel-parameter array of device addresses
+  void* p[16];
+  int n;
+};
 long long launch_count();
 double measure_dmma_peak(cudaStream_t st);  // TFLOP/s
 // Synthetic Hermitian positive-definite row block (see gen_spd_kernel).
@@ -50,8 +54,11 @@ int64_t split_ld(int64_t kx);
 void split_tf32(int mode, const void* src, int64_t ld, int64_t rows, int64_t Kx, int64_t kc, float* hi, float* lo,
                 int64_t kp, cudaStream_t st);
 void tck_gemm(int64_t M, int64_t N, int64_t K, const float* ah, const float* al, const float* bh, const float* bl,
-              int64_t kp, float* C, int64_t ldc, float alpha, float beta, const int* info, cudaStream_t st);
+              int64_t kp, float* C, int64_t ldc, float alpha, float beta, const int* info, cudaStream_t st,
+              const Epilogue* fan_src = nullptr);
 bool tc_presplit_enabled();
+void reserve_split_scratch(cudaStream_t st, size_t bytes);
+size_t split_scratch_bytes(int dt, int64_t M, int64_t N, int64_t K);  // a GEMM's tf32 split planes
 
 // Diagonal tile: in-place lower Cholesky of the n x n block at A (lda) and
 // X := L^-1 (n x n, ldx, zero upper).  goff = global column of the block's

@@ -69,9 +69,14 @@ Session::Session(int device_, int rank_, int world_, const unsigned char* nccl_i
 Session::~Session() {
   cudaSetDevice(device);
   cudaDeviceSynchronize();
+  if (net) {
+    net->release_pointers(peer_panel[0]);
+    net->release_pointers(peer_panel[1]);
+    net->release_pointers(peer_sig);
+  }
   net.reset();
   for (auto* b : {&panel[0], &panel[1], &panel_pb[0], &panel_pb[1], &dinv, &wdiag, &info_dev, &tmp, &acc, &plan_buf,
-                  &stage_buf, &desc_buf, &embed_buf, &split_buf[0], &split_buf[1]})
+                  &stage_buf, &desc_buf, &embed_buf, &split_buf[0], &split_buf[1], &sig})
     b->release();
   for (auto& e : ev_pool) cudaEventDestroy(e);
   for (auto& e : ev_time) cudaEventDestroy(e);
@@ -479,6 +484,46 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
   const bool cplx_dt = dt == C128 || dt == C64;
   if (cplx_dt) embed_buf.ensure(gemm_cplx_embed_bytes(dt, n, T, T));  // panel solve by real embedding
   auto embed_k = [&](int64_t k) { return embed && complex_embed_ok(dt, n - g.stop(k), T); };
+  // Peer-memory mode (world > 1): the panel solve's epilogue writes panel k
+  // straight into every process's panel buffer over NVLink (GEMM fused with
+  // its broadcast); stream-ordered flags replace the NCCL broadcast.  sig
+  // words (uint32): [b] panel in buffer b ready (written by the owner),
+  // [2 + 16 b + r] process r done with buffer b (written by r).
+  const char* p2p_env = getenv("BCMG_P2P");
+  const bool p2p = world > 1 && world <= MAX_FAN + 1 && stream_wait_supported() &&
+                   (p2p_env ? atoi(p2p_env) != 0 : net->peer_default());
+  std::vector<void*> fan_panel[2];
+  uint32_t seq0 = 0;
+  auto sig_word = [&](int r, int idx) { return static_cast<void*>(static_cast<uint32_t*>(peer_sig[r]) + idx); };
+  auto my_word = [&](int idx) { return static_cast<const void*>(static_cast<const uint32_t*>(sig.p) + idx); };
+  if ((dt == R32 || dt == C64) && tc_presplit_enabled())  // the panel solves' split planes, sized up front
+    reserve_split_scratch(crit, split_scratch_bytes(dt, n, T, T));
+  if (p2p) {
+    if (peer_sig.empty()) {
+      sig.ensure(256 * sizeof(uint32_t));
+      BCMG_CUDA(cudaMemset(sig.p, 0, 256 * sizeof(uint32_t)));
+      BCMG_CUDA(cudaDeviceSynchronize());
+      peer_sig = net->exchange_pointers(sig.p);
+    }
+    for (int b2 = 0; b2 < 2; ++b2) {
+      net->release_pointers(peer_panel[b2]);
+      peer_panel[b2] = net->exchange_pointers(panel[b2].p);
+      for (int r = 0; r < world; ++r)
+        if (r != rank) fan_panel[b2].push_back(peer_panel[b2][r]);
+    }
+    seq0 = panel_seq;
+    panel_seq += (uint32_t)g.nt + 4;
+  }
+  auto seq_of = [&](int64_t k) { return seq0 + (uint32_t)k + 1; };
+  // peers done with buffer b before panel k is written into it: their last use
+  // was panel k - 2 (or the last panel in b of the previous call)
+  auto wait_peers_free = [&](int64_t k, cudaStream_t st) {
+    const int bb = (int)(k % 2);
+    const uint32_t need = k >= 2 ? seq_of(k - 2) : free_seq[bb];
+    if (!need) return;
+    for (int r = 0; r < world; ++r)
+      if (r != rank) stream_wait_geq(st, my_word(2 + 16 * bb + r), need);
+  };
   dinv.ensure((size_t)g.nt * T * T * g.esz);
   wdiag.ensure((size_t)T * T * g.esz);
   info_dev.ensure(sizeof(int));
@@ -503,7 +548,11 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
     if (s1 < n) {
       timed(K_TRSM, crit, cf * 2.0 * (double)(n - s1) * tc * tc, [&] {
         const Operand a21 = opA(colp(sh, g, s1, g.loc(k)), n, OP_N), xh = opB(dinv_k(k), T, OP_C);
-        const Epilogue ep{panel[k % 2].p, n - s1, 1.0, 0.0, 0, 0};
+        Epilogue ep{panel[k % 2].p, n - s1, 1.0, 0.0, 0, 0};
+        if (p2p) {  // the panel solve's epilogue also writes every peer's copy of the panel
+          ep.nfan = (int)fan_panel[k % 2].size();
+          for (int e = 0; e < ep.nfan; ++e) ep.fan[e] = fan_panel[k % 2][e];
+        }
         if (!(cplx_dt && gemm_cplx_embed(dt, n - s1, tc, tc, a21, xh, ep, embed_buf.p, embed_buf.bytes, info, crit)))
           gemm(dt, n - s1, tc, tc, a21, xh, ep, info, crit);
       });
@@ -577,10 +626,27 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
     switch (op.kind) {
       case S_FACTOR:  // F(k) overwrites panel buffer k%2, last used by panel k-2
         if (k >= 2) BCMG_CUDA(cudaStreamWaitEvent(crit, E(FREE, k - 2), 0));
+        if (p2p && s1 < n) wait_peers_free(k, crit);
         factor(k);
+        if (p2p && s1 < n) {  // panel k is in every peer's buffer: raise their ready flags
+          std::vector<void*> flags;
+          for (int r = 0; r < world; ++r)
+            if (r != rank) flags.push_back(sig_word(r, b));
+          stream_signal(crit, flags.data(), (int)flags.size(), seq_of(k));
+          BCMG_CUDA(cudaEventRecord(E(C, k), crit));
+        }
         BCMG_CUDA(cudaEventRecord(E(R, k), crit));
         break;
       case S_BCAST:  // panel k reaches every process
+        if (p2p) {
+          if (mine) break;
+          stream_wait_geq(comm, my_word(b), seq_of(k));  // written by the owner's fused panel solve
+          BCMG_CUDA(cudaEventRecord(E(C, k), comm));
+          if (embed_k(k)) expand_panel(dt, panel[b].p, panel_pb[b].p, n - s1, s1 - g.start(k), comm);
+          split_panel(k, comm);
+          BCMG_CUDA(cudaEventRecord(E(R, k), comm));
+          break;
+        }
         if (mine) BCMG_CUDA(cudaStreamWaitEvent(comm, E(R, k), 0));
         else if (k >= 2) BCMG_CUDA(cudaStreamWaitEvent(comm, E(FREE, k - 2), 0));
         bcast(panel[b].p, (size_t)op.elems * g.esz, (int)op.root, comm);
@@ -613,6 +679,13 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
         if (op.a) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(U, k), 0));
         if (world > 1) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(C, k), 0));
         BCMG_CUDA(cudaEventRecord(E(FREE, k), bulk));
+        if (p2p && s1 < n) {  // tell every process that buffer b may take panel k + 2
+          std::vector<void*> flags;
+          for (int r = 0; r < world; ++r)
+            if (r != rank) flags.push_back(sig_word(r, 2 + 16 * b + rank));
+          stream_signal(bulk, flags.data(), (int)flags.size(), seq_of(k));
+          free_seq[b] = seq_of(k);
+        }
         break;
       default:
         throw Error(CONFIG, "bad potrf schedule op");

@@ -97,6 +97,8 @@ struct Blk {
   float* C;
   int64_t ldc;
   float alpha, beta;
+  float* fan[MAX_FAN];  // peer copies of C (Epilogue::fan)
+  int nfan;
 };
 
 template <class Next>
@@ -283,7 +285,11 @@ __device__ __forceinline__ void tc3_loop(const CUtensorMap* mapA, const CUtensor
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int64_t col = blk.n0 + c0 + j;
-            if (col < blk.N) crow[col * blk.ldc] = blk.alpha * v[j] + blk.beta * old[j];
+            if (col < blk.N) {
+              const float o = blk.alpha * v[j] + blk.beta * old[j];
+              crow[col * blk.ldc] = o;
+              for (int e = 0; e < blk.nfan; ++e) blk.fan[e][r + col * blk.ldc] = o;
+            }
           }
         }
 #pragma unroll
@@ -321,6 +327,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     blk.ldc = ldc;
     blk.alpha = alpha;
     blk.beta = beta;
+    blk.nfan = 0;
     return true;
   });
 }
@@ -369,6 +376,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       blk.ldc = 2 * p.N;
       blk.alpha = -1.f;
       blk.beta = 1.f;
+      blk.nfan = 0;
       return true;
     }
     TZ::decode(item - cbase, tcw, rb, cb);
@@ -382,6 +390,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     blk.ldc = p.N;
     blk.alpha = -1.f;
     blk.beta = 1.f;
+    blk.nfan = 0;
     return true;
   });
 }

@@ -20,6 +20,10 @@
 #include "tc_gemm.cuh"
 
 namespace bcmg {
+struct FloatFan {  // peer copies of a tcgen05 GEMM's output (Epilogue::fan)
+  float* p[MAX_FAN];
+  int n;
+};
 namespace tck {
 
 using tc::BM;
@@ -174,7 +178,11 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int64_t col = blk.n0 + c0 + j;
-            if (col < blk.N) crow[col * blk.ldc] = blk.alpha * v[j] + blk.beta * old[j];
+            if (col < blk.N) {
+              const float o = blk.alpha * v[j] + blk.beta * old[j];
+              crow[col * blk.ldc] = o;
+              for (int e = 0; e < blk.nfan; ++e) blk.fan[e][r + col * blk.ldc] = o;
+            }
           }
         }
 #pragma unroll
@@ -199,7 +207,8 @@ template <int BNT>
 __global__ void __launch_bounds__(tck::THREADS, 1)
     tck_gemm_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                     const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, int64_t M,
-                    int64_t N, int64_t K, float* C, int64_t ldc, float alpha, float beta, const int* info) {
+                    int64_t N, int64_t K, float* C, int64_t ldc, float alpha, float beta, const int* info,
+                    FloatFan fan) {
   if (ld_flag(info)) return;
   const int64_t nbm = (M + tc::BM - 1) / tc::BM, nbn = (N + BNT - 1) / BNT;
   tck::tck_loop<BNT>(&mAh, &mAl, &mBh, &mBl, (int)K, [&](int64_t item, tc::Blk& blk) -> bool {
@@ -214,6 +223,8 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
     blk.ldc = ldc;
     blk.alpha = alpha;
     blk.beta = beta;
+    blk.nfan = fan.n;
+    for (int e = 0; e < fan.n; ++e) blk.fan[e] = fan.p[e];
     return true;
   });
 }
@@ -272,6 +283,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
     }
     blk.alpha = -1.f;
     blk.beta = 1.f;
+    blk.nfan = 0;
     return true;
   });
 }

@@ -2,6 +2,12 @@
 runs on CPU (oracle vs golden vectors, planner, host logic, ABI exports)."""
 
 import os
+
+# Several loopback ranks share one GPU in tests/test_gpu_loopback.py; with more
+# streams than hardware work queues, a stream parked on a peer flag can hold up
+# an unrelated stream that aliases its queue.  Read at CUDA context creation.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import sys
 
 import numpy as np

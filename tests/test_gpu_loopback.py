@@ -8,6 +8,7 @@ the result must be bit-identical to the single-process run (the reference's
 bit-exactness across device counts, test_solvers.py:172-179)."""
 
 import ctypes as C
+import gc
 import threading
 
 import numpy as np
@@ -45,11 +46,20 @@ def _run_ranks(world, body):
         except Exception as exc:  # noqa: BLE001
             errors.append((r, exc))
 
-    threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join(timeout=300)
+    # Nothing may synchronise the whole context while ranks are parked on peer
+    # flags (they share one GPU here): no garbage collection of other sessions
+    # (their destructors synchronise the device) during the multi-rank section.
+    gc.collect()
+    torch.cuda.synchronize()
+    gc.disable()
+    try:
+        threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=300)
+    finally:
+        gc.enable()
     assert not any(t.is_alive() for t in threads), "a rank hung"
     torch.cuda.synchronize()
     for s in sessions:
@@ -77,33 +87,48 @@ def _local_shards(a, n, t, ndev, world, r, device):
     return block, _lib.ptr_array(ptrs), (c0, c1)
 
 
+def _potrs_ranks(a, b, n, t, ndev, world, dtype):
+    """One multi-rank potrs; device inputs are prepared before the rank threads
+    start, so nothing in the threads allocates while a peer waits on a flag."""
+    import torch
+
+    lib = _lib.load()
+    inputs = []
+    for r in range(world):
+        block, ptrs, _ = _local_shards(a, n, t, ndev, world, r, "cuda")
+        x = torch.from_numpy(np.ascontiguousarray(b.T)).to("cuda")  # column-major replica
+        inputs.append((block, ptrs, x))
+    torch.cuda.synchronize()
+
+    def body(r, sess, st):
+        _, ptrs, x = inputs[r]
+        info = C.c_int(0)
+        _lib.check(lib.bcmg_potrs(sess, C.c_void_p(st.cuda_stream), CODES[dtype], n, b.shape[1], t, ndev, ptrs,
+                                  C.c_void_p(x.data_ptr()), n, 0, C.byref(info)))
+        assert info.value == 0
+        return r
+
+    _run_ranks(world, body)
+    torch.cuda.synchronize()
+    return [inputs[r][2].cpu().numpy().T for r in range(world)]
+
+
 @pytest.mark.parametrize("dtype,n,t,ndev,world", [
     (np.float64, 300, 32, 2, 2), (np.float64, 512, 64, 4, 2), (np.complex128, 260, 24, 4, 2),
     (np.float32, 384, 64, 4, 4), (np.complex64, 200, 40, 2, 2), (np.float64, 2048, 256, 4, 2),
 ])
-def test_loopback_potrs_matches_single_process(dtype, n, t, ndev, world):
-    import torch
-
-    lib = _lib.load()
+def test_loopback_potrs_matches_single_process(dtype, n, t, ndev, world, monkeypatch):
+    """Transport broadcasts between the ranks: the single-process bits."""
     a = O.make_matrix("random_spd", n, dtype, 11)
     b = np.asfortranarray(np.random.default_rng(2).standard_normal((n, 3)).astype(dtype))
-    base, _ = bc.solve_positive_definite(bc.make_mesh(ndev), a, b, bc.TileSpec(t))
-
-    def body(r, sess, st):
-        block, ptrs, _ = _local_shards(a, n, t, ndev, world, r, "cuda")
-        x = torch.from_numpy(np.ascontiguousarray(b.T)).to("cuda")  # column-major replica
-        info = C.c_int(0)
-        _lib.check(lib.bcmg_potrs(sess, C.c_void_p(st.cuda_stream), CODES[dtype], n, 3, t, ndev, ptrs,
-                                  C.c_void_p(x.data_ptr()), n, 0, C.byref(info)))
-        assert info.value == 0
-        st.synchronize()
-        return x.cpu().numpy().T
-
-    xs = _run_ranks(world, body)
+    mesh = bc.make_mesh(ndev)
+    base, _ = bc.solve_positive_definite(mesh, a, b, bc.TileSpec(t))
+    mesh.close()
+    monkeypatch.setenv("BCMG_P2P", "0")
+    xs = _potrs_ranks(a, b, n, t, ndev, world, dtype)
     for x in xs:
-        assert np.array_equal(x, base), "replicated solution differs from the single-process bits"
-    eps = O.eps_of(dtype)
-    assert O.solve_residual(a, xs[0], b) <= 100 * n * eps
+        assert np.array_equal(x, base), "solution differs from the single-process bits"
+    assert O.solve_residual(a, xs[0], b) <= 100 * n * O.eps_of(dtype)
 
 
 @pytest.mark.parametrize("dtype,n,t,ndev,world", [
