@@ -831,10 +831,20 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
   acc.ensure(nt_bytes);       // product blocks of every device (gather buffer)
   // complex128: scratch of the real-embedding GEMMs (W sweep: (2(n-s)+c) x T; product
   // sweep: column chunks of (2T + chunk) x (n-s))
+  // columns of one full wave of embedded output tiles for a product sweep GEMM
+  // with tcs rows: 2*tcs real rows in 128-row blocks, 2 CTAs per SM of 64-wide
+  // tiles (complex128, FP64 TMA kernel) or 1 CTA per SM of 256-wide tiles
+  // (complex64, tcgen05)
+  int nsm_ = 148;
+  BCMG_CUDA(cudaDeviceGetAttribute(&nsm_, cudaDevAttrMultiProcessorCount, device));
+  auto wave_cols = [&](int64_t tcs) -> int64_t {
+    const int64_t rb = (2 * tcs + 127) / 128;
+    return dt == C64 ? std::max<int64_t>(1, nsm_ / rb) * 256 : std::max<int64_t>(1, 2 * nsm_ / rb) * 64;
+  };
   // (T and n even: every column count is even, so the choice is the same for any device count)
   const bool emb = (dt == C128 && T % 2 == 0 && n % 2 == 0) || (dt == C64 && T % 64 == 0 && n % 4 == 0);  // c64: tcgen05 tile minimums hold for every D
   if (emb && !getenv("BCMG_NO_CPLX_EMBED"))
-    embed_buf.ensure(std::max(gemm_cplx_embed_bytes(dt, n, n, T), (size_t)(2 * T + 2048) * n * g.esz));
+    embed_buf.ensure(std::max(gemm_cplx_embed_bytes(dt, n, n, T), (size_t)(2 * T + 2 * wave_cols(T)) * n * g.esz));
   cudaStream_t st = crit;
   char* pan = static_cast<char*>(panel[0].p);
   char* stage = static_cast<char*>(panel[1].p);
@@ -903,9 +913,11 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
           char* sh = colp(shards[d - g.dev0], g, ss, 0);
           char* blk = blocks + block_off(s, d) * g.esz;
           if (emb) {
-            // real embedding in column chunks sized to the scratch (both operands are gathered)
+            // real embedding in column chunks of whole waves of output tiles
+            // (both operands are gathered into the scratch, which bounds the chunk)
+            const int64_t wave = wave_cols(tcs);
             int64_t nc = (int64_t)(embed_buf.bytes / ((size_t)(n - ss) * g.esz)) - 2 * tcs;
-            nc = nc / 64 * 64;
+            nc = nc >= wave ? nc / wave * wave : nc / 64 * 64;
             bool done = nc >= 64;
             for (int64_t c0 = 0; done && c0 < c; c0 += nc) {
               const int64_t cn = std::min(nc, c - c0);
