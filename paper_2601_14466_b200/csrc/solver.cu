@@ -564,8 +564,16 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
   // crit stream, the bulk update is a persistent grid capped at (SMs - reserve)
   // CTAs: its CTAs fill an SM's shared memory, so the cap is what leaves SMs
   // on which the latency-bound critical path can overlap the bulk GEMM.
-  int reserve = 2;  // measured at N=32768, T=1024: 2 -> 28.9, 4 -> 27.7, 8 -> 28.2 TFLOP/s
-  if (const char* e = getenv("BCMG_RESERVE_SMS")) reserve = std::max(0, atoi(e));
+  // Per step: while the trailing matrix is at least 32 tiles wide the bulk
+  // update dwarfs the critical path and gets every SM; below that, 2 SMs stay
+  // free for it (measured, f64 T=1024: N=131072 reserve 0/1/2 -> 34.3/34.2/
+  // 33.9 TFLOP/s; N=32768 reserve 2/4/8 -> 28.9/27.7/28.2).
+  int reserve_fixed = -1;
+  if (const char* e = getenv("BCMG_RESERVE_SMS"); e && *e) reserve_fixed = std::max(0, atoi(e));
+  auto reserve_at = [&](int64_t k) {
+    if (reserve_fixed >= 0) return reserve_fixed;
+    return (n - g.stop(k)) / T >= 32 ? 0 : 2;
+  };
   int nsm = 148;
   BCMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   auto trail = [&](int64_t k, int64_t m_first, int64_t m_last, cudaStream_t st, int cap = 0) {
@@ -667,7 +675,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
           // first; otherwise both persistent grids would race for the SMs and
           // the critical path could be queued behind the whole bulk update
           if (op.root) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(U, k), 0));
-          trail(k, op.a, op.b, bulk, op.root ? std::max(1, nsm - reserve) : 0);
+          trail(k, op.a, op.b, bulk, op.root ? std::max(1, nsm - reserve_at(k)) : 0);
         }
         break;
       case S_COPYBACK:  // factor below the diagonal back into A (potrs/potri read it there)
