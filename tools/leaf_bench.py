@@ -6,7 +6,7 @@ import paper_2601_14466_b200 as bc
 from paper_2601_14466_b200 import _lib
 lib = _lib.load()
 mesh = bc.make_mesh(1)
-for n in [8, 64, 128, 256, 512, 1024]:
+for n in [int(v) for v in (sys.argv[1].split(",") if len(sys.argv) > 1 else "8,64,128,256,512,1024".split(","))]:
     A0 = torch.rand(n, n, dtype=torch.float64, device="cuda")
     A0 = A0 + A0.t() + n * torch.eye(n, dtype=torch.float64, device="cuda")
     A = A0.clone()
