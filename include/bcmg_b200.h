@@ -133,6 +133,15 @@ int bcmg_close(bcmg_session* s);
    overwritten by the factor in block-cyclic order. *info = LAPACK pivot. */
 int bcmg_potrs(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t nrhs, int64_t tile, int ndev,
                void* const* shards, void* b, int64_t ldb, int flags, int* info);
+/* bcmg_potrs for one process and one device with A in pinned HOST memory
+   (a_host, n x n column-major -- the row-major bytes of the drop-in call): A is
+   copied into a_dev (device, n x n) tile column by tile column while the
+   factorisation already runs on the arrived tiles (left-looking for the first
+   quarter of the tiles, then a catch-up update and the right-looking
+   schedule; float64), so the upload overlaps compute.  Same result contract
+   as bcmg_potrs (agreement to rounding with it). */
+int bcmg_potrs_streamed(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t nrhs, int64_t tile,
+                        void* a_dev, const void* a_host, void* b, int64_t ldb, int flags, int* info);
 /* A's shards (contiguous layout) are overwritten by the full Hermitian inverse,
    contiguous layout. */
 int bcmg_potri(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev, void* const* shards,

@@ -109,7 +109,19 @@ def potrs(A, b, T_A: int, mesh: DeviceMesh | None = None, in_specs=None, *, over
 
     mesh = mesh or make_mesh()
     _check_specs(in_specs, mesh, 2)
-    A, et, n = _prepare_a(A, mesh, overwrite_a)
+    # pinned host A on one device: stream it in while the factorisation starts
+    # (bcmg_potrs_streamed) instead of uploading it first
+    host_src = None
+    if (isinstance(A, torch.Tensor) and A.device.type == "cpu" and A.is_pinned() and A.is_contiguous()
+            and A.ndim == 2 and mesh.num_devices == 1 and mesh.world == 1):
+        host_src = A
+        et = ElementType.from_dtype(A.dtype)
+        n = int(A.shape[1])
+        if int(A.shape[0]) != n:
+            raise DescriptorError("dimension-mismatch", f"row shard {tuple(A.shape)} does not tile an {n}x{n} matrix")
+        A = torch.empty((n, n), dtype=A.dtype, device=mesh.torch_device)
+    else:
+        A, et, n = _prepare_a(A, mesh, overwrite_a)
     validate_tile(TileSpec(int(T_A)), n)
     if isinstance(b, np.ndarray):
         b = torch.from_numpy(np.ascontiguousarray(b))
@@ -126,9 +138,15 @@ def potrs(A, b, T_A: int, mesh: DeviceMesh | None = None, in_specs=None, *, over
     x.copy_(b2.t())
     info = C.c_int(0)
     with mesh.coordinated():
-        rc = _lib.load().bcmg_potrs(mesh.session, mesh.stream_handle(), et.code, n, nrhs, int(T_A), mesh.num_devices,
-                                    _shard_ptrs(A, mesh, n, int(T_A), et.width), C.c_void_p(x.data_ptr()), n,
-                                    _lib.BCMG_FLAG_ROW_SHARDED, C.byref(info))
+        if host_src is not None:
+            rc = _lib.load().bcmg_potrs_streamed(mesh.session, mesh.stream_handle(), et.code, n, nrhs, int(T_A),
+                                                 C.c_void_p(A.data_ptr()), C.c_void_p(host_src.data_ptr()),
+                                                 C.c_void_p(x.data_ptr()), n, _lib.BCMG_FLAG_ROW_SHARDED,
+                                                 C.byref(info))
+        else:
+            rc = _lib.load().bcmg_potrs(mesh.session, mesh.stream_handle(), et.code, n, nrhs, int(T_A),
+                                        mesh.num_devices, _shard_ptrs(A, mesh, n, int(T_A), et.width),
+                                        C.c_void_p(x.data_ptr()), n, _lib.BCMG_FLAG_ROW_SHARDED, C.byref(info))
     _raise_for(rc, info.value)
     out = x.t()
     return out.reshape(-1) if one_dim else out

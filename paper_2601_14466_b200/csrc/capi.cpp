@@ -286,6 +286,40 @@ int bcmg_potrs(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t nrhs
   return rc;
 }
 
+int bcmg_potrs_streamed(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t nrhs, int64_t tile,
+                        void* a_dev, const void* a_host, void* b, int64_t ldb, int flags, int* info) {
+  int rc = guarded([&] {
+    auto* S = live(s);
+    if (bcmg::dtype_size(dtype) == 0) throw bcmg::Error(BCMG_ERR_CONFIG, "unknown element-type code");
+    if (!a_dev || !a_host) throw bcmg::Error(BCMG_ERR_CONFIG, "null matrix pointer");
+    if (S->world != 1) throw bcmg::Error(BCMG_ERR_CONFIG, "streamed input is single-process");
+    if (nrhs < 1) throw bcmg::Error(BCMG_ERR_CONFIG, "right-hand side must be non-empty");
+    if (ldb < n) throw bcmg::Error(BCMG_ERR_CONFIG, "ldb < n");
+    if (tile < 1 || tile > n) throw bcmg::Error(BCMG_ERR_CONFIG, "tile width out of range");
+    Entry e(S, stream);
+    const bool conj = (flags & BCMG_FLAG_ROW_SHARDED) && bcmg::dtype_complex(dtype);
+    S->mark(bcmg::T_BEGIN);
+    if (conj) bcmg::conj2d(dtype, b, ldb, n, nrhs, S->user);
+    S->mark(bcmg::T_REDIST);  // one device: the block-cyclic layout is the contiguous one
+    void* shards[1] = {a_dev};
+    *info = S->potrf(dtype, n, tile, 1, shards, a_host);
+    S->mark(bcmg::T_POTRF);
+    if (*info) {
+      S->mark(bcmg::T_SOLVE);
+      finish_timings(S, false);
+      throw bcmg::Error(BCMG_ERR_NOT_POSITIVE_DEFINITE,
+                        "matrix is not positive definite: leading minor of order " + std::to_string(*info) +
+                            " (pivot=" + std::to_string(*info) + ")");
+    }
+    S->begin(S->user);
+    S->potrs(dtype, n, nrhs, tile, 1, shards, b, ldb);
+    if (conj) bcmg::conj2d(dtype, b, ldb, n, nrhs, S->user);
+    S->mark(bcmg::T_SOLVE);
+    finish_timings(S, false);
+  });
+  return rc;
+}
+
 int bcmg_potri(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev, void* const* shards,
                int flags, int* info) {
   (void)flags;  // inv(conj(A)) = conj(inv(A)) is the row-major view of inv(A): no fix-up needed

@@ -447,8 +447,9 @@ std::vector<SchedOp> potrs_schedule(int64_t n, int64_t T, int ndev, int world, i
 // Panel k lives in panel[k % 2] with rows [stop_k, n) (ld = n - stop_k): only
 // the rows the trailing update reads (the reference copies the full-height
 // panel, solvers.py:389-394).  X_kk = L_kk^-1 is kept in dinv for potrs/potri.
-int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) {
+int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, const void* host) {
   const Geo g = make_geo(*this, dt, n, T, ndev);
+  if (host && (world != 1 || ndev != 1)) throw Error(CONFIG, "streamed host input needs one process and one device");
   const size_t panel_bytes = (size_t)n * T * g.esz;
   // complex128: the panel is followed by -iP, plus a planar copy (TrailParams::cplx)
   // float32 / complex64 on tcgen05: the panel is split once per step into tf32
@@ -620,6 +621,68 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
     if (flops > 0) timed(K_TRAIL, st, flops, [&] { trailing_update(dt, p, info, st); });
   };
 
+  // Streamed host input (one device): the tile columns are copied from pinned
+  // host memory on the comm stream in order; while they arrive, tiles [0, j)
+  // are factored LEFT-looking (tile m -= L[:, 0:m] L[m rows, 0:m]^H, one GEMM
+  // with K = m T, then its diagonal factor and panel solve), so the GPU works
+  // during the upload; once everything is resident the trailing tiles receive
+  // the update of panels [0, j) in one trailing-update launch (K = j T) and the
+  // right-looking schedule continues from step j.  (float64; other types
+  // upload first.)  The summation order of those first updates differs from
+  // the device-input path, so results agree to rounding, not bit for bit.
+  int64_t k0 = 0;
+  if (host) {
+    std::vector<cudaEvent_t> up(g.nt);
+    char* dev = static_cast<char*>(shards[0]);
+    const char* src = static_cast<const char*>(host);
+    BCMG_CUDA(cudaStreamWaitEvent(comm, ev(kJoin + 4), 0));
+    for (int64_t m = 0; m < g.nt; ++m) {
+      const size_t off = (size_t)g.start(m) * n * g.esz, bytes = (size_t)(g.stop(m) - g.start(m)) * n * g.esz;
+      BCMG_CUDA(cudaMemcpyAsync(dev + off, src + off, bytes, cudaMemcpyHostToDevice, comm));
+      BCMG_CUDA(cudaEventCreateWithFlags(&up[m], cudaEventDisableTiming));
+      BCMG_CUDA(cudaEventRecord(up[m], comm));
+    }
+    const int64_t j = (dt == R64 && g.nt >= 8 && !getenv("BCMG_NO_STREAMED_LEFT")) ? g.nt / 4 : 0;
+    for (int64_t m = 0; m < j; ++m) {
+      const int64_t ms = g.start(m), me = g.stop(m), tc = me - ms;
+      BCMG_CUDA(cudaStreamWaitEvent(crit, up[m], 0));
+      if (m > 0) {
+        char* A = static_cast<char*>(shards[0]);
+        gemm(dt, n - ms, tc, ms, opA(A + ms * g.esz, n, OP_N), opB(A + ms * g.esz, n, OP_C),
+             Epilogue{A + (ms + ms * n) * g.esz, n, -1.0, 1.0, 0, 0}, info, crit);
+      }
+      factor(m);
+      if (me < n) copy2d(dt, panel[m % 2].p, n - me, colp(shards[0], g, me, g.loc(m)), n, n - me, tc, false, info,
+                         crit);
+    }
+    BCMG_CUDA(cudaStreamWaitEvent(crit, up[g.nt - 1], 0));
+    if (j > 0 && j < g.nt) {  // catch-up: tiles [j, nt) -= L[:, 0:jT] L[tile rows, 0:jT]^H
+      TrailParams p{};
+      p.P = static_cast<char*>(shards[0]) + g.start(j) * g.esz;
+      p.ldp = n;
+      p.prow0 = g.start(j);
+      p.N = n;
+      p.T = T;
+      p.K = g.start(j);
+      p.D = 1;
+      p.dev0 = 0;
+      p.nloc = 1;
+      p.shards[0] = shards[0];
+      p.m_first = j;
+      p.m_last = g.nt;
+      double flops = 0;
+      for (int64_t m = j; m < g.nt; ++m) {
+        const double rows = (double)(n - m * T), tcm = (double)std::min<int64_t>(T, n - m * T);
+        flops += 2.0 * (double)p.K * (rows * tcm - tcm * (tcm - 1) / 2);
+      }
+      timed(K_TRAIL, crit, flops, [&] { trailing_update(dt, p, info, crit); });
+    }
+    for (cudaEvent_t e : up) cudaEventDestroy(e);
+    sync_streams(bulk, crit);
+    sync_streams(comm, crit);
+    k0 = j;
+  }
+
   // Execute this process's schedule (potrf_schedule).  Event slots:
   // type*8 + k%8 (dependencies reach back at most two steps).
   //   R[k]    panel k usable on this process     C[k] broadcast of panel k done
@@ -628,6 +691,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards) 
   enum { R = 0, C = 1, B = 2, U = 3, FREE = 4 };
   auto E = [&](int type, int64_t k) { return ev(type * 8 + (int)(k % 8)); };
   for (const SchedOp& op : potrf_schedule(n, T, ndev, world, rank)) {
+    if (op.k < k0) continue;  // factored left-looking during a streamed upload
     const int64_t k = op.k, s1 = g.stop(k);
     const bool mine = g.owns(k);
     const int b = (int)(k % 2);

@@ -115,7 +115,9 @@ struct Session {
   void redistribute_multi(int dt, int64_t n_rows, int64_t n_cols, int64_t T, int ndev, void* const* shards,
                           bool inverse);
   DevBuf stage_buf, desc_buf;
-  int potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards);
+  // host != nullptr: shards[0] (one device) is filled from pinned host memory
+  // (same layout) while the factorisation starts (see solver.cu)
+  int potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, const void* host = nullptr);
   void potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* const* shards, void* x, int64_t ldx);
   void potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards);
 };

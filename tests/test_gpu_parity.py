@@ -341,3 +341,25 @@ def test_staged_redistribution_path(meshes, monkeypatch, n, t, d, rows, chunk):
     assert np.array_equal(device_concat(mesh, cyc), O.deal_columns(a, t, d))
     back = bc.redistribute_out(mesh, cyc)
     assert np.array_equal(device_concat(mesh, back), a)
+
+
+@pytest.mark.parametrize("dtype,n,t", [(np.float64, 2048, 128), (np.float64, 1000, 96), (np.complex128, 768, 96),
+                                       (np.float32, 1024, 128)])
+def test_dropin_streamed_host_input(meshes, dtype, n, t):
+    """Pinned host A on one device streams in while the factorisation starts
+    (bcmg_potrs_streamed; float64: first quarter of the tiles left-looking):
+    same answer as the device-resident call to rounding, reference tolerances."""
+    import torch
+
+    a = O.make_matrix("random_spd", n, dtype, 17)
+    b = np.random.default_rng(4).standard_normal((n, 2)).astype(dtype)
+    mesh = meshes(1)
+    host = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    x = bc.potrs(host, torch.from_numpy(b), T_A=t, mesh=mesh).cpu().numpy()
+    xd = bc.potrs(host.cuda(), torch.from_numpy(b), T_A=t, mesh=mesh).cpu().numpy()
+    eps = O.eps_of(dtype)
+    xr = O.solve_unblocked(a, b)
+    assert np.abs(x - xr).max() <= 10 * n * eps * max(1.0, np.abs(xr).max())
+    assert np.abs(x - xd).max() <= 10 * n * eps * max(1.0, np.abs(xd).max())
+    assert O.solve_residual(a, x, b) <= 100 * n * eps
+    assert np.array_equal(host.numpy(), np.ascontiguousarray(a)), "caller's host A must be untouched"
