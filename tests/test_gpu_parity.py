@@ -363,3 +363,18 @@ def test_dropin_streamed_host_input(meshes, dtype, n, t):
     assert np.abs(x - xd).max() <= 10 * n * eps * max(1.0, np.abs(xd).max())
     assert O.solve_residual(a, x, b) <= 100 * n * eps
     assert np.array_equal(host.numpy(), np.ascontiguousarray(a)), "caller's host A must be untouched"
+
+
+@pytest.mark.parametrize("bad", [150, 700])
+def test_dropin_streamed_not_positive_definite(meshes, bad):
+    """A failing pivot in the left-looking upload phase (tile 2) or in the
+    right-looking phase (tile 10) raises with the LAPACK pivot."""
+    import torch
+
+    n, t = 1024, 64
+    a = np.diag(np.arange(1.0, n + 1))
+    a[bad, bad] = -1.0
+    host = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    with pytest.raises(bc.NotPositiveDefiniteError) as ei:
+        bc.potrs(host, torch.ones(n, dtype=torch.float64), T_A=t, mesh=meshes(1))
+    assert ei.value.pivot == bad + 1
