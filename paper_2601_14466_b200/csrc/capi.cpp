@@ -263,6 +263,7 @@ int bcmg_potrs(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t nrhs
     if (ldb < n) throw bcmg::Error(BCMG_ERR_CONFIG, "ldb < n");
     if (tile < 1 || tile > n) throw bcmg::Error(BCMG_ERR_CONFIG, "tile width out of range");
     Entry e(S, stream);
+    S->reserve_workspace(1, dtype, n, tile, ndev, nrhs);
     const bool conj = (flags & BCMG_FLAG_ROW_SHARDED) && bcmg::dtype_complex(dtype);
     S->mark(bcmg::T_BEGIN);
     if (conj) bcmg::conj2d(dtype, b, ldb, n, nrhs, S->user);
@@ -297,6 +298,7 @@ int bcmg_potrs_streamed(bcmg_session* s, void* stream, int dtype, int64_t n, int
     if (ldb < n) throw bcmg::Error(BCMG_ERR_CONFIG, "ldb < n");
     if (tile < 1 || tile > n) throw bcmg::Error(BCMG_ERR_CONFIG, "tile width out of range");
     Entry e(S, stream);
+    S->reserve_workspace(1, dtype, n, tile, 1, nrhs);
     const bool conj = (flags & BCMG_FLAG_ROW_SHARDED) && bcmg::dtype_complex(dtype);
     S->mark(bcmg::T_BEGIN);
     if (conj) bcmg::conj2d(dtype, b, ldb, n, nrhs, S->user);
@@ -328,6 +330,7 @@ int bcmg_potri(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile
     check_common(dtype, ndev, shards);
     if (tile < 1 || tile > n) throw bcmg::Error(BCMG_ERR_CONFIG, "tile width out of range");
     Entry e(S, stream);
+    S->reserve_workspace(2, dtype, n, tile, ndev, 1);
     S->mark(bcmg::T_BEGIN);
     S->redistribute(dtype, n, n, tile, ndev, shards, false);
     S->mark(bcmg::T_REDIST);

@@ -443,6 +443,43 @@ std::vector<SchedOp> potrs_schedule(int64_t n, int64_t T, int ndev, int world, i
   return ops;
 }
 
+// ------------------------------------------------------------------ workspace
+// Every buffer a pipeline will need, allocated BEFORE it moves any data, so an
+// out-of-memory failure leaves the caller's shards untouched (the reference
+// raises before any data movement, test_solvers.py:344-352).  The drivers'
+// own ensure() calls then find the buffers large enough (grow-only).
+void Session::reserve_workspace(int routine, int dt, int64_t n, int64_t T, int ndev, int64_t nrhs) {
+  const Geo g = make_geo(*this, dt, n, T, ndev);
+  const size_t panel_bytes = (size_t)n * T * g.esz;
+  const bool presplit = (dt == R32 || dt == C64) && tc_presplit_enabled();
+  if (presplit) {
+    const size_t plane = (size_t)n * split_ld(dt == C64 ? 2 * T : T) * 4;
+    split_buf[0].ensure(dt == C64 ? 6 * plane : 2 * plane);
+    split_buf[1].ensure(dt == C64 ? 6 * plane : 2 * plane);
+    reserve_split_scratch(crit, split_scratch_bytes(dt, n, T, T));
+  }
+  const bool embed = !presplit && complex_embed_ok(dt, 0, T);
+  panel[0].ensure(embed ? 2 * panel_bytes : panel_bytes);
+  panel[1].ensure(embed ? 2 * panel_bytes : panel_bytes);
+  if (embed) {
+    panel_pb[0].ensure(panel_bytes);
+    panel_pb[1].ensure(panel_bytes);
+  }
+  if (dt == C128 || dt == C64) embed_buf.ensure(gemm_cplx_embed_bytes(dt, n, T, T));
+  dinv.ensure((size_t)g.nt * T * T * g.esz);
+  wdiag.ensure((size_t)T * T * g.esz);
+  info_dev.ensure(sizeof(int));
+  if (routine == 1) {  // potrs: split-K slabs + (multi-process) the solution hand-off buffer
+    const size_t parts_bytes = (size_t)64 * T * nrhs * g.esz;
+    tmp.ensure(std::max<size_t>(4096, parts_bytes + (world > 1 ? (size_t)n * nrhs * g.esz : 0)));
+  } else {
+    tmp.ensure(4096);
+  }
+  if (routine == 2) {  // potri: the W-tile / block buffers (the embedding scratch is sized in potri)
+    acc.ensure(panel_bytes);
+  }
+}
+
 // ------------------------------------------------------------------ potrf
 // Panel k lives in panel[k % 2] with rows [stop_k, n) (ld = n - stop_k): only
 // the rows the trailing update reads (the reference copies the full-height

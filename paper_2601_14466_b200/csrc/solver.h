@@ -118,6 +118,8 @@ struct Session {
   // host != nullptr: shards[0] (one device) is filled from pinned host memory
   // (same layout) while the factorisation starts (see solver.cu)
   int potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, const void* host = nullptr);
+  // routine: 1 potrs pipeline, 2 potri pipeline (throws OUT_OF_MEMORY before any data moves)
+  void reserve_workspace(int routine, int dt, int64_t n, int64_t T, int ndev, int64_t nrhs);
   void potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* const* shards, void* x, int64_t ldx);
   void potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards);
 };

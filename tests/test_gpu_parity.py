@@ -378,3 +378,31 @@ def test_dropin_streamed_not_positive_definite(meshes, bad):
     with pytest.raises(bc.NotPositiveDefiniteError) as ei:
         bc.potrs(host, torch.ones(n, dtype=torch.float64), T_A=t, mesh=meshes(1))
     assert ei.value.pivot == bad + 1
+
+
+def test_out_of_memory_before_any_data_movement(meshes):
+    """Workspace is reserved before the pipeline touches the shards: an
+    impossible workspace fails with OUT_OF_MEMORY and the input is unchanged
+    (reference test_solvers.py:344-352)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2601_14466_b200 import _lib
+
+    lib = _lib.load()
+    mesh = meshes(1)
+    buf = torch.arange(4096, dtype=torch.float64, device="cuda")
+    before = buf.clone()
+    n, t = 2_000_000, 100_000  # panels alone would need ~1.6 TB
+    x = torch.zeros(16, dtype=torch.float64, device="cuda")
+    info = C.c_int(0)
+    rc = lib.bcmg_potrs(mesh.session, mesh.stream_handle(), 1, n, 1, t, 1, _lib.ptr_array([buf.data_ptr()]),
+                        C.c_void_p(x.data_ptr()), n, 0, C.byref(info))
+    assert rc == _lib.BCMG_ERR_OUT_OF_MEMORY
+    torch.cuda.synchronize()
+    assert torch.equal(buf, before)
+    # the session is still usable afterwards
+    a = O.make_matrix("random_spd", 64, np.float64, 1)
+    xs, _ = bc.solve_positive_definite(mesh, a, np.ones((64, 1)), bc.TileSpec(16))
+    assert O.solve_residual(a, xs, np.ones((64, 1))) <= 100 * 64 * O.eps_of(np.float64)
