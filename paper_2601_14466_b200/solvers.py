@@ -227,17 +227,32 @@ def redistribute_out(mesh: DeviceMesh, dmat: DistributedMatrix) -> DistributedMa
 def workspace_nbytes(routine: str, desc: MatrixDescriptor, tile: TileSpec, num_devices: int, n_rhs: int = 1) -> list[int]:
     """Device bytes per logical device incl. shards (solvers.py:279-308).
 
-    Native workspace per process: two panels (n x T), the diagonal-block
-    inverses (ceil(n/T) x T^2), a T^2 scratch; potrs adds the replicated RHS
-    and split-K partials, potri an n x T accumulator."""
+    The native pipelines reserve all of it before moving any data, so an
+    out-of-memory error leaves the shards untouched; potrs adds the
+    replicated RHS and split-K partials, potri an n x T accumulator."""
     esz = desc.element_type.width
+    et = desc.element_type
     n, T = desc.n_rows, tile.tile_width
     nt = -(-n // T)
-    base = 2 * n * T * esz + nt * T * T * esz + T * T * esz
+    # mirrors Session::reserve_workspace (csrc/solver.cu): two panels (x2 plus a
+    # planar copy for the complex128 [P | -iP] embedding), tf32 hi/lo split
+    # planes for real32/complex64, the complex embedding scratch, the diagonal
+    # block inverses and T x T scratch
+    panel = n * T * esz
+    kp = -(-(2 * T if et.is_complex else T) // 4) * 4
+    if et in (ElementType.real32, ElementType.complex64):
+        base = 2 * panel + 2 * (6 if et.is_complex else 2) * n * kp * 4
+    elif et is ElementType.complex128 and T % 2 == 0:
+        base = 2 * 2 * panel + 2 * panel
+    else:
+        base = 2 * panel
+    if et.is_complex:
+        base += (2 * n + T) * T * esz
+    base += nt * T * T * esz + T * T * esz
     if routine == "potrs":
-        extra = base + n * n_rhs * esz + (-(-n // 8192) + 1) * T * n_rhs * esz
+        extra = base + n * n_rhs * esz + 64 * T * n_rhs * esz
     elif routine == "potri":
-        extra = base + n * T * esz
+        extra = base + panel
     else:
         raise ValueError(f"unknown routine {routine!r}")
     return [c * desc.column_nbytes + extra for c in device_column_counts(desc.n_cols, tile, num_devices)]
