@@ -81,7 +81,8 @@ class NcclComm final : public Comm {
       if (r != me_ && ptrs[r]) cudaIpcCloseMemHandle(ptrs[r]);
     ptrs.clear();
   }
-  bool peer_default() const override { return true; }
+  // opt-in (BCMG_P2P=1) until the fused path has been measured across GPUs
+  bool peer_default() const override { return false; }
   int allreduce_min(int v, void* scratch, cudaStream_t st) override {
     int* d = static_cast<int*>(scratch);
     BCMG_CUDA(cudaMemcpyAsync(d, &v, sizeof(int), cudaMemcpyHostToDevice, st));

@@ -40,10 +40,11 @@ class Comm {
   // (collective, same call order on every rank).  Empty if unsupported.
   virtual std::vector<void*> exchange_pointers(void* local) = 0;
   virtual void release_pointers(std::vector<void*>& ptrs) = 0;
-  // peer-memory hand-offs by default?  Across GPUs yes; for loopback ranks
-  // sharing one context only on request (BCMG_P2P=1): a context-wide
-  // synchronisation there (lazy kernel loading, cudaFree) waits for streams
-  // parked on flags that the synchronising rank has yet to raise.
+  // peer-memory hand-offs by default?  No for now: on request (BCMG_P2P=1)
+  // only.  Loopback ranks share one context, where a context-wide
+  // synchronisation (lazy kernel loading, cudaFree) waits for streams parked
+  // on flags that the synchronising rank has yet to raise; across GPUs the
+  // path has not been measured yet, so NCCL's broadcast stays the default.
   virtual bool peer_default() const = 0;
 };
 
