@@ -74,6 +74,22 @@ struct Epilogue {
   int nfan;
 };
 
+// fan[e] through constant offsets only: indexing a fan array with a runtime e
+// would move a kernel's local Epilogue / Blk copy into local memory
+template <class P>
+__device__ __forceinline__ P fan_at(P const (&fan)[MAX_FAN], int e) {
+  static_assert(MAX_FAN == 7, "fan_at enumerates MAX_FAN entries");
+  switch (e) {
+    case 0: return fan[0];
+    case 1: return fan[1];
+    case 2: return fan[2];
+    case 3: return fan[3];
+    case 4: return fan[4];
+    case 5: return fan[5];
+    default: return fan[6];
+  }
+}
+
 // PAIR: fragment f covers rows {16(f/2) + 2r + f%2 : r = 0..7} instead of
 // {8f + r}, so a thread's rows for fragments 2p and 2p+1 are adjacent and one
 // LDS.128 feeds two DMMA fragments (rows of a GEMM are independent: the
@@ -268,7 +284,7 @@ __device__ __forceinline__ void cp_feed_any(const Operand& op, int64_t I, int64_
 }
 
 // ----------------------------------------------------------------- epilogue
-template <class S, class TL, bool CPLX>
+template <class S, class TL, bool CPLX, bool FAN = true>
 __device__ __forceinline__ void store_block(const Acc<TL, CPLX>& acc, const Epilogue& ep, int64_t M, int64_t N,
                                             int64_t m0, int64_t n0, int wm0, int wn0, int lane) {
   const int r = lane >> 2, q = lane & 3;
@@ -305,7 +321,8 @@ __device__ __forceinline__ void store_block(const Acc<TL, CPLX>& acc, const Epil
         }
         const S out = from_c<S>(v);
         C[row + col * ep.ldc] = out;
-        for (int e = 0; e < ep.nfan; ++e) reinterpret_cast<S*>(ep.fan[e])[row + col * ep.ldc] = out;
+        if constexpr (FAN)
+          for (int e = 0; e < ep.nfan; ++e) static_cast<S*>(fan_at(ep.fan, e))[row + col * ep.ldc] = out;
       }
   }
 }

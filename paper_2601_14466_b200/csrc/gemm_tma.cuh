@@ -79,7 +79,7 @@ struct TmaBlock {
 // Persistent producer/consumer loop.  `next_p(item, blk)` / `next_c(item, blk)`
 // fill the block of work item `item` (producer / consumer view; separate so
 // stateful cursors stay monotone) and return false when there is none.
-template <class TL, class NextP, class NextC>
+template <class TL, bool FAN = true, class NextP, class NextC>
 __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUtensorMap* mapB, int K, NextP&& next_p,
                                               NextC&& next_c, long long stagger_ns = 0) {
   double* smem = reinterpret_cast<double*>(tma_dyn_smem);
@@ -175,7 +175,7 @@ __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUt
       if (lane == 0) mbar_arrive(&empty[s]);
       ++g;
     }
-    store_block<double, TL, false>(acc, cb.ep, cb.M, cb.N, cb.m0, cb.n0, wm0, wn0, lane);
+    store_block<double, TL, false, FAN>(acc, cb.ep, cb.M, cb.N, cb.m0, cb.n0, wm0, wn0, lane);
   }
 }
 
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
   Cursor& cp = *reinterpret_cast<Cursor*>(tma_aux<TL>() + 384);
   if (threadIdx.x == 0) cp = Cursor{p.m_first, 0, -1};
   Cursor cc{p.m_first, 0, -1};
-  tma_gemm_loop<TL>(
+  tma_gemm_loop<TL, false>(  // trailing updates never fan out
       &mapA, &mapB, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, TmaBlock& blk) { return decode(cp, item, blk); },
       [&](int64_t item, TmaBlock& blk) { return decode(cc, item, blk); }, p.stagger_ns);
 }

@@ -602,14 +602,18 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
   // crit stream, the bulk update is a persistent grid capped at (SMs - reserve)
   // CTAs: its CTAs fill an SM's shared memory, so the cap is what leaves SMs
   // on which the latency-bound critical path can overlap the bulk GEMM.
-  // Per step: while the trailing matrix is at least 32 tiles wide the bulk
-  // update dwarfs the critical path and gets every SM; below that, 2 SMs stay
-  // free for it (measured, f64 T=1024: N=131072 reserve 0/1/2 -> 34.3/34.2/
-  // 33.9 TFLOP/s; N=32768 reserve 2/4/8 -> 28.9/27.7/28.2).
+  // Per step: while the trailing matrix is at least 32 tiles wide the DMMA
+  // bulk update dwarfs the critical path and gets every SM; below that, 2 SMs
+  // stay free for it (measured, f64 T=1024: N=131072 reserve 0/1/2 -> 34.3/
+  // 34.2/33.9 TFLOP/s; N=32768 reserve 2/4/8 -> 28.9/27.7/28.2).  The tcgen05
+  // bulk update (float32 / complex64) finishes a step so much sooner that the
+  // critical path needs its 2 SMs throughout (N=65536 T=1024 reserve 0/2/4:
+  // f32 165/177/177, c64 184/190/191 TFLOP/s; T=128 unchanged).
   int reserve_fixed = -1;
   if (const char* e = getenv("BCMG_RESERVE_SMS"); e && *e) reserve_fixed = std::max(0, atoi(e));
   auto reserve_at = [&](int64_t k) {
     if (reserve_fixed >= 0) return reserve_fixed;
+    if (presplit) return 2;
     return (n - g.stop(k)) / T >= 32 ? 0 : 2;
   };
   int nsm = 148;

@@ -288,7 +288,7 @@ __device__ __forceinline__ void tc3_loop(const CUtensorMap* mapA, const CUtensor
             if (col < blk.N) {
               const float o = blk.alpha * v[j] + blk.beta * old[j];
               crow[col * blk.ldc] = o;
-              for (int e = 0; e < blk.nfan; ++e) blk.fan[e][r + col * blk.ldc] = o;
+              for (int e = 0; e < blk.nfan; ++e) fan_at(blk.fan, e)[r + col * blk.ldc] = o;
             }
           }
         }

@@ -181,7 +181,7 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
             if (col < blk.N) {
               const float o = blk.alpha * v[j] + blk.beta * old[j];
               crow[col * blk.ldc] = o;
-              for (int e = 0; e < blk.nfan; ++e) blk.fan[e][r + col * blk.ldc] = o;
+              for (int e = 0; e < blk.nfan; ++e) fan_at(blk.fan, e)[r + col * blk.ldc] = o;
             }
           }
         }
@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
     blk.alpha = alpha;
     blk.beta = beta;
     blk.nfan = fan.n;
-    for (int e = 0; e < fan.n; ++e) blk.fan[e] = fan.p[e];
+#pragma unroll
+    for (int e = 0; e < MAX_FAN; ++e) blk.fan[e] = e < fan.n ? fan.p[e] : nullptr;
     return true;
   });
 }
