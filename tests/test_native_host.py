@@ -135,3 +135,20 @@ def test_workspace_ordering():
     i = bc.workspace_nbytes("potri", desc, bc.TileSpec(128), 4)
     assert len(s) == 4 and all(x > 1024 * 256 * 8 for x in s)
     assert all(b >= a for a, b in zip(s, i)) or True
+
+
+def test_hot_kernels_keep_their_state_in_registers():
+    """ptxas report of the in-tree build (-Xptxas -v): the tensor-core trailing
+    updates and GEMMs have no local-memory stack frame.  A runtime-indexed array
+    in their tile state (the epilogue fan-out once did this) moves it to local
+    memory and halved float32 throughput at small T without failing any test."""
+    log = os.path.join(ROOT, "paper_2601_14466_b200", "csrc", "build", "kernels.ptxas.log")
+    if not os.path.exists(log):
+        pytest.skip("no in-tree build log (run __graft_entry__.build())")
+    text = open(log).read()
+    frames = dict(re.findall(r"Compiling entry function '(\w+)'.*?(\d+) bytes stack frame", text, flags=re.S))
+    hot = {k: int(v) for k, v in frames.items() if "tck_trail_kernel" in k or "tck_gemm_kernel" in k}
+    assert len(hot) >= 4, sorted(frames)[:5]
+    assert all(v == 0 for v in hot.values()), hot
+    dmma = {k: int(v) for k, v in frames.items() if "trail_tma_kernel" in k}
+    assert dmma and all(v <= 64 for v in dmma.values()), dmma
