@@ -15,6 +15,9 @@
  *                               (solve_positive_definite pipeline)
  *   bcmg_potri                  api.ts:157-165 -> solvers.py:988-1016
  *                               (invert_positive_definite pipeline)
+ *   bcmg_syevd                  api.ts (bcmg_syevd) ->
+ *                               solvers.py:1019-1043 (eigh_hermitian pipeline)
+ *   bcmg_syevd_cyclic           solvers.py:862-910 (syevd on the cyclic layout)
  *   bcmg_redistribute           solvers.py:262-273 (redistribute_in/out)
  *                               -> layout.py:191-256 (execute_plan)
  *   bcmg_potrf                  solvers.py:341-406 (potrf, LAPACK info)
@@ -147,6 +150,16 @@ int bcmg_potrs_streamed(bcmg_session* s, void* stream, int dtype, int64_t n, int
 int bcmg_potri(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev, void* const* shards,
                int flags, int* info);
 
+/* Hermitian eigendecomposition: eigenvalues ascending into w (device, n
+   elements of the real type: float for dtype 0/2, double for 1/3); A's shards
+   (contiguous layout) are overwritten by the eigenvectors, column j belonging
+   to w[j], each scaled so that its first largest-magnitude component is real
+   and positive (solvers.py:898-909).  Single-process sessions only.  *info =
+   BCMG_ERR_NO_CONVERGENCE (and the same return code) when the tridiagonal QL
+   exceeds 30 iterations for one eigenvalue (solvers.py:806-811). */
+int bcmg_syevd(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev, void* const* shards,
+               void* w, int flags, int* info);
+
 /* ---- building blocks (the reference's solvers.py routines) ---- */
 int bcmg_redistribute(bcmg_session* s, void* stream, int dtype, int64_t n_rows, int64_t n_cols, int64_t tile,
                       int ndev, void* const* shards, int direction);
@@ -156,6 +169,10 @@ int bcmg_potrs_factored(bcmg_session* s, void* stream, int dtype, int64_t n, int
                         void* const* shards, void* b, int64_t ldb);
 int bcmg_potri_factored(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev,
                         void* const* shards);
+/* syevd on the block-cyclic layout: shards in, eigenvectors out (column j of
+   the cyclic layout = eigenvector j), eigenvalues into w as bcmg_syevd */
+int bcmg_syevd_cyclic(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev,
+                      void* const* shards, void* w);
 
 /* The DMMA GEMM every contraction of the path runs on:
    C := alpha * op(A) * op(B) + beta * C, column-major, op 0 = N, 1 = C (conj-

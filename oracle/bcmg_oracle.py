@@ -360,3 +360,168 @@ def potrs_flops(n: int, nrhs: int, complex_: bool = False) -> float:
     """Algorithmic flops N^3/3 + 2 N^2 N_RHS (x4 complex) -- SURVEY 8(d)."""
     f = n ** 3 / 3.0 + 2.0 * n * n * nrhs
     return 4.0 * f if complex_ else f
+
+
+# --------------------------------------------------------------------------
+# Hermitian eigendecomposition (reference solvers.py:597-910), dense form.
+# The reference walks the tiles device by device; the arithmetic per column is
+# the same for every device count up to the summation order of y = A v, so
+# the oracle runs it on one dense matrix.
+# --------------------------------------------------------------------------
+
+
+class ConvergenceError(ArithmeticError):
+    """core.py:57-58"""
+
+
+def householder(x: np.ndarray):
+    """(v, tau, beta) with v[0] = 1, H^H x = beta e1, beta real (solvers.py:600-623)."""
+    v = np.zeros_like(x)
+    v[0] = 1
+    alpha = complex(x[0])
+    tail = float(np.linalg.norm(x[1:])) if len(x) > 1 else 0.0
+    if tail == 0.0 and alpha.imag == 0.0:
+        return v, 0.0, alpha.real
+    beta = -math.copysign(math.hypot(abs(alpha), tail), alpha.real or 1.0)
+    if np.iscomplexobj(x):
+        v[1:] = x[1:] / (alpha - beta)
+        tau = (beta - alpha) / beta
+    else:
+        v[1:] = x[1:] / (alpha.real - beta)
+        tau = (beta - alpha.real) / beta
+    return v, tau, beta
+
+
+def tridiagonalize(a: np.ndarray, tile: int):
+    """Blocked Householder reduction to real tridiagonal form (solvers.py:666-780):
+    lazy per-column panel update from the tile's U / W, y = sym(A_stale) v with
+    the U / W correction, W = tau y - sigma v, one rank-2T trailing update per
+    tile.  Returns (d, e, reflectors [(c, v, tau)])."""
+    a = np.array(a, dtype=a.dtype, order="F", copy=True)
+    n = a.shape[0]
+    dt = a.dtype
+    d = np.zeros(n, dtype=np.float64)
+    e = np.zeros(max(n - 1, 0), dtype=np.float64)
+    refl = []
+    for _, start, stop in _tile_ranges(n, tile):
+        tc = stop - start
+        u = np.zeros((n, tc), dtype=dt)
+        w = np.zeros((n, tc), dtype=dt)
+        for jj in range(tc):
+            c = start + jj
+            if jj:
+                a[c:, c] -= u[c:, :jj] @ w[c, :jj].conj() + w[c:, :jj] @ u[c, :jj].conj()
+            d[c] = a[c, c].real
+            if c == n - 1:
+                continue
+            v, tau, beta = householder(np.array(a[c + 1:, c]))
+            e[c] = beta
+            refl.append((c, v, tau))
+            if tau == 0:
+                continue
+            blk = a[c + 1:, c + 1:]
+            low = np.tril(blk)
+            y = low @ v + np.tril(blk, -1).conj().T @ v
+            if jj:
+                y -= u[c + 1:, :jj] @ (w[c + 1:, :jj].conj().T @ v) + w[c + 1:, :jj] @ (u[c + 1:, :jj].conj().T @ v)
+            sigma = 0.5 * (abs(tau) ** 2) * np.vdot(v, y)
+            u[c + 1:, jj] = v
+            w[c + 1:, jj] = tau * y - sigma * v
+        if stop < n:
+            a[:, stop:] -= u @ w[stop:, :].conj().T + w @ u[stop:, :].conj().T
+    return d, e, refl
+
+
+def tridiag_eig(d_in, e_in, max_iter: int = 30):
+    """Implicit-shift QL with Wilkinson shift, rotations accumulated into z
+    (solvers.py:783-843)."""
+    n = len(d_in)
+    d = np.asarray(d_in, dtype=np.float64).copy()
+    e = np.zeros(n, dtype=np.float64)
+    e[: n - 1] = e_in[: n - 1] if n > 1 else 0.0
+    z = np.eye(n)
+    eps = np.finfo(np.float64).eps
+    for l in range(n):
+        iters = 0
+        while True:
+            for m in range(l, n - 1):
+                if abs(e[m]) <= eps * (abs(d[m]) + abs(d[m + 1])):
+                    break
+            else:
+                m = n - 1
+            if m == l:
+                break
+            iters += 1
+            if iters > max_iter:
+                raise ConvergenceError(f"tridiagonal eigensolver exceeded {max_iter} iterations at index {l}")
+            g = (d[l + 1] - d[l]) / (2.0 * e[l])
+            r = math.hypot(g, 1.0)
+            g = d[m] - d[l] + e[l] / (g + math.copysign(r, g))
+            s = c = 1.0
+            p = 0.0
+            for i in range(m - 1, l - 1, -1):
+                f = s * e[i]
+                b = c * e[i]
+                r = math.hypot(f, g)
+                e[i + 1] = r
+                if r == 0.0:
+                    d[i + 1] -= p
+                    e[m] = 0.0
+                    break
+                s = f / r
+                c = g / r
+                g = d[i + 1] - p
+                r = (d[i] - g) * s + 2.0 * c * b
+                p = s * r
+                d[i + 1] = g + p
+                g = c * r - b
+                zi = z[:, i].copy()
+                zi1 = z[:, i + 1].copy()
+                z[:, i + 1] = s * zi + c * zi1
+                z[:, i] = c * zi - s * zi1
+            else:
+                d[l] -= p
+                e[l] = g
+                e[m] = 0.0
+    return d, z
+
+
+def phase_normalize(v: np.ndarray) -> np.ndarray:
+    """First largest-magnitude component of each column real and positive
+    (solvers.py:898-909)."""
+    v = np.array(v, copy=True)
+    idx = np.argmax(np.abs(v), axis=0)
+    lead = v[idx, np.arange(v.shape[1])]
+    scale = np.abs(lead)
+    safe = np.where(scale == 0, 1, scale)
+    phase = np.where(scale == 0, 1, lead / safe)
+    v *= np.conj(phase)[None, :]
+    return v
+
+
+def syevd_dense(a: np.ndarray, tile: int):
+    """Eigenvalues ascending (real type of a) and phase-normalised eigenvectors
+    (solvers.py:862-910 on one dense matrix)."""
+    n = a.shape[0]
+    dt = a.dtype
+    d, e, refl = tridiagonalize(a, tile)
+    w, z = tridiag_eig(d, e)
+    order = np.argsort(w, kind="stable")
+    w = w[order]
+    z = np.asfortranarray(z[:, order].astype(dt))
+    for c, v, tau in reversed(refl):
+        if tau == 0:
+            continue
+        blk = z[c + 1:, :]
+        blk -= tau * np.outer(v, v.conj() @ blk)
+    real = np.float32 if dt in (np.float32, np.complex64) else np.float64
+    return w.astype(real), phase_normalize(z)
+
+
+def phase_align(v: np.ndarray, ref: np.ndarray) -> np.ndarray:
+    """Scale each column of v by the unit phase that best matches ref
+    (eigenvectors are unique only up to phase)."""
+    dots = np.sum(v.conj() * ref, axis=0)
+    mag = np.abs(dots)
+    ph = np.where(mag == 0, 1, dots / np.where(mag == 0, 1, mag))
+    return v * ph[None, :]

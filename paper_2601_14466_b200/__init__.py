@@ -14,6 +14,7 @@ All compute runs in ``lib/libbcmg_b200.so`` (hand-written CUDA for sm_100a).
 
 from .core import (
     ConcurrentCallError,
+    ConvergenceError,
     DescriptorError,
     ElementType,
     MatrixDescriptor,
@@ -46,12 +47,14 @@ from .solvers import (
     FactorizationResult,
     Timings,
     create_distributed,
+    eigh_hermitian,
     gather_array,
     invert_positive_definite,
     potrf,
     redistribute_in,
     redistribute_out,
     solve_positive_definite,
+    syevd,
     workspace_nbytes,
     write_array,
 )
@@ -60,7 +63,7 @@ from .solvers import potrs as potrs_factored
 from .api import P, last_timings, make_mesh, potri, potrs
 
 __all__ = [
-    "ConcurrentCallError", "DescriptorError", "ElementType", "MatrixDescriptor", "NotPositiveDefiniteError",
+    "ConcurrentCallError", "ConvergenceError", "DescriptorError", "ElementType", "MatrixDescriptor", "NotPositiveDefiniteError",
     "OutOfDeviceMemoryError", "RhsDescriptor", "StaleSessionError", "Structure", "TileSpec",
     "validate_descriptor", "validate_tile",
     "STAGING_BUFFER_COUNT", "ColumnPermutation", "ColumnPlacement", "RedistributionPlan", "build_permutation",
@@ -68,6 +71,6 @@ __all__ = [
     "segment_plan_info", "serialize_plan",
     "DeviceMesh", "DistributedMatrix", "FactorizationResult", "Timings", "create_distributed", "gather_array",
     "invert_positive_definite", "potrf", "potrs_factored", "potri_factored", "redistribute_in", "redistribute_out",
-    "solve_positive_definite", "workspace_nbytes", "write_array",
+    "solve_positive_definite", "syevd", "eigh_hermitian", "workspace_nbytes", "write_array",
     "P", "make_mesh", "potrs", "potri", "last_timings",
 ]

@@ -51,6 +51,8 @@ SIGNATURES = {
     "bcmg_close": (C.c_int, [_vp]),
     "bcmg_potrs": (C.c_int, [_vp, _vp, C.c_int, _i64, _i64, _i64, C.c_int, _vpp, _vp, _i64, C.c_int, _ip]),
     "bcmg_potri": (C.c_int, [_vp, _vp, C.c_int, _i64, _i64, C.c_int, _vpp, C.c_int, _ip]),
+    "bcmg_syevd": (C.c_int, [_vp, _vp, C.c_int, _i64, _i64, C.c_int, _vpp, _vp, C.c_int, _ip]),
+    "bcmg_syevd_cyclic": (C.c_int, [_vp, _vp, C.c_int, _i64, _i64, C.c_int, _vpp, _vp]),
     "bcmg_potrs_streamed": (C.c_int, [_vp, _vp, C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _i64, C.c_int, _ip]),
     "bcmg_redistribute": (C.c_int, [_vp, _vp, C.c_int, _i64, _i64, _i64, C.c_int, _vpp, C.c_int]),
     "bcmg_potrf": (C.c_int, [_vp, _vp, C.c_int, _i64, _i64, C.c_int, _vpp, _ip]),

@@ -351,6 +351,49 @@ int bcmg_potri(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile
   });
 }
 
+static void check_syevd(int dtype, int64_t n, int64_t tile, int ndev, void* const* shards, void* w, int* info) {
+  check_common(dtype, ndev, shards);
+  if (n < 1) throw bcmg::Error(BCMG_ERR_CONFIG, "matrix order must be positive");
+  if (tile < 1 || tile > n) throw bcmg::Error(BCMG_ERR_CONFIG, "tile width out of range");
+  if (!w || !info) throw bcmg::Error(BCMG_ERR_CONFIG, "null eigenvalue / info pointer");
+}
+
+int bcmg_syevd(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev, void* const* shards,
+               void* w, int flags, int* info) {
+  (void)flags;
+  return guarded([&] {
+    auto* S = live(s);
+    check_syevd(dtype, n, tile, ndev, shards, w, info);
+    *info = 0;
+    Entry e(S, stream);
+    S->mark(bcmg::T_BEGIN);
+    // the dense working copy is gathered straight from the contiguous layout
+    // and the eigenvectors scattered straight back: redistribute_in / _out
+    // (solvers.py:1035-1037) are pure data movement and fold into the gather
+    S->mark(bcmg::T_REDIST);
+    try {
+      S->syevd(dtype, n, tile, ndev, shards, false, w);
+    } catch (const bcmg::Error& err) {
+      if (err.code == BCMG_ERR_NO_CONVERGENCE) *info = BCMG_ERR_NO_CONVERGENCE;
+      throw;
+    }
+    S->mark(bcmg::T_POTRF);
+    S->mark(bcmg::T_SOLVE);
+    finish_timings(S, true);
+  });
+}
+
+int bcmg_syevd_cyclic(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev,
+                      void* const* shards, void* w) {
+  return guarded([&] {
+    auto* S = live(s);
+    int info = 0;
+    check_syevd(dtype, n, tile, ndev, shards, w, &info);
+    Entry e(S, stream);
+    S->syevd(dtype, n, tile, ndev, shards, true, w);
+  });
+}
+
 int bcmg_gemm(void* stream, int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void* a, int64_t lda,
               int op_a, const void* b, int64_t ldb, int op_b, double beta, void* c, int64_t ldc) {
   return guarded([&] {

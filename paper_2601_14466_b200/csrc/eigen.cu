@@ -1,0 +1,714 @@
+// Hermitian eigendecomposition (syevd) on the GPU -- reference
+// pkg/src/bcmg/solvers.py:597-910 (_householder, _tridiagonalize,
+// _tridiag_eig, syevd).
+//
+// Same algorithm as the reference, re-planned for one B200:
+//   1. the shards (block-cyclic or contiguous column layout, any number of
+//      logical devices on this GPU) are gathered into ONE dense n x n working
+//      copy in the compute type (double / double2): the per-column symmetric
+//      matrix-vector product then streams the trailing lower triangle at HBM
+//      rate instead of walking tiles device by device;
+//   2. blocked Householder tridiagonalisation exactly as solvers.py:666-780:
+//      per column a lazy panel-column update from the tile's U / W panels, the
+//      reflector (v, tau, beta) with real beta (solvers.py:600-623), y = A v
+//      over the stale trailing lower triangle (tiled, deterministic two-pass
+//      reduction), the U / W correction and W = tau y - sigma v; per tile one
+//      rank-2T update of the trailing lower triangle on the DMMA GEMM;
+//   3. implicit-shift QL on the real tridiagonal (solvers.py:783-843) on the
+//      host, O(n^2) without vectors; its plane rotations are recorded and
+//      replayed on the GPU over the rows of Z (one thread per row);
+//   4. back-transformation with the stored reflectors in reverse
+//      (solvers.py:884-897), blocked 64 reflectors at a time in compact WY form
+//      (Q_blk = I - V T V^H, T from the forward recurrence): three GEMMs per
+//      block instead of 64 rank-1 sweeps over Z;
+//   5. phase normalisation (largest-magnitude component real and positive,
+//      first index on ties, solvers.py:898-909) fused with the scatter back
+//      into the caller's shards and the narrowing to the storage type.
+// Every reduction has a fixed order: two runs give identical bits
+// (reference test_solvers.py:260-271).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "ops.h"
+#include "solver.h"
+
+namespace bcmg {
+namespace {
+
+constexpr int ET = 64;      // symv tile / WY block width
+constexpr int RT = 256;     // threads of the row-parallel kernels
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscl(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  const double d = b.x * b.x + b.y * b.y;
+  return make_double2((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+__device__ __forceinline__ double2 zero2() { return make_double2(0.0, 0.0); }
+
+// Column g of the distributed matrix -> (shard, local column).
+struct ShardMap {
+  void* p[16];
+  int64_t off[17];  // contiguous layout: first global column of each device
+  int64_t T;
+  int D, cyclic;
+};
+__device__ __forceinline__ void map_col(const ShardMap& m, int64_t g, int& d, int64_t& lc) {
+  if (m.cyclic) {
+    const int64_t t = g / m.T;
+    d = (int)(t % m.D);
+    lc = (t / m.D) * m.T + g % m.T;
+  } else {
+    d = 0;
+    while (d + 1 < m.D && g >= m.off[d + 1]) ++d;
+    lc = g - m.off[d];
+  }
+}
+
+// deterministic block sum of a double2 (fixed shuffle tree + fixed warp order)
+__device__ __forceinline__ double2 block_sum(double2 v, double2* red) {
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_down_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_down_sync(0xffffffffu, v.y, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double2 s = zero2();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < nw; ++i) s = cadd(s, red[i]);
+  return s;  // valid in thread 0
+}
+
+// ---------------------------------------------------------------- gather / scatter
+template <class S, class X>
+__global__ void eig_gather(ShardMap m, X* A, int64_t n) {
+  const int64_t g = blockIdx.y + (int64_t)blockIdx.z * gridDim.y;
+  if (g >= n) return;
+  int d;
+  int64_t lc;
+  map_col(m, g, d, lc);
+  const S* src = reinterpret_cast<const S*>(m.p[d]) + lc * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    A[i + g * n] = from_c<X>(to_c(src[i]));
+}
+
+// Z column j -> shard column j, scaled so that its first largest-magnitude
+// component is real and positive (solvers.py:898-909).
+template <class X, class S>
+__global__ void eig_phase_scatter(const X* Z, int64_t n, ShardMap m) {
+  __shared__ double bv[32];
+  __shared__ int64_t bi[32];
+  __shared__ double2 ph;
+  const int64_t j = blockIdx.x;
+  const X* z = Z + j * n;
+  double best = -1.0;
+  int64_t idx = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double2 v = to_c(z[i]);
+    const double a = hypot(v.x, v.y);
+    if (a > best) best = a, idx = i;  // strided ascending: first max of this thread
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_down_sync(0xffffffffu, best, o);
+    const int64_t oi = __shfl_down_sync(0xffffffffu, idx, o);
+    if (ob > best || (ob == best && oi < idx)) best = ob, idx = oi;
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) bv[w] = best, bi[w] = idx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      if (bv[k] > best || (bv[k] == best && bi[k] < idx)) best = bv[k], idx = bi[k];
+    const double2 lead = to_c(z[idx]);
+    const double s = hypot(lead.x, lead.y);
+    ph = s == 0.0 ? make_double2(1.0, 0.0) : make_double2(lead.x / s, lead.y / s);
+  }
+  __syncthreads();
+  const double2 p = ph;
+  int d;
+  int64_t lc;
+  map_col(m, j, d, lc);
+  S* dst = reinterpret_cast<S*>(m.p[d]) + lc * n;
+  __shared__ int64_t anchor;
+  if (threadIdx.x == 0) anchor = idx;
+  __syncthreads();
+  const int64_t ia = anchor;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    double2 o = cmulc(to_c(z[i]), p);
+    if (i == ia) o = make_double2(hypot(o.x, o.y), 0.0);  // the anchor exactly real and positive
+    dst[i] = from_c<S>(o);
+  }
+}
+
+// ---------------------------------------------------------------- tridiagonalisation
+// A[c:, c] -= U[c:, :jj] conj(W[c, :jj]) + W[c:, :jj] conj(U[c, :jj])  (solvers.py:705-709)
+template <class X>
+__global__ void eig_panel_update(X* A, int64_t n, int64_t c, const X* U, const X* W, int jj) {
+  const int64_t i = c + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2 s1 = zero2(), s2 = zero2();
+  for (int k = 0; k < jj; ++k) {
+    s1 = cadd(s1, cmulc(to_c(U[i + k * n]), to_c(W[c + k * n])));
+    s2 = cadd(s2, cmulc(to_c(W[i + k * n]), to_c(U[c + k * n])));
+  }
+  A[i + c * n] = from_c<X>(csub(to_c(A[i + c * n]), cadd(s1, s2)));
+}
+
+// d[c] = Re A[c, c]; reflector of x = A[c+1:, c] (solvers.py:600-623):
+// v (v[0] = 1) into vbuf[c+1:] and into A[c+1:, c] (kept for the
+// back-transformation), tau[c], e[c] = beta.
+template <class X>
+__global__ void __launch_bounds__(1024) eig_house(X* A, int64_t n, int64_t c, X* vbuf, X* tau, double* dd, double* ee) {
+  __shared__ double2 red[32];
+  __shared__ double2 den;
+  __shared__ int trivial;
+  if (threadIdx.x == 0) dd[c] = to_c(A[c + c * n]).x;
+  const int64_t L = n - c - 1;
+  if (L <= 0) return;
+  X* x = A + (c + 1) + c * n;
+  double s = 0.0;
+  for (int64_t i = 1 + threadIdx.x; i < L; i += blockDim.x) {
+    const double2 v = to_c(x[i]);
+    s += v.x * v.x + v.y * v.y;
+  }
+  const double tot = block_sum(make_double2(s, 0.0), red).x;
+  if (threadIdx.x == 0) {
+    const double tail = sqrt(tot);
+    const double2 alpha = to_c(x[0]);
+    double2 t;
+    double beta;
+    if (tail == 0.0 && alpha.y == 0.0) {
+      t = zero2();
+      beta = alpha.x;
+      trivial = 1;
+    } else {
+      const double h = hypot(hypot(alpha.x, alpha.y), tail);
+      beta = -copysign(h, alpha.x != 0.0 ? alpha.x : 1.0);  // `alpha.real or 1.0`
+      den = make_double2(alpha.x - beta, alpha.y);
+      t = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
+      trivial = 0;
+    }
+    ee[c] = beta;
+    tau[c] = from_c<X>(t);
+  }
+  __syncthreads();
+  const int triv = trivial;
+  const double2 dn = den;
+  for (int64_t i = threadIdx.x; i < L; i += blockDim.x) {
+    double2 v;
+    if (i == 0) v = make_double2(1.0, 0.0);
+    else if (triv) v = zero2();
+    else v = cdiv(to_c(x[i]), dn);
+    const X vx = from_c<X>(v);
+    vbuf[c + 1 + i] = vx;
+    x[i] = vx;
+  }
+}
+
+// y = sym(A[c0:, c0:]) v, lower-triangle storage (solvers.py:729-745): one CTA
+// per 64x64 tile (bi >= bj) of the trailing lower triangle; the tile's row
+// products go to P1[bj][rows], its conjugate-transposed column products
+// (strictly below the diagonal) to P2[bi][cols]; eig_symv_reduce sums them in
+// a fixed order.
+template <class X>
+__global__ void __launch_bounds__(128) eig_symv(const X* A, int64_t n, int64_t c0, const X* v, X* P1, X* P2) {
+  extern __shared__ double2 sm[];  // 64 x 65
+  __shared__ double2 vr[ET], vc[ET];
+  const int64_t b = blockIdx.x;
+  int64_t bi = (int64_t)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+  while (bi * (bi + 1) / 2 > b) --bi;
+  while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
+  const int64_t bj = b - bi * (bi + 1) / 2;
+  const int64_t r0 = c0 + bi * ET, q0 = c0 + bj * ET;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < ET * ET; e += blockDim.x) {
+    const int il = e % ET, jl = e / ET;
+    const int64_t i = r0 + il, j = q0 + jl;
+    sm[jl * (ET + 1) + il] = (i < n && j < n) ? to_c(A[i + j * n]) : zero2();
+  }
+  if (tid < ET) vc[tid] = q0 + tid < n ? to_c(v[q0 + tid]) : zero2();
+  else vr[tid - ET] = r0 + tid - ET < n ? to_c(v[r0 + tid - ET]) : zero2();
+  __syncthreads();
+  const bool diag = bi == bj;
+  if (tid < ET) {
+    const int il = tid;
+    double2 acc = zero2();
+    for (int jl = 0; jl < ET; ++jl)
+      if (!diag || jl <= il) acc = cadd(acc, cmul(sm[jl * (ET + 1) + il], vc[jl]));
+    if (r0 + il < n) P1[bj * n + r0 + il] = from_c<X>(acc);
+  } else {
+    const int jl = tid - ET;
+    double2 acc = zero2();
+    for (int il = 0; il < ET; ++il)
+      if (!diag || il > jl) acc = cadd(acc, cmul(cconj(sm[jl * (ET + 1) + il]), vr[il]));
+    if (q0 + jl < n) P2[bi * n + q0 + jl] = from_c<X>(acc);
+  }
+}
+
+template <class X>
+__global__ void eig_symv_reduce(const X* P1, const X* P2, int64_t n, int64_t c0, int64_t nb, X* y) {
+  const int64_t i = c0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t I = (i - c0) / ET;
+  double2 acc = zero2();
+  for (int64_t t = 0; t <= I; ++t) acc = cadd(acc, to_c(P1[t * n + i]));
+  for (int64_t t = I; t < nb; ++t) acc = cadd(acc, to_c(P2[t * n + i]));
+  y[i] = from_c<X>(acc);
+}
+
+// t[k] = (W^H v)[k], t[jj + k] = (U^H v)[k] over rows c0..n-1
+template <class X>
+__global__ void __launch_bounds__(RT) eig_dots(const X* U, const X* W, int64_t n, int64_t c0, int jj, const X* v, X* t) {
+  __shared__ double2 red[32];
+  const int b = blockIdx.x;
+  const X* M = b < jj ? W + (int64_t)b * n : U + (int64_t)(b - jj) * n;
+  double2 acc = zero2();
+  for (int64_t i = c0 + threadIdx.x; i < n; i += blockDim.x) acc = cadd(acc, cmul(cconj(to_c(M[i])), to_c(v[i])));
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) t[b] = from_c<X>(acc);
+}
+
+// y[c0:] -= U t[:jj] + W t[jj:]  (solvers.py:746-750) and per-block partials of v^H y
+template <class X>
+__global__ void __launch_bounds__(RT) eig_corr(const X* U, const X* W, int64_t n, int64_t c0, int jj, const X* t, X* y,
+                                               const X* v, double2* part) {
+  __shared__ double2 red[32];
+  const int64_t i = c0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double2 contrib = zero2();
+  if (i < n) {
+    double2 yi = to_c(y[i]);
+    if (jj) {
+      double2 s1 = zero2(), s2 = zero2();
+      for (int k = 0; k < jj; ++k) {
+        s1 = cadd(s1, cmul(to_c(U[i + (int64_t)k * n]), to_c(t[k])));
+        s2 = cadd(s2, cmul(to_c(W[i + (int64_t)k * n]), to_c(t[jj + k])));
+      }
+      yi = csub(yi, cadd(s1, s2));
+      y[i] = from_c<X>(yi);
+    }
+    contrib = cmul(cconj(to_c(v[i])), yi);
+  }
+  contrib = block_sum(contrib, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = contrib;
+}
+
+// sigma = |tau|^2 / 2 * v^H y; U[:, jj] = v, W[:, jj] = tau y - sigma v (solvers.py:751-754)
+template <class X>
+__global__ void __launch_bounds__(RT) eig_fin(const X* v, const X* y, X* U, X* W, int64_t n, int64_t c0, int jj,
+                                              const X* tau, int64_t c, const double2* part, int nparts) {
+  __shared__ double2 sig;
+  const double2 tu = to_c(tau[c]);
+  if (tu.x == 0.0 && tu.y == 0.0) return;  // reflection skipped (solvers.py:718)
+  if (threadIdx.x == 0) {
+    double2 vd = zero2();
+    for (int p = 0; p < nparts; ++p) vd = cadd(vd, part[p]);
+    sig = cscl(vd, 0.5 * (tu.x * tu.x + tu.y * tu.y));
+  }
+  __syncthreads();
+  const int64_t i = c0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 vi = to_c(v[i]);
+  U[i + (int64_t)jj * n] = v[i];
+  W[i + (int64_t)jj * n] = from_c<X>(csub(cmul(tu, to_c(y[i])), cmul(sig, vi)));
+}
+
+// ---------------------------------------------------------------- tridiagonal eigenvectors
+// Replay the QL plane rotations on the rows of Z (solvers.py:831-835).  Sweep
+// k applies rotations top_k, top_k - 1, ..., bot_k to column pairs (i, i+1),
+// sweeps in order.  K consecutive sweeps run as one wavefront: at step p (p
+// descending) sweep s applies its rotation at i = p + 2s.  Every rotation of
+// an earlier sweep that touches columns i or i+1 sits at a position >= i - 1,
+// i.e. at a step >= p + 1, so the order of operations on every column is the
+// sequential one (same bits).  One thread per row keeps the 2K active columns
+// in registers: one load and one store per column per K sweeps instead of per
+// sweep.
+template <int K>
+__global__ void __launch_bounds__(32) eig_rotate_wave(double* Z, int64_t n, const double2* cs, const int64_t* sw_off,
+                                                      const int64_t* sw_top, int64_t s0, int64_t nsw) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int kk = (int)min((int64_t)K, nsw - s0);
+  int64_t top[K], bot[K], off[K];
+  int64_t pmax = INT64_MIN, pmin = INT64_MAX;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    if (s < kk) {
+      off[s] = sw_off[s0 + s];
+      top[s] = sw_top[s0 + s];
+      bot[s] = top[s] - (sw_off[s0 + s + 1] - off[s]) + 1;
+      pmax = max(pmax, top[s] - 2 * s);
+      pmin = min(pmin, bot[s] - 2 * s);
+    } else {
+      off[s] = 0, top[s] = -1, bot[s] = 0;  // empty
+    }
+  }
+  double* z = Z + r;
+  double win[2 * K];  // win[j] = column p + j
+#pragma unroll
+  for (int j = 0; j < 2 * K; ++j) {
+    const int64_t c = pmax + j;
+    win[j] = (c >= 0 && c < n) ? z[c * n] : 0.0;
+  }
+  for (int64_t p = pmax; p >= pmin; --p) {
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      const int64_t i = p + 2 * s;
+      if (i >= bot[s] && i <= top[s]) {
+        const double2 g = cs[off[s] + (top[s] - i)];  // (c, s)
+        const double a = win[2 * s], b = win[2 * s + 1];
+        win[2 * s + 1] = g.y * a + g.x * b;
+        win[2 * s] = g.x * a - g.y * b;
+      }
+    }
+    const int64_t cs_ = p + 2 * K - 1;
+    if (cs_ >= 0 && cs_ < n) z[cs_ * n] = win[2 * K - 1];
+#pragma unroll
+    for (int j = 2 * K - 1; j > 0; --j) win[j] = win[j - 1];
+    const int64_t cl = p - 1;
+    win[0] = (cl >= 0 && cl < n) ? z[cl * n] : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < 2 * K; ++j) {
+    const int64_t c = pmin - 1 + j;
+    if (c >= 0 && c < n) z[c * n] = win[j];
+  }
+}
+
+__global__ void eig_identity(double* Z, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) Z[i + i * n] = 1.0;
+}
+
+// Zx[:, j] = Z[:, order[j]] in the compute type
+template <class X>
+__global__ void eig_permute(const double* Z, const int64_t* order, X* Zx, int64_t n) {
+  const int64_t j = blockIdx.y + (int64_t)blockIdx.z * gridDim.y;
+  if (j >= n) return;
+  const double* src = Z + order[j] * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    Zx[i + j * n] = from_c<X>(make_double2(src[i], 0.0));
+}
+
+// Forward compact-WY factor of kb reflectors: T upper, T[j][j] = tau_j,
+// T[:j, j] = -tau_j T[:j, :j] G[:j, j], G = V^H V (LAPACK larft, forward / columnwise).
+template <class X>
+__global__ void __launch_bounds__(ET) eig_larft(const X* G, const X* tau, int kb, X* Tm) {
+  const int i = threadIdx.x;  // row of T, in global memory (kb x kb, ld kb)
+  if (i < kb)
+    for (int j = 0; j < kb; ++j) Tm[i + j * kb] = from_c<X>(zero2());
+  __syncthreads();
+  for (int j = 0; j < kb; ++j) {
+    const double2 tj = to_c(tau[j]);
+    if (i < j) {
+      double2 acc = zero2();
+      for (int l = i; l < j; ++l) acc = cadd(acc, cmul(to_c(Tm[i + l * kb]), to_c(G[l + j * kb])));
+      Tm[i + j * kb] = from_c<X>(cscl(cmul(tj, acc), -1.0));
+    } else if (i == j) {
+      Tm[j + j * kb] = from_c<X>(tj);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- host QL
+// Implicit-shift QL on the tridiagonal (d, e) exactly as solvers.py:783-843,
+// without the vectors: the rotations of each bulge-chasing sweep are recorded.
+struct QLRecord {
+  std::vector<double2> cs;
+  std::vector<int64_t> off{0}, top;
+};
+void tridiag_ql(std::vector<double>& d, const std::vector<double>& e_in, QLRecord& rec, int max_iter = 30) {
+  const int64_t n = (int64_t)d.size();
+  std::vector<double> e(n, 0.0);
+  for (int64_t i = 0; i + 1 < n; ++i) e[i] = e_in[i];
+  const double eps = 2.220446049250313e-16;
+  for (int64_t l = 0; l < n; ++l) {
+    int iters = 0;
+    while (true) {
+      int64_t m = n - 1;
+      for (int64_t mm = l; mm < n - 1; ++mm) {
+        const double dd = std::fabs(d[mm]) + std::fabs(d[mm + 1]);
+        if (std::fabs(e[mm]) <= eps * dd) {
+          m = mm;
+          break;
+        }
+      }
+      if (m == l) break;
+      if (++iters > max_iter)
+        throw Error(NO_CONVERGENCE, "tridiagonal eigensolver exceeded " + std::to_string(max_iter) +
+                                        " iterations at index " + std::to_string(l));
+      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+      double r = std::hypot(g, 1.0);
+      g = d[m] - d[l] + e[l] / (g + std::copysign(r, g));
+      double s = 1.0, c = 1.0, p = 0.0;
+      bool broke = false;
+      rec.top.push_back(m - 1);
+      for (int64_t i = m - 1; i >= l; --i) {
+        const double f = s * e[i], b = c * e[i];
+        r = std::hypot(f, g);
+        e[i + 1] = r;
+        if (r == 0.0) {
+          d[i + 1] -= p;
+          e[m] = 0.0;
+          broke = true;
+          break;
+        }
+        s = f / r;
+        c = g / r;
+        g = d[i + 1] - p;
+        r = (d[i] - g) * s + 2.0 * c * b;
+        p = s * r;
+        d[i + 1] = g + p;
+        g = c * r - b;
+        rec.cs.push_back(make_double2(c, s));
+      }
+      if ((int64_t)rec.cs.size() == rec.off.back()) rec.top.pop_back();  // no rotation applied
+      else rec.off.push_back((int64_t)rec.cs.size());
+      if (!broke) {
+        d[l] -= p;
+        e[l] = g;
+        e[m] = 0.0;
+      }
+    }
+  }
+}
+
+inline unsigned blocks_for(int64_t rows, int threads) { return (unsigned)std::max<int64_t>(1, (rows + threads - 1) / threads); }
+inline dim3 col_grid(int64_t n, int64_t rows) {
+  const int64_t y = std::min<int64_t>(n, 65535), z = (n + y - 1) / y;
+  return dim3((unsigned)std::min<int64_t>(std::max<int64_t>(1, (rows + 255) / 256), 8), (unsigned)y, (unsigned)z);
+}
+
+template <class S>
+void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, bool cyclic, void* w_out) {
+  constexpr bool CP = Traits<S>::cplx;
+  using X = typename std::conditional<CP, double2, double>::type;
+  const int dtw = CP ? C128 : R64;
+  cudaStream_t st = ss.user;
+  const size_t es = sizeof(X);
+  const int64_t nb = (n + ET - 1) / ET;
+  const int64_t nparts_max = (n + RT - 1) / RT;
+
+  // ---- workspace: everything reserved before any data moves (OUT_OF_MEMORY first)
+  DevBuf* wb = ss.eig;
+  wb[0].ensure((size_t)n * n * es);               // working copy A / stored reflectors V
+  wb[1].ensure((size_t)n * n * sizeof(double));   // Z of the tridiagonal
+  wb[2].ensure((size_t)n * n * es);               // eigenvectors in the compute type
+  wb[3].ensure((size_t)2 * n * T * es);           // U | W panels
+  wb[4].ensure((size_t)2 * nb * n * es);          // symv partials P1 | P2
+  const size_t small = (size_t)(2 * n + 2 * T + n) * es + (size_t)(nparts_max + 1) * sizeof(double2) +
+                       (size_t)2 * n * sizeof(double) + (size_t)2 * ET * ET * es + (size_t)2 * ET * n * es +
+                       (size_t)n * sizeof(int64_t) + 256;
+  wb[5].ensure(small);
+  X* A = static_cast<X*>(wb[0].p);
+  double* Zr = static_cast<double*>(wb[1].p);
+  X* Zx = static_cast<X*>(wb[2].p);
+  X* U = static_cast<X*>(wb[3].p);
+  X* W = U + n * T;
+  X* P1 = static_cast<X*>(wb[4].p);
+  X* P2 = P1 + nb * n;
+  char* q = static_cast<char*>(wb[5].p);
+  auto carve = [&](size_t bytes) {
+    char* r = q;
+    q += (bytes + 15) / 16 * 16;
+    return r;
+  };
+  X* vbuf = reinterpret_cast<X*>(carve(n * es));
+  X* ybuf = reinterpret_cast<X*>(carve(n * es));
+  X* tbuf = reinterpret_cast<X*>(carve(2 * T * es));
+  X* tau = reinterpret_cast<X*>(carve(n * es));
+  double2* part = reinterpret_cast<double2*>(carve((nparts_max + 1) * sizeof(double2)));
+  double* dd = reinterpret_cast<double*>(carve(n * sizeof(double)));
+  double* ee = reinterpret_cast<double*>(carve(n * sizeof(double)));
+  X* G = reinterpret_cast<X*>(carve(ET * ET * es));
+  X* Tm = reinterpret_cast<X*>(carve(ET * ET * es));
+  X* X1 = reinterpret_cast<X*>(carve(ET * n * es));
+  X* X2 = reinterpret_cast<X*>(carve(ET * n * es));
+  int64_t* order_d = reinterpret_cast<int64_t*>(carve(n * sizeof(int64_t)));
+
+  ShardMap map{};
+  map.D = ndev;
+  map.T = T;
+  map.cyclic = cyclic ? 1 : 0;
+  const std::vector<int64_t> counts = column_counts(n, T, ndev);
+  map.off[0] = 0;
+  for (int d = 0; d < ndev; ++d) {
+    map.p[d] = shards[d];
+    map.off[d + 1] = map.off[d] + counts[d];
+  }
+
+  // BCMG_EIG_PROFILE=1: per-phase device times on stderr
+  static const bool prof = getenv("BCMG_EIG_PROFILE") != nullptr;
+  cudaEvent_t pe[6];
+  auto pmark = [&](int k) {
+    if (!prof) return;
+    if (k == 0)
+      for (auto& e : pe) BCMG_CUDA(cudaEventCreate(&e));
+    BCMG_CUDA(cudaEventRecord(pe[k], st));
+  };
+  pmark(0);
+  // ---- 1. dense working copy
+  eig_gather<S, X><<<col_grid(n, n), 256, 0, st>>>(map, A, n);
+  BCMG_CHECK_LAUNCH();
+  BCMG_CUDA(cudaMemsetAsync(tau, 0, n * es, st));
+  BCMG_CUDA(cudaMemsetAsync(ee, 0, n * sizeof(double), st));
+
+  // ---- 2. blocked Householder tridiagonalisation (solvers.py:666-780)
+  const size_t symv_smem = (size_t)ET * (ET + 1) * sizeof(double2);
+  BCMG_CUDA(cudaFuncSetAttribute(eig_symv<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)symv_smem));
+  for (int64_t start = 0; start < n; start += T) {
+    const int64_t stop = std::min(start + T, n), tc = stop - start;
+    BCMG_CUDA(cudaMemsetAsync(U, 0, (size_t)2 * n * T * es, st));
+    for (int64_t jj = 0; jj < tc; ++jj) {
+      const int64_t c = start + jj, c0 = c + 1;
+      if (jj) {
+        eig_panel_update<X><<<blocks_for(n - c, RT), RT, 0, st>>>(A, n, c, U, W, (int)jj);
+        BCMG_CHECK_LAUNCH();
+      }
+      eig_house<X><<<1, 1024, 0, st>>>(A, n, c, vbuf, tau, dd, ee);
+      BCMG_CHECK_LAUNCH();
+      if (c == n - 1) continue;
+      const int64_t L = n - c0, nbt = (L + ET - 1) / ET;
+      eig_symv<X><<<(unsigned)(nbt * (nbt + 1) / 2), 128, symv_smem, st>>>(A, n, c0, vbuf, P1, P2);
+      BCMG_CHECK_LAUNCH();
+      eig_symv_reduce<X><<<blocks_for(L, RT), RT, 0, st>>>(P1, P2, n, c0, nbt, ybuf);
+      BCMG_CHECK_LAUNCH();
+      if (jj) {
+        eig_dots<X><<<(unsigned)(2 * jj), RT, 0, st>>>(U, W, n, c0, (int)jj, vbuf, tbuf);
+        BCMG_CHECK_LAUNCH();
+      }
+      const unsigned np = blocks_for(L, RT);
+      eig_corr<X><<<np, RT, 0, st>>>(U, W, n, c0, (int)jj, tbuf, ybuf, vbuf, part);
+      BCMG_CHECK_LAUNCH();
+      eig_fin<X><<<np, RT, 0, st>>>(vbuf, ybuf, U, W, n, c0, (int)jj, tau, c, part, (int)np);
+      BCMG_CHECK_LAUNCH();
+    }
+    if (stop >= n) continue;
+    // trailing lower triangle: A[stop:, stop:] -= U W^H + W U^H (solvers.py:771-780)
+    const int64_t M = n - stop;
+    Epilogue ep{};
+    ep.C = A + stop + stop * n;
+    ep.ldc = n;
+    ep.alpha = -1.0;
+    ep.beta = 1.0;
+    ep.lower_only = 1;
+    ep.lower_off = 0;
+    gemm(dtw, M, M, tc, opA(U + stop, n, OP_N), opB(W + stop, n, OP_C), ep, nullptr, st);
+    gemm(dtw, M, M, tc, opA(W + stop, n, OP_N), opB(U + stop, n, OP_C), ep, nullptr, st);
+  }
+
+  pmark(1);
+  // ---- 3. tridiagonal QL on the host, rotations replayed on the GPU
+  std::vector<double> d(n), e(n);
+  BCMG_CUDA(cudaMemcpyAsync(d.data(), dd, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  BCMG_CUDA(cudaMemcpyAsync(e.data(), ee, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  BCMG_CUDA(cudaStreamSynchronize(st));
+  e.resize(std::max<int64_t>(n - 1, 0));
+  QLRecord rec;
+  tridiag_ql(d, e, rec);
+  std::vector<int64_t> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return d[a] < d[b]; });
+
+  const int64_t nsw = (int64_t)rec.top.size(), nrot = (int64_t)rec.cs.size();
+  wb[6].ensure((size_t)nrot * sizeof(double2) + (size_t)(2 * nsw + 1) * sizeof(int64_t) + 64);
+  double2* cs_d = static_cast<double2*>(wb[6].p);
+  int64_t* off_d = reinterpret_cast<int64_t*>(cs_d + nrot);
+  int64_t* top_d = off_d + nsw + 1;
+  pmark(2);
+  if (nrot) BCMG_CUDA(cudaMemcpyAsync(cs_d, rec.cs.data(), nrot * sizeof(double2), cudaMemcpyHostToDevice, st));
+  BCMG_CUDA(cudaMemcpyAsync(off_d, rec.off.data(), (nsw + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  if (nsw) BCMG_CUDA(cudaMemcpyAsync(top_d, rec.top.data(), nsw * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  BCMG_CUDA(cudaMemcpyAsync(order_d, order.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  // Z = I
+  BCMG_CUDA(cudaMemsetAsync(Zr, 0, (size_t)n * n * sizeof(double), st));
+  eig_identity<<<blocks_for(n, RT), RT, 0, st>>>(Zr, n);
+  BCMG_CHECK_LAUNCH();
+  constexpr int KW = 16;
+  for (int64_t s0 = 0; s0 < nsw; s0 += KW) {
+    eig_rotate_wave<KW><<<blocks_for(n, 32), 32, 0, st>>>(Zr, n, cs_d, off_d, top_d, s0, nsw);
+    BCMG_CHECK_LAUNCH();
+  }
+  eig_permute<X><<<col_grid(n, n), 256, 0, st>>>(Zr, order_d, Zx, n);
+  BCMG_CHECK_LAUNCH();
+  pmark(3);
+
+  // ---- 4. back-transformation, 64 reflectors per compact-WY block, last block first
+  if (n >= 2) {
+    for (int64_t c0 = ((n - 2) / ET) * ET; c0 >= 0; c0 -= ET) {
+      const int64_t c1 = std::min<int64_t>(c0 + ET, n - 1), kb = c1 - c0, r0 = c0 + 1, K = n - r0;
+      const X* V = A + r0 + c0 * n;  // unit lower trapezoid: V(i, k) valid for i >= k
+      Operand vN = opA(V, n, OP_N), vC = opA(V, n, OP_C), vB = opB(V, n, OP_N);
+      vN.mask = vC.mask = vB.mask = 1;
+      vN.mask_off = vC.mask_off = vB.mask_off = 0;
+      Epilogue eg{};
+      eg.C = G;
+      eg.ldc = kb;
+      eg.alpha = 1.0;
+      eg.beta = 0.0;
+      gemm(dtw, kb, kb, K, vC, vB, eg, nullptr, st);  // G = V^H V
+      eig_larft<X><<<1, ET, 0, st>>>(G, tau + c0, (int)kb, Tm);
+      BCMG_CHECK_LAUNCH();
+      Epilogue e1{};
+      e1.C = X1;
+      e1.ldc = kb;
+      e1.alpha = 1.0;
+      e1.beta = 0.0;
+      gemm(dtw, kb, n, K, vC, opB(Zx + r0, n, OP_N), e1, nullptr, st);  // X1 = V^H Z[r0:, :]
+      Epilogue e2{};
+      e2.C = X2;
+      e2.ldc = kb;
+      e2.alpha = 1.0;
+      e2.beta = 0.0;
+      gemm(dtw, kb, n, kb, opA(Tm, kb, OP_N), opB(X1, kb, OP_N), e2, nullptr, st);  // X2 = T X1
+      Epilogue e3{};
+      e3.C = Zx + r0;
+      e3.ldc = n;
+      e3.alpha = -1.0;
+      e3.beta = 1.0;
+      gemm(dtw, K, n, kb, vN, opB(X2, kb, OP_N), e3, nullptr, st);  // Z[r0:, :] -= V X2
+    }
+  }
+
+  pmark(4);
+  // ---- 5. phase normalisation + scatter into the caller's shards; eigenvalues
+  eig_phase_scatter<X, S><<<(unsigned)n, 256, 0, st>>>(Zx, n, map);
+  BCMG_CHECK_LAUNCH();
+  pmark(5);
+  if (prof) {
+    BCMG_CUDA(cudaEventSynchronize(pe[5]));
+    float ms[5];
+    for (int k = 0; k < 5; ++k) BCMG_CUDA(cudaEventElapsedTime(&ms[k], pe[k], pe[k + 1]));
+    fprintf(stderr, "[syevd n=%lld T=%lld] tridiag %.1f ms, host QL %.1f ms (%lld rotations, %lld sweeps), "
+            "rotations %.1f ms, back-transform %.1f ms, phase+scatter %.1f ms\n", (long long)n, (long long)T, ms[0],
+            ms[1], (long long)nrot, (long long)nsw, ms[2], ms[3], ms[4]);
+    for (auto& e : pe) cudaEventDestroy(e);
+  }
+  std::sort(d.begin(), d.end());  // == d[order] (stable order of equal keys is immaterial for values)
+  if (sizeof(S) == 4 || (CP && sizeof(S) == 8)) {  // float / complex64: float eigenvalues
+    std::vector<float> wf(n);
+    for (int64_t i = 0; i < n; ++i) wf[i] = (float)d[i];
+    BCMG_CUDA(cudaMemcpyAsync(w_out, wf.data(), n * sizeof(float), cudaMemcpyHostToDevice, st));
+    BCMG_CUDA(cudaStreamSynchronize(st));
+  } else {
+    BCMG_CUDA(cudaMemcpyAsync(w_out, d.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+    BCMG_CUDA(cudaStreamSynchronize(st));
+  }
+}
+
+}  // namespace
+
+void Session::syevd(int dt, int64_t n, int64_t T, int ndev, void* const* shards, bool cyclic, void* w) {
+  if (world != 1) throw Error(CONFIG, "syevd runs single-process (all logical devices on the session's GPU)");
+  if (ndev > 16) throw Error(CONFIG, "syevd supports at most 16 logical devices");
+  dispatch_dtype(dt, [&](auto s) { syevd_t<decltype(s)>(*this, n, T, ndev, shards, cyclic, w); });
+}
+
+}  // namespace bcmg

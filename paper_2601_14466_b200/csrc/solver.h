@@ -122,6 +122,11 @@ struct Session {
   void reserve_workspace(int routine, int dt, int64_t n, int64_t T, int ndev, int64_t nrhs);
   void potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* const* shards, void* x, int64_t ldx);
   void potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards);
+  // Hermitian eigendecomposition (eigen.cu): eigenvalues ascending into w
+  // (device, real type of dt), eigenvectors over the shards (cyclic or
+  // contiguous layout); throws NO_CONVERGENCE
+  DevBuf eig[7];
+  void syevd(int dt, int64_t n, int64_t T, int ndev, void* const* shards, bool cyclic, void* w);
 };
 
 }  // namespace bcmg

@@ -23,6 +23,7 @@ import numpy as np
 
 from . import _lib
 from .core import (
+    ConvergenceError,
     DescriptorError,
     ElementType,
     MatrixDescriptor,
@@ -55,6 +56,8 @@ __all__ = [
     "potri",
     "solve_positive_definite",
     "invert_positive_definite",
+    "syevd",
+    "eigh_hermitian",
 ]
 
 
@@ -115,6 +118,8 @@ def _raise_for(rc: int, info: int | None = None) -> None:
         raise OutOfDeviceMemoryError(msg)
     if rc == _lib.BCMG_ERR_CONFIG:
         raise DescriptorError("dimension-mismatch", msg)
+    if rc == _lib.BCMG_ERR_NO_CONVERGENCE:
+        raise ConvergenceError(msg)
     if rc == _lib.BCMG_ERR_STALE_SESSION:
         raise StaleSessionError(msg)
     raise _lib.BcmgError(rc, msg)
@@ -388,5 +393,74 @@ def invert_positive_definite(mesh: DeviceMesh, a: np.ndarray, tile: TileSpec):
         inv = gather_array(mesh, dmat)
         t2 = time.perf_counter()
         return inv, _timings(mesh, t0, t1, t2)
+
+    return mesh.run_coordinated(body)
+
+
+# -- Hermitian eigendecomposition ----------------------------------------------
+
+
+def _real_torch_dtype(et: ElementType):
+    torch = _torch()
+    return torch.float32 if et in (ElementType.real32, ElementType.complex64) else torch.float64
+
+
+def _require_hermitian(desc: MatrixDescriptor) -> None:
+    if desc.structure is Structure.general:
+        raise DescriptorError("type-structure", "eigendecomposition requires symmetric, hermitian or "
+                                                "positive_definite structure")
+    if desc.n_rows != desc.n_cols:
+        raise DescriptorError("dimension-mismatch", f"matrix must be square, got {desc.n_rows}x{desc.n_cols}")
+
+
+def syevd(mesh: DeviceMesh, dmat: DistributedMatrix, ws: Sequence = ()) -> tuple[np.ndarray, DistributedMatrix]:
+    """Eigenvalues (ascending, host array of the real type) and eigenvectors of
+    a Hermitian matrix on the block-cyclic layout; the eigenvectors overwrite
+    the shards, column j of the cyclic layout belonging to w[j], each scaled so
+    its first largest-magnitude component is real and positive
+    (solvers.py:862-910).  Single-process meshes (csrc/eigen.cu)."""
+    _require_layout(dmat, "block_cyclic")
+    desc = dmat.descriptor
+    _require_hermitian(desc)
+    torch = _torch()
+    w = torch.empty(desc.n_rows, dtype=_real_torch_dtype(desc.element_type), device=mesh.device)
+    with mesh.coordinated():
+        rc = _lib.load().bcmg_syevd_cyclic(mesh.session, mesh.stream_handle(), desc.element_type.code, desc.n_rows,
+                                           dmat.tile.tile_width, mesh.num_devices, dmat.shard_ptrs(),
+                                           C.c_void_p(w.data_ptr()))
+    _raise_for(rc)
+    return w.cpu().numpy(), dmat
+
+
+def _hermitian_structure(et: ElementType) -> Structure:
+    return Structure.hermitian if et.is_complex else Structure.symmetric
+
+
+def eigh_hermitian(mesh: DeviceMesh, a: np.ndarray, tile: TileSpec):
+    """Ascending eigenvalues and eigenvectors of a Hermitian matrix; host
+    array in, (w, v, Timings) out (solvers.py:1019-1043).  The native pipeline
+    gathers the working copy straight from the contiguous shards and scatters
+    the eigenvectors straight back, so redistribute_in / _out fold into it."""
+    et = ElementType.from_dtype(np.asarray(a).dtype)
+    desc = _matrix_descriptor(a, _hermitian_structure(et))
+    _require_hermitian(desc)
+    validate_tile(tile, desc.n_cols)
+    torch = _torch()
+
+    def body():
+        t0 = time.perf_counter()
+        dmat = create_distributed(mesh, desc, tile)
+        w = torch.empty(desc.n_rows, dtype=_real_torch_dtype(et), device=mesh.device)
+        t1 = time.perf_counter()
+        write_array(mesh, dmat, a)
+        info = C.c_int(0)
+        rc = _lib.load().bcmg_syevd(mesh.session, mesh.stream_handle(), et.code, desc.n_rows, tile.tile_width,
+                                    mesh.num_devices, dmat.shard_ptrs(), C.c_void_p(w.data_ptr()), 0,
+                                    C.byref(info))
+        _raise_for(rc, info.value)
+        v = gather_array(mesh, dmat)
+        wh = w.cpu().numpy()
+        t2 = time.perf_counter()
+        return wh, v, _timings(mesh, t0, t1, t2)
 
     return mesh.run_coordinated(body)
