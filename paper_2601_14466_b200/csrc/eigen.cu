@@ -332,8 +332,12 @@ __global__ void __launch_bounds__(RT) eig_fin(const X* v, const X* y, X* U, X* W
 template <int K>
 __global__ void __launch_bounds__(32) eig_rotate_wave(double* Z, int64_t n, const double2* cs, const int64_t* sw_off,
                                                       const int64_t* sw_top, int64_t s0, int64_t nsw) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= n) return;
+  constexpr int W = 2 * K;  // window columns == steps per parameter chunk == warp width
+  static_assert(W == 32, "one parameter per lane and step");
+  __shared__ double2 prm[K][W];
+  const int lane = threadIdx.x;
+  const int64_t r = blockIdx.x * (int64_t)W + lane;
+  const bool live = r < n;
   const int kk = (int)min((int64_t)K, nsw - s0);
   int64_t top[K], bot[K], off[K];
   int64_t pmax = INT64_MIN, pmin = INT64_MAX;
@@ -349,35 +353,48 @@ __global__ void __launch_bounds__(32) eig_rotate_wave(double* Z, int64_t n, cons
       off[s] = 0, top[s] = -1, bot[s] = 0;  // empty
     }
   }
-  double* z = Z + r;
-  double win[2 * K];  // win[j] = column p + j
+  double* z = Z + (live ? r : 0);
+  // column c lives in slot (c - pmax) mod W: every index below is static
+  double win[W];
 #pragma unroll
-  for (int j = 0; j < 2 * K; ++j) {
+  for (int j = 0; j < W; ++j) {
     const int64_t c = pmax + j;
-    win[j] = (c >= 0 && c < n) ? z[c * n] : 0.0;
+    win[j] = (live && c >= 0 && c < n) ? z[c * n] : 0.0;
   }
-  for (int64_t p = pmax; p >= pmin; --p) {
+  for (int64_t p0 = pmax; p0 >= pmin; p0 -= W) {
+    __syncwarp();
 #pragma unroll
-    for (int s = 0; s < K; ++s) {
-      const int64_t i = p + 2 * s;
-      if (i >= bot[s] && i <= top[s]) {
-        const double2 g = cs[off[s] + (top[s] - i)];  // (c, s)
-        const double a = win[2 * s], b = win[2 * s + 1];
-        win[2 * s + 1] = g.y * a + g.x * b;
-        win[2 * s] = g.x * a - g.y * b;
-      }
+    for (int s = 0; s < K; ++s) {  // lane u stages sweep s's rotation for step p0 - u (identity when idle)
+      const int64_t i = p0 - lane + 2 * s;
+      double2 g = make_double2(1.0, 0.0);
+      if (i >= bot[s] && i <= top[s]) g = cs[off[s] + (top[s] - i)];
+      prm[s][lane] = g;
     }
-    const int64_t cs_ = p + 2 * K - 1;
-    if (cs_ >= 0 && cs_ < n) z[cs_ * n] = win[2 * K - 1];
+    __syncwarp();
 #pragma unroll
-    for (int j = 2 * K - 1; j > 0; --j) win[j] = win[j - 1];
-    const int64_t cl = p - 1;
-    win[0] = (cl >= 0 && cl < n) ? z[cl * n] : 0.0;
+    for (int u = 0; u < W; ++u) {
+      const int64_t p = p0 - u;
+      if (p < pmin) break;
+#pragma unroll
+      for (int s = 0; s < K; ++s) {  // sweep s: columns p + 2s, p + 2s + 1
+        const double2 g = prm[s][u];
+        const int sa = ((2 * s - u) % W + W) % W, sb = ((2 * s + 1 - u) % W + W) % W;
+        const double x = win[sa], y = win[sb];
+        win[sb] = g.y * x + g.x * y;
+        win[sa] = g.x * x - g.y * y;
+      }
+      const int sl = W - 1 - u;  // column p + W - 1 leaves, column p - 1 enters
+      const int64_t co = p + W - 1, ci = p - 1;
+      if (live && co >= 0 && co < n) z[co * n] = win[sl];
+      win[sl] = (live && ci >= 0 && ci < n) ? z[ci * n] : 0.0;
+    }
   }
+  // the window now holds columns pmin - 1 .. pmin + W - 2
+  const int64_t first = pmin - 1, shift = ((first - pmax) % W + W) % W;
 #pragma unroll
-  for (int j = 0; j < 2 * K; ++j) {
-    const int64_t c = pmin - 1 + j;
-    if (c >= 0 && c < n) z[c * n] = win[j];
+  for (int sl = 0; sl < W; ++sl) {
+    const int64_t c = first + (((int64_t)sl - shift) % W + W) % W;
+    if (live && c >= 0 && c < n) z[c * n] = win[sl];
   }
 }
 
@@ -424,7 +441,9 @@ struct QLRecord {
   std::vector<double2> cs;
   std::vector<int64_t> off{0}, top;
 };
-void tridiag_ql(std::vector<double>& d, const std::vector<double>& e_in, QLRecord& rec, int max_iter = 30) {
+template <class F>
+void tridiag_ql(std::vector<double>& d, const std::vector<double>& e_in, QLRecord& rec, F&& after_sweep,
+                int max_iter = 30) {
   const int64_t n = (int64_t)d.size();
   std::vector<double> e(n, 0.0);
   for (int64_t i = 0; i + 1 < n; ++i) e[i] = e_in[i];
@@ -470,7 +489,10 @@ void tridiag_ql(std::vector<double>& d, const std::vector<double>& e_in, QLRecor
         rec.cs.push_back(make_double2(c, s));
       }
       if ((int64_t)rec.cs.size() == rec.off.back()) rec.top.pop_back();  // no rotation applied
-      else rec.off.push_back((int64_t)rec.cs.size());
+      else {
+        rec.off.push_back((int64_t)rec.cs.size());
+        after_sweep();
+      }
       if (!broke) {
         d[l] -= p;
         e[l] = g;
@@ -611,31 +633,67 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
   BCMG_CUDA(cudaMemcpyAsync(e.data(), ee, n * sizeof(double), cudaMemcpyDeviceToHost, st));
   BCMG_CUDA(cudaStreamSynchronize(st));
   e.resize(std::max<int64_t>(n - 1, 0));
-  QLRecord rec;
-  tridiag_ql(d, e, rec);
-  std::vector<int64_t> order(n);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return d[a] < d[b]; });
-
-  const int64_t nsw = (int64_t)rec.top.size(), nrot = (int64_t)rec.cs.size();
-  wb[6].ensure((size_t)nrot * sizeof(double2) + (size_t)(2 * nsw + 1) * sizeof(int64_t) + 64);
-  double2* cs_d = static_cast<double2*>(wb[6].p);
-  int64_t* off_d = reinterpret_cast<int64_t*>(cs_d + nrot);
-  int64_t* top_d = off_d + nsw + 1;
-  pmark(2);
-  if (nrot) BCMG_CUDA(cudaMemcpyAsync(cs_d, rec.cs.data(), nrot * sizeof(double2), cudaMemcpyHostToDevice, st));
-  BCMG_CUDA(cudaMemcpyAsync(off_d, rec.off.data(), (nsw + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  if (nsw) BCMG_CUDA(cudaMemcpyAsync(top_d, rec.top.data(), nsw * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  BCMG_CUDA(cudaMemcpyAsync(order_d, order.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  // Z = I
+  // Z = I first: rotation batches replay on the GPU while the host iterates
   BCMG_CUDA(cudaMemsetAsync(Zr, 0, (size_t)n * n * sizeof(double), st));
   eig_identity<<<blocks_for(n, RT), RT, 0, st>>>(Zr, n);
   BCMG_CHECK_LAUNCH();
-  constexpr int KW = 16;
-  for (int64_t s0 = 0; s0 < nsw; s0 += KW) {
-    eig_rotate_wave<KW><<<blocks_for(n, 32), 32, 0, st>>>(Zr, n, cs_d, off_d, top_d, s0, nsw);
-    BCMG_CHECK_LAUNCH();
-  }
+  // rotation parameters stream through NSLOT pinned -> device slots of CH sweeps
+  constexpr int KW = 16, CH = 4 * KW, NSLOT = 3;
+  const size_t cap_rot = (size_t)CH * (size_t)std::max<int64_t>(n, 1);
+  const size_t slot_bytes = (cap_rot * sizeof(double2) + (2 * CH + 1) * sizeof(int64_t) + 255) / 256 * 256;
+  wb[6].ensure(NSLOT * slot_bytes);
+  struct Ring {
+    void* host = nullptr;
+    cudaEvent_t done[NSLOT] = {};
+    cudaStream_t st;
+    ~Ring() {
+      cudaStreamSynchronize(st);
+      if (host) cudaFreeHost(host);
+      for (auto e : done)
+        if (e) cudaEventDestroy(e);
+    }
+  } ring;
+  ring.st = st;
+  BCMG_CUDA(cudaHostAlloc(&ring.host, NSLOT * slot_bytes, cudaHostAllocDefault));
+  for (auto& e : ring.done) BCMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  int64_t nrot = 0, nsw = 0, nflush = 0;
+  QLRecord rec;
+  auto flush = [&] {
+    const int64_t ns = (int64_t)rec.top.size(), nr = (int64_t)rec.cs.size();
+    if (!ns) return;
+    const int k = (int)(nflush++ % NSLOT);
+    BCMG_CUDA(cudaEventSynchronize(ring.done[k]));  // the slot's previous batch has run
+    char* hb = static_cast<char*>(ring.host) + k * slot_bytes;
+    char* db = static_cast<char*>(wb[6].p) + k * slot_bytes;
+    int64_t* hmeta = reinterpret_cast<int64_t*>(hb + cap_rot * sizeof(double2));
+    std::copy(rec.cs.begin(), rec.cs.end(), reinterpret_cast<double2*>(hb));
+    std::copy(rec.off.begin(), rec.off.end(), hmeta);
+    std::copy(rec.top.begin(), rec.top.end(), hmeta + ns + 1);
+    BCMG_CUDA(cudaMemcpyAsync(db, hb, nr * sizeof(double2), cudaMemcpyHostToDevice, st));
+    int64_t* dmeta = reinterpret_cast<int64_t*>(db + cap_rot * sizeof(double2));
+    BCMG_CUDA(cudaMemcpyAsync(dmeta, hmeta, (2 * ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    for (int64_t s0 = 0; s0 < ns; s0 += KW) {
+      eig_rotate_wave<KW><<<blocks_for(n, 32), 32, 0, st>>>(Zr, n, reinterpret_cast<const double2*>(db), dmeta,
+                                                            dmeta + ns + 1, s0, ns);
+      BCMG_CHECK_LAUNCH();
+    }
+    BCMG_CUDA(cudaEventRecord(ring.done[k], st));
+    nrot += nr;
+    nsw += ns;
+    rec.cs.clear();
+    rec.off.assign(1, 0);
+    rec.top.clear();
+  };
+  rec.cs.reserve(cap_rot);
+  tridiag_ql(d, e, rec, [&] {
+    if ((int64_t)rec.top.size() >= CH) flush();
+  });
+  flush();
+  std::vector<int64_t> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return d[a] < d[b]; });
+  BCMG_CUDA(cudaMemcpyAsync(order_d, order.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  pmark(2);
   eig_permute<X><<<col_grid(n, n), 256, 0, st>>>(Zr, order_d, Zx, n);
   BCMG_CHECK_LAUNCH();
   pmark(3);
@@ -686,8 +744,8 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
     BCMG_CUDA(cudaEventSynchronize(pe[5]));
     float ms[5];
     for (int k = 0; k < 5; ++k) BCMG_CUDA(cudaEventElapsedTime(&ms[k], pe[k], pe[k + 1]));
-    fprintf(stderr, "[syevd n=%lld T=%lld] tridiag %.1f ms, host QL %.1f ms (%lld rotations, %lld sweeps), "
-            "rotations %.1f ms, back-transform %.1f ms, phase+scatter %.1f ms\n", (long long)n, (long long)T, ms[0],
+    fprintf(stderr, "[syevd n=%lld T=%lld] tridiag %.1f ms, host QL + overlapped rotation replay %.1f ms (%lld rotations, "
+            "%lld sweeps), permute %.1f ms, back-transform %.1f ms, phase+scatter %.1f ms\n", (long long)n, (long long)T, ms[0],
             ms[1], (long long)nrot, (long long)nsw, ms[2], ms[3], ms[4]);
     for (auto& e : pe) cudaEventDestroy(e);
   }
