@@ -53,6 +53,11 @@ def main():
     sepc = qc @ np.diag(np.arange(1.0, 21.0)) @ qc.conj().T
     add("sep20_c128", np.asfortranarray((sepc + sepc.conj().T) / 2), 3, 4)
     np.savez_compressed(OUT, **cases)
+    # BCMG matrix files written by the reference's own write_matrix (core.py:255-273)
+    from bcmg import write_matrix
+    gold = os.path.dirname(OUT)
+    write_matrix(os.path.join(gold, "ref_random_spd5_c64.bcmg"), cli.make_matrix("random_spd", 5, ElementType.complex64, 2))
+    write_matrix(os.path.join(gold, "ref_vector3_f32.bcmg"), np.array([1.5, -2.0, 3.25], dtype=np.float32))
     print(f"wrote {OUT}: {len(cases) // 4} cases")
 
 

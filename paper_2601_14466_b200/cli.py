@@ -15,10 +15,12 @@ pkg/src/bcmg/cli.py), on the B200 path.
   memory, 2 configuration error (cli.py:462-482).
 
 Matrix sources: ``diag`` (diag(1..n)), ``random_spd`` (B B^H + n I, B from
-numpy Philox(key=seed), cli.py:81-103 -- host-generated, O(n^3)) and
+numpy Philox(key=seed), cli.py:81-103 -- host-generated, O(n^3)),
 ``device_spd`` ((R + R^H)/2 + n I generated on the GPU by bcmg_generate_spd,
-for large n).  Out of scope here: syevd, the mpmd mode, the
-BCMG matrix file format (``file:`` sources, ``gen``) and copy transcripts
+for large n) and ``file:PATH`` (a BCMG matrix file, core.py:255-303; ``gen``
+writes one, cli.py:449-458).  Routines: potrs, potri and syevd (eigen-residual,
+orthonormality, ascending order and the diag(1..n) spectrum, cli.py:320-337).
+Out of scope here: the mpmd mode and copy transcripts
 (``--trace``); they are rejected as configuration errors.
 """
 
@@ -33,9 +35,10 @@ import sys
 import numpy as np
 
 from . import _lib
-from .core import DescriptorError, ElementType, NotPositiveDefiniteError, OutOfDeviceMemoryError, TileSpec
+from .core import (ConvergenceError, DescriptorError, ElementType, MatrixFileError, NotPositiveDefiniteError,
+                   OutOfDeviceMemoryError, TileSpec, read_matrix, write_matrix)
 from .mesh import DeviceMesh
-from .solvers import invert_positive_definite, solve_positive_definite
+from .solvers import eigh_hermitian, invert_positive_definite, solve_positive_definite
 
 ROUTINES = ("potrs", "potri", "syevd")
 MATRIX_KINDS = ("diag", "random_spd", "device_spd")
@@ -120,12 +123,39 @@ def inverse_residual(a: np.ndarray, inv: np.ndarray, device="cuda") -> float:
     return float(torch.linalg.vector_norm(R) / np.sqrt(n))
 
 
+def eigen_residual(a: np.ndarray, w: np.ndarray, v: np.ndarray, device="cuda") -> float:
+    """||A V - V diag(w)||_F / ||A||_F at 64-bit precision (cli.py:128-133):
+    A V through bcmg_gemm, minus V diag(w) on the device."""
+    import torch
+
+    A, V, AV = _gemm_residual(a, v, np.zeros(v.shape, dtype=np.result_type(a, v)), device)
+    W = torch.from_numpy(np.asarray(w, dtype=np.float64)).to(device)
+    R = AV - V * W[:, None].to(V.dtype)  # column-major buffers: row j of the .T view is column j
+    den = torch.linalg.vector_norm(A)
+    num = torch.linalg.vector_norm(R)
+    return float(num / den) if float(den) else float(num)
+
+
+def orthonormality_defect(v: np.ndarray, device="cuda") -> float:
+    """||V^H V - I||_F at 64-bit precision (cli.py:136-140)."""
+    import torch
+
+    V = _wide(v, device)  # rows of V are the columns of v
+    n = v.shape[1]
+    G = V.conj() @ V.T
+    return float(torch.linalg.vector_norm(G - torch.eye(n, dtype=G.dtype, device=device)))
+
+
 def _residual_tol(et: ElementType, n: int) -> float:
     return 100.0 * n * et.eps
 
 
 def _elementwise_tol(et: ElementType) -> float:
     return 1e-12 if et.eps < 1e-10 else 1e-4
+
+
+def _eigen_diag_tol(et: ElementType) -> float:
+    return 1e-10 if et.eps < 1e-10 else 1e-4
 
 
 # ----------------------------------------------------------------- parser
@@ -141,7 +171,7 @@ def _common(p: argparse.ArgumentParser) -> None:
     p.add_argument("--devices", type=_int_list, default=[1], help="logical device count(s), comma list")
     p.add_argument("--dtype", choices=sorted(_DTYPE_NAMES.values()), default="f64")
     p.add_argument("--mode", choices=("spmd", "mpmd"), default=None)
-    p.add_argument("--matrix", default="diag", metavar="SOURCE", help="diag, random_spd or device_spd")
+    p.add_argument("--matrix", default="diag", metavar="SOURCE", help="diag, random_spd, device_spd or file:PATH")
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--nrhs", type=int, default=1)
     p.add_argument("--trace", metavar="PATH", help="(not supported on the GPU path)")
@@ -153,7 +183,10 @@ def build_parser() -> argparse.ArgumentParser:
     sub = parser.add_subparsers(dest="command", required=True)
     v = sub.add_parser("verify", help="run a routine and check invariants")
     v.add_argument("--routine", required=True, choices=ROUTINES)
-    v.add_argument("--n", type=int, required=True)
+    v.add_argument("--n", type=int, default=None, help="matrix order (from the file for file:PATH)")
+    v.add_argument("--rhs", metavar="PATH", help="read the right-hand side from a matrix file (potrs)")
+    v.add_argument("--result-out", metavar="PATH", help="write the solution / inverse / eigenvectors")
+    v.add_argument("--eigenvalues-out", metavar="PATH", help="write the eigenvalues as an n x 1 matrix (syevd)")
     v.add_argument("--tolerance", type=float, default=None)
     _common(v)
     b = sub.add_parser("bench", help="time repeated runs, CSV per rep")
@@ -162,63 +195,111 @@ def build_parser() -> argparse.ArgumentParser:
     b.add_argument("--reps", type=int, default=5)
     b.add_argument("--out", default="-", metavar="PATH")
     _common(b)
+    g = sub.add_parser("gen", help="write a test matrix file")
+    g.add_argument("--kind", required=True, choices=("diag", "random_spd", "ones"))
+    g.add_argument("--n", type=int, required=True)
+    g.add_argument("--nrhs", type=int, default=1, help="columns for --kind ones")
+    g.add_argument("--dtype", choices=sorted(_DTYPE_NAMES.values()), default="f64")
+    g.add_argument("--seed", type=int, default=1)
+    g.add_argument("--out", required=True, metavar="PATH")
     return parser
 
 
 def _check_scope(args) -> None:
-    if args.routine == "syevd":
-        raise DescriptorError("type-structure", "syevd is not part of the B200 solve path (DESIGN.md §7)")
     if (args.mode or "spmd") != "spmd":
         raise DescriptorError("type-structure", "only the spmd mode is supported (mpmd: DESIGN.md §7)")
     if args.trace:
         raise DescriptorError("type-structure", "--trace: the GPU rotation keeps no copy transcript")
+    if args.matrix.startswith("file:"):
+        return
     if args.matrix not in MATRIX_KINDS:
-        raise DescriptorError("type-structure", f"--matrix must be one of {MATRIX_KINDS}, got {args.matrix!r}")
+        raise DescriptorError("type-structure",
+                              f"--matrix must be one of {MATRIX_KINDS} or file:PATH, got {args.matrix!r}")
     if args.n is None or args.n < 1:
         raise DescriptorError("dimension-mismatch", f"--n must be >= 1, got {args.n}")
     if any(d < 1 for d in args.devices):
         raise DescriptorError("dimension-mismatch", f"--devices must be >= 1, got {args.devices}")
 
 
-def _tiles(args) -> list[int]:
-    return args.tile if args.tile else [min(64, args.n)]
+def _tiles(args, n: int) -> list[int]:
+    return args.tile if args.tile else [min(64, n)]
+
+
+def _load_problem(args):
+    """(A, element type, generator kind or None for a file) -- cli.py:263-285."""
+    if args.matrix.startswith("file:"):
+        a = read_matrix(args.matrix[len("file:"):])
+        if a.shape[0] != a.shape[1]:
+            raise DescriptorError("dimension-mismatch", f"input matrix must be square, got {a.shape[0]}x{a.shape[1]}")
+        return a, ElementType.from_dtype(a.dtype), None
+    et = ElementType.from_name(args.dtype)
+    return make_matrix(args.matrix, args.n, et, args.seed), et, args.matrix
 
 
 def _flops(routine: str, n: int, nrhs: int, et: ElementType) -> float:
+    if routine == "syevd":  # tridiagonalisation 4/3 n^3 + back-transformation 2 n^3 (LAWN-41)
+        return (10 * n ** 3 / 3) * (4 if et.is_complex else 1)
     f = n ** 3 / 3 + 2 * n * n * nrhs if routine == "potrs" else n ** 3
     return f * (4 if et.is_complex else 1)
 
 
 # ----------------------------------------------------------------- commands
-def _cmd_verify(args) -> int:
-    _check_scope(args)
-    et = ElementType.from_name(args.dtype)
-    n = args.n
-    a = make_matrix(args.matrix, n, et, args.seed)
+def _verify_one(args, a, et, kind, tile, devices):
+    """One configuration: [(check, value, tol)] (cli.py:288-345)."""
+    n = a.shape[0]
     res_tol = args.tolerance if args.tolerance is not None else _residual_tol(et, n)
     elem_tol = args.tolerance if args.tolerance is not None else _elementwise_tol(et)
-    failed = []
-    for tile in _tiles(args):
-        for devices in args.devices:
-            mesh = DeviceMesh(devices)
-            checks = []
-            if args.routine == "potrs":
-                b = np.ones((n, args.nrhs), dtype=et.dtype, order="F")
-                x, _ = solve_positive_definite(mesh, a, b, TileSpec(tile))
-                checks.append(("solve-residual", solve_residual(a, x, b), res_tol))
-                if args.matrix == "diag":
-                    expected = 1.0 / np.arange(1, n + 1, dtype=np.float64)
-                    checks.append(("diag-solution", float(np.abs(x.astype(np.complex128) - expected[:, None]).max()),
-                                   elem_tol))
+    mesh = DeviceMesh(devices)
+    checks = []
+    try:
+        if args.routine == "potrs":
+            if args.rhs:
+                b = read_matrix(args.rhs)
+                if ElementType.from_dtype(b.dtype) is not et:
+                    raise DescriptorError("type-structure", "right-hand side element type does not match the matrix")
             else:
-                inv, _ = invert_positive_definite(mesh, a, TileSpec(tile))
-                checks.append(("inverse-residual", inverse_residual(a, inv), res_tol))
-                if args.matrix == "diag":
-                    expected = np.diag(1.0 / np.arange(1, n + 1, dtype=np.float64))
-                    checks.append(("diag-inverse", float(np.abs(inv.astype(np.complex128) - expected).max()),
-                                   elem_tol))
-            mesh.close()
-            for name, value, tol in checks:
+                b = np.ones((n, args.nrhs), dtype=et.dtype, order="F")
+            x, _ = solve_positive_definite(mesh, a, b, TileSpec(tile))
+            checks.append(("solve-residual", solve_residual(a, x, b), res_tol))
+            if kind == "diag" and not args.rhs:
+                expected = 1.0 / np.arange(1, n + 1, dtype=np.float64)
+                checks.append(("diag-solution", float(np.abs(x.astype(np.complex128) - expected[:, None]).max()),
+                               elem_tol))
+            result = x
+        elif args.routine == "potri":
+            inv, _ = invert_positive_definite(mesh, a, TileSpec(tile))
+            checks.append(("inverse-residual", inverse_residual(a, inv), res_tol))
+            if kind == "diag":
+                expected = np.diag(1.0 / np.arange(1, n + 1, dtype=np.float64))
+                checks.append(("diag-inverse", float(np.abs(inv.astype(np.complex128) - expected).max()), elem_tol))
+            result = inv
+        else:
+            w, v, _ = eigh_hermitian(mesh, a, TileSpec(tile))
+            checks.append(("eigen-residual", eigen_residual(a, w, v), res_tol))
+            checks.append(("orthonormal", orthonormality_defect(v), res_tol))
+            ascent = float(max(0.0, np.max(w[:-1] - w[1:]))) if n > 1 else 0.0
+            checks.append(("ascending", ascent, 0.0))
+            if kind == "diag":
+                err = float(np.max(np.abs(w.astype(np.float64) - np.arange(1, n + 1, dtype=np.float64))))
+                checks.append(("diag-eigenvalues", err,
+                               args.tolerance if args.tolerance is not None else _eigen_diag_tol(et)))
+            if args.eigenvalues_out:
+                write_matrix(args.eigenvalues_out, w.reshape(-1, 1))
+            result = v
+        if args.result_out:
+            write_matrix(args.result_out, result)
+    finally:
+        mesh.close()
+    return checks
+
+
+def _cmd_verify(args) -> int:
+    _check_scope(args)
+    a, et, kind = _load_problem(args)
+    failed = []
+    for tile in _tiles(args, a.shape[0]):
+        for devices in args.devices:
+            for name, value, tol in _verify_one(args, a, et, kind, tile, devices):
                 ok = value <= tol  # False for NaN as well
                 if not ok:
                     failed.append(name)
@@ -229,18 +310,30 @@ def _cmd_verify(args) -> int:
     return 0
 
 
+def _cmd_gen(args) -> int:
+    """Write a test matrix file (cli.py:449-458)."""
+    et = ElementType.from_name(args.dtype)
+    if args.n < 1:
+        raise DescriptorError("dimension-mismatch", f"--n must be >= 1, got {args.n}")
+    if args.kind == "ones":
+        arr = np.ones((args.n, args.nrhs), dtype=et.dtype, order="F")
+    else:
+        arr = make_matrix(args.kind, args.n, et, args.seed)
+    write_matrix(args.out, arr)
+    return 0
+
+
 def _cmd_bench(args) -> int:
     _check_scope(args)
     if args.reps < 1:
         raise DescriptorError("dimension-mismatch", "--reps must be >= 1")
-    et = ElementType.from_name(args.dtype)
-    n = args.n
-    a = make_matrix(args.matrix, n, et, args.seed)
+    a, et, _ = _load_problem(args)
+    n = a.shape[0]
     out = open(args.out, "w", newline="") if args.out != "-" else sys.stdout
     try:
         w = csv.writer(out, lineterminator="\n")
         w.writerow(BENCH_COLUMNS + EXTRA_COLUMNS)
-        for tile in _tiles(args):
+        for tile in _tiles(args, n):
             for devices in args.devices:
                 mesh = DeviceMesh(devices)
                 solves, allocs = [], []
@@ -249,9 +342,12 @@ def _cmd_bench(args) -> int:
                         b = np.ones((n, args.nrhs), dtype=et.dtype, order="F")
                         x, tm = solve_positive_definite(mesh, a, b, TileSpec(tile))
                         residual = solve_residual(a, x, b)
-                    else:
+                    elif args.routine == "potri":
                         inv, tm = invert_positive_definite(mesh, a, TileSpec(tile))
                         residual = inverse_residual(a, inv)
+                    else:
+                        ev, vecs, tm = eigh_hermitian(mesh, a, TileSpec(tile))
+                        residual = eigen_residual(a, ev, vecs)
                     solves.append(tm.solve_seconds)
                     allocs.append(tm.alloc_seconds)
                     tflops = _flops(args.routine, n, args.nrhs, et) / (tm.device_ms * 1e-3) / 1e12 if tm.device_ms else 0
@@ -271,7 +367,12 @@ def _cmd_bench(args) -> int:
 def main(argv=None) -> int:
     args = build_parser().parse_args(argv)
     try:
+        if args.command == "gen":
+            return _cmd_gen(args)
         return _cmd_verify(args) if args.command == "verify" else _cmd_bench(args)
+    except MatrixFileError as exc:
+        print(f"configuration error: {exc}", file=sys.stderr)
+        return 2
     except (DescriptorError, ValueError) as exc:
         print(f"configuration error: {exc}", file=sys.stderr)
         return 2
@@ -280,6 +381,12 @@ def main(argv=None) -> int:
         return 1
     except OutOfDeviceMemoryError as exc:
         print(f"out of device memory: {exc}", file=sys.stderr)
+        return 1
+    except ConvergenceError as exc:
+        print(f"did not converge: {exc}", file=sys.stderr)
+        return 1
+    except OSError as exc:
+        print(f"i/o error: {exc}", file=sys.stderr)
         return 1
 
 

@@ -11,10 +11,10 @@ from paper_2601_14466_b200 import cli
 
 
 @pytest.mark.parametrize("argv", [
-    ["verify", "--routine", "syevd", "--n", "8"],
     ["verify", "--routine", "potrs", "--n", "8", "--mode", "mpmd"],
     ["verify", "--routine", "potrs", "--n", "8", "--trace", "t.csv"],
-    ["verify", "--routine", "potrs", "--n", "8", "--matrix", "file:x.bcmg"],
+    ["verify", "--routine", "potrs", "--n", "8", "--matrix", "nonsense"],
+    ["gen", "--kind", "diag", "--n", "0", "--out", "x.bcmg"],
     ["bench", "--routine", "potri", "--n", "8", "--devices", "0"],
     ["bench", "--routine", "potrs", "--n", "8", "--reps", "0"],
 ])
@@ -77,3 +77,81 @@ def test_gpu_residuals_match_host():
     assert cli.solve_residual(a, x, b) == pytest.approx(O.solve_residual(a, x, b), rel=1e-6)
     inv = np.linalg.inv(a) + 1e-10
     assert cli.inverse_residual(a, inv) == pytest.approx(O.inverse_residual(a, inv), rel=1e-6)
+    w, v = np.linalg.eigh(a)
+    w = w + 1e-9
+    host = np.linalg.norm(a @ v - v * w) / np.linalg.norm(a)
+    assert cli.eigen_residual(a, w, v) == pytest.approx(host, rel=1e-6)
+    assert cli.orthonormality_defect(v + 1e-9) == pytest.approx(
+        np.linalg.norm((v + 1e-9).conj().T @ (v + 1e-9) - np.eye(64)), rel=1e-6)
+
+
+def test_gen_writes_reference_format(tmp_path):
+    """gen (cli.py:449-458) writes the reference's matrix file byte for byte:
+    compare with a file the reference's own write_matrix produced."""
+    from conftest import GOLDEN
+
+    out = tmp_path / "a.bcmg"
+    assert cli.main(["gen", "--kind", "random_spd", "--n", "5", "--dtype", "c64", "--seed", "2",
+                     "--out", str(out)]) == 0
+    assert out.read_bytes() == open(f"{GOLDEN}/ref_random_spd5_c64.bcmg", "rb").read()
+    ones = tmp_path / "b.bcmg"
+    assert cli.main(["gen", "--kind", "ones", "--n", "6", "--nrhs", "2", "--out", str(ones)]) == 0
+    from paper_2601_14466_b200.core import read_matrix
+
+    assert np.array_equal(read_matrix(ones), np.ones((6, 2)))
+
+
+def test_bad_matrix_file_is_configuration_error(tmp_path):
+    """MatrixFileError -> exit 2 (cli.py:471-473)."""
+    bad = tmp_path / "bad.bcmg"
+    bad.write_bytes(b"NOPE" + bytes(12))
+    err = io.StringIO()
+    with contextlib.redirect_stderr(err):
+        assert cli.main(["verify", "--routine", "potrs", "--matrix", f"file:{bad}"]) == 2
+    assert "configuration error" in err.getvalue()
+
+
+@pytest.mark.gpu
+def test_verify_syevd_on_gpu(capsys):
+    """reference test_cli.py:44-60, 100-110: syevd verify lines."""
+    assert cli.main(["verify", "--routine", "syevd", "--n", "32", "--tile", "4", "--devices", "2", "--dtype", "c128",
+                     "--matrix", "random_spd"]) == 0
+    lines = capsys.readouterr().out.splitlines()
+    assert [ln.split()[1] for ln in lines] == ["eigen-residual", "orthonormal", "ascending"]
+    assert all(ln.startswith("PASS") for ln in lines)
+    assert cli.main(["verify", "--routine", "syevd", "--n", "64", "--tile", "16", "--devices", "2",
+                     "--matrix", "diag"]) == 0
+    lines = capsys.readouterr().out.splitlines()
+    assert lines[-1].startswith("PASS diag-eigenvalues")
+
+
+@pytest.mark.gpu
+def test_verify_files_on_gpu(tmp_path, capsys):
+    """reference test_cli.py:86-150: file: sources, --result-out, --rhs,
+    --eigenvalues-out; not-positive-definite file -> exit 1 with the pivot."""
+    from paper_2601_14466_b200.core import read_matrix, write_matrix
+
+    bad = tmp_path / "bad.bcmg"
+    write_matrix(bad, np.asfortranarray(np.diag([1.0, -1.0])))
+    err = io.StringIO()
+    with contextlib.redirect_stderr(err):
+        assert cli.main(["verify", "--routine", "potrs", "--tile", "1", "--devices", "2",
+                         "--matrix", f"file:{bad}"]) == 1
+    assert "not positive definite: pivot=2" in err.getvalue()
+    out_path = tmp_path / "x.bcmg"
+    assert cli.main(["verify", "--routine", "potrs", "--n", "8", "--tile", "2", "--devices", "2", "--matrix", "diag",
+                     "--result-out", str(out_path)]) == 0
+    x = read_matrix(out_path)
+    assert x.shape == (8, 1) and np.max(np.abs(x[:, 0] - 1.0 / np.arange(1.0, 9.0))) <= 1e-15
+    rhs = tmp_path / "b.bcmg"
+    write_matrix(rhs, np.asfortranarray(2.0 * np.ones((8, 1))))
+    assert cli.main(["verify", "--routine", "potrs", "--n", "8", "--tile", "4", "--matrix", "diag",
+                     "--rhs", str(rhs)]) == 0
+    w_path = tmp_path / "w.bcmg"
+    assert cli.main(["verify", "--routine", "syevd", "--n", "6", "--tile", "2", "--devices", "2", "--matrix", "diag",
+                     "--eigenvalues-out", str(w_path)]) == 0
+    assert np.allclose(read_matrix(w_path)[:, 0], np.arange(1.0, 7.0), atol=1e-12)
+    a_path = tmp_path / "a.bcmg"
+    assert cli.main(["gen", "--kind", "random_spd", "--n", "40", "--dtype", "f32", "--out", str(a_path)]) == 0
+    assert cli.main(["verify", "--routine", "syevd", "--matrix", f"file:{a_path}", "--tile", "8"]) == 0
+    capsys.readouterr()
