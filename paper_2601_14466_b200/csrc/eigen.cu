@@ -18,7 +18,7 @@
 //      host, O(n^2) without vectors; its plane rotations are recorded and
 //      replayed on the GPU over the rows of Z (one thread per row);
 //   4. back-transformation with the stored reflectors in reverse
-//      (solvers.py:884-897), blocked 64 reflectors at a time in compact WY form
+//      (solvers.py:884-897), blocked 256 reflectors at a time in compact WY form
 //      (Q_blk = I - V T V^H, T from the forward recurrence): three GEMMs per
 //      block instead of 64 rank-1 sweeps over Z;
 //   5. phase normalisation (largest-magnitude component real and positive,
@@ -27,6 +27,7 @@
 // Every reduction has a fixed order: two runs give identical bits
 // (reference test_solvers.py:260-271).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <numeric>
@@ -39,7 +40,8 @@
 namespace bcmg {
 namespace {
 
-constexpr int ET = 64;      // symv tile / WY block width
+constexpr int ET = 64;      // symv tile
+constexpr int WY = 256;     // reflectors per compact-WY block of the back-transformation
 constexpr int RT = 256;     // threads of the row-parallel kernels
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -148,40 +150,149 @@ __global__ void eig_phase_scatter(const X* Z, int64_t n, ShardMap m) {
 }
 
 // ---------------------------------------------------------------- tridiagonalisation
-// A[c:, c] -= U[c:, :jj] conj(W[c, :jj]) + W[c:, :jj] conj(U[c, :jj])  (solvers.py:705-709)
+// y = sym(A[c0:, c0:]) v, lower-triangle storage (solvers.py:729-745): one CTA
+// per 64x64 tile (bi >= bj) of the trailing lower triangle; the tile's row
+// products go to P1[bj][rows], its conjugate-transposed column products
+// (strictly below the diagonal) to P2[bi][cols]; eig_symv_reduce sums them in
+// a fixed order.
 template <class X>
-__global__ void eig_panel_update(X* A, int64_t n, int64_t c, const X* U, const X* W, int jj) {
-  const int64_t i = c + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double2 s1 = zero2(), s2 = zero2();
-  for (int k = 0; k < jj; ++k) {
-    s1 = cadd(s1, cmulc(to_c(U[i + k * n]), to_c(W[c + k * n])));
-    s2 = cadd(s2, cmulc(to_c(W[i + k * n]), to_c(U[c + k * n])));
+__global__ void __launch_bounds__(256) eig_symv(const X* A, int64_t n, int64_t c0, const X* v, X* P1, X* P2,
+                                               int64_t ntri, const X* U, const X* W, int jj, X* t) {
+  if ((int64_t)blockIdx.x >= ntri) {  // t[k] = (W^H v)[k], t[jj + k] = (U^H v)[k]
+    __shared__ double2 dred[32];
+    const int b = (int)(blockIdx.x - ntri);
+    const X* M = b < jj ? W + (int64_t)b * n : U + (int64_t)(b - jj) * n;
+    double2 acc = zero2();
+    for (int64_t i = c0 + threadIdx.x; i < n; i += blockDim.x) acc = cadd(acc, cmul(cconj(to_c(M[i])), to_c(v[i])));
+    acc = block_sum(acc, dred);
+    if (threadIdx.x == 0) t[b] = from_c<X>(acc);
+    return;
   }
-  A[i + c * n] = from_c<X>(csub(to_c(A[i + c * n]), cadd(s1, s2)));
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  X* sm = reinterpret_cast<X*>(sm_raw);  // 64 x 65, column-major tile
+  __shared__ double2 vr[ET], vc[ET], half[2][2][ET];
+  const int64_t b = blockIdx.x;
+  int64_t bi = (int64_t)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
+  while (bi * (bi + 1) / 2 > b) --bi;
+  while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
+  const int64_t bj = b - bi * (bi + 1) / 2;
+  const int64_t r0 = c0 + bi * ET, q0 = c0 + bj * ET;
+  const int tid = threadIdx.x;
+  X ld[ET * ET / 256];
+#pragma unroll
+  for (int q = 0; q < ET * ET / 256; ++q) {  // all loads in flight, then stage
+    const int e = tid + q * 256, il = e % ET, jl = e / ET;
+    const int64_t i = r0 + il, j = q0 + jl;
+    ld[q] = (i < n && j < n) ? A[i + j * n] : from_c<X>(zero2());
+  }
+#pragma unroll
+  for (int q = 0; q < ET * ET / 256; ++q) {
+    const int e = tid + q * 256;
+    sm[(e / ET) * (ET + 1) + e % ET] = ld[q];
+  }
+  if (tid < ET) vc[tid] = q0 + tid < n ? to_c(v[q0 + tid]) : zero2();
+  else if (tid < 2 * ET) vr[tid - ET] = r0 + tid - ET < n ? to_c(v[r0 + tid - ET]) : zero2();
+  __syncthreads();
+  const bool diag = bi == bj;
+  const int part = tid >> 7, h = (tid >> 6) & 1, x = tid & 63;
+  double2 acc = zero2();
+  if (part == 0) {  // row x, columns 32h .. 32h+31
+    for (int jl = 32 * h; jl < 32 * h + 32; ++jl)
+      if (!diag || jl <= x) acc = cadd(acc, cmul(to_c(sm[jl * (ET + 1) + x]), vc[jl]));
+  } else {  // column x, rows 32h .. 32h+31 (strictly below the diagonal on diagonal tiles)
+    for (int il = 32 * h; il < 32 * h + 32; ++il)
+      if (!diag || il > x) acc = cadd(acc, cmul(cconj(to_c(sm[x * (ET + 1) + il])), vr[il]));
+  }
+  half[part][h][x] = acc;
+  __syncthreads();
+  if (tid < ET) {
+    if (r0 + tid < n) P1[bj * n + r0 + tid] = from_c<X>(cadd(half[0][0][tid], half[0][1][tid]));
+  } else if (tid < 2 * ET) {
+    const int jl = tid - ET;
+    if (q0 + jl < n) P2[bi * n + q0 + jl] = from_c<X>(cadd(half[1][0][jl], half[1][1][jl]));
+  }
 }
 
-// d[c] = Re A[c, c]; reflector of x = A[c+1:, c] (solvers.py:600-623):
-// v (v[0] = 1) into vbuf[c+1:] and into A[c+1:, c] (kept for the
-// back-transformation), tau[c], e[c] = beta.
+// ---- fused per-column kernels (3 launches per column).  Grid-wide steps use
+// the last-block pattern: every block publishes its partial, the block that
+// takes the last ticket reduces them in a fixed order (same bits every run)
+// and does the serial tail; it also re-arms the ticket counter.
+__device__ __forceinline__ bool last_block(unsigned* counter) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+
 template <class X>
-__global__ void __launch_bounds__(1024) eig_house(X* A, int64_t n, int64_t c, X* vbuf, X* tau, double* dd, double* ee) {
-  __shared__ double2 red[32];
+__device__ __forceinline__ double2 ldcg_c(const X* p) {
+  if constexpr (sizeof(X) == 16) {
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+    return v;
+  } else {
+    return make_double2(__ldcg(reinterpret_cast<const double*>(p)), 0.0);
+  }
+}
+
+// K1: lazy panel-column update A[c:, c] -= U conj(W[c]) + W conj(U[c])
+// (solvers.py:705-709), then -- in the last block -- d[c] and the reflector of
+// A[c+1:, c] (solvers.py:600-623, 712-716).
+template <class X>
+__global__ void __launch_bounds__(256) eig_col_prep(X* A, int64_t n, int64_t c, const X* U, const X* W, int jj,
+                                                     X* vbuf, X* tau, double* dd, double* ee, double* npart,
+                                                     unsigned* counter) {
+  __shared__ double2 sred[32];
+  __shared__ double wsq[8];
   __shared__ double2 den;
   __shared__ int trivial;
-  if (threadIdx.x == 0) dd[c] = to_c(A[c + c * n]).x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // one warp per row, lanes over k
+  const int64_t i = c + blockIdx.x * 8 + w;
+  double2 s = zero2();
+  if (i < n)
+    for (int k = lane; k < jj; k += 32)
+      s = cadd(s, cadd(cmulc(to_c(U[i + k * n]), to_c(W[c + k * n])), cmulc(to_c(W[i + k * n]), to_c(U[c + k * n]))));
+  for (int o = 16; o > 0; o >>= 1) {
+    s.x += __shfl_down_sync(0xffffffffu, s.x, o);
+    s.y += __shfl_down_sync(0xffffffffu, s.y, o);
+  }
+  if (lane == 0) {
+    double sq = 0.0;
+    if (i < n) {
+      X val = A[i + c * n];
+      if (jj) {
+        val = from_c<X>(csub(to_c(val), s));
+        A[i + c * n] = val;
+      }
+      if (i >= c + 2) {
+        const double2 q = to_c(val);
+        sq = q.x * q.x + q.y * q.y;
+      }
+    }
+    wsq[w] = sq;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sq = 0.0;
+    for (int q = 0; q < 8; ++q) sq += wsq[q];
+    npart[blockIdx.x] = sq;
+  }
+  if (!last_block(counter)) return;
+  if (threadIdx.x == 0) {
+    *counter = 0u;
+    dd[c] = ldcg_c(A + c + c * n).x;
+  }
   const int64_t L = n - c - 1;
   if (L <= 0) return;
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) acc += __ldcg(npart + b);
+  const double tot = block_sum(make_double2(acc, 0.0), sred).x;
   X* x = A + (c + 1) + c * n;
-  double s = 0.0;
-  for (int64_t i = 1 + threadIdx.x; i < L; i += blockDim.x) {
-    const double2 v = to_c(x[i]);
-    s += v.x * v.x + v.y * v.y;
-  }
-  const double tot = block_sum(make_double2(s, 0.0), red).x;
   if (threadIdx.x == 0) {
     const double tail = sqrt(tot);
-    const double2 alpha = to_c(x[0]);
+    const double2 alpha = ldcg_c(x);
     double2 t;
     double beta;
     if (tail == 0.0 && alpha.y == 0.0) {
@@ -201,122 +312,75 @@ __global__ void __launch_bounds__(1024) eig_house(X* A, int64_t n, int64_t c, X*
   __syncthreads();
   const int triv = trivial;
   const double2 dn = den;
-  for (int64_t i = threadIdx.x; i < L; i += blockDim.x) {
+#pragma unroll 4
+  for (int64_t r = threadIdx.x; r < L; r += blockDim.x) {
     double2 v;
-    if (i == 0) v = make_double2(1.0, 0.0);
+    if (r == 0) v = make_double2(1.0, 0.0);
     else if (triv) v = zero2();
-    else v = cdiv(to_c(x[i]), dn);
+    else v = cdiv(ldcg_c(x + r), dn);
     const X vx = from_c<X>(v);
-    vbuf[c + 1 + i] = vx;
-    x[i] = vx;
+    vbuf[c + 1 + r] = vx;
+    x[r] = vx;
   }
 }
 
-// y = sym(A[c0:, c0:]) v, lower-triangle storage (solvers.py:729-745): one CTA
-// per 64x64 tile (bi >= bj) of the trailing lower triangle; the tile's row
-// products go to P1[bj][rows], its conjugate-transposed column products
-// (strictly below the diagonal) to P2[bi][cols]; eig_symv_reduce sums them in
-// a fixed order.
+// K3: y = sum of the symv partials minus U t[:jj] + W t[jj:] (solvers.py:746-750),
+// then -- in the last block -- sigma = |tau|^2/2 v^H y and the panel columns
+// U[:, jj] = v, W[:, jj] = tau y - sigma v (solvers.py:751-754).
 template <class X>
-__global__ void __launch_bounds__(128) eig_symv(const X* A, int64_t n, int64_t c0, const X* v, X* P1, X* P2) {
-  extern __shared__ double2 sm[];  // 64 x 65
-  __shared__ double2 vr[ET], vc[ET];
-  const int64_t b = blockIdx.x;
-  int64_t bi = (int64_t)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
-  while (bi * (bi + 1) / 2 > b) --bi;
-  while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
-  const int64_t bj = b - bi * (bi + 1) / 2;
-  const int64_t r0 = c0 + bi * ET, q0 = c0 + bj * ET;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < ET * ET; e += blockDim.x) {
-    const int il = e % ET, jl = e / ET;
-    const int64_t i = r0 + il, j = q0 + jl;
-    sm[jl * (ET + 1) + il] = (i < n && j < n) ? to_c(A[i + j * n]) : zero2();
-  }
-  if (tid < ET) vc[tid] = q0 + tid < n ? to_c(v[q0 + tid]) : zero2();
-  else vr[tid - ET] = r0 + tid - ET < n ? to_c(v[r0 + tid - ET]) : zero2();
-  __syncthreads();
-  const bool diag = bi == bj;
-  if (tid < ET) {
-    const int il = tid;
-    double2 acc = zero2();
-    for (int jl = 0; jl < ET; ++jl)
-      if (!diag || jl <= il) acc = cadd(acc, cmul(sm[jl * (ET + 1) + il], vc[jl]));
-    if (r0 + il < n) P1[bj * n + r0 + il] = from_c<X>(acc);
-  } else {
-    const int jl = tid - ET;
-    double2 acc = zero2();
-    for (int il = 0; il < ET; ++il)
-      if (!diag || il > jl) acc = cadd(acc, cmul(cconj(sm[jl * (ET + 1) + il]), vr[il]));
-    if (q0 + jl < n) P2[bi * n + q0 + jl] = from_c<X>(acc);
-  }
-}
-
-template <class X>
-__global__ void eig_symv_reduce(const X* P1, const X* P2, int64_t n, int64_t c0, int64_t nb, X* y) {
-  const int64_t i = c0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t I = (i - c0) / ET;
-  double2 acc = zero2();
-  for (int64_t t = 0; t <= I; ++t) acc = cadd(acc, to_c(P1[t * n + i]));
-  for (int64_t t = I; t < nb; ++t) acc = cadd(acc, to_c(P2[t * n + i]));
-  y[i] = from_c<X>(acc);
-}
-
-// t[k] = (W^H v)[k], t[jj + k] = (U^H v)[k] over rows c0..n-1
-template <class X>
-__global__ void __launch_bounds__(RT) eig_dots(const X* U, const X* W, int64_t n, int64_t c0, int jj, const X* v, X* t) {
-  __shared__ double2 red[32];
-  const int b = blockIdx.x;
-  const X* M = b < jj ? W + (int64_t)b * n : U + (int64_t)(b - jj) * n;
-  double2 acc = zero2();
-  for (int64_t i = c0 + threadIdx.x; i < n; i += blockDim.x) acc = cadd(acc, cmul(cconj(to_c(M[i])), to_c(v[i])));
-  acc = block_sum(acc, red);
-  if (threadIdx.x == 0) t[b] = from_c<X>(acc);
-}
-
-// y[c0:] -= U t[:jj] + W t[jj:]  (solvers.py:746-750) and per-block partials of v^H y
-template <class X>
-__global__ void __launch_bounds__(RT) eig_corr(const X* U, const X* W, int64_t n, int64_t c0, int jj, const X* t, X* y,
-                                               const X* v, double2* part) {
-  __shared__ double2 red[32];
-  const int64_t i = c0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  double2 contrib = zero2();
-  if (i < n) {
-    double2 yi = to_c(y[i]);
-    if (jj) {
-      double2 s1 = zero2(), s2 = zero2();
-      for (int k = 0; k < jj; ++k) {
-        s1 = cadd(s1, cmul(to_c(U[i + (int64_t)k * n]), to_c(t[k])));
-        s2 = cadd(s2, cmul(to_c(W[i + (int64_t)k * n]), to_c(t[jj + k])));
-      }
-      yi = csub(yi, cadd(s1, s2));
-      y[i] = from_c<X>(yi);
-    }
-    contrib = cmul(cconj(to_c(v[i])), yi);
-  }
-  contrib = block_sum(contrib, red);
-  if (threadIdx.x == 0) part[blockIdx.x] = contrib;
-}
-
-// sigma = |tau|^2 / 2 * v^H y; U[:, jj] = v, W[:, jj] = tau y - sigma v (solvers.py:751-754)
-template <class X>
-__global__ void __launch_bounds__(RT) eig_fin(const X* v, const X* y, X* U, X* W, int64_t n, int64_t c0, int jj,
-                                              const X* tau, int64_t c, const double2* part, int nparts) {
+__global__ void __launch_bounds__(256) eig_col_finish(const X* P1, const X* P2, int64_t n, int64_t c0, int64_t nb,
+                                                       X* U, X* W, int jj, const X* t, X* y, const X* v,
+                                                       const X* tau, int64_t c, double2* part, unsigned* counter) {
+  __shared__ double2 sred[32];
   __shared__ double2 sig;
+  __shared__ double2 wc[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // one warp per row
+  const int64_t i = c0 + blockIdx.x * 8 + w;
+  double2 s = zero2(), corr = zero2();
+  if (i < n) {
+    const int64_t I = (i - c0) / ET;
+    for (int64_t q = lane; q <= I; q += 32) s = cadd(s, to_c(P1[q * n + i]));
+    for (int64_t q = I + lane; q < nb; q += 32) s = cadd(s, to_c(P2[q * n + i]));
+    for (int k = lane; k < jj; k += 32)
+      corr = cadd(corr, cadd(cmul(to_c(U[i + (int64_t)k * n]), to_c(t[k])),
+                             cmul(to_c(W[i + (int64_t)k * n]), to_c(t[jj + k]))));
+  }
+  double2 yi = csub(s, corr);
+  for (int o = 16; o > 0; o >>= 1) {
+    yi.x += __shfl_down_sync(0xffffffffu, yi.x, o);
+    yi.y += __shfl_down_sync(0xffffffffu, yi.y, o);
+  }
+  if (lane == 0) {
+    double2 contrib = zero2();
+    if (i < n) {
+      const X yx = from_c<X>(yi);
+      y[i] = yx;
+      contrib = cmul(cconj(to_c(v[i])), to_c(yx));
+    }
+    wc[w] = contrib;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 tot = zero2();
+    for (int q = 0; q < 8; ++q) tot = cadd(tot, wc[q]);
+    part[blockIdx.x] = tot;
+  }
+  if (!last_block(counter)) return;
+  if (threadIdx.x == 0) *counter = 0u;
   const double2 tu = to_c(tau[c]);
   if (tu.x == 0.0 && tu.y == 0.0) return;  // reflection skipped (solvers.py:718)
-  if (threadIdx.x == 0) {
-    double2 vd = zero2();
-    for (int p = 0; p < nparts; ++p) vd = cadd(vd, part[p]);
-    sig = cscl(vd, 0.5 * (tu.x * tu.x + tu.y * tu.y));
-  }
+  double2 acc = zero2();
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) acc = cadd(acc, ldcg_c(part + b));
+  acc = block_sum(acc, sred);
+  if (threadIdx.x == 0) sig = cscl(acc, 0.5 * (tu.x * tu.x + tu.y * tu.y));
   __syncthreads();
-  const int64_t i = c0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double2 vi = to_c(v[i]);
-  U[i + (int64_t)jj * n] = v[i];
-  W[i + (int64_t)jj * n] = from_c<X>(csub(cmul(tu, to_c(y[i])), cmul(sig, vi)));
+  const double2 sg = sig;
+#pragma unroll 4
+  for (int64_t r = c0 + threadIdx.x; r < n; r += blockDim.x) {
+    const double2 vi = to_c(v[r]);
+    U[r + (int64_t)jj * n] = v[r];
+    W[r + (int64_t)jj * n] = from_c<X>(csub(cmul(tu, ldcg_c(y + r)), cmul(sg, vi)));
+  }
 }
 
 // ---------------------------------------------------------------- tridiagonal eigenvectors
@@ -416,7 +480,7 @@ __global__ void eig_permute(const double* Z, const int64_t* order, X* Zx, int64_
 // Forward compact-WY factor of kb reflectors: T upper, T[j][j] = tau_j,
 // T[:j, j] = -tau_j T[:j, :j] G[:j, j], G = V^H V (LAPACK larft, forward / columnwise).
 template <class X>
-__global__ void __launch_bounds__(ET) eig_larft(const X* G, const X* tau, int kb, X* Tm) {
+__global__ void __launch_bounds__(WY) eig_larft(const X* G, const X* tau, int kb, X* Tm) {
   const int i = threadIdx.x;  // row of T, in global memory (kb x kb, ld kb)
   if (i < kb)
     for (int j = 0; j < kb; ++j) Tm[i + j * kb] = from_c<X>(zero2());
@@ -437,6 +501,15 @@ __global__ void __launch_bounds__(ET) eig_larft(const X* G, const X* tau, int kb
 // ---------------------------------------------------------------- host QL
 // Implicit-shift QL on the tridiagonal (d, e) exactly as solvers.py:783-843,
 // without the vectors: the rotations of each bulge-chasing sweep are recorded.
+// hypot through one correctly rounded sqrt when neither square can overflow or
+// lose precision to underflow (within 1 ulp of hypot, ~4x cheaper); the
+// library hypot otherwise
+inline double fast_hypot(double a, double b) {
+  const double m = std::fmax(std::fabs(a), std::fabs(b));
+  if (m < 1e150 && m > 1e-140) return std::sqrt(a * a + b * b);
+  return std::hypot(a, b);
+}
+
 struct QLRecord {
   std::vector<double2> cs;
   std::vector<int64_t> off{0}, top;
@@ -471,7 +544,7 @@ void tridiag_ql(std::vector<double>& d, const std::vector<double>& e_in, QLRecor
       rec.top.push_back(m - 1);
       for (int64_t i = m - 1; i >= l; --i) {
         const double f = s * e[i], b = c * e[i];
-        r = std::hypot(f, g);
+        r = fast_hypot(f, g);
         e[i + 1] = r;
         if (r == 0.0) {
           d[i + 1] -= p;
@@ -516,7 +589,7 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
   cudaStream_t st = ss.user;
   const size_t es = sizeof(X);
   const int64_t nb = (n + ET - 1) / ET;
-  const int64_t nparts_max = (n + RT - 1) / RT;
+  const int64_t nparts_max = (n + 7) / 8;  // eig_col_prep / eig_col_finish blocks (one warp per row)
 
   // ---- workspace: everything reserved before any data moves (OUT_OF_MEMORY first)
   DevBuf* wb = ss.eig;
@@ -526,8 +599,8 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
   wb[3].ensure((size_t)2 * n * T * es);           // U | W panels
   wb[4].ensure((size_t)2 * nb * n * es);          // symv partials P1 | P2
   const size_t small = (size_t)(2 * n + 2 * T + n) * es + (size_t)(nparts_max + 1) * sizeof(double2) +
-                       (size_t)2 * n * sizeof(double) + (size_t)2 * ET * ET * es + (size_t)2 * ET * n * es +
-                       (size_t)n * sizeof(int64_t) + 256;
+                       (size_t)2 * n * sizeof(double) + (size_t)2 * WY * WY * es + (size_t)2 * WY * n * es +
+                       (size_t)n * sizeof(int64_t) + (size_t)nparts_max * sizeof(double) + 512;
   wb[5].ensure(small);
   X* A = static_cast<X*>(wb[0].p);
   double* Zr = static_cast<double*>(wb[1].p);
@@ -549,11 +622,13 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
   double2* part = reinterpret_cast<double2*>(carve((nparts_max + 1) * sizeof(double2)));
   double* dd = reinterpret_cast<double*>(carve(n * sizeof(double)));
   double* ee = reinterpret_cast<double*>(carve(n * sizeof(double)));
-  X* G = reinterpret_cast<X*>(carve(ET * ET * es));
-  X* Tm = reinterpret_cast<X*>(carve(ET * ET * es));
-  X* X1 = reinterpret_cast<X*>(carve(ET * n * es));
-  X* X2 = reinterpret_cast<X*>(carve(ET * n * es));
+  X* G = reinterpret_cast<X*>(carve(WY * WY * es));
+  X* Tm = reinterpret_cast<X*>(carve(WY * WY * es));
+  X* X1 = reinterpret_cast<X*>(carve(WY * n * es));
+  X* X2 = reinterpret_cast<X*>(carve(WY * n * es));
   int64_t* order_d = reinterpret_cast<int64_t*>(carve(n * sizeof(int64_t)));
+  double* npart = reinterpret_cast<double*>(carve(nparts_max * sizeof(double)));
+  unsigned* tickets = reinterpret_cast<unsigned*>(carve(2 * sizeof(unsigned)));
 
   ShardMap map{};
   map.D = ndev;
@@ -581,35 +656,27 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
   BCMG_CHECK_LAUNCH();
   BCMG_CUDA(cudaMemsetAsync(tau, 0, n * es, st));
   BCMG_CUDA(cudaMemsetAsync(ee, 0, n * sizeof(double), st));
+  BCMG_CUDA(cudaMemsetAsync(tickets, 0, 2 * sizeof(unsigned), st));
 
   // ---- 2. blocked Householder tridiagonalisation (solvers.py:666-780)
-  const size_t symv_smem = (size_t)ET * (ET + 1) * sizeof(double2);
+  const size_t symv_smem = (size_t)ET * (ET + 1) * sizeof(X);
   BCMG_CUDA(cudaFuncSetAttribute(eig_symv<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)symv_smem));
   for (int64_t start = 0; start < n; start += T) {
     const int64_t stop = std::min(start + T, n), tc = stop - start;
     BCMG_CUDA(cudaMemsetAsync(U, 0, (size_t)2 * n * T * es, st));
     for (int64_t jj = 0; jj < tc; ++jj) {
       const int64_t c = start + jj, c0 = c + 1;
-      if (jj) {
-        eig_panel_update<X><<<blocks_for(n - c, RT), RT, 0, st>>>(A, n, c, U, W, (int)jj);
-        BCMG_CHECK_LAUNCH();
-      }
-      eig_house<X><<<1, 1024, 0, st>>>(A, n, c, vbuf, tau, dd, ee);
+      const unsigned g1 = blocks_for(n - c, 8);
+      eig_col_prep<X><<<g1, 256, 0, st>>>(A, n, c, U, W, (int)jj, vbuf, tau, dd, ee, npart, tickets);
       BCMG_CHECK_LAUNCH();
       if (c == n - 1) continue;
-      const int64_t L = n - c0, nbt = (L + ET - 1) / ET;
-      eig_symv<X><<<(unsigned)(nbt * (nbt + 1) / 2), 128, symv_smem, st>>>(A, n, c0, vbuf, P1, P2);
+      const int64_t L = n - c0, nbt = (L + ET - 1) / ET, ntri = nbt * (nbt + 1) / 2;
+      eig_symv<X><<<(unsigned)(ntri + 2 * jj), 256, symv_smem, st>>>(A, n, c0, vbuf, P1, P2, ntri, U, W, (int)jj,
+                                                                     tbuf);
       BCMG_CHECK_LAUNCH();
-      eig_symv_reduce<X><<<blocks_for(L, RT), RT, 0, st>>>(P1, P2, n, c0, nbt, ybuf);
-      BCMG_CHECK_LAUNCH();
-      if (jj) {
-        eig_dots<X><<<(unsigned)(2 * jj), RT, 0, st>>>(U, W, n, c0, (int)jj, vbuf, tbuf);
-        BCMG_CHECK_LAUNCH();
-      }
-      const unsigned np = blocks_for(L, RT);
-      eig_corr<X><<<np, RT, 0, st>>>(U, W, n, c0, (int)jj, tbuf, ybuf, vbuf, part);
-      BCMG_CHECK_LAUNCH();
-      eig_fin<X><<<np, RT, 0, st>>>(vbuf, ybuf, U, W, n, c0, (int)jj, tau, c, part, (int)np);
+      const unsigned np = blocks_for(L, 8);
+      eig_col_finish<X><<<np, 256, 0, st>>>(P1, P2, n, c0, nbt, U, W, (int)jj, tbuf, ybuf, vbuf, tau, c, part,
+                                            tickets + 1);
       BCMG_CHECK_LAUNCH();
     }
     if (stop >= n) continue;
@@ -685,10 +752,12 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
     rec.top.clear();
   };
   rec.cs.reserve(cap_rot);
+  const auto ql0 = std::chrono::steady_clock::now();
   tridiag_ql(d, e, rec, [&] {
     if ((int64_t)rec.top.size() >= CH) flush();
   });
   flush();
+  const double host_ql_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ql0).count();
   std::vector<int64_t> order(n);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return d[a] < d[b]; });
@@ -698,10 +767,10 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
   BCMG_CHECK_LAUNCH();
   pmark(3);
 
-  // ---- 4. back-transformation, 64 reflectors per compact-WY block, last block first
+  // ---- 4. back-transformation, WY reflectors per compact-WY block, last block first
   if (n >= 2) {
-    for (int64_t c0 = ((n - 2) / ET) * ET; c0 >= 0; c0 -= ET) {
-      const int64_t c1 = std::min<int64_t>(c0 + ET, n - 1), kb = c1 - c0, r0 = c0 + 1, K = n - r0;
+    for (int64_t c0 = ((n - 2) / WY) * WY; c0 >= 0; c0 -= WY) {
+      const int64_t c1 = std::min<int64_t>(c0 + WY, n - 1), kb = c1 - c0, r0 = c0 + 1, K = n - r0;
       const X* V = A + r0 + c0 * n;  // unit lower trapezoid: V(i, k) valid for i >= k
       Operand vN = opA(V, n, OP_N), vC = opA(V, n, OP_C), vB = opB(V, n, OP_N);
       vN.mask = vC.mask = vB.mask = 1;
@@ -712,7 +781,7 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
       eg.alpha = 1.0;
       eg.beta = 0.0;
       gemm(dtw, kb, kb, K, vC, vB, eg, nullptr, st);  // G = V^H V
-      eig_larft<X><<<1, ET, 0, st>>>(G, tau + c0, (int)kb, Tm);
+      eig_larft<X><<<1, WY, 0, st>>>(G, tau + c0, (int)kb, Tm);
       BCMG_CHECK_LAUNCH();
       Epilogue e1{};
       e1.C = X1;
@@ -744,9 +813,9 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
     BCMG_CUDA(cudaEventSynchronize(pe[5]));
     float ms[5];
     for (int k = 0; k < 5; ++k) BCMG_CUDA(cudaEventElapsedTime(&ms[k], pe[k], pe[k + 1]));
-    fprintf(stderr, "[syevd n=%lld T=%lld] tridiag %.1f ms, host QL + overlapped rotation replay %.1f ms (%lld rotations, "
-            "%lld sweeps), permute %.1f ms, back-transform %.1f ms, phase+scatter %.1f ms\n", (long long)n, (long long)T, ms[0],
-            ms[1], (long long)nrot, (long long)nsw, ms[2], ms[3], ms[4]);
+    fprintf(stderr, "[syevd n=%lld T=%lld] tridiag %.1f ms, host QL + overlapped rotation replay %.1f ms (host loop %.1f ms, "
+            "%lld rotations, %lld sweeps), permute %.1f ms, back-transform %.1f ms, phase+scatter %.1f ms\n", (long long)n, (long long)T, ms[0],
+            ms[1], host_ql_ms, (long long)nrot, (long long)nsw, ms[2], ms[3], ms[4]);
     for (auto& e : pe) cudaEventDestroy(e);
   }
   std::sort(d.begin(), d.end());  // == d[order] (stable order of equal keys is immaterial for values)
