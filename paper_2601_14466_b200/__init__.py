@@ -54,13 +54,13 @@ from .solvers import (
     redistribute_in,
     redistribute_out,
     solve_positive_definite,
-    syevd,
     workspace_nbytes,
     write_array,
 )
 from .solvers import potri as potri_factored
 from .solvers import potrs as potrs_factored
-from .api import P, last_timings, make_mesh, potri, potrs
+from .solvers import syevd as syevd_cyclic
+from .api import P, last_timings, make_mesh, potri, potrs, syevd
 
 __all__ = [
     "ConcurrentCallError", "ConvergenceError", "DescriptorError", "ElementType", "MatrixDescriptor", "NotPositiveDefiniteError",
@@ -71,6 +71,6 @@ __all__ = [
     "segment_plan_info", "serialize_plan",
     "DeviceMesh", "DistributedMatrix", "FactorizationResult", "Timings", "create_distributed", "gather_array",
     "invert_positive_definite", "potrf", "potrs_factored", "potri_factored", "redistribute_in", "redistribute_out",
-    "solve_positive_definite", "syevd", "eigh_hermitian", "workspace_nbytes", "write_array",
-    "P", "make_mesh", "potrs", "potri", "last_timings",
+    "solve_positive_definite", "syevd_cyclic", "eigh_hermitian", "workspace_nbytes", "write_array",
+    "P", "make_mesh", "potrs", "potri", "syevd", "last_timings",
 ]

@@ -168,6 +168,39 @@ def potri(A, T_A: int, mesh: DeviceMesh | None = None, in_specs=None, *, overwri
     return A
 
 
+def syevd(A, T_A: int, mesh: DeviceMesh | None = None, in_specs=None, *, return_eigenvectors: bool = True,
+          overwrite_a: bool = False):
+    """Eigenvalues (ascending) and eigenvectors of a Hermitian matrix
+    (cusolverMgSyevd semantics; reference eigh_hermitian,
+    solvers.py:1019-1043).  Returns (w, V) -- or w alone -- on A's device; V is
+    row-major with V[:, j] the eigenvector of w[j], its first largest-magnitude
+    component real and positive.  Single-process meshes.
+
+    The row-major buffer of A is the column-major conj(A) (Hermitian), so the
+    native call computes the eigenvectors of conj(A), which are conj(V) under
+    the same phase convention; V is that buffer conjugate-transposed."""
+    import torch
+
+    mesh = mesh or make_mesh()
+    _check_specs(in_specs, mesh, 1)
+    if mesh.world != 1:
+        raise DescriptorError("dimension-mismatch", "syevd runs single-process (DESIGN.md §3b)")
+    A, et, n = _prepare_a(A, mesh, overwrite_a)
+    validate_tile(TileSpec(int(T_A)), n)
+    real = torch.float32 if et in (ElementType.real32, ElementType.complex64) else torch.float64
+    w = torch.empty(n, dtype=real, device=mesh.torch_device)
+    info = C.c_int(0)
+    with mesh.coordinated():
+        rc = _lib.load().bcmg_syevd(mesh.session, mesh.stream_handle(), et.code, n, int(T_A), mesh.num_devices,
+                                    _shard_ptrs(A, mesh, n, int(T_A), et.width), C.c_void_p(w.data_ptr()), 0,
+                                    C.byref(info))
+    _raise_for(rc, info.value)
+    if not return_eigenvectors:
+        return w
+    V = A.t().conj() if et.is_complex else A.t()
+    return w, V.contiguous().resolve_conj()
+
+
 def last_timings(mesh: DeviceMesh) -> dict:
     """Device-side phase split (ms) of the last potrs/potri on ``mesh``."""
     ms = (C.c_float * 4)()

@@ -241,15 +241,15 @@ __device__ __forceinline__ double2 ldcg_c(const X* p) {
 // (solvers.py:705-709), then -- in the last block -- d[c] and the reflector of
 // A[c+1:, c] (solvers.py:600-623, 712-716).
 template <class X>
-__global__ void __launch_bounds__(256) eig_col_prep(X* A, int64_t n, int64_t c, const X* U, const X* W, int jj,
+__global__ void __launch_bounds__(1024) eig_col_prep(X* A, int64_t n, int64_t c, const X* U, const X* W, int jj,
                                                      X* vbuf, X* tau, double* dd, double* ee, double* npart,
                                                      unsigned* counter) {
   __shared__ double2 sred[32];
-  __shared__ double wsq[8];
+  __shared__ double wsq[32];
   __shared__ double2 den;
   __shared__ int trivial;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // one warp per row, lanes over k
-  const int64_t i = c + blockIdx.x * 8 + w;
+  const int64_t i = c + blockIdx.x * 32 + w;
   double2 s = zero2();
   if (i < n)
     for (int k = lane; k < jj; k += 32)
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256) eig_col_prep(X* A, int64_t n, int64_t c, 
   __syncthreads();
   if (threadIdx.x == 0) {
     double sq = 0.0;
-    for (int q = 0; q < 8; ++q) sq += wsq[q];
+    for (int q = 0; q < 32; ++q) sq += wsq[q];
     npart[blockIdx.x] = sq;
   }
   if (!last_block(counter)) return;
@@ -328,14 +328,14 @@ __global__ void __launch_bounds__(256) eig_col_prep(X* A, int64_t n, int64_t c, 
 // then -- in the last block -- sigma = |tau|^2/2 v^H y and the panel columns
 // U[:, jj] = v, W[:, jj] = tau y - sigma v (solvers.py:751-754).
 template <class X>
-__global__ void __launch_bounds__(256) eig_col_finish(const X* P1, const X* P2, int64_t n, int64_t c0, int64_t nb,
+__global__ void __launch_bounds__(1024) eig_col_finish(const X* P1, const X* P2, int64_t n, int64_t c0, int64_t nb,
                                                        X* U, X* W, int jj, const X* t, X* y, const X* v,
                                                        const X* tau, int64_t c, double2* part, unsigned* counter) {
   __shared__ double2 sred[32];
   __shared__ double2 sig;
-  __shared__ double2 wc[8];
+  __shared__ double2 wc[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;  // one warp per row
-  const int64_t i = c0 + blockIdx.x * 8 + w;
+  const int64_t i = c0 + blockIdx.x * 32 + w;
   double2 s = zero2(), corr = zero2();
   if (i < n) {
     const int64_t I = (i - c0) / ET;
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(256) eig_col_finish(const X* P1, const X* P2, 
   __syncthreads();
   if (threadIdx.x == 0) {
     double2 tot = zero2();
-    for (int q = 0; q < 8; ++q) tot = cadd(tot, wc[q]);
+    for (int q = 0; q < 32; ++q) tot = cadd(tot, wc[q]);
     part[blockIdx.x] = tot;
   }
   if (!last_block(counter)) return;
@@ -589,7 +589,7 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
   cudaStream_t st = ss.user;
   const size_t es = sizeof(X);
   const int64_t nb = (n + ET - 1) / ET;
-  const int64_t nparts_max = (n + 7) / 8;  // eig_col_prep / eig_col_finish blocks (one warp per row)
+  const int64_t nparts_max = (n + 31) / 32;  // eig_col_prep / eig_col_finish blocks (one warp per row)
 
   // ---- workspace: everything reserved before any data moves (OUT_OF_MEMORY first)
   DevBuf* wb = ss.eig;
@@ -666,16 +666,16 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
     BCMG_CUDA(cudaMemsetAsync(U, 0, (size_t)2 * n * T * es, st));
     for (int64_t jj = 0; jj < tc; ++jj) {
       const int64_t c = start + jj, c0 = c + 1;
-      const unsigned g1 = blocks_for(n - c, 8);
-      eig_col_prep<X><<<g1, 256, 0, st>>>(A, n, c, U, W, (int)jj, vbuf, tau, dd, ee, npart, tickets);
+      const unsigned g1 = blocks_for(n - c, 32);
+      eig_col_prep<X><<<g1, 1024, 0, st>>>(A, n, c, U, W, (int)jj, vbuf, tau, dd, ee, npart, tickets);
       BCMG_CHECK_LAUNCH();
       if (c == n - 1) continue;
       const int64_t L = n - c0, nbt = (L + ET - 1) / ET, ntri = nbt * (nbt + 1) / 2;
       eig_symv<X><<<(unsigned)(ntri + 2 * jj), 256, symv_smem, st>>>(A, n, c0, vbuf, P1, P2, ntri, U, W, (int)jj,
                                                                      tbuf);
       BCMG_CHECK_LAUNCH();
-      const unsigned np = blocks_for(L, 8);
-      eig_col_finish<X><<<np, 256, 0, st>>>(P1, P2, n, c0, nbt, U, W, (int)jj, tbuf, ybuf, vbuf, tau, c, part,
+      const unsigned np = blocks_for(L, 32);
+      eig_col_finish<X><<<np, 1024, 0, st>>>(P1, P2, n, c0, nbt, U, W, (int)jj, tbuf, ybuf, vbuf, tau, c, part,
                                             tickets + 1);
       BCMG_CHECK_LAUNCH();
     }
@@ -714,14 +714,20 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
     cudaEvent_t done[NSLOT] = {};
     cudaStream_t st;
     ~Ring() {
-      cudaStreamSynchronize(st);
-      if (host) cudaFreeHost(host);
+      cudaStreamSynchronize(st);  // the pinned slots are reused by the next call
       for (auto e : done)
         if (e) cudaEventDestroy(e);
     }
   } ring;
   ring.st = st;
-  BCMG_CUDA(cudaHostAlloc(&ring.host, NSLOT * slot_bytes, cudaHostAllocDefault));
+  if (ss.eig_host_bytes < NSLOT * slot_bytes) {  // session-owned, grow-only
+    if (ss.eig_host) BCMG_CUDA(cudaFreeHost(ss.eig_host));
+    ss.eig_host = nullptr;
+    ss.eig_host_bytes = 0;
+    BCMG_CUDA(cudaHostAlloc(&ss.eig_host, NSLOT * slot_bytes, cudaHostAllocDefault));
+    ss.eig_host_bytes = NSLOT * slot_bytes;
+  }
+  ring.host = ss.eig_host;
   for (auto& e : ring.done) BCMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   int64_t nrot = 0, nsw = 0, nflush = 0;
   QLRecord rec;

@@ -78,6 +78,8 @@ Session::~Session() {
   for (auto* b : {&panel[0], &panel[1], &panel_pb[0], &panel_pb[1], &dinv, &wdiag, &info_dev, &tmp, &acc, &plan_buf,
                   &stage_buf, &desc_buf, &embed_buf, &split_buf[0], &split_buf[1], &sig})
     b->release();
+  for (auto& b : eig) b.release();
+  if (eig_host) cudaFreeHost(eig_host);
   for (auto& e : ev_pool) cudaEventDestroy(e);
   for (auto& e : ev_time) cudaEventDestroy(e);
   for (auto& k : kstat)

@@ -126,6 +126,8 @@ struct Session {
   // (device, real type of dt), eigenvectors over the shards (cyclic or
   // contiguous layout); throws NO_CONVERGENCE
   DevBuf eig[7];
+  void* eig_host = nullptr;  // pinned staging of the QL rotation ring (grow-only)
+  size_t eig_host_bytes = 0;
   void syevd(int dt, int64_t n, int64_t T, int ndev, void* const* shards, bool cyclic, void* w);
 };
 

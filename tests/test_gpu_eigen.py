@@ -153,7 +153,7 @@ def test_cyclic_building_block(meshes):
     dm = bc.create_distributed(mesh, desc, bc.TileSpec(4))
     bc.write_array(mesh, dm, a)
     cyc = bc.redistribute_in(mesh, dm)
-    w, vecs = bc.syevd(mesh, cyc)
+    w, vecs = bc.syevd_cyclic(mesh, cyc)
     out = bc.redistribute_out(mesh, vecs)
     v = bc.gather_array(mesh, out)
     w2, v2, _ = bc.eigh_hermitian(mesh, a, bc.TileSpec(4))
@@ -168,4 +168,24 @@ def test_rejections(meshes):
     desc = bc.MatrixDescriptor(4, 4, bc.ElementType.real64, bc.Structure.general)
     dm = bc.create_distributed(mesh, desc, bc.TileSpec(2))
     with pytest.raises(bc.DescriptorError):
-        bc.syevd(mesh, bc.redistribute_in(mesh, dm))
+        bc.syevd_cyclic(mesh, bc.redistribute_in(mesh, dm))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.complex128, np.float32])
+def test_paper_api_row_sharded(meshes, dtype):
+    """jaxmg.syevd-style call on a row-major torch tensor:
+    the caller's A is untouched, V[:, j] is the eigenvector of w[j]."""
+    import torch
+
+    a = G["sep20_c128__a"] if np.dtype(dtype).kind == "c" else G["sep32_f64__a"]
+    a = a.astype(dtype)
+    n = a.shape[0]
+    At = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    keep = At.clone()
+    w, V = bc.syevd(At, T_A=4, mesh=meshes(1), in_specs=(bc.P("x", None),))
+    assert torch.equal(At, keep)
+    w_ref, v_ref = O.syevd_dense(a, 4)
+    eps = _eps(dtype)
+    assert np.max(np.abs(w.cpu().numpy() - w_ref)) <= 10 * n * eps * np.max(np.abs(w_ref))
+    assert np.max(np.abs(V.cpu().numpy() - v_ref)) <= 100 * n * eps
+    assert torch.equal(bc.syevd(At, T_A=4, mesh=meshes(1), return_eigenvectors=False), w)
