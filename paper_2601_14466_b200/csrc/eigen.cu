@@ -158,11 +158,14 @@ __global__ void eig_phase_scatter(const X* Z, int64_t n, ShardMap m) {
 template <class X>
 __global__ void __launch_bounds__(256) eig_symv(const X* A, int64_t n, int64_t c0, const X* v, X* P1, X* P2,
                                                int64_t ntri, const X* U, const X* W, int jj, X* t) {
-  if ((int64_t)blockIdx.x >= ntri) {  // t[k] = (W^H v)[k], t[jj + k] = (U^H v)[k]
+  // the first 2*jj blocks (dispatched first, so they overlap the tiles instead
+  // of trailing them): t[k] = (W^H v)[k], t[jj + k] = (U^H v)[k]
+  if ((int64_t)blockIdx.x < 2 * jj) {
     __shared__ double2 dred[32];
-    const int b = (int)(blockIdx.x - ntri);
+    const int b = (int)blockIdx.x;
     const X* M = b < jj ? W + (int64_t)b * n : U + (int64_t)(b - jj) * n;
     double2 acc = zero2();
+#pragma unroll 4
     for (int64_t i = c0 + threadIdx.x; i < n; i += blockDim.x) acc = cadd(acc, cmul(cconj(to_c(M[i])), to_c(v[i])));
     acc = block_sum(acc, dred);
     if (threadIdx.x == 0) t[b] = from_c<X>(acc);
@@ -171,7 +174,7 @@ __global__ void __launch_bounds__(256) eig_symv(const X* A, int64_t n, int64_t c
   extern __shared__ __align__(16) unsigned char sm_raw[];
   X* sm = reinterpret_cast<X*>(sm_raw);  // 64 x 65, column-major tile
   __shared__ double2 vr[ET], vc[ET], half[2][2][ET];
-  const int64_t b = blockIdx.x;
+  const int64_t b = blockIdx.x - 2 * jj;
   int64_t bi = (int64_t)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
   while (bi * (bi + 1) / 2 > b) --bi;
   while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
