@@ -199,12 +199,34 @@ __global__ void __launch_bounds__(256) eig_symv(const X* A, int64_t n, int64_t c
   const bool diag = bi == bj;
   const int part = tid >> 7, h = (tid >> 6) & 1, x = tid & 63;
   double2 acc = zero2();
-  if (part == 0) {  // row x, columns 32h .. 32h+31
-    for (int jl = 32 * h; jl < 32 * h + 32; ++jl)
-      if (!diag || jl <= x) acc = cadd(acc, cmul(to_c(sm[jl * (ET + 1) + x]), vc[jl]));
-  } else {  // column x, rows 32h .. 32h+31 (strictly below the diagonal on diagonal tiles)
-    for (int il = 32 * h; il < 32 * h + 32; ++il)
-      if (!diag || il > x) acc = cadd(acc, cmul(cconj(to_c(sm[x * (ET + 1) + il])), vr[il]));
+  if constexpr (!Traits<X>::cplx) {  // real: plain FMAs, branch-free off the diagonal
+    double a = 0.0;
+    if (part == 0) {  // row x, columns 32h .. 32h+31
+      const double* row = reinterpret_cast<const double*>(sm) + x;
+      if (!diag) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) a = fma(row[(32 * h + q) * (ET + 1)], vc[32 * h + q].x, a);
+      } else {
+        for (int jl = 32 * h; jl < 32 * h + 32 && jl <= x; ++jl) a = fma(row[jl * (ET + 1)], vc[jl].x, a);
+      }
+    } else {  // column x, rows 32h .. 32h+31 (strictly below the diagonal on diagonal tiles)
+      const double* col = reinterpret_cast<const double*>(sm) + x * (ET + 1);
+      if (!diag) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) a = fma(col[32 * h + q], vr[32 * h + q].x, a);
+      } else {
+        for (int il = max(32 * h, x + 1); il < 32 * h + 32; ++il) a = fma(col[il], vr[il].x, a);
+      }
+    }
+    acc.x = a;
+  } else {
+    if (part == 0) {  // row x, columns 32h .. 32h+31
+      for (int jl = 32 * h; jl < 32 * h + 32; ++jl)
+        if (!diag || jl <= x) acc = cadd(acc, cmul(to_c(sm[jl * (ET + 1) + x]), vc[jl]));
+    } else {  // column x, rows 32h .. 32h+31 (strictly below the diagonal on diagonal tiles)
+      for (int il = 32 * h; il < 32 * h + 32; ++il)
+        if (!diag || il > x) acc = cadd(acc, cmul(cconj(to_c(sm[x * (ET + 1) + il])), vr[il]));
+    }
   }
   half[part][h][x] = acc;
   __syncthreads();
@@ -514,7 +536,8 @@ inline double fast_hypot(double a, double b) {
 }
 
 struct QLRecord {
-  std::vector<double2> cs;
+  double2* cs = nullptr;  // rotations of the pending sweeps, written straight into a pinned slot
+  int64_t ncs = 0;
   std::vector<int64_t> off{0}, top;
 };
 template <class F>
@@ -562,11 +585,11 @@ void tridiag_ql(std::vector<double>& d, const std::vector<double>& e_in, QLRecor
         p = s * r;
         d[i + 1] = g + p;
         g = c * r - b;
-        rec.cs.push_back(make_double2(c, s));
+        rec.cs[rec.ncs++] = make_double2(c, s);
       }
-      if ((int64_t)rec.cs.size() == rec.off.back()) rec.top.pop_back();  // no rotation applied
+      if (rec.ncs == rec.off.back()) rec.top.pop_back();  // no rotation applied
       else {
-        rec.off.push_back((int64_t)rec.cs.size());
+        rec.off.push_back(rec.ncs);
         after_sweep();
       }
       if (!broke) {
@@ -732,17 +755,16 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
   }
   ring.host = ss.eig_host;
   for (auto& e : ring.done) BCMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  int64_t nrot = 0, nsw = 0, nflush = 0;
+  int64_t nrot = 0, nsw = 0;
+  int cur = 0;  // slot the host is writing
   QLRecord rec;
+  rec.cs = reinterpret_cast<double2*>(ring.host);
   auto flush = [&] {
-    const int64_t ns = (int64_t)rec.top.size(), nr = (int64_t)rec.cs.size();
+    const int64_t ns = (int64_t)rec.top.size(), nr = rec.ncs;
     if (!ns) return;
-    const int k = (int)(nflush++ % NSLOT);
-    BCMG_CUDA(cudaEventSynchronize(ring.done[k]));  // the slot's previous batch has run
-    char* hb = static_cast<char*>(ring.host) + k * slot_bytes;
-    char* db = static_cast<char*>(wb[6].p) + k * slot_bytes;
+    char* hb = static_cast<char*>(ring.host) + cur * slot_bytes;
+    char* db = static_cast<char*>(wb[6].p) + cur * slot_bytes;
     int64_t* hmeta = reinterpret_cast<int64_t*>(hb + cap_rot * sizeof(double2));
-    std::copy(rec.cs.begin(), rec.cs.end(), reinterpret_cast<double2*>(hb));
     std::copy(rec.off.begin(), rec.off.end(), hmeta);
     std::copy(rec.top.begin(), rec.top.end(), hmeta + ns + 1);
     BCMG_CUDA(cudaMemcpyAsync(db, hb, nr * sizeof(double2), cudaMemcpyHostToDevice, st));
@@ -753,14 +775,16 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
                                                             dmeta + ns + 1, s0, ns);
       BCMG_CHECK_LAUNCH();
     }
-    BCMG_CUDA(cudaEventRecord(ring.done[k], st));
+    BCMG_CUDA(cudaEventRecord(ring.done[cur], st));
     nrot += nr;
     nsw += ns;
-    rec.cs.clear();
+    cur = (cur + 1) % NSLOT;
+    BCMG_CUDA(cudaEventSynchronize(ring.done[cur]));  // that slot's previous batch has been copied and run
+    rec.cs = reinterpret_cast<double2*>(static_cast<char*>(ring.host) + cur * slot_bytes);
+    rec.ncs = 0;
     rec.off.assign(1, 0);
     rec.top.clear();
   };
-  rec.cs.reserve(cap_rot);
   const auto ql0 = std::chrono::steady_clock::now();
   tridiag_ql(d, e, rec, [&] {
     if ((int64_t)rec.top.size() >= CH) flush();
