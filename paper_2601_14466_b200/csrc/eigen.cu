@@ -14,13 +14,15 @@
 //      over the stale trailing lower triangle (tiled, deterministic two-pass
 //      reduction), the U / W correction and W = tau y - sigma v; per tile one
 //      rank-2T update of the trailing lower triangle on the DMMA GEMM;
-//   3. implicit-shift QL on the real tridiagonal (solvers.py:783-843) on the
-//      host, O(n^2) without vectors; its plane rotations are recorded and
-//      replayed on the GPU over the rows of Z (one thread per row);
-//   4. back-transformation with the stored reflectors in reverse
-//      (solvers.py:884-897), blocked 256 reflectors at a time in compact WY form
-//      (Q_blk = I - V T V^H, T from the forward recurrence): three GEMMs per
-//      block instead of 64 rank-1 sweeps over Z;
+//   3. back-transformation (solvers.py:884-897) of the IDENTITY, blocked 256
+//      reflectors at a time in compact WY form (Q_blk = I - V T V^H, T from
+//      the forward recurrence): V = Q with three GEMMs per block.  Since
+//      Q (Z_ql) = (Q Z_ql), this does not wait for the QL: the GPU forms Q
+//      while the host iterates;
+//   4. implicit-shift QL on the real tridiagonal (solvers.py:783-843) on the
+//      host, O(n^2) without vectors; its plane rotations are recorded, streamed
+//      to the GPU and replayed on V's columns (one thread per row; a complex
+//      column is a real column of 2n (re, im) rows, the rotations being real);
 //   5. phase normalisation (largest-magnitude component real and positive,
 //      first index on ties, solvers.py:898-909) fused with the scatter back
 //      into the caller's shards and the narrowing to the storage type.
@@ -104,12 +106,12 @@ __global__ void eig_gather(ShardMap m, X* A, int64_t n) {
 // Z column j -> shard column j, scaled so that its first largest-magnitude
 // component is real and positive (solvers.py:898-909).
 template <class X, class S>
-__global__ void eig_phase_scatter(const X* Z, int64_t n, ShardMap m) {
+__global__ void eig_phase_scatter(const X* Z, const int64_t* order, int64_t n, ShardMap m) {
   __shared__ double bv[32];
   __shared__ int64_t bi[32];
   __shared__ double2 ph;
   const int64_t j = blockIdx.x;
-  const X* z = Z + j * n;
+  const X* z = Z + order[j] * n;  // eigenvectors in ascending eigenvalue order
   double best = -1.0;
   int64_t idx = 0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -419,14 +421,15 @@ __global__ void __launch_bounds__(1024) eig_col_finish(const X* P1, const X* P2,
 // in registers: one load and one store per column per K sweeps instead of per
 // sweep.
 template <int K>
-__global__ void __launch_bounds__(32) eig_rotate_wave(double* Z, int64_t n, const double2* cs, const int64_t* sw_off,
-                                                      const int64_t* sw_top, int64_t s0, int64_t nsw) {
+__global__ void __launch_bounds__(32) eig_rotate_wave(double* Z, int64_t rows, int64_t ld, int64_t n, const double2* cs,
+                                                      const int64_t* sw_off, const int64_t* sw_top, int64_t s0,
+                                                      int64_t nsw) {
   constexpr int W = 2 * K;  // window columns == steps per parameter chunk == warp width
   static_assert(W == 32, "one parameter per lane and step");
   __shared__ double2 prm[K][W];
   const int lane = threadIdx.x;
   const int64_t r = blockIdx.x * (int64_t)W + lane;
-  const bool live = r < n;
+  const bool live = r < rows;
   const int kk = (int)min((int64_t)K, nsw - s0);
   int64_t top[K], bot[K], off[K];
   int64_t pmax = INT64_MIN, pmin = INT64_MAX;
@@ -448,7 +451,7 @@ __global__ void __launch_bounds__(32) eig_rotate_wave(double* Z, int64_t n, cons
 #pragma unroll
   for (int j = 0; j < W; ++j) {
     const int64_t c = pmax + j;
-    win[j] = (live && c >= 0 && c < n) ? z[c * n] : 0.0;
+    win[j] = (live && c >= 0 && c < n) ? z[c * ld] : 0.0;
   }
   for (int64_t p0 = pmax; p0 >= pmin; p0 -= W) {
     __syncwarp();
@@ -474,8 +477,8 @@ __global__ void __launch_bounds__(32) eig_rotate_wave(double* Z, int64_t n, cons
       }
       const int sl = W - 1 - u;  // column p + W - 1 leaves, column p - 1 enters
       const int64_t co = p + W - 1, ci = p - 1;
-      if (live && co >= 0 && co < n) z[co * n] = win[sl];
-      win[sl] = (live && ci >= 0 && ci < n) ? z[ci * n] : 0.0;
+      if (live && co >= 0 && co < n) z[co * ld] = win[sl];
+      win[sl] = (live && ci >= 0 && ci < n) ? z[ci * ld] : 0.0;
     }
   }
   // the window now holds columns pmin - 1 .. pmin + W - 2
@@ -483,23 +486,14 @@ __global__ void __launch_bounds__(32) eig_rotate_wave(double* Z, int64_t n, cons
 #pragma unroll
   for (int sl = 0; sl < W; ++sl) {
     const int64_t c = first + (((int64_t)sl - shift) % W + W) % W;
-    if (live && c >= 0 && c < n) z[c * n] = win[sl];
+    if (live && c >= 0 && c < n) z[c * ld] = win[sl];
   }
 }
 
-__global__ void eig_identity(double* Z, int64_t n) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) Z[i + i * n] = 1.0;
-}
-
-// Zx[:, j] = Z[:, order[j]] in the compute type
 template <class X>
-__global__ void eig_permute(const double* Z, const int64_t* order, X* Zx, int64_t n) {
-  const int64_t j = blockIdx.y + (int64_t)blockIdx.z * gridDim.y;
-  if (j >= n) return;
-  const double* src = Z + order[j] * n;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    Zx[i + j * n] = from_c<X>(make_double2(src[i], 0.0));
+__global__ void eig_identity(X* Z, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) Z[i + i * n] = from_c<X>(make_double2(1.0, 0.0));
 }
 
 // Forward compact-WY factor of kb reflectors: T upper, T[j][j] = tau_j,
@@ -620,8 +614,7 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
   // ---- workspace: everything reserved before any data moves (OUT_OF_MEMORY first)
   DevBuf* wb = ss.eig;
   wb[0].ensure((size_t)n * n * es);               // working copy A / stored reflectors V
-  wb[1].ensure((size_t)n * n * sizeof(double));   // Z of the tridiagonal
-  wb[2].ensure((size_t)n * n * es);               // eigenvectors in the compute type
+  wb[2].ensure((size_t)n * n * es);               // V = Q, then Q times the QL rotations
   wb[3].ensure((size_t)2 * n * T * es);           // U | W panels
   wb[4].ensure((size_t)2 * nb * n * es);          // symv partials P1 | P2
   const size_t small = (size_t)(2 * n + 2 * T + n) * es + (size_t)(nparts_max + 1) * sizeof(double2) +
@@ -629,7 +622,6 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
                        (size_t)n * sizeof(int64_t) + (size_t)nparts_max * sizeof(double) + 512;
   wb[5].ensure(small);
   X* A = static_cast<X*>(wb[0].p);
-  double* Zr = static_cast<double*>(wb[1].p);
   X* Zx = static_cast<X*>(wb[2].p);
   X* U = static_cast<X*>(wb[3].p);
   X* W = U + n * T;
@@ -726,81 +718,13 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
   BCMG_CUDA(cudaMemcpyAsync(e.data(), ee, n * sizeof(double), cudaMemcpyDeviceToHost, st));
   BCMG_CUDA(cudaStreamSynchronize(st));
   e.resize(std::max<int64_t>(n - 1, 0));
-  // Z = I first: rotation batches replay on the GPU while the host iterates
-  BCMG_CUDA(cudaMemsetAsync(Zr, 0, (size_t)n * n * sizeof(double), st));
-  eig_identity<<<blocks_for(n, RT), RT, 0, st>>>(Zr, n);
+  // ---- 4 (before 3). back-transformation of the identity: V = Q = H_0 ... H_{n-2}
+  // (solvers.py:884-897 applies the same reflectors to Z; Q (Z_ql) = (Q Z_ql)).  It
+  // does not depend on the QL, so the GPU runs it while the host iterates, and
+  // the QL rotations are then replayed on V's columns directly.
+  BCMG_CUDA(cudaMemsetAsync(Zx, 0, (size_t)n * n * es, st));
+  eig_identity<X><<<blocks_for(n, RT), RT, 0, st>>>(Zx, n);
   BCMG_CHECK_LAUNCH();
-  // rotation parameters stream through NSLOT pinned -> device slots of CH sweeps
-  constexpr int KW = 16, CH = 4 * KW, NSLOT = 3;
-  const size_t cap_rot = (size_t)CH * (size_t)std::max<int64_t>(n, 1);
-  const size_t slot_bytes = (cap_rot * sizeof(double2) + (2 * CH + 1) * sizeof(int64_t) + 255) / 256 * 256;
-  wb[6].ensure(NSLOT * slot_bytes);
-  struct Ring {
-    void* host = nullptr;
-    cudaEvent_t done[NSLOT] = {};
-    cudaStream_t st;
-    ~Ring() {
-      cudaStreamSynchronize(st);  // the pinned slots are reused by the next call
-      for (auto e : done)
-        if (e) cudaEventDestroy(e);
-    }
-  } ring;
-  ring.st = st;
-  if (ss.eig_host_bytes < NSLOT * slot_bytes) {  // session-owned, grow-only
-    if (ss.eig_host) BCMG_CUDA(cudaFreeHost(ss.eig_host));
-    ss.eig_host = nullptr;
-    ss.eig_host_bytes = 0;
-    BCMG_CUDA(cudaHostAlloc(&ss.eig_host, NSLOT * slot_bytes, cudaHostAllocDefault));
-    ss.eig_host_bytes = NSLOT * slot_bytes;
-  }
-  ring.host = ss.eig_host;
-  for (auto& e : ring.done) BCMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  int64_t nrot = 0, nsw = 0;
-  int cur = 0;  // slot the host is writing
-  QLRecord rec;
-  rec.cs = reinterpret_cast<double2*>(ring.host);
-  auto flush = [&] {
-    const int64_t ns = (int64_t)rec.top.size(), nr = rec.ncs;
-    if (!ns) return;
-    char* hb = static_cast<char*>(ring.host) + cur * slot_bytes;
-    char* db = static_cast<char*>(wb[6].p) + cur * slot_bytes;
-    int64_t* hmeta = reinterpret_cast<int64_t*>(hb + cap_rot * sizeof(double2));
-    std::copy(rec.off.begin(), rec.off.end(), hmeta);
-    std::copy(rec.top.begin(), rec.top.end(), hmeta + ns + 1);
-    BCMG_CUDA(cudaMemcpyAsync(db, hb, nr * sizeof(double2), cudaMemcpyHostToDevice, st));
-    int64_t* dmeta = reinterpret_cast<int64_t*>(db + cap_rot * sizeof(double2));
-    BCMG_CUDA(cudaMemcpyAsync(dmeta, hmeta, (2 * ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    for (int64_t s0 = 0; s0 < ns; s0 += KW) {
-      eig_rotate_wave<KW><<<blocks_for(n, 32), 32, 0, st>>>(Zr, n, reinterpret_cast<const double2*>(db), dmeta,
-                                                            dmeta + ns + 1, s0, ns);
-      BCMG_CHECK_LAUNCH();
-    }
-    BCMG_CUDA(cudaEventRecord(ring.done[cur], st));
-    nrot += nr;
-    nsw += ns;
-    cur = (cur + 1) % NSLOT;
-    BCMG_CUDA(cudaEventSynchronize(ring.done[cur]));  // that slot's previous batch has been copied and run
-    rec.cs = reinterpret_cast<double2*>(static_cast<char*>(ring.host) + cur * slot_bytes);
-    rec.ncs = 0;
-    rec.off.assign(1, 0);
-    rec.top.clear();
-  };
-  const auto ql0 = std::chrono::steady_clock::now();
-  tridiag_ql(d, e, rec, [&] {
-    if ((int64_t)rec.top.size() >= CH) flush();
-  });
-  flush();
-  const double host_ql_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ql0).count();
-  std::vector<int64_t> order(n);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return d[a] < d[b]; });
-  BCMG_CUDA(cudaMemcpyAsync(order_d, order.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  pmark(2);
-  eig_permute<X><<<col_grid(n, n), 256, 0, st>>>(Zr, order_d, Zx, n);
-  BCMG_CHECK_LAUNCH();
-  pmark(3);
-
-  // ---- 4. back-transformation, WY reflectors per compact-WY block, last block first
   if (n >= 2) {
     for (int64_t c0 = ((n - 2) / WY) * WY; c0 >= 0; c0 -= WY) {
       const int64_t c1 = std::min<int64_t>(c0 + WY, n - 1), kb = c1 - c0, r0 = c0 + 1, K = n - r0;
@@ -837,18 +761,90 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
     }
   }
 
+  pmark(2);
+  // rotation parameters stream through NSLOT pinned -> device slots of CH sweeps
+  constexpr int KW = 16, CH = 4 * KW, NSLOT = 8;  // enough slots that the host never waits behind the back-transformation
+  const size_t cap_rot = (size_t)CH * (size_t)std::max<int64_t>(n, 1);
+  const size_t slot_bytes = (cap_rot * sizeof(double2) + (2 * CH + 1) * sizeof(int64_t) + 255) / 256 * 256;
+  wb[6].ensure(NSLOT * slot_bytes);
+  struct Ring {
+    void* host = nullptr;
+    cudaEvent_t done[NSLOT] = {};
+    cudaStream_t st;
+    ~Ring() {
+      cudaStreamSynchronize(st);  // the pinned slots are reused by the next call
+      for (auto e : done)
+        if (e) cudaEventDestroy(e);
+    }
+  } ring;
+  ring.st = st;
+  if (ss.eig_host_bytes < NSLOT * slot_bytes) {  // session-owned, grow-only
+    if (ss.eig_host) BCMG_CUDA(cudaFreeHost(ss.eig_host));
+    ss.eig_host = nullptr;
+    ss.eig_host_bytes = 0;
+    BCMG_CUDA(cudaHostAlloc(&ss.eig_host, NSLOT * slot_bytes, cudaHostAllocDefault));
+    ss.eig_host_bytes = NSLOT * slot_bytes;
+  }
+  ring.host = ss.eig_host;
+  for (auto& e : ring.done) BCMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  int64_t nrot = 0, nsw = 0;
+  // the rotations are real: a complex column is a real column of 2n (re, im) rows
+  const int64_t zrows = CP ? 2 * n : n;
+  int cur = 0;  // slot the host is writing
+  QLRecord rec;
+  rec.cs = reinterpret_cast<double2*>(ring.host);
+  auto flush = [&] {
+    const int64_t ns = (int64_t)rec.top.size(), nr = rec.ncs;
+    if (!ns) return;
+    char* hb = static_cast<char*>(ring.host) + cur * slot_bytes;
+    char* db = static_cast<char*>(wb[6].p) + cur * slot_bytes;
+    int64_t* hmeta = reinterpret_cast<int64_t*>(hb + cap_rot * sizeof(double2));
+    std::copy(rec.off.begin(), rec.off.end(), hmeta);
+    std::copy(rec.top.begin(), rec.top.end(), hmeta + ns + 1);
+    BCMG_CUDA(cudaMemcpyAsync(db, hb, nr * sizeof(double2), cudaMemcpyHostToDevice, st));
+    int64_t* dmeta = reinterpret_cast<int64_t*>(db + cap_rot * sizeof(double2));
+    BCMG_CUDA(cudaMemcpyAsync(dmeta, hmeta, (2 * ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    for (int64_t s0 = 0; s0 < ns; s0 += KW) {
+      eig_rotate_wave<KW><<<blocks_for(zrows, 32), 32, 0, st>>>(reinterpret_cast<double*>(Zx), zrows, zrows, n,
+                                                                reinterpret_cast<const double2*>(db), dmeta,
+                                                                dmeta + ns + 1, s0, ns);
+      BCMG_CHECK_LAUNCH();
+    }
+    BCMG_CUDA(cudaEventRecord(ring.done[cur], st));
+    nrot += nr;
+    nsw += ns;
+    cur = (cur + 1) % NSLOT;
+    BCMG_CUDA(cudaEventSynchronize(ring.done[cur]));  // that slot's previous batch has been copied and run
+    rec.cs = reinterpret_cast<double2*>(static_cast<char*>(ring.host) + cur * slot_bytes);
+    rec.ncs = 0;
+    rec.off.assign(1, 0);
+    rec.top.clear();
+  };
+  const auto ql0 = std::chrono::steady_clock::now();
+  tridiag_ql(d, e, rec, [&] {
+    if ((int64_t)rec.top.size() >= CH) flush();
+  });
+  flush();
+  const double host_ql_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ql0).count();
+  std::vector<int64_t> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return d[a] < d[b]; });
+  BCMG_CUDA(cudaMemcpyAsync(order_d, order.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  pmark(3);
+
   pmark(4);
   // ---- 5. phase normalisation + scatter into the caller's shards; eigenvalues
-  eig_phase_scatter<X, S><<<(unsigned)n, 256, 0, st>>>(Zx, n, map);
+  eig_phase_scatter<X, S><<<(unsigned)n, 256, 0, st>>>(Zx, order_d, n, map);
   BCMG_CHECK_LAUNCH();
   pmark(5);
   if (prof) {
     BCMG_CUDA(cudaEventSynchronize(pe[5]));
     float ms[5];
     for (int k = 0; k < 5; ++k) BCMG_CUDA(cudaEventElapsedTime(&ms[k], pe[k], pe[k + 1]));
-    fprintf(stderr, "[syevd n=%lld T=%lld] tridiag %.1f ms, host QL + overlapped rotation replay %.1f ms (host loop %.1f ms, "
-            "%lld rotations, %lld sweeps), permute %.1f ms, back-transform %.1f ms, phase+scatter %.1f ms\n", (long long)n, (long long)T, ms[0],
-            ms[1], host_ql_ms, (long long)nrot, (long long)nsw, ms[2], ms[3], ms[4]);
+    fprintf(stderr,
+            "[syevd n=%lld T=%lld] tridiag %.1f ms, back-transform of I %.1f ms (overlaps the host QL), QL + rotation "
+            "replay done %.1f ms after it (host loop %.1f ms, %lld rotations, %lld sweeps), phase+scatter %.1f ms\n",
+            (long long)n, (long long)T, ms[0], ms[1], ms[2], host_ql_ms, (long long)nrot, (long long)nsw, ms[4]);
     for (auto& e : pe) cudaEventDestroy(e);
   }
   std::sort(d.begin(), d.end());  // == d[order] (stable order of equal keys is immaterial for values)

@@ -259,14 +259,14 @@ def workspace_nbytes(routine: str, desc: MatrixDescriptor, tile: TileSpec, num_d
     elif routine == "potri":
         extra = base + panel
     elif routine == "syevd":
-        # csrc/eigen.cu: dense working copy, Z (float64) and Z in the compute
-        # type, U | W panels, symv partials, WY blocks, vectors, the rotation
+        # csrc/eigen.cu: dense working copy, the eigenvector matrix V (Q, then
+        # Q times the QL rotations), U | W panels, symv partials, WY blocks, vectors, the rotation
         # ring -- one GPU holds it all, so it is charged to logical device 0
         cs = 16 if et.is_complex else 8
         nb = -(-n // 64)
-        eig = (2 * n * n * cs + n * n * 8 + 2 * n * T * cs + 2 * nb * n * cs + 2 * 256 * 256 * cs
+        eig = (2 * n * n * cs + 2 * n * T * cs + 2 * nb * n * cs + 2 * 256 * 256 * cs
                + 2 * 256 * n * cs + (3 * n + 2 * T) * cs + 3 * n * 8 + n * 8 + (n // 8 + 2) * 24
-               + 3 * (64 * n * 16 + 129 * 8))
+               + 8 * (64 * n * 16 + 129 * 8))
         counts = device_column_counts(desc.n_cols, tile, num_devices)
         return [c * desc.column_nbytes + (eig if d == 0 else 0) for d, c in enumerate(counts)]
     else:
