@@ -189,3 +189,25 @@ def test_paper_api_row_sharded(meshes, dtype):
     assert np.max(np.abs(w.cpu().numpy() - w_ref)) <= 10 * n * eps * np.max(np.abs(w_ref))
     assert np.max(np.abs(V.cpu().numpy() - v_ref)) <= 100 * n * eps
     assert torch.equal(bc.syevd(At, T_A=4, mesh=meshes(1), return_eigenvectors=False), w)
+
+
+@pytest.mark.parametrize("n,t,d", [(1, 1, 1), (2, 2, 2), (3, 1, 3), (65, 64, 1), (129, 64, 5), (300, 256, 2),
+                                   (97, 13, 8), (257, 128, 4)])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64, np.complex64, np.complex128])
+def test_edge_shapes(meshes, n, t, d, dtype):
+    """Orders that do not divide the tile, tiles wider than the 64-wide symv
+    tile and the 256-reflector WY block edge, n = 1 and 2, up to 8 devices."""
+    rng = np.random.default_rng(1000 * n + t)
+    b = rng.uniform(-1, 1, (n, n))
+    if np.dtype(dtype).kind == "c":
+        b = b + 1j * rng.uniform(-1, 1, (n, n))
+    a = np.asfortranarray(((b + b.conj().T) / 2).astype(dtype))
+    w, v, _ = bc.eigh_hermitian(meshes(d), a, bc.TileSpec(t))
+    eps = _eps(dtype)
+    assert w.shape == (n,) and v.shape == (n, n) and np.all(np.diff(w) >= 0)
+    res, orth = _quality(a, w, v)
+    scale = max(1.0, n)
+    assert res <= 100 * scale * eps and orth <= 100 * scale * eps, (res, orth)
+    wide = np.complex128 if np.dtype(dtype).kind == "c" else np.float64
+    w_ref = np.linalg.eigvalsh(a.astype(wide))
+    assert np.max(np.abs(w.astype(np.float64) - w_ref)) <= 100 * scale * eps * max(1.0, np.max(np.abs(w_ref)))
