@@ -313,7 +313,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "gpu_launches": int(launches),
         "e2e": e2e,
         "redistribute": redist,
-        "cpu_baseline": cpu_baseline() if not args.no_cpu else None,
+        "cpu_baseline": cpu_baseline() if world == 1 and not args.no_cpu else None,  # rank 0 at N=1 only
     }
     print(json.dumps(line), flush=True)
     if world > 1:
