@@ -457,6 +457,11 @@ struct TrailParams {
   int64_t m_first, m_last;
   int max_ctas;       // host-side: persistent grid cap (0 = all SMs)
   long long stagger_ns;  // delay of the second half of the grid (two CTAs per SM)
+  // tcgen05 trailing update with one column block per tile (T <= tile width):
+  // items of `band` consecutive owned tile columns are interleaved by absolute
+  // row block, so a wave reuses each panel row block across the band from L2
+  // instead of streaming the whole panel from HBM once per tile column (0 = off)
+  int band;
 };
 
 template <int B>

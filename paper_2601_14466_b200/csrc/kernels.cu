@@ -620,6 +620,15 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
     total += p.cplx ? TZC::count(rows, tcm) : TZ::count(rows, tcm);
   }
   if (total == 0) return;
+  TrailParams q = p;
+  {
+    static int band = -1;
+    if (band < 0) {
+      const char* e = getenv("BCMG_TRAIL_BAND");
+      band = e && *e ? std::max(0, atoi(e)) : 8;
+    }
+    q.band = (!p.cplx && p.T <= BNT && p.T % tc::BM == 0 && (p.nloc == 1 || p.nloc == p.D)) ? band : 0;
+  }
   const int64_t prow = p.N - p.prow0, arows = p.cplx ? 2 * prow : prow;
   const CUtensorMap ah = make_map_kmajor(p.split[0], arows, p.split_ld[0]);
   const CUtensorMap al = make_map_kmajor(p.split[1], arows, p.split_ld[0]);
@@ -629,7 +638,7 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   set_smem(tck_trail_kernel<BNT>, smem);
   const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, num_sms()) : num_sms();
   const int64_t grid = std::min<int64_t>(total, sms);
-  tck_trail_kernel<BNT><<<(unsigned)grid, tck::THREADS, smem, st>>>(ah, al, bh, bl, p, info);
+  tck_trail_kernel<BNT><<<(unsigned)grid, tck::THREADS, smem, st>>>(ah, al, bh, bl, q, info);
   BCMG_CHECK_LAUNCH();
 }
 
