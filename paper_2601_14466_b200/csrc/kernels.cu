@@ -627,7 +627,8 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
       const char* e = getenv("BCMG_TRAIL_BAND");
       band = e && *e ? std::max(0, atoi(e)) : 8;
     }
-    q.band = (!p.cplx && p.T <= BNT && p.T % tc::BM == 0 && (p.nloc == 1 || p.nloc == p.D)) ? band : 0;
+    const int64_t rb = p.cplx ? tc::BM / 2 : tc::BM;
+    q.band = (p.T <= BNT && p.T % rb == 0 && (p.nloc == 1 || p.nloc == p.D)) ? band : 0;
   }
   const int64_t prow = p.N - p.prow0, arows = p.cplx ? 2 * prow : prow;
   const CUtensorMap ah = make_map_kmajor(p.split[0], arows, p.split_ld[0]);

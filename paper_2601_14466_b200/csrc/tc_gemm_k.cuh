@@ -241,19 +241,20 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
   using TZC = TrapR<tc::BM / 2, BNT>;
   if (ld_flag(info)) return;
   int64_t cm = p.m_first, cbase = 0, ccnt = -1;
-  // band mode (real, T <= BNT, T % BM == 0, owned columns evenly spaced): see TrailParams::band
+  // band mode (T <= BNT, T a multiple of the row block, owned columns evenly spaced): see TrailParams::band
   const int64_t sc = p.nloc == p.D ? 1 : p.D;
   if (p.band > 0 && sc > 1) cm += ((p.dev0 - cm % p.D) + p.D) % p.D;  // first owned column
   int64_t bg = 0, ba0 = 0, btop = 0;
   tck::tck_loop<BNT>(&mAh, &mAl, &mBh, &mBl, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, tc::Blk& blk) -> bool {
     if (p.band > 0) {
-      const int64_t step = sc * p.T / tc::BM, aend = (p.N + tc::BM - 1) / tc::BM;
+      const int64_t RB = p.cplx ? tc::BM / 2 : tc::BM;  // matrix rows per row block (complex64: embedded pairs)
+      const int64_t step = sc * p.T / RB, aend = (p.N + RB - 1) / RB;
       for (;;) {
         if (cm >= p.m_last) return false;
         if (ccnt < 0) {
           bg = (p.m_last - cm + sc - 1) / sc;
           if (bg > p.band) bg = p.band;
-          ba0 = cm * p.T / tc::BM;
+          ba0 = cm * p.T / RB;
           btop = step * bg * (bg - 1) / 2;
           ccnt = bg * (aend - ba0) - btop;
         }
@@ -277,14 +278,15 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
       const int64_t c = cm + i * sc, ms = c * p.T, rows = p.N - ms;
       const int dev = (int)(c % p.D);
       float* shard = reinterpret_cast<float*>(p.shards[dev - p.dev0]);
-      blk.a_row = (int)(ms - p.prow0);
+      const int64_t cx = p.cplx ? 2 : 1;
+      blk.a_row = (int)(cx * (ms - p.prow0));
       blk.b_row = (int)(ms - p.prow0);
-      blk.m0 = (A - ms / tc::BM) * tc::BM;
+      blk.m0 = (A - ms / RB) * tc::BM;
       blk.n0 = 0;
-      blk.M = rows;
+      blk.M = cx * rows;
       blk.N = p.T < rows ? p.T : rows;
-      blk.C = shard + ms + (c / p.D) * p.T * p.N;
-      blk.ldc = p.N;
+      blk.C = shard + cx * (ms + (c / p.D) * p.T * p.N);
+      blk.ldc = cx * p.N;
       blk.alpha = -1.f;
       blk.beta = 1.f;
       blk.nfan = 0;
