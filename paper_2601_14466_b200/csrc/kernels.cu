@@ -628,7 +628,9 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
       band = e && *e ? std::max(0, atoi(e)) : 8;
     }
     const int64_t rb = p.cplx ? tc::BM / 2 : tc::BM;
-    q.band = (p.T <= BNT && p.T % rb == 0 && (p.nloc == 1 || p.nloc == p.D)) ? band : 0;
+    const bool cols = p.T <= BNT && p.T % rb == 0 && (p.nloc == 1 || p.nloc == p.D);
+    const bool blocks = p.T > BNT && p.T % BNT == 0 && p.N % p.T == 0 && p.nloc == p.D;
+    q.band = cols || blocks ? band : 0;
   }
   const int64_t prow = p.N - p.prow0, arows = p.cplx ? 2 * prow : prow;
   const CUtensorMap ah = make_map_kmajor(p.split[0], arows, p.split_ld[0]);

@@ -241,30 +241,36 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
   using TZC = TrapR<tc::BM / 2, BNT>;
   if (ld_flag(info)) return;
   int64_t cm = p.m_first, cbase = 0, ccnt = -1;
-  // band mode (T <= BNT, T a multiple of the row block, owned columns evenly spaced): see TrailParams::band
+  // band mode (see TrailParams::band).  The band interleaves "units" that all
+  // end at row N: owned tile columns (T <= BNT, spaced sc tiles), or, with one
+  // process owning every column and T a multiple of BNT, the BNT-wide column
+  // blocks of consecutive tiles (spaced BNT rows).
   const int64_t sc = p.nloc == p.D ? 1 : p.D;
+  const int64_t ncb = p.T > BNT ? p.T / BNT : 1;
   if (p.band > 0 && sc > 1) cm += ((p.dev0 - cm % p.D) + p.D) % p.D;  // first owned column
-  int64_t bg = 0, ba0 = 0, btop = 0;
+  const int64_t nunits = ncb == 1 ? (p.m_last - cm + sc - 1) / sc : (p.m_last - p.m_first) * ncb;
+  const int64_t cm0 = cm;
+  auto unit_row = [&](int64_t k) { return ncb == 1 ? (cm0 + k * sc) * p.T : (p.m_first * ncb + k) * BNT; };
+  int64_t ku = 0, bg = 0, ba0 = 0, btop = 0;
   tck::tck_loop<BNT>(&mAh, &mAl, &mBh, &mBl, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, tc::Blk& blk) -> bool {
     if (p.band > 0) {
       const int64_t RB = p.cplx ? tc::BM / 2 : tc::BM;  // matrix rows per row block (complex64: embedded pairs)
-      const int64_t step = sc * p.T / RB, aend = (p.N + RB - 1) / RB;
+      const int64_t step = (ncb == 1 ? sc * p.T : (int64_t)BNT) / RB, aend = (p.N + RB - 1) / RB;
       for (;;) {
-        if (cm >= p.m_last) return false;
+        if (ku >= nunits) return false;
         if (ccnt < 0) {
-          bg = (p.m_last - cm + sc - 1) / sc;
-          if (bg > p.band) bg = p.band;
-          ba0 = cm * p.T / RB;
+          bg = nunits - ku < p.band ? nunits - ku : p.band;
+          ba0 = unit_row(ku) / RB;
           btop = step * bg * (bg - 1) / 2;
           ccnt = bg * (aend - ba0) - btop;
         }
         if (item < cbase + ccnt) break;
         cbase += ccnt;
-        cm += bg * sc;
+        ku += bg;
         ccnt = -1;
       }
       int64_t o = item - cbase, A, i;
-      if (o < btop) {  // level j: row blocks [ba0 + j step, ba0 + (j+1) step) of columns 0..j
+      if (o < btop) {  // level j: row blocks [ba0 + j step, ba0 + (j+1) step) of units 0..j
         int64_t j = 0;
         while (step * (j + 1) * (j + 2) / 2 <= o) ++j;
         o -= step * j * (j + 1) / 2;
@@ -275,14 +281,17 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
         A = ba0 + (bg - 1) * step + o / bg;
         i = o % bg;
       }
-      const int64_t c = cm + i * sc, ms = c * p.T, rows = p.N - ms;
+      const int64_t k = ku + i;
+      const int64_t c = ncb == 1 ? cm0 + k * sc : (p.m_first * ncb + k) / ncb;
+      const int64_t cb = ncb == 1 ? 0 : (p.m_first * ncb + k) % ncb;
+      const int64_t ms = c * p.T, rows = p.N - ms;
       const int dev = (int)(c % p.D);
       float* shard = reinterpret_cast<float*>(p.shards[dev - p.dev0]);
       const int64_t cx = p.cplx ? 2 : 1;
       blk.a_row = (int)(cx * (ms - p.prow0));
       blk.b_row = (int)(ms - p.prow0);
       blk.m0 = (A - ms / RB) * tc::BM;
-      blk.n0 = 0;
+      blk.n0 = cb * BNT;
       blk.M = cx * rows;
       blk.N = p.T < rows ? p.T : rows;
       blk.C = shard + cx * (ms + (c / p.D) * p.T * p.N);
