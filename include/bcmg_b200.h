@@ -187,6 +187,16 @@ int bcmg_last_timings(bcmg_session* s, float* ms /* [4] */);
 /* algorithmic bytes (read + write) moved by the last redistribution */
 int64_t bcmg_last_moved_bytes(bcmg_session* s);
 
+/* Device workspace of one process for a pipeline (routine 1: potrs, 2:
+   potri), excluding the shards: the exact bytes bcmg_potrs / bcmg_potri
+   reserve before moving any data (reference solvers.py:279-308
+   workspace_nbytes; the OUT_OF_MEMORY-before-movement contract of
+   test_solvers.py:344-352).  Needs no GPU (148 SMs assumed without one). */
+int bcmg_workspace_nbytes(int routine, int dtype, int64_t n, int64_t tile, int ndev, int world, int64_t nrhs,
+                          int64_t* bytes);
+/* device bytes the session's workspace holds now (grow-only buffers) */
+int bcmg_session_workspace_bytes(bcmg_session* s, int64_t* bytes);
+
 /* Per-kernel timing: when on, every launch of a kernel kind is bracketed by
    CUDA events on the stream it is launched on.  kind: 0 trailing update
    (DMMA GEMM), 1 panel TRSM, 2 diagonal factor+inverse, 3 cycle rotation.

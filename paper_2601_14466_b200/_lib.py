@@ -62,6 +62,8 @@ SIGNATURES = {
                             C.c_double, _vp, _i64]),
     "bcmg_last_timings": (C.c_int, [_vp, C.POINTER(C.c_float)]),
     "bcmg_last_moved_bytes": (C.c_int64, [_vp]),
+    "bcmg_workspace_nbytes": (C.c_int, [C.c_int, C.c_int, _i64, _i64, C.c_int, C.c_int, _i64, _i64p]),
+    "bcmg_session_workspace_bytes": (C.c_int, [_vp, _i64p]),
     "bcmg_set_profiling": (C.c_int, [_vp, C.c_int]),
     "bcmg_kernel_stats": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_double)]),
     "bcmg_launch_count": (C.c_int64, []),

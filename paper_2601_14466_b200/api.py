@@ -92,7 +92,9 @@ def _prepare_a(A, mesh: DeviceMesh, overwrite_a: bool):
 def _shard_ptrs(A, mesh: DeviceMesh, n: int, tile: int, esz: int):
     counts = device_column_counts(n, TileSpec(tile), mesh.num_devices)
     local = [counts[d] for d in mesh.local_devices]
-    if mesh.world > 1 and any(c * mesh.world != n for c in local):
+    # this process's logical devices together hold exactly its row block (N / world
+    # columns of the symmetric A); a mesh may put several logical devices on a process
+    if mesh.world > 1 and sum(local) * mesh.world != n:
         raise DescriptorError("dimension-mismatch",
                               f"row shards of N/{mesh.world} need N % (T_A * devices) == 0 (N={n}, T_A={tile})")
     base, ptrs, off = A.data_ptr(), [], 0

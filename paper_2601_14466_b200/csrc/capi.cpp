@@ -67,6 +67,33 @@ void check_common(int dtype, int ndev, void* const* shards) {
   if (!shards) throw bcmg::Error(BCMG_ERR_CONFIG, "null shard table");
 }
 
+// Conjugates a complex right-hand side for the row-sharded pipeline and
+// restores it if the call fails before the solve completes, so the caller's b
+// is never left conjugated on an error path.
+struct ConjGuard {
+  int dt;
+  void* b;
+  int64_t ldb, n, nrhs;
+  cudaStream_t st;
+  bool armed = false;
+  ConjGuard(bool on, int dt_, void* b_, int64_t ldb_, int64_t n_, int64_t nrhs_, cudaStream_t st_)
+      : dt(dt_), b(b_), ldb(ldb_), n(n_), nrhs(nrhs_), st(st_), armed(on) {
+    if (armed) bcmg::conj2d(dt, b, ldb, n, nrhs, st);
+  }
+  void finish() {  // the solution is conjugated back as part of the result
+    if (armed) bcmg::conj2d(dt, b, ldb, n, nrhs, st);
+    armed = false;
+  }
+  ~ConjGuard() {
+    if (!armed) return;
+    try {
+      bcmg::conj2d(dt, b, ldb, n, nrhs, st);
+      cudaStreamSynchronize(st);
+    } catch (...) {
+    }
+  }
+};
+
 void finish_timings(bcmg::Session* s, bool has_redist_out) {
   (void)has_redist_out;
   BCMG_CUDA(cudaEventSynchronize(s->ev_time[bcmg::T_SOLVE]));
@@ -266,7 +293,7 @@ int bcmg_potrs(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t nrhs
     S->reserve_workspace(1, dtype, n, tile, ndev, nrhs);
     const bool conj = (flags & BCMG_FLAG_ROW_SHARDED) && bcmg::dtype_complex(dtype);
     S->mark(bcmg::T_BEGIN);
-    if (conj) bcmg::conj2d(dtype, b, ldb, n, nrhs, S->user);
+    ConjGuard cg(conj, dtype, b, ldb, n, nrhs, S->user);
     S->redistribute(dtype, n, n, tile, ndev, shards, false);
     S->mark(bcmg::T_REDIST);
     *info = S->potrf(dtype, n, tile, ndev, shards);
@@ -280,7 +307,7 @@ int bcmg_potrs(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t nrhs
     }
     S->begin(S->user);
     S->potrs(dtype, n, nrhs, tile, ndev, shards, b, ldb);
-    if (conj) bcmg::conj2d(dtype, b, ldb, n, nrhs, S->user);
+    cg.finish();
     S->mark(bcmg::T_SOLVE);
     finish_timings(S, false);
   });
@@ -301,7 +328,7 @@ int bcmg_potrs_streamed(bcmg_session* s, void* stream, int dtype, int64_t n, int
     S->reserve_workspace(1, dtype, n, tile, 1, nrhs);
     const bool conj = (flags & BCMG_FLAG_ROW_SHARDED) && bcmg::dtype_complex(dtype);
     S->mark(bcmg::T_BEGIN);
-    if (conj) bcmg::conj2d(dtype, b, ldb, n, nrhs, S->user);
+    ConjGuard cg(conj, dtype, b, ldb, n, nrhs, S->user);
     S->mark(bcmg::T_REDIST);  // one device: the block-cyclic layout is the contiguous one
     void* shards[1] = {a_dev};
     *info = S->potrf(dtype, n, tile, 1, shards, a_host);
@@ -315,7 +342,7 @@ int bcmg_potrs_streamed(bcmg_session* s, void* stream, int dtype, int64_t n, int
     }
     S->begin(S->user);
     S->potrs(dtype, n, nrhs, tile, 1, shards, b, ldb);
-    if (conj) bcmg::conj2d(dtype, b, ldb, n, nrhs, S->user);
+    cg.finish();
     S->mark(bcmg::T_SOLVE);
     finish_timings(S, false);
   });
@@ -413,6 +440,25 @@ int bcmg_last_timings(bcmg_session* s, float* ms) {
 }
 
 int64_t bcmg_last_moved_bytes(bcmg_session* s) { return (s && s->impl) ? s->impl->last_moved_bytes : -1; }
+
+int bcmg_workspace_nbytes(int routine, int dtype, int64_t n, int64_t tile, int ndev, int world, int64_t nrhs,
+                          int64_t* bytes) {
+  return guarded([&] {
+    if (!bytes) throw bcmg::Error(BCMG_ERR_CONFIG, "null output");
+    if (nrhs < 1) throw bcmg::Error(BCMG_ERR_CONFIG, "right-hand side must be non-empty");
+    int nsm = 148, dev = 0, cnt = 0;
+    if (cudaGetDeviceCount(&cnt) == cudaSuccess && cnt > 0 && cudaGetDevice(&dev) == cudaSuccess) {
+      int v = 0;
+      if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) nsm = v;
+    }
+    cudaGetLastError();
+    *bytes = (int64_t)bcmg::workspace_plan(routine, dtype, n, tile, ndev, world, nrhs, nsm).total();
+  });
+}
+
+int bcmg_session_workspace_bytes(bcmg_session* s, int64_t* bytes) {
+  return guarded([&] { *bytes = (int64_t)live(s)->held_workspace_bytes(); });
+}
 
 int bcmg_set_profiling(bcmg_session* s, int on) {
   return guarded([&] { live(s)->profiling = on != 0; });

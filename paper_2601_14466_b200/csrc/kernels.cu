@@ -41,13 +41,12 @@ using TileMed = Tile<64, 64, 16, 32, 32, 3>;      // 128 threads, general
 using TileNarrow = Tile<128, 16, 16, 32, 16, 3>;  // 128 threads, N <= 16 (RHS blocks)
 
 static int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
+  static const int sms = [] {
+    int dev = 0, v = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
   return sms;
 }
 
@@ -96,7 +95,7 @@ static bool use_tma();
 static unsigned ew_grid(int64_t total);
 static bool use_tc();
 static bool use_presplit();
-static float* split_scratch(cudaStream_t st, size_t bytes);
+static float* split_scratch(cudaStream_t st, size_t bytes, size_t* held = nullptr);
 static void gemm_tck_generic(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
                              const int* info, cudaStream_t st);
 static bool tc_ok(const void* p, int64_t ld);
@@ -288,11 +287,10 @@ static void launch_trail_tma_t(const TrailParams& p, const int* info, cudaStream
 }
 
 static int trail_tile_choice() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {
     const char* e = getenv("BCMG_TRAIL_TILE");
-    v = e ? atoi(e) : 2;
-  }
+    return e ? atoi(e) : 2;
+  }();
   return v;
 }
 
@@ -469,12 +467,11 @@ bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, 
 }
 
 static bool use_tma() {
-  static int v = -1;
-  if (v < 0) {
+  static const bool v = [] {
     const char* e = getenv("BCMG_NO_TMA");
-    v = (e && atoi(e)) ? 0 : 1;
-  }
-  return v == 1;
+    return !(e && atoi(e));
+  }();
+  return v;
 }
 
 // ============================================================== tcgen05 3xTF32 (float32)
@@ -494,12 +491,11 @@ static CUtensorMap make_map_f32_sw128(const void* base, int64_t rows, int64_t co
 static bool tc_ok(const void* p, int64_t ld) { return aligned16(p) && ld % 4 == 0; }
 
 static bool use_tc() {
-  static int v = -1;
-  if (v < 0) {
+  static const bool v = [] {
     const char* e = getenv("BCMG_NO_TCGEN05");
-    v = (e && atoi(e)) ? 0 : 1;
-  }
-  return v == 1;
+    return !(e && atoi(e));
+  }();
+  return v;
 }
 
 static void launch_tc3_gemm(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
@@ -588,22 +584,20 @@ static CUtensorMap make_map_kmajor(const float* base, int64_t rows, int64_t kp, 
 
 bool tc_presplit_enabled();
 static bool use_presplit() {
-  static int v = -1;
-  if (v < 0) {
+  static const bool v = [] {
     const char* e = getenv("BCMG_TC_INLINE_SPLIT");
-    v = (e && atoi(e)) ? 0 : 1;
-  }
-  return v == 1;
+    return !(e && atoi(e));
+  }();
+  return v;
 }
 
 bool tc_presplit_enabled() { return use_tc() && use_presplit(); }
 
 static int tck_width(int64_t n) {
-  static int forced = -1;
-  if (forced < 0) {
+  static const int forced = [] {
     const char* e = getenv("BCMG_TCK_N");
-    forced = e ? atoi(e) : 0;
-  }
+    return e ? atoi(e) : 0;
+  }();
   if (forced == 128 || forced == 256) return forced;
   return n >= 256 ? 256 : 128;
 }
@@ -622,11 +616,10 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   if (total == 0) return;
   TrailParams q = p;
   {
-    static int band = -1;
-    if (band < 0) {
+    static const int band = [] {
       const char* e = getenv("BCMG_TRAIL_BAND");
-      band = e && *e ? std::max(0, atoi(e)) : 8;
-    }
+      return e && *e ? std::max(0, atoi(e)) : 8;
+    }();
     const int64_t rb = p.cplx ? tc::BM / 2 : tc::BM;
     const bool cols = p.T <= BNT && p.T % rb == 0 && (p.nloc == 1 || p.nloc == p.D);
     const bool blocks = p.T > BNT && p.T % BNT == 0 && p.N % p.T == 0 && p.nloc == p.D;
@@ -683,12 +676,18 @@ void tck_gemm(int64_t M, int64_t N, int64_t K, const float* ah, const float* al,
 
 // gemm() for float32 on tcgen05: both operands split into a scratch owned by
 // the calling thread and stream (grow-only; stream order makes reuse safe).
-static float* split_scratch(cudaStream_t st, size_t bytes) {
+static float* split_scratch(cudaStream_t st, size_t bytes, size_t* held) {
   struct Buf {
     void* p = nullptr;
     size_t n = 0;
   };
   thread_local std::vector<std::pair<cudaStream_t, Buf>> bufs;
+  if (held) {  // query only
+    *held = 0;
+    for (auto& e : bufs)
+      if (e.first == st) *held = e.second.n;
+    return nullptr;
+  }
   Buf* b = nullptr;
   for (auto& e : bufs)
     if (e.first == st) b = &e.second;
@@ -718,6 +717,11 @@ static float* split_scratch(cudaStream_t st, size_t bytes) {
 // not happen while another rank's stream waits for a flag this thread has yet
 // to raise (peer-memory mode).
 void reserve_split_scratch(cudaStream_t st, size_t bytes) { split_scratch(st, bytes); }
+size_t split_scratch_held(cudaStream_t st) {
+  size_t h = 0;
+  split_scratch(st, 0, &h);
+  return h;
+}
 size_t split_scratch_bytes(int dt, int64_t M, int64_t N, int64_t K) {
   return dt == C64 ? (size_t)2 * (2 * M + N) * split_ld(2 * K) * 4 : (size_t)2 * (M + N) * split_ld(K) * 4;
 }

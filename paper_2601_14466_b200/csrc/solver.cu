@@ -63,6 +63,7 @@ Session::Session(int device_, int rank_, int world_, const unsigned char* nccl_i
   for (auto& e : ev_pool) BCMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : ev_time) BCMG_CUDA(cudaEventCreate(&e));
   BCMG_CUDA(cudaMallocHost(&info_host, sizeof(int)));
+  BCMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   if (world > 1) net = make_comm(rank, world, nccl_id);
 }
 
@@ -450,36 +451,143 @@ std::vector<SchedOp> potrs_schedule(int64_t n, int64_t T, int ndev, int world, i
 // out-of-memory failure leaves the caller's shards untouched (the reference
 // raises before any data movement, test_solvers.py:344-352).  The drivers'
 // own ensure() calls then find the buffers large enough (grow-only).
-void Session::reserve_workspace(int routine, int dt, int64_t n, int64_t T, int ndev, int64_t nrhs) {
-  const Geo g = make_geo(*this, dt, n, T, ndev);
-  const size_t panel_bytes = (size_t)n * T * g.esz;
+static int64_t cols_below(const Geo& g, int d, int64_t s);
+static int64_t cols_upto(const Geo& g, int d, int64_t s);
+
+// potri's complex real-embedding scratch: column chunks of whole waves of
+// output tiles for the product sweep (2*tcs real rows in 128-row blocks; 2 CTAs
+// per SM of 64-wide tiles for complex128 on the FP64 TMA kernel, 1 CTA per SM
+// of 256-wide tiles for complex64 on tcgen05)
+static int64_t potri_wave_cols(int dt, int64_t tcs, int nsm) {
+  const int64_t rb = (2 * tcs + 127) / 128;
+  return dt == C64 ? std::max<int64_t>(1, nsm / rb) * 256 : std::max<int64_t>(1, 2 * nsm / rb) * 64;
+}
+// (T and n even: every column count is even, so the choice is the same for any
+// device count; complex64: the tcgen05 tile minimums hold for every D)
+static bool potri_embeds(int dt, int64_t n, int64_t T) {
+  if (getenv("BCMG_NO_CPLX_EMBED")) return false;
+  return (dt == C128 && T % 2 == 0 && n % 2 == 0) || (dt == C64 && T % 64 == 0 && n % 4 == 0);
+}
+static size_t potri_embed_bytes(int dt, int64_t n, int64_t T, int nsm) {
+  const size_t esz = dtype_size(dt);
+  return std::max(gemm_cplx_embed_bytes(dt, n, n, T), (size_t)(2 * T + 2 * potri_wave_cols(dt, T, nsm)) * n * esz);
+}
+// columns per product-sweep chunk of the embedded GEMM for a W tile starting at ss
+static int64_t potri_chunk_cols(int dt, int64_t n, int64_t ss, int64_t tcs, size_t emb_bytes, int nsm) {
+  const int64_t wave = potri_wave_cols(dt, tcs, nsm);
+  int64_t nc = (int64_t)(emb_bytes / ((size_t)(n - ss) * dtype_size(dt))) - 2 * tcs;
+  return nc >= wave ? nc / wave * wave : nc / 64 * 64;
+}
+// the tf32 split planes gemm() (float32, tcgen05) requests for an M x N x K product, 0 if it stays off tcgen05
+static size_t f32_gemm_split(int64_t M, int64_t N, int64_t K) {
+  if (!tc_presplit_enabled() || M < 256 || N < 64 || K < 32) return 0;
+  return split_scratch_bytes(R32, M, N, K);
+}
+
+WsPlan workspace_plan(int routine, int dt, int64_t n, int64_t T, int ndev, int world, int64_t nrhs, int nsm) {
+  if (routine != 1 && routine != 2) throw Error(CONFIG, "unknown routine");
+  if (n < 1 || T < 1 || T > n || ndev < 1 || world < 1 || ndev % world)
+    throw Error(CONFIG, "bad matrix order / tile width / device grid");
+  const size_t esz = dtype_size(dt);
+  if (!esz) throw Error(CONFIG, "unknown element-type code");
+  const int64_t nt = (n + T - 1) / T;
+  WsPlan w;
+  const size_t panel_bytes = (size_t)n * T * esz;
   const bool presplit = (dt == R32 || dt == C64) && tc_presplit_enabled();
   if (presplit) {
     const size_t plane = (size_t)n * split_ld(dt == C64 ? 2 * T : T) * 4;
-    split_buf[0].ensure(dt == C64 ? 6 * plane : 2 * plane);
-    split_buf[1].ensure(dt == C64 ? 6 * plane : 2 * plane);
-    reserve_split_scratch(crit, split_scratch_bytes(dt, n, T, T));
+    w.split = dt == C64 ? 6 * plane : 2 * plane;
+    w.split_scratch = split_scratch_bytes(dt, n, T, T);  // the panel solves
   }
   const bool embed = !presplit && complex_embed_ok(dt, 0, T);
-  panel[0].ensure(embed ? 2 * panel_bytes : panel_bytes);
-  panel[1].ensure(embed ? 2 * panel_bytes : panel_bytes);
-  if (embed) {
-    panel_pb[0].ensure(panel_bytes);
-    panel_pb[1].ensure(panel_bytes);
-  }
-  if (dt == C128 || dt == C64) embed_buf.ensure(gemm_cplx_embed_bytes(dt, n, T, T));
-  dinv.ensure((size_t)g.nt * T * T * g.esz);
-  wdiag.ensure((size_t)T * T * g.esz);
-  info_dev.ensure(sizeof(int));
+  w.panel = embed ? 2 * panel_bytes : panel_bytes;
+  if (embed) w.panel_pb = panel_bytes;
+  if (dt == C128 || dt == C64) w.embed = gemm_cplx_embed_bytes(dt, n, T, T);
+  w.dinv = (size_t)nt * T * T * esz;
+  w.wdiag = (size_t)T * T * esz;
+  w.info = sizeof(int);
   if (routine == 1) {  // potrs: split-K slabs + (multi-process) the solution hand-off buffer
-    const size_t parts_bytes = (size_t)64 * T * nrhs * g.esz;
-    tmp.ensure(std::max<size_t>(4096, parts_bytes + (world > 1 ? (size_t)n * nrhs * g.esz : 0)));
-  } else {
-    tmp.ensure(4096);
+    const size_t parts_bytes = (size_t)64 * T * nrhs * esz;
+    w.tmp = std::max<size_t>(4096, parts_bytes + (world > 1 ? (size_t)n * nrhs * esz : 0));
+    if (dt == R32)  // forward substitution x[stop:] -= L x_k when the split-K slabs do not fit
+      for (int64_t k = 0; k < nt; ++k) {
+        const int64_t s1 = std::min(n, (k + 1) * T);
+        if (s1 < n && (int64_t)(parts_bytes / ((size_t)(n - s1) * nrhs * esz)) < 2)
+          w.split_scratch = std::max(w.split_scratch, f32_gemm_split(n - s1, nrhs, s1 - k * T));
+      }
+    return w;
   }
-  if (routine == 2) {  // potri: the W-tile / block buffers (the embedding scratch is sized in potri)
-    acc.ensure(panel_bytes);
+  // potri: the W-tile / block buffers and the GEMMs of both sweeps
+  w.tmp = 4096;
+  w.panel = std::max(w.panel, panel_bytes);
+  w.acc = panel_bytes;
+  const bool emb = potri_embeds(dt, n, T);
+  if (emb) w.embed = std::max(w.embed, potri_embed_bytes(dt, n, T, nsm));
+  if (dt == R32 || (dt == C64 && emb && presplit)) {
+    Geo g{};
+    g.n = n;
+    g.T = T;
+    g.nt = nt;
+    g.D = ndev;
+    g.nloc = ndev / world;
+    for (int r = 0; r < world; ++r)
+      for (int64_t s = 0; s < nt; ++s) {
+        const int64_t ss = s * T, se = std::min(n, ss + T), tcs = se - ss;
+        if (dt == R32 && se < n) w.split_scratch = std::max(w.split_scratch, f32_gemm_split(n - se, tcs, tcs));
+        for (int d = r * g.nloc; d < (r + 1) * g.nloc; ++d) {
+          const int64_t cb = cols_below(g, d, s), cu = cols_upto(g, d, s);
+          if (dt == R32) {
+            if (cb) w.split_scratch = std::max(w.split_scratch, f32_gemm_split(n - ss, cb, tcs));
+            if (cu) w.split_scratch = std::max(w.split_scratch, f32_gemm_split(tcs, cu, n - ss));
+            continue;
+          }
+          // complex64 through the embedded tcgen05 GEMM (gemm_cplx_embed's shape rules)
+          auto emb_split = [&](int64_t M, int64_t N, int64_t K) -> size_t {
+            if (N % 4 || (2 * M) % 4 || 2 * M < 256 || N < 64 || K <= 0) return 0;
+            if (w.embed < gemm_cplx_embed_bytes(dt, M, N, K)) return 0;
+            return split_scratch_bytes(C64, M, N, K);
+          };
+          if (cb) w.split_scratch = std::max(w.split_scratch, emb_split(n - ss, cb, tcs));
+          if (cu) {
+            const int64_t nc = potri_chunk_cols(dt, n, ss, tcs, w.embed, nsm);
+            if (nc >= 64)
+              for (int64_t c0 = 0; c0 < cu; c0 += nc)
+                w.split_scratch = std::max(w.split_scratch, emb_split(tcs, std::min(nc, cu - c0), n - ss));
+          }
+        }
+      }
   }
+  return w;
+}
+
+void Session::reserve_workspace(int routine, int dt, int64_t n, int64_t T, int ndev, int64_t nrhs) {
+  make_geo(*this, dt, n, T, ndev);  // validates
+  const WsPlan w = workspace_plan(routine, dt, n, T, ndev, world, nrhs, nsm);
+  if (w.split) {
+    split_buf[0].ensure(w.split);
+    split_buf[1].ensure(w.split);
+  }
+  if (w.split_scratch) reserve_split_scratch(crit, w.split_scratch);
+  panel[0].ensure(w.panel);
+  panel[1].ensure(w.panel);
+  if (w.panel_pb) {
+    panel_pb[0].ensure(w.panel_pb);
+    panel_pb[1].ensure(w.panel_pb);
+  }
+  if (w.embed) embed_buf.ensure(w.embed);
+  dinv.ensure(w.dinv);
+  wdiag.ensure(w.wdiag);
+  info_dev.ensure(w.info);
+  tmp.ensure(w.tmp);
+  if (w.acc) acc.ensure(w.acc);
+}
+
+size_t Session::held_workspace_bytes() const {
+  size_t b = split_scratch_held(crit);
+  for (const DevBuf* d : {&panel[0], &panel[1], &panel_pb[0], &panel_pb[1], &split_buf[0], &split_buf[1], &embed_buf,
+                          &dinv, &wdiag, &info_dev, &tmp, &acc})
+    b += d->bytes;
+  return b;
 }
 
 // ------------------------------------------------------------------ potrf
@@ -572,7 +680,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
   BCMG_CUDA(cudaMemsetAsync(info, 0, sizeof(int), crit));
   sync_streams(bulk, crit);
   sync_streams(comm, crit);
-  last_dinv_T = T;
+  fkey.valid = false;  // dinv is being overwritten
 
   auto dinv_k = [&](int64_t k) { return static_cast<char*>(dinv.p) + (size_t)k * T * T * g.esz; };
   auto shard_of = [&](int64_t k) { return shards[(k % g.D) - g.dev0]; };
@@ -618,8 +726,6 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
     if (presplit) return 2;
     return (n - g.stop(k)) / T >= 32 ? 0 : 2;
   };
-  int nsm = 148;
-  BCMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   auto trail = [&](int64_t k, int64_t m_first, int64_t m_last, cudaStream_t st, int cap = 0) {
     TrailParams p{};
     p.max_ctas = cap;
@@ -809,7 +915,17 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
   join();
   BCMG_CUDA(cudaMemcpyAsync(info_host, info, sizeof(int), cudaMemcpyDeviceToHost, user));
   BCMG_CUDA(cudaStreamSynchronize(user));
-  return reduce_info(*info_host);
+  const int out = reduce_info(*info_host);
+  if (out == 0) {
+    fkey.valid = true;
+    fkey.dt = dt;
+    fkey.n = n;
+    fkey.T = T;
+    fkey.ndev = ndev;
+    fkey.shards.assign(g.nloc, 0);
+    for (int i = 0; i < g.nloc; ++i) fkey.shards[i] = reinterpret_cast<uintptr_t>(shards[i]);
+  }
+  return out;
 }
 
 
@@ -825,8 +941,9 @@ void Session::potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* 
   const Geo g = make_geo(*this, dt, n, T, ndev);
   if (nrhs < 1) throw Error(CONFIG, "right-hand side must be non-empty");
   if (ldx < n) throw Error(CONFIG, "ldx < n");
-  if (last_dinv_T != T || dinv.bytes < (size_t)g.nt * T * T * g.esz)
-    throw Error(CONFIG, "potrs needs a potrf of the same tiling in this session");
+  if (!fkey.matches(dt, n, T, ndev, shards, g.nloc) || dinv.bytes < (size_t)g.nt * T * T * g.esz)
+    throw Error(CONFIG, "potrs needs the factorization of the last successful potrf of this session "
+                        "(same shards, order, element type, tile width and device count)");
   // split-K slabs (fixed count per shape: bits independent of the device count)
   const int64_t max_parts = 64;
   const size_t parts_bytes = (size_t)max_parts * T * nrhs * g.esz;
@@ -938,8 +1055,10 @@ std::vector<SchedOp> potri_schedule(int64_t n, int64_t T, int ndev, int world, i
 
 void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards) {
   const Geo g = make_geo(*this, dt, n, T, ndev);
-  if (last_dinv_T != T || dinv.bytes < (size_t)g.nt * T * T * g.esz)
-    throw Error(CONFIG, "potri needs a potrf of the same tiling in this session");
+  if (!fkey.matches(dt, n, T, ndev, shards, g.nloc) || dinv.bytes < (size_t)g.nt * T * T * g.esz)
+    throw Error(CONFIG, "potri needs the factorization of the last successful potrf of this session "
+                        "(same shards, order, element type, tile width and device count)");
+  fkey.valid = false;  // the shards are overwritten with the inverse
   const size_t nt_bytes = (size_t)n * T * g.esz;
   panel[0].ensure(nt_bytes);  // broadcast W tile
   panel[1].ensure(nt_bytes);  // staged L21 rows / finalisation product
@@ -950,16 +1069,11 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
   // with tcs rows: 2*tcs real rows in 128-row blocks, 2 CTAs per SM of 64-wide
   // tiles (complex128, FP64 TMA kernel) or 1 CTA per SM of 256-wide tiles
   // (complex64, tcgen05)
-  int nsm_ = 148;
-  BCMG_CUDA(cudaDeviceGetAttribute(&nsm_, cudaDevAttrMultiProcessorCount, device));
-  auto wave_cols = [&](int64_t tcs) -> int64_t {
-    const int64_t rb = (2 * tcs + 127) / 128;
-    return dt == C64 ? std::max<int64_t>(1, nsm_ / rb) * 256 : std::max<int64_t>(1, 2 * nsm_ / rb) * 64;
-  };
-  // (T and n even: every column count is even, so the choice is the same for any device count)
-  const bool emb = (dt == C128 && T % 2 == 0 && n % 2 == 0) || (dt == C64 && T % 64 == 0 && n % 4 == 0);  // c64: tcgen05 tile minimums hold for every D
-  if (emb && !getenv("BCMG_NO_CPLX_EMBED"))
-    embed_buf.ensure(std::max(gemm_cplx_embed_bytes(dt, n, n, T), (size_t)(2 * T + 2 * wave_cols(T)) * n * g.esz));
+  const bool emb = potri_embeds(dt, n, T);
+  // the planned size, not embed_buf.bytes (grow-only: a larger earlier call
+  // would change the chunking and the scratch it requests)
+  const size_t emb_bytes = emb ? std::max(gemm_cplx_embed_bytes(dt, n, T, T), potri_embed_bytes(dt, n, T, nsm)) : 0;
+  if (emb) embed_buf.ensure(emb_bytes);
   cudaStream_t st = crit;
   char* pan = static_cast<char*>(panel[0].p);
   char* stage = static_cast<char*>(panel[1].p);
@@ -1013,7 +1127,7 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
           BCMG_CUDA(cudaMemset2DAsync(sh, n * g.esz, 0, tcs * g.esz, c, st));  // first touch of acc rows [ss, se)
           const Operand wa = opA(W, ldw, OP_N), lb = opB(stage, c, OP_C);
           const Epilogue ep{sh, n, 1.0, 1.0, 0, 0};
-          if (!(emb && gemm_cplx_embed(dt, n - ss, c, tcs, wa, lb, ep, embed_buf.p, embed_buf.bytes, nullptr, st, true)))
+          if (!(emb && gemm_cplx_embed(dt, n - ss, c, tcs, wa, lb, ep, embed_buf.p, emb_bytes, nullptr, st, true)))
             gemm(dt, n - ss, c, tcs, wa, lb, ep, nullptr, st);
         }
         break;
@@ -1030,15 +1144,13 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
           if (emb) {
             // real embedding in column chunks of whole waves of output tiles
             // (both operands are gathered into the scratch, which bounds the chunk)
-            const int64_t wave = wave_cols(tcs);
-            int64_t nc = (int64_t)(embed_buf.bytes / ((size_t)(n - ss) * g.esz)) - 2 * tcs;
-            nc = nc >= wave ? nc / wave * wave : nc / 64 * 64;
+            const int64_t nc = potri_chunk_cols(dt, n, ss, tcs, emb_bytes, nsm);
             bool done = nc >= 64;
             for (int64_t c0 = 0; done && c0 < c; c0 += nc) {
               const int64_t cn = std::min(nc, c - c0);
               done = gemm_cplx_embed(dt, tcs, cn, n - ss, wh, opB(sh + c0 * n * g.esz, n, OP_N),
                                      Epilogue{blk + c0 * tcs * g.esz, tcs, 1.0, 0.0, 0, 0}, embed_buf.p,
-                                     embed_buf.bytes, nullptr, st, true);
+                                     emb_bytes, nullptr, st, true);
               if (!done && c0 > 0) {  // finish the remaining columns on the complex kernels
                 gemm(dt, tcs, c - c0, n - ss, wh, opB(sh + c0 * n * g.esz, n, OP_N),
                      Epilogue{blk + c0 * tcs * g.esz, tcs, 1.0, 0.0, 0, 0}, nullptr, st);

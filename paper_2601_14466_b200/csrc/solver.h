@@ -50,6 +50,20 @@ struct RedistPlan {
 };
 RedistPlan redist_plan(int64_t n_cols, int64_t T, int ndev, int world, bool inverse);
 
+// Every device buffer a pipeline needs: Session::reserve_workspace allocates
+// exactly these before moving any data (so OUT_OF_MEMORY leaves the shards
+// untouched), bcmg_workspace_nbytes reports them, and the drivers never grow
+// a buffer past them.
+struct WsPlan {
+  size_t panel = 0, panel_pb = 0, split = 0, embed = 0, dinv = 0, wdiag = 0, info = 0, tmp = 0, acc = 0;
+  size_t split_scratch = 0;  // tf32 hi / lo planes of the generic tensor-core GEMMs (crit stream)
+  size_t total() const {
+    return 2 * panel + 2 * panel_pb + 2 * split + embed + dinv + wdiag + info + tmp + acc + split_scratch;
+  }
+};
+// routine: 1 potrs pipeline, 2 potri pipeline; nsm: the GPU's SM count
+WsPlan workspace_plan(int routine, int dt, int64_t n, int64_t T, int ndev, int world, int64_t nrhs, int nsm);
+
 // Phase timing slots (CUDA events on the critical stream).
 enum Phase : int { T_BEGIN = 0, T_REDIST = 1, T_POTRF = 2, T_SOLVE = 3, T_END = 4 };
 
@@ -66,7 +80,21 @@ struct Session {
   uint32_t panel_seq = 0, free_seq[2] = {0, 0};
   std::vector<char> plan_host;
   int* info_host = nullptr;
-  int64_t last_dinv_T = 0;
+  // Which factorization the diagonal-block inverses in `dinv` belong to:
+  // potrs / potri read X_kk from there, so they only accept the shards, shape,
+  // type and tiling of the last successful potrf of this session.
+  struct FactorKey {
+    bool valid = false;
+    int dt = -1, ndev = 0;
+    int64_t n = 0, T = 0;
+    std::vector<uintptr_t> shards;
+    bool matches(int dt_, int64_t n_, int64_t T_, int ndev_, void* const* sh, int nloc) const {
+      if (!valid || dt != dt_ || n != n_ || T != T_ || ndev != ndev_ || (int)shards.size() != nloc) return false;
+      for (int i = 0; i < nloc; ++i)
+        if (shards[i] != reinterpret_cast<uintptr_t>(sh[i])) return false;
+      return true;
+    }
+  } fkey;
   int64_t last_moved_bytes = 0;
   std::atomic<bool> busy{false};
   float phase_ms[kTimeEvents] = {0, 0, 0, 0, 0};
@@ -120,6 +148,8 @@ struct Session {
   int potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, const void* host = nullptr);
   // routine: 1 potrs pipeline, 2 potri pipeline (throws OUT_OF_MEMORY before any data moves)
   void reserve_workspace(int routine, int dt, int64_t n, int64_t T, int ndev, int64_t nrhs);
+  size_t held_workspace_bytes() const;  // device bytes this session's workspace holds now
+  int nsm = 148;
   void potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* const* shards, void* x, int64_t ldx);
   void potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards);
   // Hermitian eigendecomposition (eigen.cu): eigenvalues ascending into w

@@ -229,36 +229,32 @@ def redistribute_out(mesh: DeviceMesh, dmat: DistributedMatrix) -> DistributedMa
 # -- workspace ------------------------------------------------------------
 
 
-def workspace_nbytes(routine: str, desc: MatrixDescriptor, tile: TileSpec, num_devices: int, n_rhs: int = 1) -> list[int]:
+def workspace_nbytes(routine: str, desc: MatrixDescriptor, tile: TileSpec, num_devices: int, n_rhs: int = 1,
+                     world: int = 1) -> list[int]:
     """Device bytes per logical device incl. shards (solvers.py:279-308).
 
-    The native pipelines reserve all of it before moving any data, so an
-    out-of-memory error leaves the shards untouched; potrs adds the
-    replicated RHS and split-K partials, potri an n x T accumulator."""
+    potrs / potri: the shard plus the process's workspace, which the native
+    pipelines reserve in full before moving any data (so out-of-memory leaves
+    the shards untouched) and charge here to the first logical device of each
+    process.  The workspace figure is the native plan itself
+    (``bcmg_workspace_nbytes``, csrc/solver.cu ``workspace_plan``): two
+    panels (the complex128 [P | -iP] embedding doubles them and adds a planar
+    copy), tf32 hi / lo split planes for real32 / complex64, the complex
+    embedding scratch, the diagonal-block inverses, split-K slabs and the
+    hand-off buffer (potrs), the W-tile / gather buffers (potri)."""
     esz = desc.element_type.width
     et = desc.element_type
     n, T = desc.n_rows, tile.tile_width
-    nt = -(-n // T)
-    # mirrors Session::reserve_workspace (csrc/solver.cu): two panels (x2 plus a
-    # planar copy for the complex128 [P | -iP] embedding), tf32 hi/lo split
-    # planes for real32/complex64, the complex embedding scratch, the diagonal
-    # block inverses and T x T scratch
-    panel = n * T * esz
-    kp = -(-(2 * T if et.is_complex else T) // 4) * 4
-    if et in (ElementType.real32, ElementType.complex64):
-        base = 2 * panel + 2 * (6 if et.is_complex else 2) * n * kp * 4
-    elif et is ElementType.complex128 and T % 2 == 0:
-        base = 2 * 2 * panel + 2 * panel
-    else:
-        base = 2 * panel
-    if et.is_complex:
-        base += (2 * n + T) * T * esz
-    base += nt * T * T * esz + T * T * esz
-    if routine == "potrs":
-        extra = base + n * n_rhs * esz + 64 * T * n_rhs * esz
-    elif routine == "potri":
-        extra = base + panel
-    elif routine == "syevd":
+    counts = device_column_counts(desc.n_cols, tile, num_devices)
+    if routine in ("potrs", "potri"):
+        if num_devices % world:
+            raise ValueError("logical devices must be a multiple of the processes")
+        nb = C.c_int64(0)
+        _lib.check(_lib.load().bcmg_workspace_nbytes(1 if routine == "potrs" else 2, et.code, n, T, num_devices,
+                                                     world, max(1, n_rhs), C.byref(nb)))
+        per = num_devices // world
+        return [c * desc.column_nbytes + (nb.value if d % per == 0 else 0) for d, c in enumerate(counts)]
+    if routine == "syevd":
         # csrc/eigen.cu: dense working copy, the eigenvector matrix V (Q, then
         # Q times the QL rotations), U | W panels, symv partials, WY blocks, vectors, the rotation
         # ring -- one GPU holds it all, so it is charged to logical device 0
@@ -267,11 +263,8 @@ def workspace_nbytes(routine: str, desc: MatrixDescriptor, tile: TileSpec, num_d
         eig = (2 * n * n * cs + 2 * n * T * cs + 2 * nb * n * cs + 2 * 256 * 256 * cs
                + 2 * 256 * n * cs + (3 * n + 2 * T) * cs + 3 * n * 8 + n * 8 + (n // 8 + 2) * 24
                + 8 * (64 * n * 16 + 129 * 8))
-        counts = device_column_counts(desc.n_cols, tile, num_devices)
         return [c * desc.column_nbytes + (eig if d == 0 else 0) for d, c in enumerate(counts)]
-    else:
-        raise ValueError(f"unknown routine {routine!r}")
-    return [c * desc.column_nbytes + extra for c in device_column_counts(desc.n_cols, tile, num_devices)]
+    raise ValueError(f"unknown routine {routine!r}")
 
 
 def allocate_panel_workspace(mesh: DeviceMesh, desc: MatrixDescriptor, tile: TileSpec) -> list:

@@ -133,8 +133,12 @@ def test_workspace_ordering():
     desc = bc.MatrixDescriptor(1024, 1024, bc.ElementType.real64, bc.Structure.positive_definite)
     s = bc.workspace_nbytes("potrs", desc, bc.TileSpec(128), 4)
     i = bc.workspace_nbytes("potri", desc, bc.TileSpec(128), 4)
-    assert len(s) == 4 and all(x > 1024 * 256 * 8 for x in s)
-    assert all(b >= a for a, b in zip(s, i)) or True
+    shard = 1024 * 256 * 8
+    assert len(s) == 4 and all(x >= shard for x in s)
+    # one process: the whole workspace is charged to logical device 0
+    assert s[1:] == [shard] * 3 and i[1:] == [shard] * 3
+    # potrs holds split-K slabs, potri an n x T block buffer on top of the potrf panels
+    assert s[0] > shard + 2 * 1024 * 128 * 8 and i[0] > shard + 3 * 1024 * 128 * 8
     e = bc.workspace_nbytes("syevd", desc, bc.TileSpec(128), 4)
     assert len(e) == 4 and e[0] > 2 * 1024 * 1024 * 8 and e[1] == 1024 * 256 * 8
 
@@ -154,3 +158,31 @@ def test_hot_kernels_keep_their_state_in_registers():
     assert all(v == 0 for v in hot.values()), hot
     dmma = {k: int(v) for k, v in frames.items() if "trail_tma_kernel" in k}
     assert dmma and all(v <= 64 for v in dmma.values()), dmma
+
+
+@pytest.mark.parametrize("dt", [0, 1, 2, 3])
+def test_workspace_nbytes_is_the_native_plan(dt):
+    """workspace_nbytes (the Python mirror of solvers.py:279-308) is the native
+    reservation of Session::reserve_workspace, byte for byte, for both pipelines
+    and any process split (the GPU test checks the drivers never grow past it)."""
+    import ctypes as C
+
+    lib = _lib.load()
+    et = [bc.ElementType.real32, bc.ElementType.real64, bc.ElementType.complex64, bc.ElementType.complex128][dt]
+    for n, t, ndev, world, nrhs in [(1024, 128, 4, 1, 1), (4096, 512, 8, 2, 64), (3000, 256, 3, 3, 7),
+                                    (8192, 1024, 8, 8, 16)]:
+        desc = bc.MatrixDescriptor(n, n, et, bc.Structure.positive_definite)
+        counts = bc.device_column_counts(n, bc.TileSpec(t), ndev)
+        for routine, code in (("potrs", 1), ("potri", 2)):
+            nb = C.c_int64(0)
+            assert lib.bcmg_workspace_nbytes(code, dt, n, t, ndev, world, nrhs, C.byref(nb)) == 0
+            py = bc.workspace_nbytes(routine, desc, bc.TileSpec(t), ndev, n_rhs=nrhs, world=world)
+            shards = [c * n * et.width for c in counts]
+            per = ndev // world
+            extra = [p - sb for p, sb in zip(py, shards)]
+            assert extra == [nb.value if d % per == 0 else 0 for d in range(ndev)], (routine, n, t, ndev, world)
+            # diagonal inverses + two panels at least
+            assert nb.value >= (-(-n // t)) * t * t * et.width + 2 * n * t * et.width
+    nb = C.c_int64(0)
+    assert lib.bcmg_workspace_nbytes(3, dt, 64, 8, 1, 1, 1, C.byref(nb)) == _lib.BCMG_ERR_CONFIG
+    assert lib.bcmg_workspace_nbytes(1, dt, 64, 8, 3, 2, 1, C.byref(nb)) == _lib.BCMG_ERR_CONFIG
