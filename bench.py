@@ -2,23 +2,35 @@
 """Benchmark of the B200 Cholesky solve path (BASELINE.json metric:
 "potrs TFLOP/s fp64 N=131072 at 1/2/4/8 B200; block-cyclic redistribute GB/s").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--dry-run]
 
 Workload at every GPU count: BASELINE config 3 -- potrs float64 N=131072,
 T_A=1024, N_RHS=64, A row-sharded over the N GPUs (P("x", None)); at N=1 the
 whole 137 GB matrix sits on one 180 GB B200 and is factored in place
 (overwrite_a=True).  Total work is fixed as N grows ("scaling": "strong").
 
+Process model: one process per GPU.  The driver launches N > 1 with
+torch.distributed.run; `python bench.py --gpus N` without a torchrun
+environment launches the N ranks itself the same way (127.0.0.1 rendezvous,
+NCCL_DEBUG=INFO into a per-rank file whose communicator lines rank 0 quotes).
+
 A step is one potrs pipeline on a synthetic SPD matrix already resident in
 HBM: regenerate A in place (potrf destroys it; a write-only device kernel,
 bcmg_generate_spd, kept inside the timed region -- it only makes the number
-conservative), contiguous -> block-cyclic redistribution, tiled potrf, tiled
-substitution.  `value` = algorithmic TFLOP/s (N^3/3 + 2 N^2 N_RHS per step)
-over the max-over-ranks device time of the K timed steps.  `e2e` = the same
-metric through the public drop-in call `potrs(A_host, b_host, T_A, mesh)`
-with A's row block and b in pinned HOST memory and x read back to the host.
-`--impl reference` times the reference's CPU algorithm (the oracle port of
-pkg/src/bcmg/solvers.py on numpy/scipy-openblas) on a bounded sample.
+conservative), contiguous -> block-cyclic redistribution (NVLink peer copies
+between GPUs), tiled potrf, tiled substitution.  `value` = algorithmic TFLOP/s
+(N^3/3 + 2 N^2 N_RHS per step) over the max-over-ranks device time of the K
+timed steps.  `e2e` = the same metric through the public drop-in call
+`potrs(A_host, b_host, T_A, mesh)` with A's row block and b in pinned HOST
+memory and x read back to the host.
+
+`--impl reference` times the reference itself (pkg/src/bcmg, installed
+unmodified into baseline/_ref by `pip install --target`) through its own
+public `solve_positive_definite` on the host cores: each timed step one solve
+at N=4096 with config 3's T_A=1024, 8 devices and N_RHS=64, plus config 1
+exactly and an N ladder with the N^3 extrapolation to N=131072 (labelled).
+Without baseline/_ref it falls back to the oracle port (kind "port").
+`--dry-run` runs the multi-rank host logic on CPU with gloo (no GPU).
 `--n/--t/--nrhs` override the shape (probe runs only).
 """
 
@@ -54,52 +66,135 @@ def workload(world: int, args) -> dict:
                         f"{world}xB200"}
 
 
-# ---------------------------------------------------------------- CPU baseline (oracle port)
-def cpu_baseline(seconds: float = 12.0, n: int = 4096, t: int = 1024, nrhs: int = 64, full_n: int = 131072) -> dict:
-    """The reference's tiled algorithm (oracle/bcmg_oracle.py, a restatement of
-    pkg/src/bcmg/solvers.py potrf/potrs on numpy + scipy-openblas) on host cores."""
+# ---------------------------------------------------------------- CPU baseline (the reference itself)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _host_cores() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+
+        return int(max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count() or 1]))
+    except Exception:
+        return int(os.cpu_count() or 1)
+
+
+def _import_reference():
+    """The unmodified reference package (pip-installed into baseline/_ref), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "bcmg")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import bcmg  # noqa: F401
+        from bcmg import cli as ref_cli  # noqa: F401
+
+        return bcmg
+    except Exception:
+        return None
+
+
+def _ref_solve(bcmg, n: int, t: int, d: int, nrhs: int, seed: int = 1):
+    """One reference solve_positive_definite (solvers.py:931-985) on host arrays;
+    returns (seconds, residual)."""
+    import numpy as np
+    from bcmg import cli as ref_cli
+
+    a = ref_cli.make_matrix("random_spd", n, bcmg.ElementType.real64, seed)
+    b = np.ones((n, nrhs))
+    mesh = bcmg.DeviceMesh(d)
+    t0 = time.perf_counter()
+    x, _ = bcmg.solve_positive_definite(mesh, a, b, bcmg.TileSpec(t))
+    dt = time.perf_counter() - t0
+    res = float(ref_cli.solve_residual(a, x, b)) if hasattr(ref_cli, "solve_residual") else None
+    return dt, res
+
+
+def _port_solve(n: int, t: int, nrhs: int):
+    """The oracle port (oracle/bcmg_oracle.py restates solvers.py:341-474 on numpy/scipy)."""
     import numpy as np
 
     from oracle import bcmg_oracle as O
 
-    try:
-        from threadpoolctl import threadpool_info
-
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count() or 1])
-    except Exception:
-        cores = os.cpu_count() or 1
     a = O.make_matrix("random_spd", n, np.float64, 1)
     b = np.ones((n, nrhs), order="F")
     t0 = time.perf_counter()
-    reps = 0
-    while True:
-        x = O.solve_pipeline(a, b, t)
+    x = O.solve_pipeline(a, b, t)
+    return time.perf_counter() - t0, O.solve_residual(a, x, b)
+
+
+SAMPLE = {"n": 4096, "t": 1024, "d": 8, "nrhs": 64}
+
+
+def cpu_baseline(seconds: float = 12.0, full_n: int = 131072) -> dict:
+    """Bounded sample of the workload on the host cores: reference solves at
+    N=4096 (config 3's T_A, device count and N_RHS) for >= `seconds`."""
+    bcmg = _import_reference()
+    n, t, d, nrhs = SAMPLE["n"], SAMPLE["t"], SAMPLE["d"], SAMPLE["nrhs"]
+    tot, reps, res = 0.0, 0, None
+    while tot < seconds or reps == 0:
+        dt, res = _ref_solve(bcmg, n, t, d, nrhs) if bcmg else _port_solve(n, t, nrhs)
+        tot += dt
         reps += 1
-        if time.perf_counter() - t0 >= seconds:
-            break
-    dt = time.perf_counter() - t0
-    res = O.solve_residual(a, x, b)
-    return {"value": potrs_flops(n, nrhs) * reps / dt / 1e12, "unit": UNIT, "cores": int(cores), "kind": "port",
-            "sample": f"oracle port of the reference tiled potrf+potrs (solvers.py:341-474), f64 N={n} T_A={t} "
-                      f"N_RHS={nrhs}, {reps} solves in {dt:.1f}s, residual {res:.2e}; N^3 extrapolation to "
-                      f"N={full_n} = {dt / reps * (full_n / n) ** 3 / 3600:.1f} h/solve"}
+    per = tot / reps
+    kind = "reference" if bcmg else "port"
+    what = ("reference bcmg.solve_positive_definite (baseline/_ref, unmodified pkg/src/bcmg)" if bcmg else
+            "oracle port of the reference tiled potrf+potrs (solvers.py:341-474)")
+    return {"value": potrs_flops(n, nrhs) / per / 1e12, "unit": UNIT, "cores": _host_cores(), "kind": kind,
+            "sample": f"{what}, f64 N={n} T_A={t} D={d} N_RHS={nrhs}, random_spd seed 1, b = ones; {reps} solves "
+                      f"in {tot:.1f}s ({per:.2f} s/solve, residual {res if res is None else f'{res:.2e}'}); N^3 "
+                      f"extrapolation to N={full_n}: {per * (full_n / n) ** 3 / 3600:.1f} h/solve"}
+
+
+def reference_ladder(bcmg) -> dict:
+    """Config 1 exactly (min / median of 3) and an N ladder at config 3's T_A / D /
+    N_RHS, fitted to N^3 and extrapolated (labelled) to N=32768 and 131072."""
+    import numpy as np
+
+    out = {}
+    c1 = [_ref_solve(bcmg, 2048, 256, 2, 1) for _ in range(3)]
+    ts = sorted(x[0] for x in c1)
+    out["config1"] = {"what": "potrs f64 N=2048, T_A=256, N_RHS=1, DeviceMesh(2), random_spd seed 1, b = ones",
+                      "min_s": ts[0], "median_s": ts[1], "residual": c1[0][1],
+                      "tflops": potrs_flops(2048, 1) / ts[0] / 1e12}
+    pts = []
+    for n in (2048, 4096, 8192):
+        dt, res = _ref_solve(bcmg, n, 1024, 8, 64)
+        pts.append((n, dt))
+        out[f"n{n}"] = {"s": dt, "tflops": potrs_flops(n, 64) / dt / 1e12, "residual": res}
+    # t = c N^3 with c averaged over the two largest points
+    c = float(np.mean([dt / n ** 3 for n, dt in pts[1:]]))
+    out["extrapolated_N3"] = {"n32768_s": c * 32768 ** 3, "n131072_s": c * 131072 ** 3,
+                              "n131072_tflops": potrs_flops(131072, 64) / (c * 131072 ** 3) / 1e12,
+                              "label": "EXTRAPOLATED proportional to N^3 from the N=4096/8192 points, not measured"}
+    return out
 
 
 def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
     k, w = max(1, args.steps), max(0, args.warmup)
-    per = 6.0  # seconds of CPU work per timed step (bounded sample)
+    bcmg = _import_reference()
+    n, t, d, nrhs = SAMPLE["n"], SAMPLE["t"], SAMPLE["d"], SAMPLE["nrhs"]
+    solve = (lambda: _ref_solve(bcmg, n, t, d, nrhs)) if bcmg else (lambda: _port_solve(n, t, nrhs))
     for _ in range(min(w, 1)):
-        cpu_baseline(seconds=1.0)
-    vals = [cpu_baseline(seconds=per) for _ in range(k)]
-    v = sum(x["value"] for x in vals) / len(vals)
+        solve()
+    times, res = [], None
+    for _ in range(k):
+        dt, res = solve()
+        times.append(dt)
+    ms = 1000.0 * sum(times) / len(times)
+    v = potrs_flops(n, nrhs) * len(times) / sum(times) / 1e12
     cfg = workload(world, args)
+    kind = "reference" if bcmg else "port"
+    ladder = reference_ladder(bcmg) if bcmg and not args.no_ladder else None
+    sample = (f"{'reference bcmg.solve_positive_definite (baseline/_ref)' if bcmg else 'oracle port'} f64 N={n} "
+              f"T_A={t} D={d} N_RHS={nrhs} per step (config 3 scaled to a bounded CPU sample), residual {res:.2e}")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": k,
-            "warmup": w, "ms_per_step": per * 1000.0, "higher_is_better": True, "scaling": "strong",
+            "warmup": w, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "reference_sample": vals[0]["sample"]},
-            "cpu_baseline": {**vals[0], "value": v},
+            "config": {"workload": cfg["workload"], "reference_sample": sample, "ladder": ladder},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": _host_cores(), "kind": kind, "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -237,6 +332,27 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     ms = float(ms_t)
     flops = potrs_flops(n, nrhs)
     value = flops * args.steps / (ms * 1e-3) / 1e12
+    # per-phase split of the last timed step (CUDA events inside the pipeline), max over ranks
+    ph = (C.c_float * 4)()
+    _lib.check(lib.bcmg_last_timings(mesh.session, ph))
+    ph_t = torch.tensor([float(v) for v in ph], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ph_t, op=dist.ReduceOp.MAX)
+    phases = {"redistribute_ms": float(ph_t[0]), "potrf_ms": float(ph_t[1]), "potrs_ms": float(ph_t[2]),
+              "pipeline_ms": float(ph_t[3]), "of": "last timed step, max over ranks"}
+    redist_x = None
+    if world > 1:  # the cross-GPU redistribution of the last step: NVLink peer moves between the ranks
+        moved = float(lib.bcmg_last_moved_bytes(mesh.session))
+        egress, ingress = _nvlink_bytes(lib, n, t, world, rank)
+        eg = torch.tensor([egress, ingress], dtype=torch.float64, device=dev)
+        dist.all_reduce(eg, op=dist.ReduceOp.MAX)
+        sec = max(phases["redistribute_ms"], 1e-6) * 1e-3
+        redist_x = {"value": moved / sec / 1e9, "unit": "GB/s", "bytes": moved,
+                    "what": "algorithmic bytes (2 s N x moved columns, whole job) / redistribute phase time",
+                    "nvlink_bytes_per_gpu_max": float(eg[0]), "nvlink_in_bytes_per_gpu_max": float(eg[1]),
+                    "nvlink_gbs_per_gpu": float(eg[0]) / sec / 1e9, "nvlink_peak_gbs": 900.0,
+                    "nvlink_peak_source": "NVLink 5 datasheet, 900 GB/s per direction per GPU (not measured here)",
+                    "path": os.environ.get("BCMG_REDIST_NCCL") and "nccl pack/send/recv" or "in-place P2P rotation"}
 
     # redistribution GB/s: the same matrix as 8 virtual devices on this GPU (D=1 itself is the identity)
     redist = None
@@ -310,9 +426,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                      "step_fraction_of_peak": value / peak.value if peak.value else None},
         "kernels": other,
         "clocks": clocks.summary(),
+        "nccl": _nccl_summary() if world > 1 else None,
         "gpu_launches": int(launches),
         "e2e": e2e,
-        "redistribute": redist,
+        "redistribute": redist if world == 1 else redist_x,
+        "phases": phases,
         "cpu_baseline": cpu_baseline() if world == 1 and not args.no_cpu else None,  # rank 0 at N=1 only
     }
     print(json.dumps(line), flush=True)
@@ -336,6 +454,103 @@ def _profile_traffic():
         return None
 
 
+def _nvlink_bytes(lib, n: int, t: int, world: int, rank: int) -> tuple:
+    """Bytes this rank sends / receives over NVLink in the redistribution (moves whose
+    source and destination segments live on different processes)."""
+    import ctypes as C
+
+    seg, cnt = C.c_int64(0), C.c_int64(0)
+    lib.bcmg_redistribute_plan(n, t, world, world, 0, C.byref(seg), None, 0, C.byref(cnt))
+    mv = (C.c_int64 * (4 * max(cnt.value, 1)))()
+    lib.bcmg_redistribute_plan(n, t, world, world, 0, C.byref(seg), mv, cnt.value, C.byref(cnt))
+    seg_bytes = seg.value * n * 8
+    out = sum(seg_bytes for i in range(cnt.value) if mv[4 * i + 2] == rank and mv[4 * i + 3] != rank)
+    inn = sum(seg_bytes for i in range(cnt.value) if mv[4 * i + 3] == rank and mv[4 * i + 2] != rank)
+    return float(out), float(inn)
+
+
+NCCL_LOG = "/tmp/bcmg_nccl_debug.%h.%p.log"
+
+
+def _nccl_summary():
+    """Communicator facts from the NCCL_DEBUG=INFO file(s) of this host (self-launched runs)."""
+    import glob
+    import re
+
+    lines = []
+    for f in sorted(glob.glob(NCCL_LOG.replace("%h", "*").replace("%p", "*")))[:16]:
+        try:
+            for ln in open(f, errors="replace"):
+                if re.search(r"nranks|NVLS|Init COMPLETE|comm 0x", ln):
+                    lines.append(ln.strip()[:200])
+        except OSError:
+            pass
+    return {"debug_file": NCCL_LOG, "lines": lines[:24]} if lines else None
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` (N > 1) without a torchrun environment: launch the N
+    ranks exactly as the driver does (torch.distributed.run, 127.0.0.1 rendezvous)."""
+    env = dict(os.environ)
+    if not args.dry_run:
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV")
+        env.setdefault("NCCL_DEBUG_FILE", NCCL_LOG)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args, rank: int, world: int) -> None:
+    """Multi-rank host logic on CPU (gloo, no GPU): every rank builds its potrf /
+    potrs schedules and its share of the redistribution plan at the workload
+    shape; the per-rank time is reduced with MAX and rank 0 prints one line."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_14466_b200 import _lib
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg = workload(world, args)
+    n, t, nrhs = cfg["n"], cfg["t"], cfg["nrhs"]
+    lib = _lib.load()
+    t0 = time.perf_counter()
+    counts = {}
+    for routine, name in ((0, "potrf"), (1, "potrs")):
+        cnt = C.c_int64(0)
+        _lib.check(lib.bcmg_schedule(routine, n, t, world, world, rank, nrhs, None, 0, C.byref(cnt)))
+        ops = (C.c_int64 * (7 * cnt.value))()
+        _lib.check(lib.bcmg_schedule(routine, n, t, world, world, rank, nrhs, ops, cnt.value, C.byref(cnt)))
+        counts[name] = {"ops": cnt.value,
+                        "bcast_bytes": 8 * sum(ops[7 * i + 6] for i in range(cnt.value) if ops[7 * i] in (2, 8))}
+    egress, ingress = _nvlink_bytes(lib, n, t, world, rank)
+    ms = (time.perf_counter() - t0) * 1e3
+    red = torch.tensor([ms, egress, ingress], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(red, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        line = {"metric": METRIC, "value": 0.0, "unit": UNIT, "n_gpus": world, "steps": 0, "warmup": 0,
+                "ms_per_step": float(red[0]), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "dry_run": True,
+                "config": {"workload": cfg["workload"], "n": n, "tile": t, "n_rhs": nrhs, "backend": "gloo (CPU)"},
+                "schedule_rank0": counts, "nvlink_bytes_per_gpu_max": float(red[1]),
+                "nvlink_in_bytes_per_gpu_max": float(red[2])}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -346,12 +561,18 @@ def main():
     ap.add_argument("--t", type=int, default=0)
     ap.add_argument("--nrhs", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-ladder", action="store_true", help="reference arm: skip the config 1 / N ladder")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank host logic on CPU (gloo), no GPU")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", args.gpus))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.dry_run:
+        return run_dry(args, rank, world)
     run_ours(args, rank, world, local_rank)
 
 

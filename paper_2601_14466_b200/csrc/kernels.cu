@@ -675,25 +675,30 @@ void tck_gemm(int64_t M, int64_t N, int64_t K, const float* ah, const float* al,
 }
 
 // gemm() for float32 on tcgen05: both operands split into a scratch owned by
-// the calling thread and stream (grow-only; stream order makes reuse safe).
+// the stream (grow-only; stream order makes reuse safe).  Process-wide
+// registry: a session releases its streams' scratch when it closes, so a new
+// stream that happens to reuse a closed stream's handle starts empty.
+namespace {
+struct SplitBuf {
+  void* p = nullptr;
+  size_t n = 0;
+};
+std::mutex g_split_mu;
+std::vector<std::pair<cudaStream_t, SplitBuf>> g_split;
+}  // namespace
+
 static float* split_scratch(cudaStream_t st, size_t bytes, size_t* held) {
-  struct Buf {
-    void* p = nullptr;
-    size_t n = 0;
-  };
-  thread_local std::vector<std::pair<cudaStream_t, Buf>> bufs;
+  std::lock_guard<std::mutex> lk(g_split_mu);
+  SplitBuf* b = nullptr;
+  for (auto& e : g_split)
+    if (e.first == st) b = &e.second;
   if (held) {  // query only
-    *held = 0;
-    for (auto& e : bufs)
-      if (e.first == st) *held = e.second.n;
+    *held = b ? b->n : 0;
     return nullptr;
   }
-  Buf* b = nullptr;
-  for (auto& e : bufs)
-    if (e.first == st) b = &e.second;
   if (!b) {
-    bufs.emplace_back(st, Buf{});
-    b = &bufs.back().second;
+    g_split.emplace_back(st, SplitBuf{});
+    b = &g_split.back().second;
   }
   if (b->n < bytes) {
     if (b->p) {
@@ -712,15 +717,26 @@ static float* split_scratch(cudaStream_t st, size_t bytes, size_t* held) {
   return static_cast<float*>(b->p);
 }
 
-// Grow the calling thread's split scratch for `st` ahead of a schedule loop:
-// growth frees the old buffer (cudaFree synchronises the device), which must
-// not happen while another rank's stream waits for a flag this thread has yet
-// to raise (peer-memory mode).
+// Grow the split scratch of `st` ahead of a schedule loop: growth frees the
+// old buffer (cudaFree synchronises the device), which must not happen while
+// another rank's stream waits for a flag this rank has yet to raise.
 void reserve_split_scratch(cudaStream_t st, size_t bytes) { split_scratch(st, bytes); }
 size_t split_scratch_held(cudaStream_t st) {
   size_t h = 0;
   split_scratch(st, 0, &h);
   return h;
+}
+void release_split_scratch(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_split_mu);
+  for (size_t i = 0; i < g_split.size(); ++i)
+    if (g_split[i].first == st) {
+      if (g_split[i].second.p) {
+        cudaStreamSynchronize(st);
+        cudaFree(g_split[i].second.p);
+      }
+      g_split.erase(g_split.begin() + i);
+      return;
+    }
 }
 size_t split_scratch_bytes(int dt, int64_t M, int64_t N, int64_t K) {
   return dt == C64 ? (size_t)2 * (2 * M + N) * split_ld(2 * K) * 4 : (size_t)2 * (M + N) * split_ld(K) * 4;

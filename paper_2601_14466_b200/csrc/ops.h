@@ -58,7 +58,8 @@ void tck_gemm(int64_t M, int64_t N, int64_t K, const float* ah, const float* al,
               const Epilogue* fan_src = nullptr);
 bool tc_presplit_enabled();
 void reserve_split_scratch(cudaStream_t st, size_t bytes);
-size_t split_scratch_held(cudaStream_t st);  // bytes the calling thread's scratch for st holds
+size_t split_scratch_held(cudaStream_t st);  // bytes the scratch of st holds
+void release_split_scratch(cudaStream_t st);  // before the stream is destroyed
 size_t split_scratch_bytes(int dt, int64_t M, int64_t N, int64_t K);  // a GEMM's tf32 split planes
 
 // Diagonal tile: in-place lower Cholesky of the n x n block at A (lda) and

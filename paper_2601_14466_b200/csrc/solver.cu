@@ -90,9 +90,10 @@ Session::~Session() {
     }
   for (auto& e : ev_spare) cudaEventDestroy(e);
   if (info_host) cudaFreeHost(info_host);
-  cudaStreamDestroy(crit);
-  cudaStreamDestroy(bulk);
-  cudaStreamDestroy(comm);
+  for (cudaStream_t st : {crit, bulk, comm}) {
+    release_split_scratch(st);
+    cudaStreamDestroy(st);
+  }
 }
 
 cudaEvent_t Session::ev(int i) { return ev_pool[i % kEvents]; }
