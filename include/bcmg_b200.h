@@ -187,6 +187,18 @@ int bcmg_last_timings(bcmg_session* s, float* ms /* [4] */);
 /* algorithmic bytes (read + write) moved by the last redistribution */
 int64_t bcmg_last_moved_bytes(bcmg_session* s);
 
+/* MPMD / isolated-namespace handle exchange (reference runtime.py:170-233
+   HandleRegistry / _TokenChannel, publish_handle / open_handle :390-406):
+   export any device address of this process as a 72-byte token (CUDA IPC
+   handle of its allocation + the offset inside it); another process on the
+   node opens the token into its own address space (NVLink peer memory on
+   another GPU).  Opening is cached per allocation; a process cannot open its
+   own tokens (CONFIG).  bcmg_ipc_close_all unmaps every opened token. */
+#define BCMG_IPC_TOKEN_BYTES 72
+int bcmg_ipc_export(const void* ptr, unsigned char* token /* [72] */);
+int bcmg_ipc_open(const unsigned char* token /* [72] */, void** ptr);
+int bcmg_ipc_close_all(void);
+
 /* Device workspace of one process for a pipeline (routine 1: potrs, 2:
    potri), excluding the shards: the exact bytes bcmg_potrs / bcmg_potri
    reserve before moving any data (reference solvers.py:279-308

@@ -64,6 +64,9 @@ SIGNATURES = {
     "bcmg_last_moved_bytes": (C.c_int64, [_vp]),
     "bcmg_workspace_nbytes": (C.c_int, [C.c_int, C.c_int, _i64, _i64, C.c_int, C.c_int, _i64, _i64p]),
     "bcmg_session_workspace_bytes": (C.c_int, [_vp, _i64p]),
+    "bcmg_ipc_export": (C.c_int, [_vp, C.c_char_p]),
+    "bcmg_ipc_open": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
+    "bcmg_ipc_close_all": (C.c_int, []),
     "bcmg_set_profiling": (C.c_int, [_vp, C.c_int]),
     "bcmg_kernel_stats": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_double)]),
     "bcmg_launch_count": (C.c_int64, []),

@@ -456,6 +456,33 @@ int bcmg_workspace_nbytes(int routine, int dtype, int64_t n, int64_t tile, int n
   });
 }
 
+int bcmg_ipc_export(const void* ptr, unsigned char* token) {
+  return guarded([&] {
+    if (!ptr || !token) throw bcmg::Error(BCMG_ERR_CONFIG, "null pointer");
+    static_assert(sizeof(bcmg::IpcHandle) == BCMG_IPC_TOKEN_BYTES, "token layout");
+    const bcmg::IpcHandle h = bcmg::ipc_export(ptr);
+    std::memcpy(token, &h, sizeof(h));
+  });
+}
+
+int bcmg_ipc_open(const unsigned char* token, void** ptr) {
+  return guarded([&] {
+    if (!ptr || !token) throw bcmg::Error(BCMG_ERR_CONFIG, "null pointer");
+    bcmg::IpcHandle h;
+    std::memcpy(&h, token, sizeof(h));
+    try {
+      *ptr = bcmg::ipc_import(h);
+    } catch (const bcmg::Error& e) {
+      // cudaIpcOpenMemHandle refuses this process's own allocations and stale handles
+      throw bcmg::Error(BCMG_ERR_CONFIG, std::string("cannot open handle token: ") + e.what());
+    }
+  });
+}
+
+int bcmg_ipc_close_all(void) {
+  return guarded([&] { bcmg::ipc_close_all(); });
+}
+
 int bcmg_session_workspace_bytes(bcmg_session* s, int64_t* bytes) {
   return guarded([&] { *bytes = (int64_t)live(s)->held_workspace_bytes(); });
 }

@@ -8,7 +8,9 @@
 #include <chrono>
 #include <climits>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <deque>
 #include <map>
 #include <mutex>
@@ -25,16 +27,111 @@ namespace bcmg {
     if (r_ != ncclSuccess) throw Error(CUDA, std::string(#call) + ": " + ncclGetErrorString(r_));     \
   } while (0)
 
+// ------------------------------------------------------------------ CUDA IPC
+namespace {
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+AddrRangeFn addr_range_fn() {
+  static const AddrRangeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (AddrRangeFn) nullptr;
+    }
+    return reinterpret_cast<AddrRangeFn>(f);
+  }();
+  return fn;
+}
+}  // namespace
+
+IpcHandle ipc_export(const void* ptr) {
+  IpcHandle h{};
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (!addr_range_fn()) throw Error(CUDA, "cuMemGetAddressRange unavailable");
+  const CUresult r = addr_range_fn()(&base, &size, reinterpret_cast<CUdeviceptr>(ptr));
+  if (r != CUDA_SUCCESS) throw Error(CONFIG, "address is not inside a device allocation (" + std::to_string((int)r) + ")");
+  cudaIpcMemHandle_t mh;
+  BCMG_CUDA(cudaIpcGetMemHandle(&mh, reinterpret_cast<void*>(base)));
+  static_assert(sizeof(mh) == sizeof(h.bytes), "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(h.bytes, &mh, sizeof(mh));
+  h.offset = reinterpret_cast<uint64_t>(ptr) - (uint64_t)base;
+  return h;
+}
+
+// Imported allocations, one mapping per exporter allocation (opening the same
+// handle twice in a process is not allowed).
+class IpcCache {
+ public:
+  void* import(const IpcHandle& h) {
+    std::lock_guard<std::mutex> lk(mu_);
+    const std::string key(reinterpret_cast<const char*>(h.bytes), sizeof(h.bytes));
+    auto it = map_.find(key);
+    void* base = nullptr;
+    if (it != map_.end()) {
+      base = it->second;
+    } else {
+      cudaIpcMemHandle_t mh;
+      std::memcpy(&mh, h.bytes, sizeof(mh));
+      BCMG_CUDA(cudaIpcOpenMemHandle(&base, mh, cudaIpcMemLazyEnablePeerAccess));
+      map_[key] = base;
+    }
+    return static_cast<char*>(base) + h.offset;
+  }
+  void close_all() {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (auto& e : map_) cudaIpcCloseMemHandle(e.second);
+    map_.clear();
+  }
+  ~IpcCache() { close_all(); }
+
+ private:
+  std::mutex mu_;
+  std::map<std::string, void*> map_;
+};
+
+namespace {
+IpcCache& global_ipc() {
+  static IpcCache* c = new IpcCache();  // process lifetime (closed explicitly by ipc_close_all)
+  return *c;
+}
+}  // namespace
+void* ipc_import(const IpcHandle& h) { return global_ipc().import(h); }
+void ipc_close_all() { global_ipc().close_all(); }
+
+int nccl_max_ctas() {
+  static const int v = [] {
+    const char* e = getenv("BCMG_NCCL_MAX_CTAS");
+    return e && *e ? std::max(1, atoi(e)) : 8;
+  }();
+  return v;
+}
+
 // ------------------------------------------------------------------ NCCL
 class NcclComm final : public Comm {
  public:
   NcclComm(int rank, int world, const unsigned char* id) {
     ncclUniqueId u;
     std::memcpy(&u, id, sizeof(u));
-    BCMG_NCCL_CALL(ncclCommInitRank(&c_, world, u, rank));
+    // at most nccl_max_ctas() CTAs per collective: the trailing-update grid
+    // leaves that many SMs free while an NCCL panel broadcast may be in flight
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.maxCTAs = nccl_max_ctas();
+    cfg.minCTAs = 1;
+    BCMG_NCCL_CALL(ncclCommInitRankConfig(&c_, world, u, rank, &cfg));
+    world_ = world;
+    me_ = rank;
+    BCMG_CUDA(cudaMalloc(&scratch_, 256));
+    BCMG_CUDA(cudaMemset(scratch_, 0, 256));
   }
   ~NcclComm() override {
+    ipc_.close_all();
     if (c_) ncclCommDestroy(c_);
+    if (scratch_) cudaFree(scratch_);
+  }
+  void barrier(cudaStream_t st) override {
+    BCMG_NCCL_CALL(ncclAllReduce(scratch_, scratch_, 1, ncclInt32, ncclSum, c_, st));
   }
   void bcast(void* buf, size_t bytes, int root, cudaStream_t st) override {
     BCMG_NCCL_CALL(ncclBroadcast(buf, buf, bytes, ncclUint8, root, c_, st));
@@ -48,41 +145,59 @@ class NcclComm final : public Comm {
   }
   void group_end() override { BCMG_NCCL_CALL(ncclGroupEnd()); }
   std::vector<void*> exchange_pointers(void* local) override {
-    // CUDA IPC handles of every rank's allocation, all-gathered over NCCL
-    int world = 0, me = 0;
-    BCMG_NCCL_CALL(ncclCommCount(c_, &world));
-    BCMG_NCCL_CALL(ncclCommUserRank(c_, &me));
-    cudaIpcMemHandle_t h;
-    BCMG_CUDA(cudaIpcGetMemHandle(&h, local));
+    // every rank's (IPC handle, offset, ok) all-gathered over NCCL, then opened
+    struct Rec {
+      IpcHandle h;
+      int32_t ok, pad;
+    };
+    Rec mine{};
+    try {
+      mine.h = ipc_export(local);
+      mine.ok = 1;
+    } catch (const Error&) {
+      cudaGetLastError();
+      mine.ok = 0;
+    }
     void* dev = nullptr;
-    BCMG_CUDA(cudaMalloc(&dev, sizeof(h) * (size_t)(world + 1)));
-    std::vector<cudaIpcMemHandle_t> all(world);
+    BCMG_CUDA(cudaMalloc(&dev, sizeof(Rec) * (size_t)(world_ + 1)));
+    std::vector<Rec> all(world_);
     cudaStream_t st;
     BCMG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    BCMG_CUDA(cudaMemcpyAsync(static_cast<char*>(dev) + sizeof(h) * world, &h, sizeof(h), cudaMemcpyHostToDevice, st));
-    BCMG_NCCL_CALL(ncclAllGather(static_cast<char*>(dev) + sizeof(h) * world, dev, sizeof(h), ncclUint8, c_, st));
-    BCMG_CUDA(cudaMemcpyAsync(all.data(), dev, sizeof(h) * world, cudaMemcpyDeviceToHost, st));
+    char* d = static_cast<char*>(dev);
+    BCMG_CUDA(cudaMemcpyAsync(d + sizeof(Rec) * world_, &mine, sizeof(Rec), cudaMemcpyHostToDevice, st));
+    BCMG_NCCL_CALL(ncclAllGather(d + sizeof(Rec) * world_, d, sizeof(Rec), ncclUint8, c_, st));
+    BCMG_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(Rec) * world_, cudaMemcpyDeviceToHost, st));
+    BCMG_CUDA(cudaStreamSynchronize(st));
+    std::vector<void*> out(world_, nullptr);
+    int ok = 1;
+    for (int r = 0; r < world_; ++r) ok &= all[r].ok;
+    if (ok) {
+      for (int r = 0; r < world_ && ok; ++r) {
+        if (r == me_) {
+          out[r] = local;
+          continue;
+        }
+        try {
+          out[r] = ipc_.import(all[r].h);
+        } catch (const Error&) {
+          cudaGetLastError();
+          ok = 0;
+        }
+      }
+    }
+    // every rank must agree (an import can fail on one rank only)
+    int* flag = reinterpret_cast<int*>(d);
+    BCMG_CUDA(cudaMemcpyAsync(flag, &ok, sizeof(int), cudaMemcpyHostToDevice, st));
+    BCMG_NCCL_CALL(ncclAllReduce(flag, flag, 1, ncclInt32, ncclMin, c_, st));
+    BCMG_CUDA(cudaMemcpyAsync(&ok, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     BCMG_CUDA(cudaStreamSynchronize(st));
     cudaStreamDestroy(st);
     cudaFree(dev);
-    std::vector<void*> out(world, nullptr);
-    for (int r = 0; r < world; ++r) {
-      if (r == me) {
-        out[r] = local;
-        continue;
-      }
-      BCMG_CUDA(cudaIpcOpenMemHandle(&out[r], all[r], cudaIpcMemLazyEnablePeerAccess));
-    }
-    me_ = me;
+    if (!ok) return {};
     return out;
   }
-  void release_pointers(std::vector<void*>& ptrs) override {
-    for (int r = 0; r < (int)ptrs.size(); ++r)
-      if (r != me_ && ptrs[r]) cudaIpcCloseMemHandle(ptrs[r]);
-    ptrs.clear();
-  }
-  // opt-in (BCMG_P2P=1) until the fused path has been measured across GPUs
-  bool peer_default() const override { return false; }
+  // mappings stay cached (per exporter allocation) until the transport closes
+  void release_pointers(std::vector<void*>& ptrs) override { ptrs.clear(); }
   int allreduce_min(int v, void* scratch, cudaStream_t st) override {
     int* d = static_cast<int*>(scratch);
     BCMG_CUDA(cudaMemcpyAsync(d, &v, sizeof(int), cudaMemcpyHostToDevice, st));
@@ -96,7 +211,9 @@ class NcclComm final : public Comm {
 
  private:
   ncclComm_t c_ = nullptr;
-  int me_ = 0;
+  int me_ = 0, world_ = 1;
+  void* scratch_ = nullptr;
+  IpcCache ipc_;
 };
 
 // ------------------------------------------------------------------ loopback
@@ -137,6 +254,11 @@ struct Hub {
     int count = 0, reads = 0;
   };
   std::map<uint64_t, Gather> gathers;
+  struct Barrier {
+    std::vector<cudaEvent_t> ev;
+    int count = 0, reads = 0;
+  };
+  std::map<uint64_t, Barrier> barriers;
 };
 
 std::mutex g_hubs_mu;
@@ -276,7 +398,31 @@ class LoopbackComm final : public Comm {
     return out;
   }
   void release_pointers(std::vector<void*>& ptrs) override { ptrs.clear(); }
-  bool peer_default() const override { return false; }
+
+  void barrier(cudaStream_t st) override {
+    const uint64_t seq = bar_seq_++;
+    cudaEvent_t mine = new_event();
+    BCMG_CUDA(cudaEventRecord(mine, st));
+    std::vector<cudaEvent_t> others;
+    {
+      std::unique_lock<std::mutex> lk(hub_->mu);
+      auto& b = hub_->barriers[seq];
+      if (b.ev.empty()) b.ev.assign(hub_->world, nullptr);
+      b.ev[rank_] = mine;
+      b.count++;
+      hub_->cv.notify_all();
+      hub_wait(lk, [&] { return hub_->barriers[seq].count == hub_->world; });
+      others = hub_->barriers[seq].ev;
+    }
+    for (int r = 0; r < (int)others.size(); ++r)
+      if (r != rank_) BCMG_CUDA(cudaStreamWaitEvent(st, others[r], 0));
+    std::unique_lock<std::mutex> lk(hub_->mu);
+    auto& b = hub_->barriers[seq];
+    if (++b.reads == hub_->world) {  // everyone has enqueued its waits: the events may go
+      for (cudaEvent_t e : b.ev) cudaEventDestroy(e);
+      hub_->barriers.erase(seq);
+    }
+  }
 
   int allreduce_min(int v, void*, cudaStream_t) override {
     const uint64_t seq = red_seq_++;
@@ -305,7 +451,7 @@ class LoopbackComm final : public Comm {
   };
   const int rank_;
   std::shared_ptr<Hub> hub_;
-  uint64_t bc_seq_ = 0, red_seq_ = 0, gather_seq_ = 0;
+  uint64_t bc_seq_ = 0, red_seq_ = 0, gather_seq_ = 0, bar_seq_ = 0;
   std::vector<PendingSend> sends_;
   std::vector<PendingRecv> recvs_;
 };
@@ -334,6 +480,31 @@ void stream_wait_geq(cudaStream_t st, const void* addr, unsigned v) {
   const CUresult r = wait_fn()(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), v,
                                CU_STREAM_WAIT_VALUE_GEQ);
   if (r != CUDA_SUCCESS) throw Error(CUDA, "cuStreamWaitValue32 failed (" + std::to_string((int)r) + ")");
+}
+
+namespace {
+typedef CUresult (*WriteValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValueFn write_fn() {
+  static const WriteValueFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (WriteValueFn) nullptr;
+    }
+    return reinterpret_cast<WriteValueFn>(f);
+  }();
+  return fn;
+}
+}  // namespace
+
+bool stream_write_value(cudaStream_t st, void* addr, unsigned v) {
+  if (!write_fn()) return false;
+  // default flags: the write is ordered after (and made visible after) every
+  // earlier memory operation of the stream, copies included
+  return write_fn()(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), v,
+                    CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS;
 }
 
 void make_loopback_id(unsigned char* id) {

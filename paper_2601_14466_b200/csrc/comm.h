@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstddef>
+#include <cstdint>
 #include <memory>
 #include <vector>
 
@@ -34,19 +35,29 @@ class Comm {
   virtual void group_end() = 0;
   // host value in, minimum over ranks out (synchronous); scratch: 4 device bytes
   virtual int allreduce_min(int v, void* scratch, cudaStream_t st) = 0;
+  // stream-ordered barrier: work enqueued on st after it starts only once every
+  // rank's stream has reached its barrier (no kernel waits on another rank
+  // in the loopback transport; across GPUs it is one 4-byte NCCL all-reduce)
+  virtual void barrier(cudaStream_t st) = 0;
   // Peer memory (NVLink P2P through CUDA IPC handles; the shared address space
-  // of loopback ranks): every rank contributes the base of one cudaMalloc
-  // allocation and gets all ranks' bases mapped into its own address space
-  // (collective, same call order on every rank).  Empty if unsupported.
+  // of loopback ranks): every rank contributes one device address (any
+  // address inside a cudaMalloc allocation) and gets every rank's address
+  // mapped into its own address space (collective, same call order on every
+  // rank; mappings are cached per allocation and closed with the transport).
+  // Empty if unsupported on any rank (all ranks agree).
   virtual std::vector<void*> exchange_pointers(void* local) = 0;
   virtual void release_pointers(std::vector<void*>& ptrs) = 0;
-  // peer-memory hand-offs by default?  No for now: on request (BCMG_P2P=1)
-  // only.  Loopback ranks share one context, where a context-wide
-  // synchronisation (lazy kernel loading, cudaFree) waits for streams parked
-  // on flags that the synchronising rank has yet to raise; across GPUs the
-  // path has not been measured yet, so NCCL's broadcast stays the default.
-  virtual bool peer_default() const = 0;
 };
+
+// CUDA IPC export / import of any device address (the allocation's handle plus
+// the offset inside it; reference runtime.py HandleRegistry publish / open).
+struct IpcHandle {
+  unsigned char bytes[64];
+  uint64_t offset;
+};
+IpcHandle ipc_export(const void* ptr);
+void* ipc_import(const IpcHandle& h);  // cached per allocation; owner process may not import its own
+void ipc_close_all();                  // closes every imported mapping
 
 // Stream-ordered flags for peer-memory hand-offs: `signal` stores v to a
 // (possibly peer) 32-bit word from a one-thread kernel; `wait_geq` blocks the
@@ -54,6 +65,12 @@ class Comm {
 bool stream_wait_supported();
 void stream_wait_geq(cudaStream_t st, const void* addr, unsigned v);
 void stream_signal(cudaStream_t st, void* const* addrs, int n, unsigned v);
+// the same store as a stream memory operation (no kernel, no SM: issued by
+// the stream front end after everything earlier on st, with a memory
+// barrier); false if the driver refused it (nothing enqueued)
+bool stream_write_value(cudaStream_t st, void* addr, unsigned v);
+
+int nccl_max_ctas();  // CTA limit of the NCCL communicators (BCMG_NCCL_MAX_CTAS, default 8)
 
 constexpr size_t kCommIdBytes = 128;
 // id: kCommIdBytes from bcmg_nccl_unique_id (NCCL) or bcmg_loopback_id (loopback)

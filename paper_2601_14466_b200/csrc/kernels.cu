@@ -1384,6 +1384,7 @@ __global__ void __launch_bounds__(256) rotate_kernel(RotateJob j) {
     }
     *reinterpret_cast<W*>(__ldg(j.addr + b) + off) = carry;
   }
+  if (j.sys_fence) __threadfence_system();  // peer stores performed before the stream moves on
 }
 
 // Bulk-copy rotation (16-byte aligned segments): work item = (cycle, chunk of

@@ -117,6 +117,7 @@ struct RotateJob {
   int64_t n_cycles, total_lanes;
   int vec;                   // 16, 8 or 4
   int bulk;                  // 1: cp.async.bulk chunks of rotate_bulk_chunk() bytes (vec == 16)
+  int sys_fence = 0;         // 1: members include peer (NVLink) memory: system-scope fence at the end
 };
 void rotate_cycles(const RotateJob& j, cudaStream_t st);
 int64_t rotate_bulk_chunk();

@@ -222,7 +222,16 @@ void Session::redistribute(int dt, int64_t n_rows, int64_t n_cols, int64_t T, in
   // BCMG_STAGED_REDIST=1 routes a single process through the staged
   // (cross-process) algorithm too, so one GPU exercises its pack/unpack path.
   const char* staged = getenv("BCMG_STAGED_REDIST");
-  if (world > 1 || (staged && atoi(staged))) return redistribute_multi(dt, n_rows, n_cols, T, ndev, shards, inverse);
+  const char* nccl_env = getenv("BCMG_REDIST_NCCL");
+  if (world > 1 && !(nccl_env && atoi(nccl_env)) && redistribute_p2p(dt, n_rows, n_cols, T, ndev, shards, inverse)) {
+    last_redist_path = 1;
+    return;
+  }
+  if (world > 1 || (staged && atoi(staged))) {
+    last_redist_path = 2;
+    return redistribute_multi(dt, n_rows, n_cols, T, ndev, shards, inverse);
+  }
+  last_redist_path = 0;
   last_moved_bytes = 0;
   SegPlan plan = segment_plan(n_cols, T, ndev, inverse);
   const int64_t nc = (int64_t)plan.offsets.size() - 1;
@@ -276,7 +285,97 @@ void Session::redistribute(int dt, int64_t n_rows, int64_t n_cols, int64_t T, in
   sync_streams(user, crit);
 }
 
-// ------------------------------------------------------------------ cross-process redistribution
+// ------------------------------------------------------------------ cross-process redistribution (P2P)
+// The reference rotates every cycle in place with peer copies and two staging
+// columns (layout.py:191-256).  Across processes the shards
+// of every rank are mapped into each rank's address space (CUDA IPC over
+// NVLink; the shared address space of loopback ranks) and the SAME in-place
+// rotation kernel runs over them: every cycle's bytes are split into `world`
+// equal lane ranges and rank r rotates range r of every cycle -- each lane is
+// read from all its members into registers and written to the successors by
+// one thread, so no staging buffer and no pack/unpack passes: HBM traffic is
+// the algorithmic 2 s N per moved column, and a rank's NVLink traffic is the
+// members of its ranges that live on other ranks (read once, written once;
+// for 1D block-cyclic shapes this equals the point-to-point minimum on
+// average).  Stream-ordered barriers before (every rank's shards final) and
+// after (every peer store performed) -- no kernel waits on another rank.
+bool Session::redistribute_p2p(int dt, int64_t n_rows, int64_t n_cols, int64_t T, int ndev, void* const* shards,
+                               bool inverse) {
+  const int esz = dtype_size(dt);
+  const int nloc = ndev / world;
+  // every rank's i-th local shard, in this process's address space
+  std::vector<std::vector<void*>> peer(nloc);
+  for (int i = 0; i < nloc; ++i) {
+    peer[i] = net->exchange_pointers(shards[i]);
+    if ((int)peer[i].size() != world) return false;  // collective outcome: all ranks fall back together
+  }
+  last_moved_bytes = 0;
+  const SegPlan plan = segment_plan(n_cols, T, ndev, inverse);
+  const int64_t nc = (int64_t)plan.offsets.size() - 1;
+  if (nc == 0) return true;
+  const auto counts = column_counts(n_cols, T, ndev);
+  std::vector<int64_t> off(ndev, 0);
+  for (int d = 1; d < ndev; ++d) off[d] = off[d - 1] + counts[d - 1];
+  const int64_t col_bytes = n_rows * esz;
+  auto member_addr = [&](int64_t seg_pos) {
+    const int64_t pos = seg_pos * plan.seg;
+    const int d = (int)(std::upper_bound(off.begin(), off.end(), pos) - off.begin()) - 1;
+    return reinterpret_cast<uint64_t>(peer[d % nloc][d / nloc]) + (uint64_t)((pos - off[d]) * col_bytes);
+  };
+  int vec = (col_bytes % 16 == 0) ? 16 : (col_bytes % 8 == 0 ? 8 : 4);
+  for (const auto& pv : peer)
+    for (void* q : pv) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(q);
+      while (vec > 4 && a % vec) vec /= 2;
+    }
+  // this rank's lane range of every cycle
+  std::vector<uint64_t> addr;
+  std::vector<int64_t> offs{0}, lane_pref{0}, seg_bytes;
+  double my_bytes = 0;
+  for (int64_t c = 0; c < nc; ++c) {
+    const int64_t sb = plan.seg_cols[c] * col_bytes, lanes = sb / vec;
+    const int64_t lo = lanes * rank / world, hi = lanes * (rank + 1) / world;
+    const int64_t m = plan.offsets[c + 1] - plan.offsets[c];
+    last_moved_bytes += 2 * m * sb;
+    if (hi <= lo) continue;
+    for (int64_t i = plan.offsets[c]; i < plan.offsets[c + 1]; ++i)
+      addr.push_back(member_addr(plan.members[i]) + (uint64_t)(lo * vec));
+    offs.push_back((int64_t)addr.size());
+    lane_pref.push_back(lane_pref.back() + (hi - lo));
+    seg_bytes.push_back((hi - lo) * vec);
+    my_bytes += 2.0 * (double)m * (double)((hi - lo) * vec);
+  }
+  const int64_t np = (int64_t)seg_bytes.size();
+  const size_t bytes = addr.size() * 8 + (np + 1) * 8 * 2 + np * 8;
+  plan_host.resize(std::max<size_t>(bytes, 8));
+  char* h = plan_host.data();
+  std::memcpy(h, addr.data(), addr.size() * 8);
+  std::memcpy(h + addr.size() * 8, offs.data(), (np + 1) * 8);
+  std::memcpy(h + addr.size() * 8 + (np + 1) * 8, lane_pref.data(), (np + 1) * 8);
+  std::memcpy(h + addr.size() * 8 + (np + 1) * 16, seg_bytes.data(), np * 8);
+  plan_buf.ensure(std::max<size_t>(bytes, 8));
+  char* dptr = static_cast<char*>(plan_buf.p);
+  if (np) BCMG_CUDA(cudaMemcpyAsync(dptr, h, bytes, cudaMemcpyHostToDevice, crit));
+  RotateJob j;
+  j.addr = reinterpret_cast<const uint64_t*>(dptr);
+  j.offsets = reinterpret_cast<const int64_t*>(dptr + addr.size() * 8);
+  j.lane_pref = reinterpret_cast<const int64_t*>(dptr + addr.size() * 8 + (np + 1) * 8);
+  j.seg_bytes = reinterpret_cast<const int64_t*>(dptr + addr.size() * 8 + (np + 1) * 16);
+  j.n_cycles = np;
+  j.total_lanes = lane_pref.back();
+  j.vec = vec;
+  j.bulk = 0;
+  j.sys_fence = 1;
+  net->barrier(crit);  // every rank's shards hold their final contiguous data
+  timed(K_ROTATE, crit, my_bytes, [&] { rotate_cycles(j, crit); });
+  net->barrier(crit);  // every rank's peer stores have landed
+  // (cudaMemcpyAsync from pageable memory returns once the source is consumed)
+  sync_streams(user, crit);
+  return true;
+}
+
+// ------------------------------------------------------------------ cross-process redistribution (staged NCCL)
+// Fallback (BCMG_REDIST_NCCL=1, or shards that cannot be peer-mapped).
 // Same segment-level cycle plan on every process.  A move c_i -> c_{i+1}
 // between processes becomes an NCCL send/recv pair; a move inside a process a
 // device copy.  In place with bounded staging: the segments are processed in
@@ -421,11 +520,16 @@ std::vector<SchedOp> potrf_schedule(int64_t n, int64_t T, int ndev, int world, i
     if (world > 1) push(S_BCAST, STREAM_COMM, k, 0, 0, g.owner_rank(k), (n - s1) * (s1 - s0));
     const bool look = g.owns(k + 1);
     if (look) push(S_UPDATE, STREAM_CRIT, k, k + 1, k + 2, 0, 0);
+    // world > 1, owner of k+1: factor k+1 right after its lookahead update, on
+    // the whole GPU, and start the bulk update after it (root field = 2) --
+    // the others need panel k+1 as soon as they finish step k
+    const bool first = look && world > 1;
+    if (first) push(S_FACTOR, STREAM_CRIT, k + 1, 0, 0, 0, 0);
     // bulk: root field = 1 when the grid is capped to leave SMs to the lookahead path
-    push(S_UPDATE, STREAM_BULK, k, look ? k + 2 : k + 1, g.nt, look ? 1 : 0, 0);
+    push(S_UPDATE, STREAM_BULK, k, look ? k + 2 : k + 1, g.nt, first ? 2 : look ? 1 : 0, 0);
     if (g.owns(k)) push(S_COPYBACK, STREAM_BULK, k, 0, 0, 0, 0);
     push(S_STEP_END, STREAM_BULK, k, look ? 1 : 0, 0, 0, 0);
-    if (look) push(S_FACTOR, STREAM_CRIT, k + 1, 0, 0, 0, 0);
+    if (look && !first) push(S_FACTOR, STREAM_CRIT, k + 1, 0, 0, 0, 0);
   }
   return ops;
 }
@@ -633,14 +737,28 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
   const bool cplx_dt = dt == C128 || dt == C64;
   if (cplx_dt) embed_buf.ensure(gemm_cplx_embed_bytes(dt, n, T, T));  // panel solve by real embedding
   auto embed_k = [&](int64_t k) { return embed && complex_embed_ok(dt, n - g.stop(k), T); };
-  // Peer-memory mode (world > 1): the panel solve's epilogue writes panel k
-  // straight into every process's panel buffer over NVLink (GEMM fused with
-  // its broadcast); stream-ordered flags replace the NCCL broadcast.  sig
-  // words (uint32): [b] panel in buffer b ready (written by the owner),
-  // [2 + 16 b + r] process r done with buffer b (written by r).
-  const char* p2p_env = getenv("BCMG_P2P");
-  const bool p2p = world > 1 && world <= MAX_FAN + 1 && stream_wait_supported() &&
-                   (p2p_env ? atoi(p2p_env) != 0 : net->peer_default());
+  // Panel broadcast (world > 1), BCMG_PANEL_BCAST = ce | fan | nccl:
+  //   ce   (default) the owner pushes panel k into every process's panel
+  //        buffer with copy-engine peer copies (cudaMemcpyAsync over NVLink
+  //        between CUDA-IPC-mapped buffers) and raises the receivers' ready
+  //        flags with stream memory operations: no SM takes part, so the
+  //        hand-off never queues behind a persistent trailing-update grid;
+  //   fan  the panel solve's epilogue writes every element also into each
+  //        peer's buffer (the GEMM fused with its broadcast);
+  //   nccl ncclBroadcast (the fallback when peers cannot be mapped).
+  // sig words (uint32): [b] panel in buffer b ready (written by the owner),
+  // [2 + 16 b + r] process r done with buffer b (written by r).  Receivers
+  // park a stream on cuStreamWaitValue32; no kernel waits on another rank.
+  enum { BC_NCCL = 0, BC_CE = 1, BC_FAN = 2 };
+  int bc_mode = BC_NCCL;
+  if (world > 1) {
+    const char* m = getenv("BCMG_PANEL_BCAST");
+    const char* legacy = getenv("BCMG_P2P");  // round-1 name of the fan-out mode
+    bc_mode = m ? (!strcmp(m, "fan") ? BC_FAN : !strcmp(m, "nccl") ? BC_NCCL : BC_CE)
+                : (legacy ? (atoi(legacy) ? BC_FAN : BC_NCCL) : BC_CE);
+    if (!stream_wait_supported() || (bc_mode == BC_FAN && world > MAX_FAN + 1)) bc_mode = BC_NCCL;
+  }
+  bool p2p = bc_mode != BC_NCCL;
   std::vector<void*> fan_panel[2];
   uint32_t seq0 = 0;
   auto sig_word = [&](int r, int idx) { return static_cast<void*>(static_cast<uint32_t*>(peer_sig[r]) + idx); };
@@ -654,15 +772,31 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
       BCMG_CUDA(cudaDeviceSynchronize());
       peer_sig = net->exchange_pointers(sig.p);
     }
-    for (int b2 = 0; b2 < 2; ++b2) {
+    for (int b2 = 0; b2 < 2 && !peer_sig.empty(); ++b2) {
       net->release_pointers(peer_panel[b2]);
       peer_panel[b2] = net->exchange_pointers(panel[b2].p);
-      for (int r = 0; r < world; ++r)
+      for (int r = 0; r < (int)peer_panel[b2].size(); ++r)
         if (r != rank) fan_panel[b2].push_back(peer_panel[b2][r]);
     }
+    // every rank sees the same exchange outcome (collective agreement in exchange_pointers)
+    if (peer_sig.empty() || peer_panel[0].empty() || peer_panel[1].empty()) {
+      p2p = false;
+      bc_mode = BC_NCCL;
+      fan_panel[0].clear();
+      fan_panel[1].clear();
+    }
+  }
+  if (p2p) {
     seq0 = panel_seq;
     panel_seq += (uint32_t)g.nt + 4;
   }
+  last_bcast_mode = bc_mode;
+  // raise flag words on peers (stream memory operation; a one-thread kernel if the driver refuses)
+  auto signal = [&](cudaStream_t st, const std::vector<void*>& flags, uint32_t v) {
+    bool ok = true;
+    for (void* f : flags) ok = ok && stream_write_value(st, f, v);
+    if (!ok) stream_signal(st, flags.data(), (int)flags.size(), v);
+  };
   auto seq_of = [&](int64_t k) { return seq0 + (uint32_t)k + 1; };
   // peers done with buffer b before panel k is written into it: their last use
   // was panel k - 2 (or the last panel in b of the previous call)
@@ -698,7 +832,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
       timed(K_TRSM, crit, cf * 2.0 * (double)(n - s1) * tc * tc, [&] {
         const Operand a21 = opA(colp(sh, g, s1, g.loc(k)), n, OP_N), xh = opB(dinv_k(k), T, OP_C);
         Epilogue ep{panel[k % 2].p, n - s1, 1.0, 0.0, 0, 0};
-        if (p2p) {  // the panel solve's epilogue also writes every peer's copy of the panel
+        if (bc_mode == BC_FAN) {  // the panel solve's epilogue also writes every peer's copy of the panel
           ep.nfan = (int)fan_panel[k % 2].size();
           for (int e = 0; e < ep.nfan; ++e) ep.fan[e] = fan_panel[k % 2][e];
         }
@@ -727,6 +861,11 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
     if (presplit) return 2;
     return (n - g.stop(k)) / T >= 32 ? 0 : 2;
   };
+  // world > 1 with the NCCL broadcast: the NCCL kernels need SMs on every
+  // rank while the bulk grid runs, so the grid leaves the communicator's CTA
+  // limit free (NcclComm caps its CTAs at BCMG_NCCL_MAX_CTAS, default 8)
+  int bulk_cap = 0;
+  if (world > 1 && bc_mode == BC_NCCL) bulk_cap = std::max(1, nsm - nccl_max_ctas());
   auto trail = [&](int64_t k, int64_t m_first, int64_t m_last, cudaStream_t st, int cap = 0) {
     TrailParams p{};
     p.max_ctas = cap;
@@ -848,21 +987,36 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
     switch (op.kind) {
       case S_FACTOR:  // F(k) overwrites panel buffer k%2, last used by panel k-2
         if (k >= 2) BCMG_CUDA(cudaStreamWaitEvent(crit, E(FREE, k - 2), 0));
-        if (p2p && s1 < n) wait_peers_free(k, crit);
+        if (bc_mode == BC_FAN && s1 < n) wait_peers_free(k, crit);
         factor(k);
-        if (p2p && s1 < n) {  // panel k is in every peer's buffer: raise their ready flags
+        if (bc_mode == BC_FAN && s1 < n) {  // panel k is in every peer's buffer: raise their ready flags
           std::vector<void*> flags;
           for (int r = 0; r < world; ++r)
             if (r != rank) flags.push_back(sig_word(r, b));
-          stream_signal(crit, flags.data(), (int)flags.size(), seq_of(k));
+          signal(crit, flags, seq_of(k));
           BCMG_CUDA(cudaEventRecord(E(C, k), crit));
         }
         BCMG_CUDA(cudaEventRecord(E(R, k), crit));
         break;
       case S_BCAST:  // panel k reaches every process
+        if (bc_mode == BC_CE && mine) {  // copy-engine push into every peer's buffer b, then the ready flags
+          const size_t bytes = (size_t)op.elems * g.esz;
+          BCMG_CUDA(cudaStreamWaitEvent(comm, E(R, k), 0));
+          wait_peers_free(k, comm);
+          std::vector<void*> flags;
+          for (int r = 0, e = 0; r < world; ++r) {
+            if (r == rank) continue;
+            if (bytes) BCMG_CUDA(cudaMemcpyAsync(fan_panel[b][e], panel[b].p, bytes, cudaMemcpyDeviceToDevice, comm));
+            flags.push_back(sig_word(r, b));
+            ++e;
+          }
+          signal(comm, flags, seq_of(k));
+          BCMG_CUDA(cudaEventRecord(E(C, k), comm));
+          break;
+        }
         if (p2p) {
           if (mine) break;
-          stream_wait_geq(comm, my_word(b), seq_of(k));  // written by the owner's fused panel solve
+          stream_wait_geq(comm, my_word(b), seq_of(k));  // raised by the owner after its copies / fused solve
           BCMG_CUDA(cudaEventRecord(E(C, k), comm));
           if (embed_k(k)) expand_panel(dt, panel[b].p, panel_pb[b].p, n - s1, s1 - g.start(k), comm);
           split_panel(k, comm);
@@ -889,7 +1043,15 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
           // first; otherwise both persistent grids would race for the SMs and
           // the critical path could be queued behind the whole bulk update
           if (op.root) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(U, k), 0));
-          trail(k, op.a, op.b, bulk, op.root ? std::max(1, nsm - reserve_at(k)) : 0);
+          if (op.root == 2) {
+            // owner first (world > 1): panel k+1 is factored and solved on the
+            // whole GPU before this process's bulk update, so the other
+            // processes receive it while they are still busy with step k
+            BCMG_CUDA(cudaStreamWaitEvent(bulk, E(R, k + 1), 0));
+            trail(k, op.a, op.b, bulk, bulk_cap);
+          } else {
+            trail(k, op.a, op.b, bulk, op.root ? std::max(1, nsm - reserve_at(k)) : 0);
+          }
         }
         break;
       case S_COPYBACK:  // factor below the diagonal back into A (potrs/potri read it there)
@@ -905,7 +1067,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
           std::vector<void*> flags;
           for (int r = 0; r < world; ++r)
             if (r != rank) flags.push_back(sig_word(r, 2 + 16 * b + rank));
-          stream_signal(bulk, flags.data(), (int)flags.size(), seq_of(k));
+          signal(bulk, flags, seq_of(k));
           free_seq[b] = seq_of(k);
         }
         break;

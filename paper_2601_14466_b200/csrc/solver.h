@@ -142,6 +142,11 @@ struct Session {
   void redistribute(int dt, int64_t n_rows, int64_t n_cols, int64_t T, int ndev, void* const* shards, bool inverse);
   void redistribute_multi(int dt, int64_t n_rows, int64_t n_cols, int64_t T, int ndev, void* const* shards,
                           bool inverse);
+  // world > 1: in-place rotation over peer-mapped shards (false: peers not mappable, nothing done)
+  bool redistribute_p2p(int dt, int64_t n_rows, int64_t n_cols, int64_t T, int ndev, void* const* shards,
+                        bool inverse);
+  int last_redist_path = 0;  // 0 single process, 1 P2P rotation, 2 NCCL pack/exchange/unpack
+  int last_bcast_mode = 0;   // potrf panel broadcast: 0 NCCL (or none), 1 copy engines, 2 fused fan-out
   DevBuf stage_buf, desc_buf;
   // host != nullptr: shards[0] (one device) is filled from pinned host memory
   // (same layout) while the factorisation starts (see solver.cu)

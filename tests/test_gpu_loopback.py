@@ -117,14 +117,22 @@ def _potrs_ranks(a, b, n, t, ndev, world, dtype):
     (np.float64, 300, 32, 2, 2), (np.float64, 512, 64, 4, 2), (np.complex128, 260, 24, 4, 2),
     (np.float32, 384, 64, 4, 4), (np.complex64, 200, 40, 2, 2), (np.float64, 2048, 256, 4, 2),
 ])
-def test_loopback_potrs_matches_single_process(dtype, n, t, ndev, world, monkeypatch):
-    """Transport broadcasts between the ranks: the single-process bits."""
+@pytest.mark.parametrize("paths", ["ce+p2p", "nccl+staged"])
+def test_loopback_potrs_matches_single_process(dtype, n, t, ndev, world, paths, monkeypatch):
+    """The single-process bits, with either set of cross-process paths:
+    ce+p2p      -- the defaults: copy-engine panel pushes into peer-mapped panel
+                   buffers with stream-memory-operation flags, and the in-place
+                   peer rotation of the redistribution;
+    nccl+staged -- the transport's broadcast and the pack / send+recv / unpack
+                   redistribution (the fallbacks)."""
     a = O.make_matrix("random_spd", n, dtype, 11)
     b = np.asfortranarray(np.random.default_rng(2).standard_normal((n, 3)).astype(dtype))
     mesh = bc.make_mesh(ndev)
     base, _ = bc.solve_positive_definite(mesh, a, b, bc.TileSpec(t))
     mesh.close()
-    monkeypatch.setenv("BCMG_P2P", "0")
+    monkeypatch.delenv("BCMG_P2P", raising=False)
+    monkeypatch.setenv("BCMG_PANEL_BCAST", "ce" if paths == "ce+p2p" else "nccl")
+    monkeypatch.setenv("BCMG_REDIST_NCCL", "0" if paths == "ce+p2p" else "1")
     xs = _potrs_ranks(a, b, n, t, ndev, world, dtype)
     for x in xs:
         assert np.array_equal(x, base), "solution differs from the single-process bits"
@@ -134,7 +142,9 @@ def test_loopback_potrs_matches_single_process(dtype, n, t, ndev, world, monkeyp
 @pytest.mark.parametrize("dtype,n,t,ndev,world", [
     (np.float64, 256, 32, 2, 2), (np.complex128, 192, 24, 4, 2), (np.float64, 1024, 128, 4, 4),
 ])
-def test_loopback_potri_matches_single_process(dtype, n, t, ndev, world):
+@pytest.mark.parametrize("redist", ["p2p", "staged"])
+def test_loopback_potri_matches_single_process(dtype, n, t, ndev, world, redist, monkeypatch):
+    monkeypatch.setenv("BCMG_REDIST_NCCL", "0" if redist == "p2p" else "1")
     lib = _lib.load()
     a = O.make_matrix("random_spd", n, dtype, 12)
     base, _ = bc.invert_positive_definite(bc.make_mesh(ndev), a, bc.TileSpec(t))
@@ -174,3 +184,54 @@ def test_loopback_not_positive_definite_info_on_every_rank():
 
     for rc, info in _run_ranks(world, body):
         assert rc == _lib.BCMG_ERR_NOT_POSITIVE_DEFINITE and info == 71
+
+
+@pytest.mark.parametrize("redist", ["p2p", "staged"])
+@pytest.mark.parametrize("dtype,n_rows,n,t,ndev,world", [
+    (np.float64, 40, 64, 8, 4, 2), (np.float64, 33, 48, 5, 4, 4), (np.complex64, 17, 30, 3, 2, 2),
+    (np.float32, 64, 96, 7, 6, 3), (np.complex128, 128, 512, 64, 8, 4), (np.float64, 1024, 4096, 256, 8, 2),
+])
+def test_loopback_redistribution_bit_exact(dtype, n_rows, n, t, ndev, world, redist, monkeypatch):
+    """Cross-process redistribution, both paths: the in-place rotation over
+    peer-mapped shards (each rank rotates its lane range of every cycle) and the
+    staged NCCL fallback -- bit-exact dealing (oracle deal_columns, the
+    reference's execute_plan result) and an exact round trip."""
+    import torch
+
+    monkeypatch.setenv("BCMG_REDIST_NCCL", "0" if redist == "p2p" else "1")
+    from conftest import numbered_columns
+
+    lib = _lib.load()
+    a = numbered_columns(n_rows, n, dtype)
+    want = O.deal_columns(a, t, ndev)
+    arr = (C.c_int64 * ndev)()
+    _lib.check(lib.bcmg_column_counts(n, t, ndev, arr))
+    counts = list(arr)
+    nloc = ndev // world
+    blocks, ptrs = [], []
+    for r in range(world):
+        c0 = sum(counts[: r * nloc])
+        c1 = c0 + sum(counts[r * nloc:(r + 1) * nloc])
+        blk = torch.from_numpy(np.ascontiguousarray(a[:, c0:c1].T)).to("cuda")
+        p, off = [], 0
+        for d in range(r * nloc, (r + 1) * nloc):
+            p.append(blk.data_ptr() + off * n_rows * blk.element_size())
+            off += counts[d]
+        blocks.append((blk, c0, c1))
+        ptrs.append(_lib.ptr_array(p))
+    torch.cuda.synchronize()
+
+    def body(r, sess, st):
+        for direction in (0, 1):
+            _lib.check(lib.bcmg_redistribute(sess, C.c_void_p(st.cuda_stream), CODES[dtype], n_rows, n, t, ndev,
+                                             ptrs[r], direction))
+            st.synchronize()
+            if direction == 0:
+                blk, c0, c1 = blocks[r]
+                got = blk.cpu().numpy().T
+                assert np.array_equal(got, want[:, c0:c1]), f"rank {r}: dealt columns differ"
+        return r
+
+    _run_ranks(world, body)
+    for blk, c0, c1 in blocks:
+        assert np.array_equal(blk.cpu().numpy().T, a[:, c0:c1]), "round trip differs"
