@@ -54,10 +54,21 @@ template <class TL>
 constexpr int tma_box_rows_b() { return TL::LDB; }
 template <class TL>
 constexpr unsigned tma_stage_bytes() { return (unsigned)(TL::BK * (TL::LDA + TL::LDB) * 8); }
-// Dynamic shared memory: STAGES operand stages | 2*STAGES mbarriers | 512-byte
-// aux area (producer state [0,384), caller state [384,512)) -- the producer's
-// bookkeeping lives here, not in registers every consumer thread would pay for.
-constexpr int TMA_AUX_BYTES = 512;
+// One output block: rows [a_row + m0 ...) of A's map, [b_row + n0 ...) of B's map.
+struct TmaBlock {
+  int a_row, b_row;      // tensor-map row coordinate of the block's first A / B row
+  int64_t m0, n0;        // block origin inside the output (for the epilogue)
+  int64_t M, N;          // output extent (rows >= M / cols >= N are not stored)
+  Epilogue ep;
+  int live;              // 0: no more items (sentinel slot)
+};
+// Dynamic shared memory: STAGES operand stages | 2*STAGES mbarriers | aux area:
+// producer state [0,384), caller state [384,512), then a ring of decoded work
+// items [512, ...) -- the producer decodes every item once and publishes it
+// here, so neither the producer's bookkeeping nor the consumers' view of the
+// current item occupies registers next to the DMMA accumulators.
+constexpr int TMA_RING = 8;
+constexpr int TMA_AUX_BYTES = 512 + TMA_RING * (int)sizeof(TmaBlock);
 template <class TL>
 constexpr size_t tma_smem_bytes() {
   return (size_t)TL::STAGES * tma_stage_bytes<TL>() + 2 * TL::STAGES * 8 + TMA_AUX_BYTES;
@@ -68,20 +79,16 @@ __device__ __forceinline__ unsigned char* tma_aux() {
   return tma_dyn_smem + (size_t)TL::STAGES * tma_stage_bytes<TL>() + 2 * TL::STAGES * 8;
 }
 
-// One output block: rows [a_row + m0 ...) of A's map, [b_row + n0 ...) of B's map.
-struct TmaBlock {
-  int a_row, b_row;      // tensor-map row coordinate of the block's first A / B row
-  int64_t m0, n0;        // block origin inside the output (for the epilogue)
-  int64_t M, N;          // output extent (rows >= M / cols >= N are not stored)
-  Epilogue ep;
-};
-
-// Persistent producer/consumer loop.  `next_p(item, blk)` / `next_c(item, blk)`
-// fill the block of work item `item` (producer / consumer view; separate so
-// stateful cursors stay monotone) and return false when there is none.
-template <class TL, bool FAN = true, class NextP, class NextC>
+// Persistent producer/consumer loop.  `next_p(item, blk)` fills the block of
+// work item `item` (called by the producer thread only, items increasing) and
+// returns false when there is none.  The producer publishes each decoded item
+// in the aux ring before issuing its first slice; the consumers read it after
+// waiting for that slice (mbarrier release / acquire orders the ring store).
+// When the items run out the producer publishes a sentinel (live = 0) and
+// completes the next stage's barrier without a transfer.
+template <class TL, bool FAN = true, class NextP>
 __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUtensorMap* mapB, int K, NextP&& next_p,
-                                              NextC&& next_c, long long stagger_ns = 0) {
+                                              long long stagger_ns = 0) {
   double* smem = reinterpret_cast<double*>(tma_dyn_smem);
   constexpr int NW = TL::THREADS / 32;
   constexpr unsigned STAGE_BYTES = tma_stage_bytes<TL>();
@@ -106,40 +113,53 @@ __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUt
   // consumer warps no registers: slice counter gp over (item, kt)
   struct Prod {
     int64_t item;
-    TmaBlock blk;
-    uint32_t gp;
-    int kt, live;
+    uint32_t gp, seq;
+    int kt, live, done;
   };
   static_assert(sizeof(Prod) <= 384, "producer state must fit its aux slot");
   Prod& ps = *reinterpret_cast<Prod*>(tma_aux<TL>());
+  TmaBlock* ring = reinterpret_cast<TmaBlock*>(tma_aux<TL>() + 512);
   auto produce_one = [&]() {
-    if (!ps.live) return;
+    if (ps.done) return;
     const uint32_t gp = ps.gp;
     const int s = gp % TL::STAGES, kt = ps.kt;
     mbar_wait(&empty[s], ((gp / TL::STAGES) & 1) ^ 1);
+    TmaBlock& blk = ring[ps.seq % TMA_RING];
+    if (!ps.live) {  // sentinel: the consumers find live == 0 behind this stage's barrier
+      blk.live = 0;
+      mbar_arrive(&full[s]);
+      ps.done = 1;
+      return;
+    }
     double* st = smem + s * STAGE_WORDS;
     mbar_expect_tx(&full[s], STAGE_BYTES);
-    tma_load_2d(st, mapA, ps.blk.a_row + (int)ps.blk.m0, kt * TL::BK, &full[s]);
-    tma_load_2d(st + TL::BK * TL::LDA, mapB, ps.blk.b_row + (int)ps.blk.n0, kt * TL::BK, &full[s]);
+    tma_load_2d(st, mapA, blk.a_row + (int)blk.m0, kt * TL::BK, &full[s]);
+    tma_load_2d(st + TL::BK * TL::LDA, mapB, blk.b_row + (int)blk.n0, kt * TL::BK, &full[s]);
     ps.gp = gp + 1;
     if (kt + 1 == KT) {
       ps.kt = 0;
       ps.item += gridDim.x;
-      ps.live = next_p(ps.item, ps.blk);
+      ps.seq += 1;
+      TmaBlock& nb = ring[ps.seq % TMA_RING];  // consumed TMA_RING items ago (ring > stages)
+      ps.live = next_p(ps.item, nb);
+      nb.live = ps.live;
     } else {
       ps.kt = kt + 1;
     }
   };
+  static_assert(TMA_RING > TL::STAGES, "a ring slot must outlive the producer's run-ahead");
   if (tid == 0) {
     ps.item = blockIdx.x;
     ps.gp = 0;
+    ps.seq = 0;
     ps.kt = 0;
-    ps.live = next_p(ps.item, ps.blk);
+    ps.done = 0;
+    ps.live = next_p(ps.item, ring[0]);
+    ring[0].live = ps.live;
     for (int i = 0; i < TL::STAGES - 1; ++i) produce_one();
   }
 
   uint32_t g = 0;
-  TmaBlock cb;
   // C tile prefetch into L2 a few slices before the epilogue: all CTAs reach
   // their epilogues at nearly the same time (uniform items), and without it
   // the read-modify-write of 128 KB per CTA would stall every SM on HBM.
@@ -161,14 +181,16 @@ __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUt
     const long long t0 = clock64();
     while (clock64() - t0 < stagger_ns * 2) __nanosleep(1000);  // ~2 cycles per ns at ~2 GHz
   }
-  for (int64_t item = blockIdx.x; next_c(item, cb); item += gridDim.x) {
+  for (uint32_t seq = 0;; ++seq) {
+    const TmaBlock& cb = ring[seq % TMA_RING];
     Acc<TL, false> acc;
     acc.zero();
     for (int kt = 0; kt < KT; ++kt) {
-      if (kt == (KT > PREFETCH_AHEAD ? KT - PREFETCH_AHEAD : 0)) prefetch_c(cb);
       if (tid == 0) produce_one();
       const int s = g % TL::STAGES;
       mbar_wait(&full[s], (g / TL::STAGES) & 1);
+      if (kt == 0 && !cb.live) return;  // sentinel (published before this barrier completed)
+      if (kt == (KT > PREFETCH_AHEAD ? KT - PREFETCH_AHEAD : 0)) prefetch_c(cb);
       const double* st = smem + s * STAGE_WORDS;
       mma_slice<TL, false, false, false>(acc, st, st + TL::BK * TL::LDA, nullptr, nullptr, wm0, wn0, lane);
       __syncwarp();
@@ -326,10 +348,9 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
   // producer's cursor (thread 0 only) in the caller aux slot: no registers in the consumers
   Cursor& cp = *reinterpret_cast<Cursor*>(tma_aux<TL>() + 384);
   if (threadIdx.x == 0) cp = Cursor{p.m_first, 0, -1};
-  Cursor cc{p.m_first, 0, -1};
   tma_gemm_loop<TL, false>(  // trailing updates never fan out
       &mapA, &mapB, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, TmaBlock& blk) { return decode(cp, item, blk); },
-      [&](int64_t item, TmaBlock& blk) { return decode(cc, item, blk); }, p.stagger_ns);
+      p.stagger_ns);
 }
 
 // Single GEMM C := alpha A B^H (+ beta C) with A (M x K) and B (N x K) both
@@ -352,7 +373,7 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
     blk.ep = ep;
     return true;
   };
-  tma_gemm_loop<TL>(&mapA, &mapB, (int)K, decode, decode);
+  tma_gemm_loop<TL>(&mapA, &mapB, (int)K, decode);
 }
 
 }  // namespace bcmg

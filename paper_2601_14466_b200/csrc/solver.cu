@@ -64,7 +64,16 @@ Session::Session(int device_, int rank_, int world_, const unsigned char* nccl_i
   for (auto& e : ev_time) BCMG_CUDA(cudaEventCreate(&e));
   BCMG_CUDA(cudaMallocHost(&info_host, sizeof(int)));
   BCMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
-  if (world > 1) net = make_comm(rank, world, nccl_id);
+  if (world > 1) {
+    net = make_comm(rank, world, nccl_id);
+    // flag words of the peer-memory hand-offs, zeroed here: nothing inside a
+    // schedule may synchronise the whole device (loopback ranks share one
+    // context, and another rank's stream may be parked on a flag that only
+    // this rank's later work raises)
+    sig.ensure(256 * sizeof(uint32_t));
+    BCMG_CUDA(cudaMemset(sig.p, 0, 256 * sizeof(uint32_t)));
+    BCMG_CUDA(cudaDeviceSynchronize());
+  }
 }
 
 Session::~Session() {
@@ -766,12 +775,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
   if ((dt == R32 || dt == C64) && tc_presplit_enabled())  // the panel solves' split planes, sized up front
     reserve_split_scratch(crit, split_scratch_bytes(dt, n, T, T));
   if (p2p) {
-    if (peer_sig.empty()) {
-      sig.ensure(256 * sizeof(uint32_t));
-      BCMG_CUDA(cudaMemset(sig.p, 0, 256 * sizeof(uint32_t)));
-      BCMG_CUDA(cudaDeviceSynchronize());
-      peer_sig = net->exchange_pointers(sig.p);
-    }
+    if (peer_sig.empty()) peer_sig = net->exchange_pointers(sig.p);  // zeroed in the constructor
     for (int b2 = 0; b2 < 2 && !peer_sig.empty(); ++b2) {
       net->release_pointers(peer_panel[b2]);
       peer_panel[b2] = net->exchange_pointers(panel[b2].p);

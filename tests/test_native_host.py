@@ -156,8 +156,9 @@ def test_hot_kernels_keep_their_state_in_registers():
     hot = {k: int(v) for k, v in frames.items() if "tck_trail_kernel" in k or "tck_gemm_kernel" in k}
     assert len(hot) >= 4, sorted(frames)[:5]
     assert all(v == 0 for v in hot.values()), hot
-    dmma = {k: int(v) for k, v in frames.items() if "trail_tma_kernel" in k}
-    assert dmma and all(v <= 64 for v in dmma.values()), dmma
+    # the DMMA kernels keep their work-item state in shared memory (gemm_tma.cuh ring): no frame either
+    dmma = {k: int(v) for k, v in frames.items() if "trail_tma_kernel" in k or "gemm_tma_kernel" in k}
+    assert len(dmma) >= 4 and all(v == 0 for v in dmma.values()), dmma
 
 
 @pytest.mark.parametrize("dt", [0, 1, 2, 3])
