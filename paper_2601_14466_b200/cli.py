@@ -20,8 +20,12 @@ numpy Philox(key=seed), cli.py:81-103 -- host-generated, O(n^3)),
 for large n) and ``file:PATH`` (a BCMG matrix file, core.py:255-303; ``gen``
 writes one, cli.py:449-458).  Routines: potrs, potri and syevd (eigen-residual,
 orthonormality, ascending order and the diag(1..n) spectrum, cli.py:320-337).
-Out of scope here: the mpmd mode and copy transcripts
-(``--trace``); they are rejected as configuration errors.
+Modes (``--mode`` or ``$BCMG_MODE``, cli.py:62-64, 242-256): ``spmd`` -- one
+session with every logical device in one address space; ``mpmd`` -- one
+isolated worker (own session, own shard allocation) per logical device, shards
+reached only through the transport's handle exchange (isolated.py); both give
+the same bits.  Out of scope: copy transcripts (``--trace``),
+rejected as a configuration error.
 """
 
 from __future__ import annotations
@@ -34,7 +38,7 @@ import sys
 
 import numpy as np
 
-from . import _lib
+from . import _lib, isolated
 from .core import (ConvergenceError, DescriptorError, ElementType, MatrixFileError, NotPositiveDefiniteError,
                    OutOfDeviceMemoryError, TileSpec, read_matrix, write_matrix)
 from .mesh import DeviceMesh
@@ -205,9 +209,22 @@ def build_parser() -> argparse.ArgumentParser:
     return parser
 
 
+MODE_ENV_VAR = "BCMG_MODE"
+CLI_MODES = ("spmd", "mpmd")
+
+
+def _resolve_mode(args) -> str:
+    """--mode, else $BCMG_MODE, else spmd (cli.py:242-248)."""
+    import os
+
+    mode = args.mode if args.mode is not None else os.environ.get(MODE_ENV_VAR, "spmd")
+    if mode not in CLI_MODES:
+        raise DescriptorError("type-structure", f"{MODE_ENV_VAR}={mode!r} is not one of {CLI_MODES}")
+    return mode
+
+
 def _check_scope(args) -> None:
-    if (args.mode or "spmd") != "spmd":
-        raise DescriptorError("type-structure", "only the spmd mode is supported (mpmd: DESIGN.md §7)")
+    args.mode = _resolve_mode(args)
     if args.trace:
         raise DescriptorError("type-structure", "--trace: the GPU rotation keeps no copy transcript")
     if args.matrix.startswith("file:"):
@@ -249,7 +266,8 @@ def _verify_one(args, a, et, kind, tile, devices):
     n = a.shape[0]
     res_tol = args.tolerance if args.tolerance is not None else _residual_tol(et, n)
     elem_tol = args.tolerance if args.tolerance is not None else _elementwise_tol(et)
-    mesh = DeviceMesh(devices)
+    mpmd = args.mode == "mpmd"
+    mesh = None if mpmd else DeviceMesh(devices)
     checks = []
     try:
         if args.routine == "potrs":
@@ -259,7 +277,8 @@ def _verify_one(args, a, et, kind, tile, devices):
                     raise DescriptorError("type-structure", "right-hand side element type does not match the matrix")
             else:
                 b = np.ones((n, args.nrhs), dtype=et.dtype, order="F")
-            x, _ = solve_positive_definite(mesh, a, b, TileSpec(tile))
+            x, _ = (isolated.solve_positive_definite_isolated(a, b, TileSpec(tile), devices) if mpmd else
+                    solve_positive_definite(mesh, a, b, TileSpec(tile)))
             checks.append(("solve-residual", solve_residual(a, x, b), res_tol))
             if kind == "diag" and not args.rhs:
                 expected = 1.0 / np.arange(1, n + 1, dtype=np.float64)
@@ -267,14 +286,16 @@ def _verify_one(args, a, et, kind, tile, devices):
                                elem_tol))
             result = x
         elif args.routine == "potri":
-            inv, _ = invert_positive_definite(mesh, a, TileSpec(tile))
+            inv, _ = (isolated.invert_positive_definite_isolated(a, TileSpec(tile), devices) if mpmd else
+                      invert_positive_definite(mesh, a, TileSpec(tile)))
             checks.append(("inverse-residual", inverse_residual(a, inv), res_tol))
             if kind == "diag":
                 expected = np.diag(1.0 / np.arange(1, n + 1, dtype=np.float64))
                 checks.append(("diag-inverse", float(np.abs(inv.astype(np.complex128) - expected).max()), elem_tol))
             result = inv
         else:
-            w, v, _ = eigh_hermitian(mesh, a, TileSpec(tile))
+            w, v, _ = (isolated.eigh_hermitian_isolated(a, TileSpec(tile), devices) if mpmd else
+                       eigh_hermitian(mesh, a, TileSpec(tile)))
             checks.append(("eigen-residual", eigen_residual(a, w, v), res_tol))
             checks.append(("orthonormal", orthonormality_defect(v), res_tol))
             ascent = float(max(0.0, np.max(w[:-1] - w[1:]))) if n > 1 else 0.0
@@ -289,7 +310,8 @@ def _verify_one(args, a, et, kind, tile, devices):
         if args.result_out:
             write_matrix(args.result_out, result)
     finally:
-        mesh.close()
+        if mesh is not None:
+            mesh.close()
     return checks
 
 
@@ -335,27 +357,32 @@ def _cmd_bench(args) -> int:
         w.writerow(BENCH_COLUMNS + EXTRA_COLUMNS)
         for tile in _tiles(args, n):
             for devices in args.devices:
-                mesh = DeviceMesh(devices)
+                mpmd = args.mode == "mpmd"
+                mesh = None if mpmd else DeviceMesh(devices)
                 solves, allocs = [], []
                 for rep in range(args.reps):
                     if args.routine == "potrs":
                         b = np.ones((n, args.nrhs), dtype=et.dtype, order="F")
-                        x, tm = solve_positive_definite(mesh, a, b, TileSpec(tile))
+                        x, tm = (isolated.solve_positive_definite_isolated(a, b, TileSpec(tile), devices) if mpmd
+                                 else solve_positive_definite(mesh, a, b, TileSpec(tile)))
                         residual = solve_residual(a, x, b)
                     elif args.routine == "potri":
-                        inv, tm = invert_positive_definite(mesh, a, TileSpec(tile))
+                        inv, tm = (isolated.invert_positive_definite_isolated(a, TileSpec(tile), devices) if mpmd
+                                   else invert_positive_definite(mesh, a, TileSpec(tile)))
                         residual = inverse_residual(a, inv)
                     else:
-                        ev, vecs, tm = eigh_hermitian(mesh, a, TileSpec(tile))
+                        ev, vecs, tm = (isolated.eigh_hermitian_isolated(a, TileSpec(tile), devices) if mpmd
+                                        else eigh_hermitian(mesh, a, TileSpec(tile)))
                         residual = eigen_residual(a, ev, vecs)
                     solves.append(tm.solve_seconds)
                     allocs.append(tm.alloc_seconds)
                     tflops = _flops(args.routine, n, args.nrhs, et) / (tm.device_ms * 1e-3) / 1e12 if tm.device_ms else 0
-                    w.writerow([args.routine, n, tile, devices, args.dtype, "spmd", rep, repr(tm.alloc_seconds),
+                    w.writerow([args.routine, n, tile, devices, args.dtype, args.mode, rep, repr(tm.alloc_seconds),
                                 repr(tm.solve_seconds), repr(residual), tm.redistribute_ms, tm.potrf_ms, tm.finish_ms,
                                 tm.device_ms, tflops])
-                mesh.close()
-                print(f"{args.routine} n={n} tile={tile} devices={devices} dtype={args.dtype} mode=spmd "
+                if mesh is not None:
+                    mesh.close()
+                print(f"{args.routine} n={n} tile={tile} devices={devices} dtype={args.dtype} mode={args.mode} "
                       f"reps={args.reps}: alloc min={min(allocs):.9f} median={statistics.median(allocs):.9f} s; "
                       f"solve min={min(solves):.9f} median={statistics.median(solves):.9f} s", file=sys.stderr)
     finally:

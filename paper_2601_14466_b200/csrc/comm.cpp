@@ -124,11 +124,25 @@ class NcclComm final : public Comm {
     me_ = rank;
     BCMG_CUDA(cudaMalloc(&scratch_, 256));
     BCMG_CUDA(cudaMemset(scratch_, 0, 256));
+    // flag words of this rank, mapped into every peer (collective, like the init)
+    BCMG_CUDA(cudaMalloc(&flags_, kFlagSlots * sizeof(uint32_t)));
+    BCMG_CUDA(cudaMemset(flags_, 0, kFlagSlots * sizeof(uint32_t)));
+    BCMG_CUDA(cudaDeviceSynchronize());
+    if (stream_wait_supported()) peer_flags_ = exchange_pointers(flags_);
+  }
+  bool flags_supported() const override { return (int)peer_flags_.size() == world_; }
+  void post_flag(int peer, int slot, uint32_t v, cudaStream_t st) override {
+    void* w = static_cast<uint32_t*>(peer_flags_.at(peer)) + slot;
+    if (!stream_write_value(st, w, v)) stream_signal(st, &w, 1, v);  // a one-thread kernel if refused
+  }
+  void wait_flag(int slot, uint32_t v, cudaStream_t st) override {
+    stream_wait_geq(st, static_cast<uint32_t*>(flags_) + slot, v);
   }
   ~NcclComm() override {
     ipc_.close_all();
     if (c_) ncclCommDestroy(c_);
     if (scratch_) cudaFree(scratch_);
+    if (flags_) cudaFree(flags_);
   }
   void barrier(cudaStream_t st) override {
     BCMG_NCCL_CALL(ncclAllReduce(scratch_, scratch_, 1, ncclInt32, ncclSum, c_, st));
@@ -213,6 +227,8 @@ class NcclComm final : public Comm {
   ncclComm_t c_ = nullptr;
   int me_ = 0, world_ = 1;
   void* scratch_ = nullptr;
+  void* flags_ = nullptr;
+  std::vector<void*> peer_flags_;
   IpcCache ipc_;
 };
 
@@ -259,6 +275,12 @@ struct Hub {
     int count = 0, reads = 0;
   };
   std::map<uint64_t, Barrier> barriers;
+  // (rank, slot) -> posted (value, event), increasing values
+  std::map<std::pair<int, int>, std::deque<std::pair<uint32_t, cudaEvent_t>>> flags;
+  ~Hub() {
+    for (auto& kv : flags)
+      for (auto& e : kv.second) cudaEventDestroy(e.second);
+  }
 };
 
 std::mutex g_hubs_mu;
@@ -398,6 +420,30 @@ class LoopbackComm final : public Comm {
     return out;
   }
   void release_pointers(std::vector<void*>& ptrs) override { ptrs.clear(); }
+
+  bool flags_supported() const override { return true; }
+  void post_flag(int peer, int slot, uint32_t v, cudaStream_t st) override {
+    cudaEvent_t e = new_event();
+    BCMG_CUDA(cudaEventRecord(e, st));
+    std::lock_guard<std::mutex> lk(hub_->mu);
+    hub_->flags[{peer, slot}].push_back({v, e});
+    hub_->cv.notify_all();
+  }
+  void wait_flag(int slot, uint32_t v, cudaStream_t st) override {
+    std::unique_lock<std::mutex> lk(hub_->mu);
+    auto& q = hub_->flags[{rank_, slot}];
+    auto found = [&] {
+      for (size_t i = 0; i < q.size(); ++i)
+        if (q[i].first >= v) return (int)i;
+      return -1;
+    };
+    hub_wait(lk, [&] { return found() >= 0; });
+    const int i = found();
+    BCMG_CUDA(cudaStreamWaitEvent(st, q[i].second, 0));
+    // waits on a slot ask for increasing values: older posts are never needed again
+    for (int j = 0; j < i; ++j) cudaEventDestroy(q[j].second);
+    q.erase(q.begin(), q.begin() + i);
+  }
 
   void barrier(cudaStream_t st) override {
     const uint64_t seq = bar_seq_++;

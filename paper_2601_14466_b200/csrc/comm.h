@@ -47,6 +47,19 @@ class Comm {
   // Empty if unsupported on any rank (all ranks agree).
   virtual std::vector<void*> exchange_pointers(void* local) = 0;
   virtual void release_pointers(std::vector<void*>& ptrs) = 0;
+  // Stream-ordered flags of the peer-memory hand-offs: per rank kFlagSlots
+  // monotone 32-bit counters.  post_flag: once everything earlier on st is
+  // done (and visible to the peer), rank `peer`'s counter `slot` becomes v.
+  // wait_flag: work enqueued on st afterwards starts once this rank's counter
+  // `slot` is >= v.  Across GPUs these are stream memory operations on
+  // CUDA-IPC-mapped words (cuStreamWriteValue32 / cuStreamWaitValue32: no
+  // kernel, no SM, no stream of one rank parked inside another rank's
+  // context); loopback ranks match them on the host and order the streams
+  // with CUDA events (no stream ever parks in the shared context).
+  static constexpr int kFlagSlots = 64;
+  virtual bool flags_supported() const = 0;
+  virtual void post_flag(int peer, int slot, uint32_t v, cudaStream_t st) = 0;
+  virtual void wait_flag(int slot, uint32_t v, cudaStream_t st) = 0;
 };
 
 // CUDA IPC export / import of any device address (the allocation's handle plus

@@ -64,16 +64,7 @@ Session::Session(int device_, int rank_, int world_, const unsigned char* nccl_i
   for (auto& e : ev_time) BCMG_CUDA(cudaEventCreate(&e));
   BCMG_CUDA(cudaMallocHost(&info_host, sizeof(int)));
   BCMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
-  if (world > 1) {
-    net = make_comm(rank, world, nccl_id);
-    // flag words of the peer-memory hand-offs, zeroed here: nothing inside a
-    // schedule may synchronise the whole device (loopback ranks share one
-    // context, and another rank's stream may be parked on a flag that only
-    // this rank's later work raises)
-    sig.ensure(256 * sizeof(uint32_t));
-    BCMG_CUDA(cudaMemset(sig.p, 0, 256 * sizeof(uint32_t)));
-    BCMG_CUDA(cudaDeviceSynchronize());
-  }
+  if (world > 1) net = make_comm(rank, world, nccl_id);
 }
 
 Session::~Session() {
@@ -82,11 +73,10 @@ Session::~Session() {
   if (net) {
     net->release_pointers(peer_panel[0]);
     net->release_pointers(peer_panel[1]);
-    net->release_pointers(peer_sig);
   }
   net.reset();
   for (auto* b : {&panel[0], &panel[1], &panel_pb[0], &panel_pb[1], &dinv, &wdiag, &info_dev, &tmp, &acc, &plan_buf,
-                  &stage_buf, &desc_buf, &embed_buf, &split_buf[0], &split_buf[1], &sig})
+                  &stage_buf, &desc_buf, &embed_buf, &split_buf[0], &split_buf[1]})
     b->release();
   for (auto& b : eig) b.release();
   if (eig_host) cudaFreeHost(eig_host);
@@ -765,25 +755,22 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
     const char* legacy = getenv("BCMG_P2P");  // round-1 name of the fan-out mode
     bc_mode = m ? (!strcmp(m, "fan") ? BC_FAN : !strcmp(m, "nccl") ? BC_NCCL : BC_CE)
                 : (legacy ? (atoi(legacy) ? BC_FAN : BC_NCCL) : BC_CE);
-    if (!stream_wait_supported() || (bc_mode == BC_FAN && world > MAX_FAN + 1)) bc_mode = BC_NCCL;
+    if (!net->flags_supported() || (bc_mode == BC_FAN && world > MAX_FAN + 1)) bc_mode = BC_NCCL;
   }
   bool p2p = bc_mode != BC_NCCL;
   std::vector<void*> fan_panel[2];
   uint32_t seq0 = 0;
-  auto sig_word = [&](int r, int idx) { return static_cast<void*>(static_cast<uint32_t*>(peer_sig[r]) + idx); };
-  auto my_word = [&](int idx) { return static_cast<const void*>(static_cast<const uint32_t*>(sig.p) + idx); };
   if ((dt == R32 || dt == C64) && tc_presplit_enabled())  // the panel solves' split planes, sized up front
     reserve_split_scratch(crit, split_scratch_bytes(dt, n, T, T));
   if (p2p) {
-    if (peer_sig.empty()) peer_sig = net->exchange_pointers(sig.p);  // zeroed in the constructor
-    for (int b2 = 0; b2 < 2 && !peer_sig.empty(); ++b2) {
+    for (int b2 = 0; b2 < 2; ++b2) {
       net->release_pointers(peer_panel[b2]);
       peer_panel[b2] = net->exchange_pointers(panel[b2].p);
       for (int r = 0; r < (int)peer_panel[b2].size(); ++r)
         if (r != rank) fan_panel[b2].push_back(peer_panel[b2][r]);
     }
     // every rank sees the same exchange outcome (collective agreement in exchange_pointers)
-    if (peer_sig.empty() || peer_panel[0].empty() || peer_panel[1].empty()) {
+    if (peer_panel[0].empty() || peer_panel[1].empty()) {
       p2p = false;
       bc_mode = BC_NCCL;
       fan_panel[0].clear();
@@ -795,11 +782,11 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
     panel_seq += (uint32_t)g.nt + 4;
   }
   last_bcast_mode = bc_mode;
-  // raise flag words on peers (stream memory operation; a one-thread kernel if the driver refuses)
-  auto signal = [&](cudaStream_t st, const std::vector<void*>& flags, uint32_t v) {
-    bool ok = true;
-    for (void* f : flags) ok = ok && stream_write_value(st, f, v);
-    if (!ok) stream_signal(st, flags.data(), (int)flags.size(), v);
+  // flag slots (Comm::post_flag / wait_flag): [b] panel in buffer b ready,
+  // [2 + 16 b + r] process r done with buffer b
+  auto post_all = [&](cudaStream_t st, int slot_base, bool per_rank, uint32_t v) {
+    for (int r = 0; r < world; ++r)
+      if (r != rank) net->post_flag(r, slot_base + (per_rank ? rank : 0), v, st);
   };
   auto seq_of = [&](int64_t k) { return seq0 + (uint32_t)k + 1; };
   // peers done with buffer b before panel k is written into it: their last use
@@ -809,7 +796,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
     const uint32_t need = k >= 2 ? seq_of(k - 2) : free_seq[bb];
     if (!need) return;
     for (int r = 0; r < world; ++r)
-      if (r != rank) stream_wait_geq(st, my_word(2 + 16 * bb + r), need);
+      if (r != rank) net->wait_flag(2 + 16 * bb + r, need, st);
   };
   dinv.ensure((size_t)g.nt * T * T * g.esz);
   wdiag.ensure((size_t)T * T * g.esz);
@@ -994,10 +981,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
         if (bc_mode == BC_FAN && s1 < n) wait_peers_free(k, crit);
         factor(k);
         if (bc_mode == BC_FAN && s1 < n) {  // panel k is in every peer's buffer: raise their ready flags
-          std::vector<void*> flags;
-          for (int r = 0; r < world; ++r)
-            if (r != rank) flags.push_back(sig_word(r, b));
-          signal(crit, flags, seq_of(k));
+          post_all(crit, b, false, seq_of(k));
           BCMG_CUDA(cudaEventRecord(E(C, k), crit));
         }
         BCMG_CUDA(cudaEventRecord(E(R, k), crit));
@@ -1007,20 +991,15 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
           const size_t bytes = (size_t)op.elems * g.esz;
           BCMG_CUDA(cudaStreamWaitEvent(comm, E(R, k), 0));
           wait_peers_free(k, comm);
-          std::vector<void*> flags;
-          for (int r = 0, e = 0; r < world; ++r) {
-            if (r == rank) continue;
-            if (bytes) BCMG_CUDA(cudaMemcpyAsync(fan_panel[b][e], panel[b].p, bytes, cudaMemcpyDeviceToDevice, comm));
-            flags.push_back(sig_word(r, b));
-            ++e;
-          }
-          signal(comm, flags, seq_of(k));
+          for (void* dst : fan_panel[b])
+            if (bytes) BCMG_CUDA(cudaMemcpyAsync(dst, panel[b].p, bytes, cudaMemcpyDeviceToDevice, comm));
+          post_all(comm, b, false, seq_of(k));
           BCMG_CUDA(cudaEventRecord(E(C, k), comm));
           break;
         }
         if (p2p) {
           if (mine) break;
-          stream_wait_geq(comm, my_word(b), seq_of(k));  // raised by the owner after its copies / fused solve
+          net->wait_flag(b, seq_of(k), comm);  // raised by the owner after its copies / fused solve
           BCMG_CUDA(cudaEventRecord(E(C, k), comm));
           if (embed_k(k)) expand_panel(dt, panel[b].p, panel_pb[b].p, n - s1, s1 - g.start(k), comm);
           split_panel(k, comm);
@@ -1068,10 +1047,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
         if (world > 1) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(C, k), 0));
         BCMG_CUDA(cudaEventRecord(E(FREE, k), bulk));
         if (p2p && s1 < n) {  // tell every process that buffer b may take panel k + 2
-          std::vector<void*> flags;
-          for (int r = 0; r < world; ++r)
-            if (r != rank) flags.push_back(sig_word(r, 2 + 16 * b + rank));
-          signal(bulk, flags, seq_of(k));
+          post_all(bulk, 2 + 16 * b, true, seq_of(k));
           free_seq[b] = seq_of(k);
         }
         break;

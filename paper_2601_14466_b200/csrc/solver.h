@@ -74,9 +74,9 @@ struct Session {
   static constexpr int kEvents = 64, kJoin = 56, kTimeEvents = 5;
   cudaEvent_t ev_pool[kEvents];
   cudaEvent_t ev_time[kTimeEvents];
-  DevBuf panel[2], panel_pb[2], split_buf[2], dinv, wdiag, info_dev, tmp, acc, plan_buf, embed_buf, sig;
+  DevBuf panel[2], panel_pb[2], split_buf[2], dinv, wdiag, info_dev, tmp, acc, plan_buf, embed_buf;
   // peer-memory mode of potrf: every process's panel buffers and flag words
-  std::vector<void*> peer_panel[2], peer_sig;
+  std::vector<void*> peer_panel[2];
   uint32_t panel_seq = 0, free_seq[2] = {0, 0};
   std::vector<char> plan_host;
   int* info_host = nullptr;

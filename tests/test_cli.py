@@ -11,7 +11,6 @@ from paper_2601_14466_b200 import cli
 
 
 @pytest.mark.parametrize("argv", [
-    ["verify", "--routine", "potrs", "--n", "8", "--mode", "mpmd"],
     ["verify", "--routine", "potrs", "--n", "8", "--trace", "t.csv"],
     ["verify", "--routine", "potrs", "--n", "8", "--matrix", "nonsense"],
     ["gen", "--kind", "diag", "--n", "0", "--out", "x.bcmg"],
@@ -155,3 +154,42 @@ def test_verify_files_on_gpu(tmp_path, capsys):
     assert cli.main(["gen", "--kind", "random_spd", "--n", "40", "--dtype", "f32", "--out", str(a_path)]) == 0
     assert cli.main(["verify", "--routine", "syevd", "--matrix", f"file:{a_path}", "--tile", "8"]) == 0
     capsys.readouterr()
+
+
+def test_bogus_mode_env_is_configuration_error(monkeypatch):
+    """BCMG_MODE outside {spmd, mpmd} exits 2 (reference test_cli.py:161-175)."""
+    monkeypatch.setenv("BCMG_MODE", "bogus")
+    err = io.StringIO()
+    with contextlib.redirect_stderr(err):
+        assert cli.main(["verify", "--routine", "potrs", "--n", "8", "--tile", "2", "--devices", "2",
+                         "--matrix", "diag"]) == 2
+    assert "configuration error" in err.getvalue()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("routine", ["potrs", "potri", "syevd"])
+def test_mode_flag_and_env_same_output(capsys, monkeypatch, routine):
+    """--mode mpmd (isolated workers: one session and one shard allocation per
+    device, shards reached through the transport's handle exchange) prints the
+    same PASS lines as $BCMG_MODE=mpmd and as spmd, and writes the same bits
+    (reference test_cli.py:161-175)."""
+    import os
+    import tempfile
+
+    from paper_2601_14466_b200.core import read_matrix
+
+    outs, results = [], []
+    for mode, env in (("mpmd", None), (None, "mpmd"), ("spmd", None)):
+        if env:
+            monkeypatch.setenv("BCMG_MODE", env)
+        else:
+            monkeypatch.delenv("BCMG_MODE", raising=False)
+        path = os.path.join(tempfile.mkdtemp(), "r.bcmg")
+        argv = ["verify", "--routine", routine, "--n", "96", "--tile", "8", "--devices", "4", "--dtype", "c128",
+                "--matrix", "random_spd", "--result-out", path] + (["--mode", mode] if mode else [])
+        assert cli.main(argv) == 0
+        outs.append(capsys.readouterr().out)
+        results.append(read_matrix(path))
+    assert outs[0] == outs[1] and "PASS" in outs[0]
+    assert np.array_equal(results[0], results[1])
+    assert np.array_equal(results[0], results[2]), "mpmd and spmd must give the same bits"
