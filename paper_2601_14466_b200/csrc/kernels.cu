@@ -519,7 +519,7 @@ static void launch_tc3_gemm(int64_t M, int64_t N, int64_t K, const Operand& A, c
 //   mode 2: complex64 planar B = [Re P | Im P] (R x 2Kc)
 template <int MODE>
 __global__ void split_tf32_kernel(const float* __restrict__ src, int64_t ld, int64_t rows, int64_t Kx, int64_t kc,
-                                  float* __restrict__ hi, float* __restrict__ lo, int64_t kp) {
+                                  float* __restrict__ hi, float* __restrict__ lo, int64_t kp, int64_t kw) {
   __shared__ float t[32][33];
   const int64_t m0 = (int64_t)blockIdx.x * 32, k0 = (int64_t)blockIdx.y * 32;
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
@@ -545,7 +545,7 @@ __global__ void split_tf32_kernel(const float* __restrict__ src, int64_t ld, int
   __syncthreads();
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
     const int64_t m = m0 + y, k = k0 + threadIdx.x;  // coalesced along k (row-major planes)
-    if (m >= rows || k >= kp) continue;
+    if (m >= rows || k >= kw) continue;
     const float x = t[threadIdx.x][y];
     const float h = tc::tf32_rna(x);
     hi[m * kp + k] = h;
@@ -556,15 +556,27 @@ __global__ void split_tf32_kernel(const float* __restrict__ src, int64_t ld, int
 int64_t split_ld(int64_t kx) { return (kx + 3) / 4 * 4; }
 
 void split_tf32(int mode, const void* src, int64_t ld, int64_t rows, int64_t Kx, int64_t kc, float* hi, float* lo,
-                int64_t kp, cudaStream_t st) {
-  if (rows <= 0 || kp <= 0) return;
-  dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((kp + 31) / 32)), block(32, 8);
+                int64_t kp, cudaStream_t st, int64_t kw) {
+  if (kw < 0) kw = kp;
+  if (rows <= 0 || kw <= 0) return;
+  dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((kw + 31) / 32)), block(32, 8);
   const float* s = static_cast<const float*>(src);
-  if (mode == 0) split_tf32_kernel<0><<<grid, block, 0, st>>>(s, ld, rows, Kx, kc, hi, lo, kp);
-  else if (mode == 1) split_tf32_kernel<1><<<grid, block, 0, st>>>(s, ld, rows, Kx, kc, hi, lo, kp);
-  else if (mode == 2) split_tf32_kernel<2><<<grid, block, 0, st>>>(s, ld, rows, Kx, kc, hi, lo, kp);
-  else split_tf32_kernel<3><<<grid, block, 0, st>>>(s, ld, rows, Kx, kc, hi, lo, kp);
+  if (mode == 0) split_tf32_kernel<0><<<grid, block, 0, st>>>(s, ld, rows, Kx, kc, hi, lo, kp, kw);
+  else if (mode == 1) split_tf32_kernel<1><<<grid, block, 0, st>>>(s, ld, rows, Kx, kc, hi, lo, kp, kw);
+  else if (mode == 2) split_tf32_kernel<2><<<grid, block, 0, st>>>(s, ld, rows, Kx, kc, hi, lo, kp, kw);
+  else split_tf32_kernel<3><<<grid, block, 0, st>>>(s, ld, rows, Kx, kc, hi, lo, kp, kw);
   BCMG_CHECK_LAUNCH();
+}
+
+// Narrow tiles on the tcgen05 path: the trailing update is HBM-bound (each
+// pass reads and writes the whole trailing trapezoid for only K = T of
+// work), so potrf applies the panels in pairs (K = 2T) and halves the passes.
+bool pair_panels(int dt, int64_t T) {
+  static const int v = [] {
+    const char* e = getenv("BCMG_PAIR_PANELS");
+    return e && *e ? atoi(e) : 1;
+  }();
+  return v && (dt == R32 || dt == C64) && tc_presplit_enabled() && T <= 256 && T % 32 == 0;
 }
 
 // K-major plane map: dims {kp, rows}, box {32 k, 128 rows}, SWIZZLE_128B (the

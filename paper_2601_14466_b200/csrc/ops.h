@@ -51,8 +51,12 @@ bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, 
 // tf32 hi / lo pre-split (see split_tf32_kernel) and the tcgen05 GEMM on the
 // split planes.  split_ld: the K-major leading dimension for Kx columns.
 int64_t split_ld(int64_t kx);
+// kw: columns written per row (Kx, zero-padded; default kp); kp: row stride of the planes
 void split_tf32(int mode, const void* src, int64_t ld, int64_t rows, int64_t Kx, int64_t kc, float* hi, float* lo,
-                int64_t kp, cudaStream_t st);
+                int64_t kp, cudaStream_t st, int64_t kw = -1);
+// potrf on the pre-split tcgen05 path updates the trailing matrix once per
+// PAIR of panels (K = 2T) when the tile is narrow (see Session::potrf)
+bool pair_panels(int dt, int64_t T);
 void tck_gemm(int64_t M, int64_t N, int64_t K, const float* ah, const float* al, const float* bh, const float* bl,
               int64_t kp, float* C, int64_t ldc, float alpha, float beta, const int* info, cudaStream_t st,
               const Epilogue* fan_src = nullptr);

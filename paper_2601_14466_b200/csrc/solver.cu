@@ -599,7 +599,8 @@ WsPlan workspace_plan(int routine, int dt, int64_t n, int64_t T, int ndev, int w
   const size_t panel_bytes = (size_t)n * T * esz;
   const bool presplit = (dt == R32 || dt == C64) && tc_presplit_enabled();
   if (presplit) {
-    const size_t plane = (size_t)n * split_ld(dt == C64 ? 2 * T : T) * 4;
+    const int64_t kx = dt == C64 ? 2 * T : T;
+    const size_t plane = (size_t)n * (pair_panels(dt, T) ? 2 * kx : split_ld(kx)) * 4;
     w.split = dt == C64 ? 6 * plane : 2 * plane;
     w.split_scratch = split_scratch_bytes(dt, n, T, T);  // the panel solves
   }
@@ -707,23 +708,50 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
   // hi / lo K-major planes (split_buf[k % 2]) that every trailing tile reads
   const bool presplit = (dt == R32 || dt == C64) && tc_presplit_enabled();
   const int64_t kx = dt == C64 ? 2 * T : T, kp = split_ld(kx);
+  // Paired panels (pair_panels: tcgen05 path, T <= 256): panels 2j and 2j+1
+  // share split buffer split_buf[j % 2] -- K-major rows of width 2 kx starting
+  // at row stop(2j), panel 2j in columns [0, kx), panel 2j+1 in [kx, 2 kx)
+  // from row stop(2j+1) = stop(2j) + T.  Step 2j updates only its lookahead
+  // tile (K = T); step 2j+1 updates tile 2j+2 and the bulk with both panels at
+  // once (K = 2T): every trailing tile is read and written once per pair
+  // instead of once per panel.  The pairing is global, so the arithmetic (and
+  // the bits) do not depend on the device or process count.
+  const bool pair = presplit && pair_panels(dt, T);
+  const int64_t kpp = pair ? 2 * kx : kp;
   if (presplit) {
-    const size_t plane = (size_t)n * kp * 4;  // rows x kp floats (A rows: 2n for complex64)
+    const size_t plane = (size_t)n * kpp * 4;  // rows x kpp floats (A rows: 2n for complex64)
     const size_t bytes = dt == C64 ? 2 * (2 * plane) + 2 * plane : 2 * plane;
     split_buf[0].ensure(bytes);
     split_buf[1].ensure(bytes);
   }
+  // split buffer of panel k, the rows of its first panel (stride of the planes) and
+  // the row / column offset of panel k inside it
+  struct SplitAt {
+    float* base;
+    int64_t rows0, roff, coff, ld;
+  };
+  auto split_at = [&](int64_t k) {
+    if (!pair) return SplitAt{static_cast<float*>(split_buf[k % 2].p), n - g.stop(k), 0, 0, 0};
+    const int64_t k0 = k - (k % 2);
+    return SplitAt{static_cast<float*>(split_buf[(k0 / 2) % 2].p), n - g.stop(k0), k % 2 ? T : 0, k % 2 ? kx : 0,
+                   kpp};
+  };
   auto split_panel = [&](int64_t k, cudaStream_t st) {
     const int64_t rows = n - g.stop(k), tck = g.stop(k) - g.start(k);
     if (!presplit || rows <= 0) return;
-    float* b = static_cast<float*>(split_buf[k % 2].p);
-    const int64_t kpk = split_ld(dt == C64 ? 2 * tck : tck);
+    const SplitAt sa = split_at(k);
+    const int64_t kpk = pair ? kpp : split_ld(dt == C64 ? 2 * tck : tck);
+    const int64_t kw = pair ? kx : -1;
+    float* b = sa.base;
     if (dt == R32) {
-      split_tf32(0, panel[k % 2].p, rows, rows, tck, tck, b, b + rows * kpk, kpk, st);
+      float* hi = b + sa.roff * kpk + sa.coff;
+      split_tf32(0, panel[k % 2].p, rows, rows, tck, tck, hi, hi + sa.rows0 * kpk, kpk, st, kw);
     } else {
-      float* bb = b + 2 * (2 * rows) * kpk;  // B planes after the two A planes
-      split_tf32(1, panel[k % 2].p, rows, 2 * rows, 2 * tck, tck, b, b + 2 * rows * kpk, kpk, st);
-      split_tf32(2, panel[k % 2].p, rows, rows, 2 * tck, tck, bb, bb + rows * kpk, kpk, st);
+      const int64_t r0 = pair ? sa.rows0 : rows;
+      float* ah = b + 2 * sa.roff * kpk + sa.coff;
+      float* bh = b + 2 * (2 * r0) * kpk + sa.roff * kpk + sa.coff;  // B planes after the two A planes
+      split_tf32(1, panel[k % 2].p, rows, 2 * rows, 2 * tck, tck, ah, ah + 2 * r0 * kpk, kpk, st, kw);
+      split_tf32(2, panel[k % 2].p, rows, rows, 2 * tck, tck, bh, bh + r0 * kpk, kpk, st, kw);
     }
   };
   const bool embed = !presplit && complex_embed_ok(dt, 0, T);
@@ -865,18 +893,23 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
       p.cplx = 1;
       p.PB = panel_pb[k % 2].p;
     }
+    int64_t K = g.stop(k) - g.start(k);
     if (presplit) {
-      const int64_t rows = n - g.stop(k), kpk = split_ld(dt == C64 ? 2 * (g.stop(k) - g.start(k)) : g.stop(k) - g.start(k));
-      float* b = static_cast<float*>(split_buf[k % 2].p);
+      const int64_t rows = n - g.stop(k);
+      const SplitAt sa = split_at(k);
+      const int64_t kpk = pair ? kpp : split_ld(dt == C64 ? 2 * K : K);
+      const int64_t r0 = pair ? sa.rows0 : rows;  // rows of the planes
+      float* b = sa.base;
+      if (pair && k % 2) K += T;  // both panels of the pair (columns [0, 2 kx), zero-padded)
       if (dt == R32) {
-        p.split[0] = p.split[2] = b;
-        p.split[1] = p.split[3] = b + rows * kpk;
+        p.split[0] = p.split[2] = b + sa.roff * kpk;
+        p.split[1] = p.split[3] = b + r0 * kpk + sa.roff * kpk;
       } else {
         p.cplx = 1;
-        p.split[0] = b;
-        p.split[1] = b + 2 * rows * kpk;
-        p.split[2] = b + 4 * rows * kpk;
-        p.split[3] = b + 5 * rows * kpk;
+        p.split[0] = b + 2 * sa.roff * kpk;
+        p.split[1] = b + 2 * r0 * kpk + 2 * sa.roff * kpk;
+        p.split[2] = b + 4 * r0 * kpk + sa.roff * kpk;
+        p.split[3] = b + 5 * r0 * kpk + sa.roff * kpk;
       }
       p.split_ld[0] = p.split_ld[1] = kpk;
     }
@@ -884,7 +917,7 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
     p.ldp = n - p.prow0;
     p.N = n;
     p.T = T;
-    p.K = g.stop(k) - g.start(k);
+    p.K = K;
     p.D = g.D;
     p.dev0 = g.dev0;
     p.nloc = g.nloc;
@@ -1017,10 +1050,14 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
       case S_UPDATE:
         if (op.stream == STREAM_CRIT) {  // lookahead: tile k+1 first, full grid
           if (!mine) BCMG_CUDA(cudaStreamWaitEvent(crit, E(R, k), 0));
+          if (pair && k % 2) BCMG_CUDA(cudaStreamWaitEvent(crit, E(R, k - 1), 0));  // the pair's first split
           if (k >= 1) BCMG_CUDA(cudaStreamWaitEvent(crit, E(B, k - 1), 0));
           trail(k, op.a, op.b, crit);
           BCMG_CUDA(cudaEventRecord(E(U, k), crit));
         } else {
+          // paired panels: the bulk of step 2j waits for step 2j+1 (both panels at once)
+          if (pair && k % 2 == 0 && k + 2 < g.nt) break;
+          if (pair && k % 2) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(R, k - 1), 0));
           BCMG_CUDA(cudaStreamWaitEvent(bulk, E(R, k), 0));
           // with a lookahead this step, the full-grid update of tile k+1 goes
           // first; otherwise both persistent grids would race for the SMs and
