@@ -197,7 +197,10 @@ __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUt
       if (lane == 0) mbar_arrive(&empty[s]);
       ++g;
     }
-    store_block<double, TL, false, FAN>(acc, cb.ep, cb.M, cb.N, cb.m0, cb.n0, wm0, wn0, lane);
+    // the item's geometry leaves shared memory only now, after the K loop
+    const Epilogue ep = cb.ep;
+    const int64_t M = cb.M, N = cb.N, m0 = cb.m0, n0 = cb.n0;
+    store_block<double, TL, false, FAN>(acc, ep, M, N, m0, n0, wm0, wn0, lane);
   }
 }
 
@@ -351,6 +354,180 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
   tma_gemm_loop<TL, false>(  // trailing updates never fan out
       &mapA, &mapB, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, TmaBlock& blk) { return decode(cp, item, blk); },
       p.stagger_ns);
+}
+
+// Round-1 persistent loop (consumer-side decode), used by trail_tma_kernel_v1.
+// Persistent producer/consumer loop.  `next_p(item, blk)` / `next_c(item, blk)`
+// fill the block of work item `item` (producer / consumer view; separate so
+// stateful cursors stay monotone) and return false when there is none.
+template <class TL, bool FAN = true, class NextP, class NextC>
+__device__ __forceinline__ void tma_gemm_loop_v1(const CUtensorMap* mapA, const CUtensorMap* mapB, int K, NextP&& next_p,
+                                              NextC&& next_c, long long stagger_ns = 0) {
+  double* smem = reinterpret_cast<double*>(tma_dyn_smem);
+  constexpr int NW = TL::THREADS / 32;
+  constexpr unsigned STAGE_BYTES = tma_stage_bytes<TL>();
+  constexpr int STAGE_WORDS = TL::BK * (TL::LDA + TL::LDB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TL::STAGES * STAGE_WORDS);
+  uint64_t* empty = full + TL::STAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm0 = (warp % TL::WARPS_M) * TL::WM, wn0 = (warp / TL::WARPS_M) * TL::WN;
+  const int KT = (K + TL::BK - 1) / TL::BK;
+  if (tid == 0) {
+    for (int s = 0; s < TL::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(mapB) : "memory");
+  }
+  __syncthreads();
+
+  // producer state (thread 0 only) lives in shared memory so it costs the
+  // consumer warps no registers: slice counter gp over (item, kt)
+  struct Prod {
+    int64_t item;
+    TmaBlock blk;
+    uint32_t gp;
+    int kt, live;
+  };
+  static_assert(sizeof(Prod) <= 384, "producer state must fit its aux slot");
+  Prod& ps = *reinterpret_cast<Prod*>(tma_aux<TL>());
+  auto produce_one = [&]() {
+    if (!ps.live) return;
+    const uint32_t gp = ps.gp;
+    const int s = gp % TL::STAGES, kt = ps.kt;
+    mbar_wait(&empty[s], ((gp / TL::STAGES) & 1) ^ 1);
+    double* st = smem + s * STAGE_WORDS;
+    mbar_expect_tx(&full[s], STAGE_BYTES);
+    tma_load_2d(st, mapA, ps.blk.a_row + (int)ps.blk.m0, kt * TL::BK, &full[s]);
+    tma_load_2d(st + TL::BK * TL::LDA, mapB, ps.blk.b_row + (int)ps.blk.n0, kt * TL::BK, &full[s]);
+    ps.gp = gp + 1;
+    if (kt + 1 == KT) {
+      ps.kt = 0;
+      ps.item += gridDim.x;
+      ps.live = next_p(ps.item, ps.blk);
+    } else {
+      ps.kt = kt + 1;
+    }
+  };
+  if (tid == 0) {
+    ps.item = blockIdx.x;
+    ps.gp = 0;
+    ps.kt = 0;
+    ps.live = next_p(ps.item, ps.blk);
+    for (int i = 0; i < TL::STAGES - 1; ++i) produce_one();
+  }
+
+  uint32_t g = 0;
+  TmaBlock cb;
+  // C tile prefetch into L2 a few slices before the epilogue: all CTAs reach
+  // their epilogues at nearly the same time (uniform items), and without it
+  // the read-modify-write of 128 KB per CTA would stall every SM on HBM.
+  constexpr int PREFETCH_AHEAD = 6;
+  auto prefetch_c = [&](const TmaBlock& blk) {
+    if (blk.ep.beta == 0.0) return;
+    const double* C = reinterpret_cast<const double*>(blk.ep.C);
+    constexpr int SEGS = TL::BM * 8 / 128;  // 128-byte lines per column of the tile
+    for (int i = tid; i < TL::BN * SEGS; i += TL::THREADS) {
+      const int64_t col = blk.n0 + i / SEGS, row = blk.m0 + (i % SEGS) * 16;
+      if (col < blk.N && row < blk.M)
+        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(C + row + col * blk.ep.ldc));
+    }
+  };
+  // Two co-resident CTAs per SM start in lockstep and, with uniform items,
+  // would hit their epilogues together; delaying the second half of the grid
+  // by about half an item makes one CTA's epilogue overlap the other's DMMAs.
+  if (stagger_ns > 0 && blockIdx.x >= gridDim.x / 2) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < stagger_ns * 2) __nanosleep(1000);  // ~2 cycles per ns at ~2 GHz
+  }
+  for (int64_t item = blockIdx.x; next_c(item, cb); item += gridDim.x) {
+    Acc<TL, false> acc;
+    acc.zero();
+    for (int kt = 0; kt < KT; ++kt) {
+      if (kt == (KT > PREFETCH_AHEAD ? KT - PREFETCH_AHEAD : 0)) prefetch_c(cb);
+      if (tid == 0) produce_one();
+      const int s = g % TL::STAGES;
+      mbar_wait(&full[s], (g / TL::STAGES) & 1);
+      const double* st = smem + s * STAGE_WORDS;
+      mma_slice<TL, false, false, false>(acc, st, st + TL::BK * TL::LDA, nullptr, nullptr, wm0, wn0, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      ++g;
+    }
+    // the item's geometry leaves shared memory only now, after the K loop
+    const Epilogue ep = cb.ep;
+    const int64_t M = cb.M, N = cb.N, m0 = cb.m0, n0 = cb.n0;
+    store_block<double, TL, false, FAN>(acc, ep, M, N, m0, n0, wm0, wn0, lane);
+  }
+}
+
+// Round-1 form of trail_tma_kernel (consumers decode their own items; kept for A/B
+// measurement, BCMG_TRAIL_V1=1).
+template <class TL>
+__global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
+    trail_tma_kernel_v1(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TrailParams p,
+                     const int* info) {
+  using TZ = Trap<TL::BM, TL::BN>;
+  // complex embedding: real rows 2r, 2r+1 = re, im of complex row r, so a block
+  // of BM real rows covers BM/2 complex rows of the lower trapezoid
+  using TZC = Trap<(TL::BM / 2 >= TL::BN ? TL::BM / 2 : TL::BN), TL::BN>;
+  if (ld_flag(info)) return;
+  // tile cursor: items only grow for a given caller, so the walk over tiles is
+  // amortised O(1); producer and consumer each own one
+  struct Cursor {
+    int64_t m, base, cnt;
+  };
+  auto decode = [&p](Cursor& cur, int64_t item, TmaBlock& blk) -> bool {
+    for (;;) {
+      if (cur.m >= p.m_last) return false;
+      const int dev = (int)(cur.m % p.D);
+      const bool local = dev >= p.dev0 && dev < p.dev0 + p.nloc;
+      if (local) {
+        if (cur.cnt < 0) {
+          const int64_t ms = cur.m * p.T, tcm = p.T < p.N - ms ? p.T : p.N - ms;
+          cur.cnt = p.cplx ? TZC::count(p.N - ms, tcm) : TZ::count(p.N - ms, tcm);
+        }
+        if (item < cur.base + cur.cnt) break;
+        cur.base += cur.cnt;
+      }
+      ++cur.m;
+      cur.cnt = -1;
+    }
+    const int64_t m = cur.m, ms = m * p.T, rows = p.N - ms, tc = p.T < rows ? p.T : rows;
+    int64_t rb, cbk;
+    const int dev = (int)(m % p.D);
+    double* shard = reinterpret_cast<double*>(p.shards[dev - p.dev0]);
+    const int64_t loc = (m / p.D) * p.T;
+    if (p.cplx) {
+      TZC::decode(item - cur.base, tc, rb, cbk);
+      blk.a_row = (int)(2 * (ms - p.prow0));
+      blk.b_row = (int)(ms - p.prow0);
+      blk.m0 = rb * TL::BM;
+      blk.n0 = cbk * TL::BN;
+      blk.M = 2 * rows;
+      blk.N = tc;
+      blk.ep = Epilogue{shard + 2 * (ms + loc * p.N), 2 * p.N, -1.0, 1.0, 0, 0};
+      return true;
+    }
+    TZ::decode(item - cur.base, tc, rb, cbk);
+    blk.a_row = (int)(ms - p.prow0);
+    blk.b_row = (int)(ms - p.prow0);
+    blk.m0 = rb * TL::BM;
+    blk.n0 = cbk * TL::BN;
+    blk.M = rows;
+    blk.N = tc;
+    blk.ep = Epilogue{shard + ms + loc * p.N, p.N, -1.0, 1.0, 0, 0};
+    return true;
+  };
+  // producer's cursor (thread 0 only) in the caller aux slot: no registers in the consumers
+  Cursor& cp = *reinterpret_cast<Cursor*>(tma_aux<TL>() + 384);
+  if (threadIdx.x == 0) cp = Cursor{p.m_first, 0, -1};
+  Cursor cc{p.m_first, 0, -1};
+  tma_gemm_loop_v1<TL, false>(  // trailing updates never fan out
+      &mapA, &mapB, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, TmaBlock& blk) { return decode(cp, item, blk); },
+      [&](int64_t item, TmaBlock& blk) { return decode(cc, item, blk); }, p.stagger_ns);
 }
 
 // Single GEMM C := alpha A B^H (+ beta C) with A (M x K) and B (N x K) both

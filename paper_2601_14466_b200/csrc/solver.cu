@@ -931,7 +931,13 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
       flops += 2.0 * (double)p.K * (rows * tcm - tcm * (tcm - 1) / 2);
     }
     if (dtype_complex(dt)) flops *= 4.0;
+    static const int dbg = [] {
+      const char* e = getenv("BCMG_PAIR_DEBUG");
+      return e ? atoi(e) : 0;
+    }();
+    if (dbg & 1) BCMG_CUDA(cudaDeviceSynchronize());
     if (flops > 0) timed(K_TRAIL, st, flops, [&] { trailing_update(dt, p, info, st); });
+    if (dbg & 2) BCMG_CUDA(cudaDeviceSynchronize());
   };
 
   // Streamed host input (one device): the tile columns are copied from pinned
@@ -1055,10 +1061,10 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
           trail(k, op.a, op.b, crit);
           BCMG_CUDA(cudaEventRecord(E(U, k), crit));
         } else {
+          BCMG_CUDA(cudaStreamWaitEvent(bulk, E(R, k), 0));  // (also orders the copy-back of panel k)
           // paired panels: the bulk of step 2j waits for step 2j+1 (both panels at once)
           if (pair && k % 2 == 0 && k + 2 < g.nt) break;
           if (pair && k % 2) BCMG_CUDA(cudaStreamWaitEvent(bulk, E(R, k - 1), 0));
-          BCMG_CUDA(cudaStreamWaitEvent(bulk, E(R, k), 0));
           // with a lookahead this step, the full-grid update of tile k+1 goes
           // first; otherwise both persistent grids would race for the SMs and
           // the critical path could be queued behind the whole bulk update
