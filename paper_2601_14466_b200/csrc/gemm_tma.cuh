@@ -86,7 +86,7 @@ __device__ __forceinline__ unsigned char* tma_aux() {
 // waiting for that slice (mbarrier release / acquire orders the ring store).
 // When the items run out the producer publishes a sentinel (live = 0) and
 // completes the next stage's barrier without a transfer.
-template <class TL, bool FAN = true, class NextP>
+template <class TL, bool FAN = true, bool COPY = false, class NextP>
 __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUtensorMap* mapB, int K, NextP&& next_p,
                                               long long stagger_ns = 0) {
   double* smem = reinterpret_cast<double*>(tma_dyn_smem);
@@ -197,10 +197,13 @@ __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUt
       if (lane == 0) mbar_arrive(&empty[s]);
       ++g;
     }
-    // the item's geometry leaves shared memory only now, after the K loop
-    const Epilogue ep = cb.ep;
-    const int64_t M = cb.M, N = cb.N, m0 = cb.m0, n0 = cb.n0;
-    store_block<double, TL, false, FAN>(acc, ep, M, N, m0, n0, wm0, wn0, lane);
+    if constexpr (COPY) {  // the item's geometry in registers for the epilogue
+      const Epilogue ep = cb.ep;
+      const int64_t M = cb.M, N = cb.N, m0 = cb.m0, n0 = cb.n0;
+      store_block<double, TL, false, FAN>(acc, ep, M, N, m0, n0, wm0, wn0, lane);
+    } else {  // read from the ring as the epilogue needs it
+      store_block<double, TL, false, FAN>(acc, cb.ep, cb.M, cb.N, cb.m0, cb.n0, wm0, wn0, lane);
+    }
   }
 }
 
@@ -292,7 +295,7 @@ template <class TL>
 constexpr int min_blocks() { return 65536 / (TL::THREADS * 128) > 0 ? 65536 / (TL::THREADS * 128) : 1; }
 
 // Trailing update (see trail_kernel in gemm.cuh) over one panel tensor map.
-template <class TL>
+template <class TL, bool COPY = false>
 __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
     trail_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TrailParams p,
                      const int* info) {
@@ -351,7 +354,7 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
   // producer's cursor (thread 0 only) in the caller aux slot: no registers in the consumers
   Cursor& cp = *reinterpret_cast<Cursor*>(tma_aux<TL>() + 384);
   if (threadIdx.x == 0) cp = Cursor{p.m_first, 0, -1};
-  tma_gemm_loop<TL, false>(  // trailing updates never fan out
+  tma_gemm_loop<TL, false, COPY>(  // trailing updates never fan out
       &mapA, &mapB, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, TmaBlock& blk) { return decode(cp, item, blk); },
       p.stagger_ns);
 }
@@ -456,10 +459,7 @@ __device__ __forceinline__ void tma_gemm_loop_v1(const CUtensorMap* mapA, const 
       if (lane == 0) mbar_arrive(&empty[s]);
       ++g;
     }
-    // the item's geometry leaves shared memory only now, after the K loop
-    const Epilogue ep = cb.ep;
-    const int64_t M = cb.M, N = cb.N, m0 = cb.m0, n0 = cb.n0;
-    store_block<double, TL, false, FAN>(acc, ep, M, N, m0, n0, wm0, wn0, lane);
+    store_block<double, TL, false, FAN>(acc, cb.ep, cb.M, cb.N, cb.m0, cb.n0, wm0, wn0, lane);
   }
 }
 

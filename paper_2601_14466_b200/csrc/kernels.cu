@@ -267,11 +267,14 @@ static void launch_trail_tma_t(const TrailParams& p, const int* info, cudaStream
   const CUtensorMap mapB = p.cplx ? make_map(p.PB, prow, 2 * p.K, p.ldp, TL::LDB, TL::BK)
                                   : make_map(p.P, prow, p.K, p.ldp, TL::LDB, TL::BK);
   constexpr size_t smem = tma_smem_bytes<TL>();
-  static const bool v1 = [] {  // A/B switch: the round-1 consumer-side decode
-    const char* e = getenv("BCMG_TRAIL_V1");
-    return e && atoi(e) != 0;
+  // A/B switch (BCMG_TRAIL_VARIANT): 0 items in the shared-memory ring, read by
+  // the epilogue in place; 1 the round-1 consumer-side decode; 2 ring, item
+  // copied to registers for the epilogue
+  static const int variant = [] {
+    const char* e = getenv("BCMG_TRAIL_VARIANT");
+    return e ? atoi(e) : 0;
   }();
-  auto kern = v1 ? trail_tma_kernel_v1<TL> : trail_tma_kernel<TL>;
+  auto kern = variant == 1 ? trail_tma_kernel_v1<TL> : variant == 2 ? trail_tma_kernel<TL, true> : trail_tma_kernel<TL>;
   set_smem(kern, smem);
   int per_sm = 1;
   BCMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TL::THREADS, smem));

@@ -3,7 +3,7 @@
 variant: the selection is read once).  Prints one JSON line: potrs f64 N, T=1024
 on one GPU, the trailing-update launches' CUDA-event time and TF/s, the step time.
 
-    BCMG_TRAIL_V1=1 python tools/trail_ab.py --n 65536
+    BCMG_TRAIL_VARIANT=1 python tools/trail_ab.py --n 65536
 """
 import argparse
 import ctypes as C
@@ -43,7 +43,7 @@ for _ in range(a.reps):
     lib.bcmg_set_profiling(mesh.session, 0)
     s = (C.c_double * 4)()
     _lib.check(lib.bcmg_kernel_stats(mesh.session, 0, s))
-    r = {"n": a.n, "t": a.t, "v1": os.environ.get("BCMG_TRAIL_V1", "0"), "step_ms": e0.elapsed_time(e1),
+    r = {"n": a.n, "t": a.t, "variant": os.environ.get("BCMG_TRAIL_VARIANT", "0"), "step_ms": e0.elapsed_time(e1),
          "trail_ms": s[1], "trail_tflops": s[2] / (s[1] * 1e-3) / 1e12,
          "step_tflops": (a.n ** 3 / 3 + 2 * a.n ** 2 * 64) / (e0.elapsed_time(e1) * 1e-3) / 1e12}
     best = r if best is None or r["step_ms"] < best["step_ms"] else best
