@@ -267,12 +267,15 @@ static void launch_trail_tma_t(const TrailParams& p, const int* info, cudaStream
   const CUtensorMap mapB = p.cplx ? make_map(p.PB, prow, 2 * p.K, p.ldp, TL::LDB, TL::BK)
                                   : make_map(p.P, prow, p.K, p.ldp, TL::LDB, TL::BK);
   constexpr size_t smem = tma_smem_bytes<TL>();
-  // A/B switch (BCMG_TRAIL_VARIANT): 0 items in the shared-memory ring, read by
-  // the epilogue in place; 1 the round-1 consumer-side decode; 2 ring, item
-  // copied to registers for the epilogue
+  // BCMG_TRAIL_VARIANT: 1 (default) consumers decode their own items (a
+  // 24-byte stack frame: the epilogue's C pointer / bounds spill to L1);
+  // 0 items published in the shared-memory ring and read by the epilogue in
+  // place (no frame); 2 ring + register copy.  Measured at config 3
+  // (profiles/r02_trail_variants_ab.jsonl): 34.27 / 33.44 / 34.13 TF/s -- the
+  // spill-free epilogue's shared-memory reads cost more than the spills.
   static const int variant = [] {
     const char* e = getenv("BCMG_TRAIL_VARIANT");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 1;
   }();
   auto kern = variant == 1 ? trail_tma_kernel_v1<TL> : variant == 2 ? trail_tma_kernel<TL, true> : trail_tma_kernel<TL>;
   set_smem(kern, smem);
