@@ -446,10 +446,15 @@ def _hbm_peak() -> float:
 
 
 def _profile_traffic():
-    """dram bytes per trail_tma_kernel launch from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "trail_kernel_traffic.json")
+    """ncu DRAM bytes (read + write) per bulk trail_tma_kernel launch at the bench shape
+    (profiles/r02_trail_traffic_n131072.json, tools/trail_traffic.py), with the same
+    launches' algorithmic bytes."""
+    p = os.path.join(ROOT, "profiles", "r02_trail_traffic_n131072.json")
     try:
-        return json.load(open(p))["dram_bytes_per_launch"]
+        d = json.load(open(p))
+        return {"dram_bytes_per_launch": d["bulk_launch_traffic_mean"],
+                "algorithmic_bytes_per_launch": d["bulk_launch_algorithmic_mean"],
+                "ratio": d["bulk_ratio_mean"], "source": "profiles/r02_trail_traffic_n131072.json"}
     except Exception:
         return None
 
