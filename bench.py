@@ -419,7 +419,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                      "frac": achieved / peak.value if peak.value else None,
                      "peak_source": "measured live: bcmg_measure_fp64_peak (register-resident mma.sync.m8n8k4.f64 "
                                     "loop on all SMs); MEASURED_PEAKS.json has no FP64 entry",
-                     "traffic": _profile_traffic(), "launches": trail["launches"],
+                     "traffic": (_profile_traffic() or {}).get("dram_bytes_per_launch"),
+                     "traffic_detail": _profile_traffic(), "launches": trail["launches"],
                      "flops_per_launch": trail["flops"] / max(trail["launches"], 1),
                      "ms_per_launch": trail["ms"] / max(trail["launches"], 1),
                      "share_of_step": trail["ms"] / ms if ms else None,
