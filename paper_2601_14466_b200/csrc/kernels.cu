@@ -476,6 +476,72 @@ bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, 
   return true;
 }
 
+bool gemm_cplx_embed_grouped(int dt, int64_t M, int64_t K, const Operand& A, const Operand* Bs, const int64_t* ncols,
+                             int ngroups, const Epilogue& ep, void* scratch, size_t scratch_bytes, int64_t chunk,
+                             cudaStream_t st) {
+  if (getenv("BCMG_NO_CPLX_EMBED") || A.mask || ep.lower_only || ep.nfan) return false;
+  if (dt != C128 && dt != C64) return false;
+  if (dt == C128 ? !use_tma() : !(use_tc() && use_presplit())) return false;
+  const int64_t align = dt == C128 ? 2 : 4;
+  int64_t total = 0;
+  for (int i = 0; i < ngroups; ++i) {
+    if (Bs[i].mask || ncols[i] % align) return false;
+    total += ncols[i];
+  }
+  if (M <= 0 || K <= 0 || total <= 0 || chunk < 64 || chunk % align || (2 * M) % align) return false;
+  if (!aligned16(ep.C) || !aligned16(scratch) || scratch_bytes < gemm_cplx_embed_bytes(dt, M, chunk, K)) return false;
+  if (dt == C64 && 2 * M < 256) return false;  // the tcgen05 tile's minimum shape
+  const size_t csz = dt == C128 ? 16 : 8;
+  // A (M x K, op(A)) gathered ONCE as [A | -iA] (M x 2K complex), then chunk
+  // after chunk of the concatenated groups' columns as planar [Re B | -Im B]
+  // and one real GEMM per chunk into the concatenated output columns
+  char* at = static_cast<char*>(scratch);
+  char* xp = at + (size_t)2 * M * K * csz;
+  if (dt == C128) embed_gather<double2, double>(A, M, K, reinterpret_cast<double2*>(at), nullptr, M, st);
+  else embed_gather<float2, float>(A, M, K, reinterpret_cast<float2*>(at), nullptr, M, st);
+  float *ah = nullptr, *al = nullptr, *bh = nullptr, *bl = nullptr;
+  const int64_t kp = split_ld(2 * K);
+  if (dt == C64) {  // tf32 planes: A split once, B per chunk
+    float* sp = split_scratch(st, (size_t)2 * (2 * M + chunk) * kp * 4);
+    ah = sp;
+    al = sp + 2 * M * kp;
+    bh = al + 2 * M * kp;
+    bl = bh + chunk * kp;
+    split_tf32(0, at, 2 * M, 2 * M, 2 * K, 2 * K, ah, al, kp, st);
+  }
+  int gi = 0;
+  int64_t goff = 0;  // column offset inside group gi
+  for (int64_t g0 = 0; g0 < total; g0 += chunk) {
+    const int64_t cn = std::min(chunk, total - g0);
+    for (int64_t r = 0; r < cn;) {  // gather the chunk's columns group by group
+      while (goff >= ncols[gi]) {
+        goff = 0;
+        ++gi;
+      }
+      const int64_t take = std::min(cn - r, ncols[gi] - goff);
+      Operand b = Bs[gi];
+      // logical row i of B-hat is stored column i (trans) or row i
+      b.ptr = static_cast<const char*>(b.ptr) + (b.trans ? goff * b.ld : goff) * (int64_t)csz;
+      if (dt == C128) embed_gather<double2, double>(b, take, K, nullptr, reinterpret_cast<double*>(xp) + r, cn, st);
+      else embed_gather<float2, float>(b, take, K, nullptr, reinterpret_cast<float*>(xp) + r, cn, st);
+      r += take;
+      goff += take;
+    }
+    Epilogue er = ep;
+    er.C = static_cast<char*>(ep.C) + g0 * ep.ldc * (int64_t)csz;
+    if (dt == C128) {
+      er.ldc = 2 * ep.ldc;
+      launch_gemm_tma_t<TileTrail2>(2 * M, cn, 2 * K, Operand{at, 2 * M, 0, 0, 0, 0}, Operand{xp, cn, 0, 0, 0, 0}, er,
+                                    nullptr, st);
+    } else {
+      split_tf32(0, xp, cn, cn, 2 * K, 2 * K, bh, bl, kp, st);
+      tck_gemm(2 * M, cn, 2 * K, ah, al, bh, bl, kp, static_cast<float*>(er.C), 2 * ep.ldc, (float)ep.alpha,
+               (float)ep.beta, nullptr, st, &er);
+    }
+  }
+  return true;
+}
+
 static bool use_tma() {
   static const bool v = [] {
     const char* e = getenv("BCMG_NO_TMA");

@@ -47,6 +47,13 @@ void expand_panel(int dt, void* P, void* PB, int64_t rows, int64_t K, cudaStream
 size_t gemm_cplx_embed_bytes(int dt, int64_t M, int64_t N, int64_t K);
 bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
                      void* scratch, size_t scratch_bytes, const int* info, cudaStream_t st, bool always = false);
+// Several column groups B_i (ncols[i] columns each) against one A, outputs
+// concatenated in ep.C (ld ep.ldc): A is gathered (and split) once, the
+// groups' columns chunk by chunk (`chunk` columns per GEMM; scratch >=
+// gemm_cplx_embed_bytes(dt, M, chunk, K)).  False: nothing launched.
+bool gemm_cplx_embed_grouped(int dt, int64_t M, int64_t K, const Operand& A, const Operand* Bs, const int64_t* ncols,
+                             int ngroups, const Epilogue& ep, void* scratch, size_t scratch_bytes, int64_t chunk,
+                             cudaStream_t st);
 
 // tf32 hi / lo pre-split (see split_tf32_kernel) and the tcgen05 GEMM on the
 // split planes.  split_ld: the K-major leading dimension for Kx columns.

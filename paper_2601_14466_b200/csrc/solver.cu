@@ -660,6 +660,13 @@ WsPlan workspace_plan(int routine, int dt, int64_t n, int64_t T, int ndev, int w
                 w.split_scratch = std::max(w.split_scratch, emb_split(tcs, std::min(nc, cu - c0), n - ss));
           }
         }
+        // the grouped product GEMM over all local devices (gemm_cplx_embed_grouped) splits whole chunks
+        if (dt == C64 && g.nloc > 1 && 2 * tcs >= 256) {
+          int64_t tot = 0;
+          for (int d = r * g.nloc; d < (r + 1) * g.nloc; ++d) tot += cols_upto(g, d, s);
+          const int64_t nc = potri_chunk_cols(dt, n, ss, tcs, w.embed, nsm);
+          if (tot && nc >= 64) w.split_scratch = std::max(w.split_scratch, split_scratch_bytes(C64, tcs, nc, n - ss));
+        }
       }
   }
   return w;
@@ -1321,7 +1328,26 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
       case S_PGEMM: {
         int64_t ldw = 0;
         const void* W = w_of(s, &ldw);
-        for (int d = g.dev0; d < g.dev0 + g.nloc; ++d) {
+        // all local devices at once: one embedded GEMM over the concatenated
+        // columns (their product blocks are contiguous in `blocks`), W_s
+        // gathered once -- per-device GEMMs would be 1/nloc as wide
+        bool grouped = false;
+        if (emb && g.nloc > 1) {
+          std::vector<Operand> bs;
+          std::vector<int64_t> nc_d;
+          for (int d = g.dev0; d < g.dev0 + g.nloc; ++d) {
+            const int64_t c = cols_upto(g, d, s);
+            if (!c) continue;
+            bs.push_back(opB(colp(shards[d - g.dev0], g, ss, 0), n, OP_N));
+            nc_d.push_back(c);
+          }
+          const int64_t nc = potri_chunk_cols(dt, n, ss, tcs, emb_bytes, nsm);
+          grouped = !bs.empty() &&
+                    gemm_cplx_embed_grouped(dt, tcs, n - ss, opA(W, ldw, OP_C), bs.data(), nc_d.data(), (int)bs.size(),
+                                            Epilogue{blocks + block_off(s, g.dev0) * g.esz, tcs, 1.0, 0.0, 0, 0},
+                                            embed_buf.p, emb_bytes, nc, st);
+        }
+        for (int d = g.dev0; !grouped && d < g.dev0 + g.nloc; ++d) {
           const int64_t c = cols_upto(g, d, s);
           if (c == 0) continue;
           const Operand wh = opA(W, ldw, OP_C);
