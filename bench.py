@@ -254,6 +254,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
+        # communicator evidence (nranks, NVLS) into a per-rank file, not stdout: rank 0
+        # quotes it in its JSON line (also when the driver launches torchrun itself)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV")
+        os.environ.setdefault("NCCL_DEBUG_FILE", NCCL_LOG)
         dist.init_process_group("nccl", device_id=dev)
     cfg = workload(world, args)
     n, t, nrhs = cfg["n"], cfg["t"], cfg["nrhs"]
@@ -476,6 +481,7 @@ def _nvlink_bytes(lib, n: int, t: int, world: int, rank: int) -> tuple:
 
 
 NCCL_LOG = "/tmp/bcmg_nccl_debug.%h.%p.log"
+_T_START = time.time()
 
 
 def _nccl_summary():
@@ -484,7 +490,9 @@ def _nccl_summary():
     import re
 
     lines = []
-    for f in sorted(glob.glob(NCCL_LOG.replace("%h", "*").replace("%p", "*")))[:16]:
+    files = [f for f in glob.glob(NCCL_LOG.replace("%h", "*").replace("%p", "*"))
+             if os.path.getmtime(f) >= _T_START - 5]  # this job's ranks only (stale /tmp files skipped)
+    for f in sorted(files)[:16]:
         try:
             for ln in open(f, errors="replace"):
                 if re.search(r"nranks|NVLS|Init COMPLETE|comm 0x", ln):
