@@ -198,6 +198,12 @@ int64_t bcmg_last_moved_bytes(bcmg_session* s);
 int bcmg_ipc_export(const void* ptr, unsigned char* token /* [72] */);
 int bcmg_ipc_open(const unsigned char* token /* [72] */, void** ptr);
 int bcmg_ipc_close_all(void);
+/* The stream-ordered flags of the peer hand-offs (cuStreamWriteValue32 /
+   cuStreamWaitValue32 on a device word, e.g. an opened token): write v after
+   everything earlier on `stream` (CONFIG if the driver refuses the address),
+   or make `stream` wait until the word is >= v. */
+int bcmg_stream_write_flag(void* stream, void* addr, unsigned v);
+int bcmg_stream_wait_flag(void* stream, const void* addr, unsigned v);
 
 /* Device workspace of one process for a pipeline (routine 1: potrs, 2:
    potri), excluding the shards: the exact bytes bcmg_potrs / bcmg_potri

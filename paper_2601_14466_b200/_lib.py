@@ -67,6 +67,8 @@ SIGNATURES = {
     "bcmg_ipc_export": (C.c_int, [_vp, C.c_char_p]),
     "bcmg_ipc_open": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
     "bcmg_ipc_close_all": (C.c_int, []),
+    "bcmg_stream_write_flag": (C.c_int, [_vp, _vp, C.c_uint]),
+    "bcmg_stream_wait_flag": (C.c_int, [_vp, _vp, C.c_uint]),
     "bcmg_set_profiling": (C.c_int, [_vp, C.c_int]),
     "bcmg_kernel_stats": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_double)]),
     "bcmg_launch_count": (C.c_int64, []),

@@ -483,6 +483,22 @@ int bcmg_ipc_close_all(void) {
   return guarded([&] { bcmg::ipc_close_all(); });
 }
 
+int bcmg_stream_write_flag(void* stream, void* addr, unsigned v) {
+  return guarded([&] {
+    if (!addr) throw bcmg::Error(BCMG_ERR_CONFIG, "null flag address");
+    if (!bcmg::stream_write_value(static_cast<cudaStream_t>(stream), addr, v))
+      throw bcmg::Error(BCMG_ERR_CONFIG, "cuStreamWriteValue32 refused the address");
+  });
+}
+
+int bcmg_stream_wait_flag(void* stream, const void* addr, unsigned v) {
+  return guarded([&] {
+    if (!addr) throw bcmg::Error(BCMG_ERR_CONFIG, "null flag address");
+    if (!bcmg::stream_wait_supported()) throw bcmg::Error(BCMG_ERR_CONFIG, "cuStreamWaitValue32 unavailable");
+    bcmg::stream_wait_geq(static_cast<cudaStream_t>(stream), addr, v);
+  });
+}
+
 int bcmg_session_workspace_bytes(bcmg_session* s, int64_t* bytes) {
   return guarded([&] { *bytes = (int64_t)live(s)->held_workspace_bytes(); });
 }

@@ -44,9 +44,6 @@ class HandleToken:
     shape: tuple
 
 
-_DTYPES = {"float32": 4, "float64": 8, "complex64": 8, "complex128": 16}
-
-
 def publish_handle(tensor, device_index: int = 0) -> HandleToken:
     """Export a CUDA tensor of this process (runtime.py:392-397)."""
     if not getattr(tensor, "is_cuda", False):
@@ -63,7 +60,7 @@ def publish_handle(tensor, device_index: int = 0) -> HandleToken:
 class _CudaArray:
     """__cuda_array_interface__ wrapper of an opened (peer) device address."""
 
-    _TYPESTR = {"float32": "<f4", "float64": "<f8", "complex64": "<c8", "complex128": "<c16"}
+    _TYPESTR = {"float32": "<f4", "float64": "<f8", "complex64": "<c8", "complex128": "<c16", "int32": "<i4"}
 
     def __init__(self, ptr: int, token: HandleToken):
         self.__cuda_array_interface__ = {"shape": token.shape, "typestr": self._TYPESTR[token.dtype],

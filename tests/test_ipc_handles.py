@@ -57,6 +57,13 @@ t = ipc.open_handle(tok)                      # the parent's tensor, mapped into
 ok = bool(torch.equal(t.cpu(), torch.arange(1000, dtype=torch.float64).reshape(10, 100)))
 t[3:5] *= -2.0                                # write through the mapping
 torch.cuda.synchronize()
+import ctypes as C
+from paper_2601_14466_b200 import _lib
+ftok = ipc.HandleToken(bytes.fromhex(sys.stdin.readline().strip()), 0, 16, "int32", (4,))
+flag = ipc.open_handle(ftok)                  # the parent's flag words
+st = torch.cuda.current_stream()
+rc = _lib.load().bcmg_stream_write_flag(C.c_void_p(st.cuda_stream), C.c_void_p(flag.data_ptr() + 4), 7)
+st.synchronize()
 own = torch.full((7,), 5.0, dtype=torch.float64, device="cuda")
 mine = ipc.publish_handle(own, 1)
 try:
@@ -64,7 +71,7 @@ try:
     own_refused = False
 except ipc.HandleDomainError:
     own_refused = True
-print(int(ok), int(own_refused), mine.token.hex(), flush=True)
+print(int(ok), int(own_refused), mine.token.hex(), rc, flush=True)
 sys.stdin.readline()                          # keep `own` alive until the parent has read it
 ipc.close_all()
 """
@@ -79,14 +86,26 @@ def test_ipc_token_across_processes(cuda):
     view = big[4096:4096 + 1000].view(10, 100)
     view.copy_(a)
     tok = ipc.publish_handle(view)
+    flags = torch.zeros(4, dtype=torch.int32, device=cuda)
+    ftok = ipc.publish_handle(flags)
     torch.cuda.synchronize()
     p = subprocess.Popen([sys.executable, "-c", _CHILD, ROOT], stdin=subprocess.PIPE, stdout=subprocess.PIPE,
                          stderr=subprocess.PIPE, text=True)
     try:
-        p.stdin.write(tok.token.hex() + "\n")
+        p.stdin.write(tok.token.hex() + "\n" + ftok.token.hex() + "\n")
         p.stdin.flush()
         line = p.stdout.readline().split()
-        assert len(line) == 3, p.stderr.read()
+        assert len(line) == 4, p.stderr.read()
+        # the child raised flag word 1 with a stream memory operation on the opened token
+        # (the copy-engine panel hand-off's flag path, csrc/comm.cpp post_flag)
+        assert line[3] == "0", "cuStreamWriteValue32 refused an IPC-mapped address"
+        assert flags.cpu().tolist() == [0, 7, 0, 0]
+        st = torch.cuda.current_stream()
+        lib = _lib.load()
+        import ctypes as C
+
+        assert lib.bcmg_stream_wait_flag(C.c_void_p(st.cuda_stream), C.c_void_p(flags.data_ptr() + 4), 7) == 0
+        st.synchronize()  # already satisfied: returns
         assert line[0] == "1", "child saw different bytes through the mapping"
         assert line[1] == "1", "opening a process's own token must be refused"
         # the child's writes landed in our memory (the child synchronised before answering)
