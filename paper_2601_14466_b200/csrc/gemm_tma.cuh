@@ -477,70 +477,9 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
   // tile cursor: items only grow for a given caller, so the walk over tiles is
   // amortised O(1); producer and consumer each own one
   struct Cursor {
-    int64_t m, base, cnt, ar;
+    int64_t m, base, cnt;
   };
-  // Band order (p.band > 0, real, T a multiple of BM, tile columns spaced sc =
-  // 1 or D): items of `band` consecutive local tile columns interleaved by
-  // ABSOLUTE row block ar -- level ar holds, for every tile of the band that
-  // reaches row ar*BM, its column blocks of that row block -- so a panel row
-  // block (the A operand, shared by every tile at that height) is fetched once
-  // per band instead of once per tile column.  Same items, same arithmetic.
-  const int64_t sc = p.nloc == p.D ? 1 : p.D;
-  constexpr int64_t R = TL::BM / TL::BN;
-  auto lvl_cnt = [&p](int64_t mt, int64_t ar) -> int64_t {  // tile mt's column blocks at row block ar
-    const int64_t rb0 = mt * p.T / TL::BM;
-    if (ar < rb0) return 0;
-    const int64_t tc = p.T < p.N - mt * p.T ? p.T : p.N - mt * p.T, ncb = (tc + TL::BN - 1) / TL::BN;
-    const int64_t c = (ar - rb0 + 1) * R;
-    return c < ncb ? c : ncb;
-  };
-  auto decode_band = [&](Cursor& cur, int64_t item, TmaBlock& blk) -> bool {
-    const int64_t nrb = (p.N + TL::BM - 1) / TL::BM;
-    int64_t nb = 0;
-    for (;;) {
-      if (cur.m >= p.m_last) return false;
-      nb = (p.m_last - cur.m + sc - 1) / sc;
-      if (nb > p.band) nb = p.band;
-      if (cur.cnt < 0) {
-        if (cur.ar < 0) cur.ar = cur.m * p.T / TL::BM;
-        if (cur.ar >= nrb) {  // band done: the next one
-          cur.m += nb * sc;
-          cur.ar = -1;
-          continue;
-        }
-        int64_t c = 0;
-        for (int64_t j = 0; j < nb; ++j) c += lvl_cnt(cur.m + j * sc, cur.ar);
-        cur.cnt = c;
-      }
-      if (item < cur.base + cur.cnt) break;
-      cur.base += cur.cnt;
-      ++cur.ar;
-      cur.cnt = -1;
-    }
-    int64_t o = item - cur.base, m = cur.m;
-    for (int64_t j = 0; j < nb; ++j) {
-      const int64_t c = lvl_cnt(cur.m + j * sc, cur.ar);
-      if (o < c) {
-        m = cur.m + j * sc;
-        break;
-      }
-      o -= c;
-    }
-    const int64_t ms = m * p.T, rows = p.N - ms, tc = p.T < rows ? p.T : rows;
-    const int dev = (int)(m % p.D);
-    double* shard = reinterpret_cast<double*>(p.shards[dev - p.dev0]);
-    const int64_t loc = (m / p.D) * p.T;
-    blk.a_row = (int)(ms - p.prow0);
-    blk.b_row = (int)(ms - p.prow0);
-    blk.m0 = (cur.ar - ms / TL::BM) * TL::BM;
-    blk.n0 = o * TL::BN;
-    blk.M = rows;
-    blk.N = tc;
-    blk.ep = Epilogue{shard + ms + loc * p.N, p.N, -1.0, 1.0, 0, 0};
-    return true;
-  };
-  auto decode = [&](Cursor& cur, int64_t item, TmaBlock& blk) -> bool {
-    if (p.band > 0) return decode_band(cur, item, blk);
+  auto decode = [&p](Cursor& cur, int64_t item, TmaBlock& blk) -> bool {
     for (;;) {
       if (cur.m >= p.m_last) return false;
       const int dev = (int)(cur.m % p.D);
@@ -584,10 +523,8 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
   };
   // producer's cursor (thread 0 only) in the caller aux slot: no registers in the consumers
   Cursor& cp = *reinterpret_cast<Cursor*>(tma_aux<TL>() + 384);
-  // band: the first local tile column (tiles dev0, dev0 + D, ... when sc = D)
-  const int64_t m0 = p.band > 0 && sc > 1 ? p.m_first + ((p.dev0 - p.m_first % p.D) + p.D) % p.D : p.m_first;
-  if (threadIdx.x == 0) cp = Cursor{m0, 0, -1, -1};
-  Cursor cc{m0, 0, -1, -1};
+  if (threadIdx.x == 0) cp = Cursor{p.m_first, 0, -1};
+  Cursor cc{p.m_first, 0, -1};
   tma_gemm_loop_v1<TL, false>(  // trailing updates never fan out
       &mapA, &mapB, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, TmaBlock& blk) { return decode(cp, item, blk); },
       [&](int64_t item, TmaBlock& blk) { return decode(cc, item, blk); }, p.stagger_ns);

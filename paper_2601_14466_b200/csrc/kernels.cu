@@ -286,12 +286,6 @@ static void launch_trail_tma_t(const TrailParams& p, const int* info, cudaStream
   const int64_t grid = std::min<int64_t>(total, (int64_t)sms * per_sm);
   TrailParams q = p;
   q.stagger_ns = 0;
-  // band order across tile columns (trail_tma_kernel_v1; BCMG_DMMA_BAND, 0 = off)
-  static const int dmma_band = [] {
-    const char* e = getenv("BCMG_DMMA_BAND");
-    return e && *e ? std::max(0, atoi(e)) : 4;
-  }();
-  q.band = (variant == 1 && !p.cplx && p.T % TL::BM == 0 && (p.nloc == 1 || p.nloc == p.D)) ? dmma_band : 0;
   if (per_sm >= 2 && total >= 8 * grid) {
     // half an item at ~85% of the per-CTA DMMA rate (37 TF/s over 2 CTAs per SM)
     const double item_flops = 2.0 * TL::BM * TL::BN * (double)p.K * (p.cplx ? 2 : 1);
