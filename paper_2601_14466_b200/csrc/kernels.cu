@@ -690,10 +690,11 @@ static int tck_width(int64_t n) {
   return n >= 256 ? 256 : 128;
 }
 
-template <int BNT>
+template <int BNT, int CL = 1>
 static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream_t st) {
-  using TZ = TrapR<tc::BM, BNT>;
-  using TZC = TrapR<tc::BM / 2, BNT>;
+  constexpr int64_t BMX = CL * tc::BM;
+  using TZ = TrapR<BMX, BNT>;
+  using TZC = TrapR<BMX / 2, BNT>;
   int64_t total = 0;
   for (int64_t m = p.m_first; m < p.m_last; ++m) {
     const int dev = (int)(m % p.D);
@@ -708,7 +709,7 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
       const char* e = getenv("BCMG_TRAIL_BAND");
       return e && *e ? std::max(0, atoi(e)) : 8;
     }();
-    const int64_t rb = p.cplx ? tc::BM / 2 : tc::BM;
+    const int64_t rb = p.cplx ? BMX / 2 : BMX;
     const bool cols = p.T <= BNT && p.T % rb == 0 && (p.nloc == 1 || p.nloc == p.D);
     const bool blocks = p.T > BNT && p.T % BNT == 0 && p.N % p.T == 0 && p.nloc == p.D;
     q.band = cols || blocks ? band : 0;
@@ -716,18 +717,47 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   const int64_t prow = p.N - p.prow0, arows = p.cplx ? 2 * prow : prow;
   const CUtensorMap ah = make_map_kmajor(p.split[0], arows, p.split_ld[0]);
   const CUtensorMap al = make_map_kmajor(p.split[1], arows, p.split_ld[0]);
-  const CUtensorMap bh = make_map_kmajor(p.split[2], prow, p.split_ld[1], BNT);
-  const CUtensorMap bl = make_map_kmajor(p.split[3], prow, p.split_ld[1], BNT);
+  const CUtensorMap bh = make_map_kmajor(p.split[2], prow, p.split_ld[1], BNT / CL);  // CL = 2: half-tile boxes
+  const CUtensorMap bl = make_map_kmajor(p.split[3], prow, p.split_ld[1], BNT / CL);
   constexpr size_t smem = tck::Cfg<BNT>::SMEM_BYTES;
-  set_smem(tck_trail_kernel<BNT>, smem);
+  auto kern = tck_trail_kernel<BNT, CL>;
+  set_smem(kern, smem);
   const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, num_sms()) : num_sms();
-  const int64_t grid = std::min<int64_t>(total, sms);
-  tck_trail_kernel<BNT><<<(unsigned)grid, tck::THREADS, smem, st>>>(ah, al, bh, bl, q, info);
+  if constexpr (CL == 1) {
+    const int64_t grid = std::min<int64_t>(total, sms);
+    kern<<<(unsigned)grid, tck::THREADS, smem, st>>>(ah, al, bh, bl, q, info);
+  } else {  // clusters of two CTAs (one per SM of a TPC pair)
+    const int64_t pairs = std::min<int64_t>(total, sms / 2);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * std::max<int64_t>(pairs, 1)));
+    cfg.blockDim = dim3(tck::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    BCMG_CUDA(cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, q, info));
+  }
   BCMG_CHECK_LAUNCH();
 }
 
+// BCMG_TCK_CLUSTER (default 1): the 256-wide trailing update runs as CTA pairs
+// sharing the B tile through TMA multicast (tck_loop CL = 2)
+static bool tck_cluster() {
+  static const bool v = [] {
+    const char* e = getenv("BCMG_TCK_CLUSTER");
+    return !(e && *e && atoi(e) == 0);
+  }();
+  return v;
+}
+
 static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t st) {
-  if (tck_width(p.T) == 256) return launch_tck_trail_t<256>(p, info, st);
+  if (tck_width(p.T) == 256)
+    return tck_cluster() ? launch_tck_trail_t<256, 2>(p, info, st) : launch_tck_trail_t<256, 1>(p, info, st);
   launch_tck_trail_t<128>(p, info, st);
 }
 

@@ -51,9 +51,46 @@ __device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uin
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
-template <int BNT, class Next>
+// CTA-pair helpers (CL = 2: two CTAs of a cluster share the B operand, see tck_loop)
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// TMA box into the same shared-memory offset of every CTA in `mask`; each
+// destination CTA's mbarrier at the same offset receives its bytes
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+// MMA completion arrives on the mbarrier at the same offset in every CTA of `mask`
+__device__ __forceinline__ void commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+// CL = 1: one CTA per 128-row item.  CL = 2: a cluster of two CTAs per
+// 256-row item, CTA r computing rows [128 r, 128 r + 128) with its own A rows
+// but the SAME B tile, which each CTA loads half of and multicasts to both:
+// per SM the operand traffic from L2 drops from A + B to A + B/2 (96 -> 64 KB
+// per k-tile at BNT = 256), the resource the 3xTF32 pre-split operands
+// saturate.  A stage is refilled only once both CTAs' MMAs released it (the
+// MMA commit arrives on both CTAs' empty barriers, count 2).
+template <int BNT, int CL = 1, class Next>
 __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorMap* mAl, const CUtensorMap* mBh,
                                          const CUtensorMap* mBl, int K, Next&& next) {
+  static_assert(CL == 1 || CL == 2, "cluster size");
   using CF = Cfg<BNT>;
   constexpr int STAGES = CF::STAGES, STAGE_BYTES = CF::STAGE_BYTES, PLANE_A = CF::PLANE_A, PLANE_B = CF::PLANE_B;
   constexpr int BN = BNT;
@@ -66,11 +103,13 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KT = (K + BK - 1) / BK;
+  const int rank = CL == 2 ? (int)cluster_rank() : 0;
+  const int64_t first = blockIdx.x / CL, stride = gridDim.x / CL;  // items per cluster
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // released by this CTA's MMAs and (CL = 2) the peer's
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -85,6 +124,7 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
   }
   tc::fence_before();
   __syncthreads();
+  if constexpr (CL == 2) cluster_sync_all();  // the peer's barriers exist before anything is multicast to them
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -97,18 +137,31 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(mBl) : "memory");
       uint32_t g = 0;
       tc::Blk blk;
-      for (int64_t item = blockIdx.x; next(item, blk); item += gridDim.x) {
+      const int arow = rank * BM;  // this CTA's rows of a (CL x 128)-row item
+      for (int64_t item = first; next(item, blk); item += stride) {
         for (int kt = 0; kt < KT; ++kt, ++g) {
           const int s = g % STAGES;
           mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
           unsigned char* st = base + (size_t)s * STAGE_BYTES;
-          mbar_expect_tx(&full[s], STAGE_BYTES);
+          mbar_expect_tx(&full[s], STAGE_BYTES);  // A (own) + the whole B tile (half from the peer when CL = 2)
           // box {32 k, 128 rows}: coordinates (k, row)
-          tma_load_2d(st, mAh, kt * BK, blk.a_row + (int)blk.m0, &full[s]);
-          tma_load_2d(st + PLANE_A, mAl, kt * BK, blk.a_row + (int)blk.m0, &full[s]);
-          tma_load_2d(st + 2 * PLANE_A, mBh, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
-          tma_load_2d(st + 2 * PLANE_A + PLANE_B, mBl, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
+          tma_load_2d(st, mAh, kt * BK, blk.a_row + (int)blk.m0 + arow, &full[s]);
+          tma_load_2d(st + PLANE_A, mAl, kt * BK, blk.a_row + (int)blk.m0 + arow, &full[s]);
+          if constexpr (CL == 1) {
+            tma_load_2d(st + 2 * PLANE_A, mBh, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
+            tma_load_2d(st + 2 * PLANE_A + PLANE_B, mBl, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
+          } else {  // B rows [rank BNT/2, ...) of the tile, into both CTAs (box {32 k, BNT/2 rows})
+            const int brow = blk.b_row + (int)blk.n0 + rank * (BN / 2);
+            const size_t boff = (size_t)rank * (PLANE_B / 2);  // whole 1 KB swizzle atoms
+            tma_load_2d_mc(st + 2 * PLANE_A + boff, mBh, kt * BK, brow, &full[s], 0x3);
+            tma_load_2d_mc(st + 2 * PLANE_A + PLANE_B + boff, mBl, kt * BK, brow, &full[s], 0x3);
+          }
         }
+      }
+      if constexpr (CL == 2) {
+        // the peer's last MMA commits arrive on our empty barriers: let them land before exit
+        for (uint32_t q = g > (uint32_t)STAGES ? g - STAGES : 0; q < g; ++q)
+          mbar_wait(&empty[q % STAGES], (q / STAGES) & 1);
       }
     }
   } else if (warp == 1) {
@@ -116,7 +169,7 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
     if (lane == 0) {
       uint32_t g = 0, t = 0;
       tc::Blk blk;
-      for (int64_t item = blockIdx.x; next(item, blk); item += gridDim.x, ++t) {
+      for (int64_t item = first; next(item, blk); item += stride, ++t) {
         const int b = t & 1;
         mbar_wait(&tempty[b], ((t >> 1) & 1) ^ 1);
         tc::fence_after();
@@ -134,7 +187,8 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
             mma(d, tc::sdesc(ahi + off), tc::sdesc(blo + off), CF::IDESC, 1);
             mma(d, tc::sdesc(ahi + off), tc::sdesc(bhi + off), CF::IDESC, 1);
           }
-          tc::commit(&empty[s]);  // stage reusable once these MMAs have read it
+          if constexpr (CL == 1) tc::commit(&empty[s]);  // stage reusable once these MMAs have read it
+          else commit_mc(&empty[s], 0x3);              // ... in both CTAs (the B half came from the peer)
         }
         tc::commit(&tfull[b]);
       }
@@ -146,9 +200,9 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
     const int row = 32 * q + lane;
     uint32_t t = 0;
     tc::Blk blk;
-    for (int64_t item = blockIdx.x; next(item, blk); item += gridDim.x, ++t) {
+    for (int64_t item = first; next(item, blk); item += stride, ++t) {
       const int b = t & 1;
-      const int64_t r = blk.m0 + row;
+      const int64_t r = blk.m0 + rank * BM + row;
       float* __restrict__ crow = blk.C + r;
       auto load_chunk = [&](int c0, float* dst) {
 #pragma unroll
@@ -160,7 +214,7 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
       const int cbeg = ch * (BN / 2), cend = cbeg + BN / 2;
       if (blk.beta != 0.f) {  // pull this warp's 32-row block into L2 during the MMAs
         constexpr int PER = BN / 2 / 32;
-        const int64_t col = blk.n0 + cbeg + PER * lane, r0 = blk.m0 + 32 * q;
+        const int64_t col = blk.n0 + cbeg + PER * lane, r0 = blk.m0 + rank * BM + 32 * q;
 #pragma unroll
         for (int j = 0; j < PER; ++j)
           if (col + j < blk.N && r0 < blk.M) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(blk.C + r0 + (col + j) * blk.ldc));
@@ -194,6 +248,7 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
     }
   }
   __syncthreads();
+  if constexpr (CL == 2) cluster_sync_all();  // no CTA leaves while its peer may still write to it
   if (warp == 1) {
     tc::fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(CF::TMEM_COLS));
@@ -232,14 +287,16 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
 
 // potrf trailing update on the pre-split panel (TrailParams::split_*): same
 // item decode as tc3_trail_kernel (real, or the complex64 embedding).
-template <int BNT>
+template <int BNT, int CL = 1>
 __global__ void __launch_bounds__(tck::THREADS, 1)
     tck_trail_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                      const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, TrailParams p,
                      const int* info) {
-  using TZ = TrapR<tc::BM, BNT>;
-  using TZC = TrapR<tc::BM / 2, BNT>;
-  if (ld_flag(info)) return;
+  constexpr int64_t BMX = CL * tc::BM;  // rows per item (a CTA pair covers 256)
+  using TZ = TrapR<BMX, BNT>;
+  using TZC = TrapR<BMX / 2, BNT>;
+  // (a CTA pair must not split on a flag another stream may be writing: only single CTAs skip)
+  if (CL == 1 && ld_flag(info)) return;
   int64_t cm = p.m_first, cbase = 0, ccnt = -1;
   // band mode (see TrailParams::band).  The band interleaves "units" that all
   // end at row N: owned tile columns (T <= BNT, spaced sc tiles), or, with one
@@ -252,9 +309,9 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
   const int64_t cm0 = cm;
   auto unit_row = [&](int64_t k) { return ncb == 1 ? (cm0 + k * sc) * p.T : (p.m_first * ncb + k) * BNT; };
   int64_t ku = 0, bg = 0, ba0 = 0, btop = 0;
-  tck::tck_loop<BNT>(&mAh, &mAl, &mBh, &mBl, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, tc::Blk& blk) -> bool {
+  tck::tck_loop<BNT, CL>(&mAh, &mAl, &mBh, &mBl, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, tc::Blk& blk) -> bool {
     if (p.band > 0) {
-      const int64_t RB = p.cplx ? tc::BM / 2 : tc::BM;  // matrix rows per row block (complex64: embedded pairs)
+      const int64_t RB = p.cplx ? BMX / 2 : BMX;  // matrix rows per row block (complex64: embedded pairs)
       const int64_t step = (ncb == 1 ? sc * p.T : (int64_t)BNT) / RB, aend = (p.N + RB - 1) / RB;
       for (;;) {
         if (ku >= nunits) return false;
@@ -290,7 +347,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
       const int64_t cx = p.cplx ? 2 : 1;
       blk.a_row = (int)(cx * (ms - p.prow0));
       blk.b_row = (int)(ms - p.prow0);
-      blk.m0 = (A - ms / RB) * tc::BM;
+      blk.m0 = (A - ms / RB) * BMX;
       blk.n0 = cb * BNT;
       blk.M = cx * rows;
       blk.N = p.T < rows ? p.T : rows;
@@ -324,7 +381,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
       TZC::decode(item - cbase, tcw, rb, cb);
       blk.a_row = (int)(2 * (ms - p.prow0));
       blk.b_row = (int)(ms - p.prow0);
-      blk.m0 = rb * tc::BM;
+      blk.m0 = rb * BMX;
       blk.n0 = cb * BNT;
       blk.M = 2 * rows;
       blk.N = tcw;
@@ -334,7 +391,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
       TZ::decode(item - cbase, tcw, rb, cb);
       blk.a_row = (int)(ms - p.prow0);
       blk.b_row = (int)(ms - p.prow0);
-      blk.m0 = rb * tc::BM;
+      blk.m0 = rb * BMX;
       blk.n0 = cb * BNT;
       blk.M = rows;
       blk.N = tcw;
