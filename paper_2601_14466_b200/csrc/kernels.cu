@@ -692,7 +692,7 @@ static int tck_width(int64_t n) {
 
 template <int BNT, int CL = 1>
 static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream_t st) {
-  constexpr int64_t BMX = CL * tc::BM;
+  constexpr int64_t BMX = (CL == 1 ? 1 : 2) * tc::BM;
   using TZ = TrapR<BMX, BNT>;
   using TZC = TrapR<BMX / 2, BNT>;
   int64_t total = 0;
@@ -717,9 +717,9 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   const int64_t prow = p.N - p.prow0, arows = p.cplx ? 2 * prow : prow;
   const CUtensorMap ah = make_map_kmajor(p.split[0], arows, p.split_ld[0]);
   const CUtensorMap al = make_map_kmajor(p.split[1], arows, p.split_ld[0]);
-  const CUtensorMap bh = make_map_kmajor(p.split[2], prow, p.split_ld[1], BNT / CL);  // CL = 2: half-tile boxes
-  const CUtensorMap bl = make_map_kmajor(p.split[3], prow, p.split_ld[1], BNT / CL);
-  constexpr size_t smem = tck::Cfg<BNT>::SMEM_BYTES;
+  const CUtensorMap bh = make_map_kmajor(p.split[2], prow, p.split_ld[1], CL == 1 ? BNT : BNT / 2);  // pairs: halves
+  const CUtensorMap bl = make_map_kmajor(p.split[3], prow, p.split_ld[1], CL == 1 ? BNT : BNT / 2);
+  constexpr size_t smem = CL == 3 ? tck::Pair::SMEM_BYTES : tck::Cfg<BNT>::SMEM_BYTES;
   auto kern = tck_trail_kernel<BNT, CL>;
   set_smem(kern, smem);
   const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, num_sms()) : num_sms();
@@ -745,19 +745,24 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   BCMG_CHECK_LAUNCH();
 }
 
-// BCMG_TCK_CLUSTER (default 1): the 256-wide trailing update runs as CTA pairs
-// sharing the B tile through TMA multicast (tck_loop CL = 2)
-static bool tck_cluster() {
-  static const bool v = [] {
+// BCMG_TCK_CLUSTER, the 256-wide trailing update: 0 one CTA per 128 x 256 tile;
+// 1 CTA pairs sharing the B tile through TMA multicast (tck_loop CL = 2);
+// 2 (default) CTA pairs on 256 x 256 tiles with the 2-SM UMMA (tck_loop_pair)
+static int tck_cluster() {
+  static const int v = [] {
     const char* e = getenv("BCMG_TCK_CLUSTER");
-    return !(e && *e && atoi(e) == 0);
+    return e && *e ? atoi(e) : 2;
   }();
   return v;
 }
 
 static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t st) {
-  if (tck_width(p.T) == 256)
-    return tck_cluster() ? launch_tck_trail_t<256, 2>(p, info, st) : launch_tck_trail_t<256, 1>(p, info, st);
+  if (tck_width(p.T) == 256) {
+    const int c = tck_cluster();
+    if (c == 2) return launch_tck_trail_t<256, 3>(p, info, st);
+    if (c == 1) return launch_tck_trail_t<256, 2>(p, info, st);
+    return launch_tck_trail_t<256, 1>(p, info, st);
+  }
   launch_tck_trail_t<128>(p, info, st);
 }
 

@@ -255,6 +255,218 @@ __device__ __forceinline__ void tck_loop(const CUtensorMap* mAh, const CUtensorM
   }
 }
 
+// ----------------------------------------------------------------- 2-SM UMMA
+// CTA pair on one 256 x 256 output tile with tcgen05.mma.cta_group::2 (M = 256,
+// N = 256): CTA r holds rows [128 r, 128 r + 128) of A and rows
+// [128 r, 128 r + 128) of B (the tile's output columns) in its own shared
+// memory, and its 128 rows of the accumulator in its own TMEM; the leader
+// (rank 0) issues the MMAs over both CTAs' operands.  Per SM the tensor core
+// reads 4 + 4 KB per k8 MMA instead of 4 + 8 KB, TMA writes 64 instead of 96
+// KB per k-tile, and a stage is 64 KB so three fit (two at N = 256 in one CTA):
+// the shared-memory bandwidth and pipeline depth that bound the one-CTA
+// 128 x 256 kernel.
+//   both CTAs  warp 0: TMA of their A / B halves, completion on the LEADER's
+//              full barrier (.cta_group::2); stage refilled after the leader's
+//              MMA commit arrives on this CTA's empty barrier (multicast)
+//   leader     warp 1: MMA issuer; commits to both CTAs' empty / tfull
+//   both CTAs  warps 4-11: epilogue of their 128 rows; "TMEM drained" arrives
+//              on the leader's tempty (count 16)
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.cta_group::2"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void mma_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar_cluster) : "memory");
+}
+
+struct Pair {
+  static constexpr int BN = 256;                      // output columns per tile (UMMA N)
+  static constexpr int PA = BM * BK * 4;              // 16 KB: 128 A rows x 32 k
+  static constexpr int PB = (BN / 2) * BK * 4;        // 16 KB: this CTA's 128 B rows
+  static constexpr int STAGE_BYTES = 2 * (PA + PB);   // A hi, A lo, B hi, B lo
+  static constexpr int STAGES = 3;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                    ((uint32_t)(256 >> 4) << 24);
+};
+
+template <class Next>
+__device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUtensorMap* mAl, const CUtensorMap* mBh,
+                                              const CUtensorMap* mBl, int K, Next&& next) {
+  using P = Pair;
+  constexpr int STAGES = P::STAGES, STAGE_BYTES = P::STAGE_BYTES, PA = P::PA, PB = P::PB, BN = P::BN;
+  extern __shared__ __align__(1024) unsigned char tck_smem_raw[];
+  unsigned char* base = tck_smem_raw + ((1024 - (smem_u32(tck_smem_raw) & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int KT = (K + BK - 1) / BK;
+  const int rank = (int)cluster_rank();
+  const bool leader = rank == 0;
+  const int64_t first = blockIdx.x / 2, stride = gridDim.x / 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);   // leader: its producer's arrive.expect_tx (both CTAs' bytes)
+      mbar_init(&empty[s], 1);  // the leader's MMA commit (multicast)
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 16);  // leader: 8 epilogue warps of each CTA
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {  // pair allocation: the same columns in both CTAs' TMEM
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(P::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc::fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- TMA producer (both CTAs)
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(mAh) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(mAl) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(mBh) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(mBl) : "memory");
+      uint32_t g = 0;
+      tc::Blk blk;
+      const int arow = rank * BM, brow = rank * (BN / 2);
+      for (int64_t item = first; next(item, blk); item += stride) {
+        for (int kt = 0; kt < KT; ++kt, ++g) {
+          const int s = g % STAGES;
+          mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+          unsigned char* st = base + (size_t)s * STAGE_BYTES;
+          const uint32_t fb = mapa_u32(smem_u32(&full[s]), 0);  // the leader's full barrier
+          if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+          tma_load_2d_pair(st, mAh, kt * BK, blk.a_row + (int)blk.m0 + arow, fb);
+          tma_load_2d_pair(st + PA, mAl, kt * BK, blk.a_row + (int)blk.m0 + arow, fb);
+          tma_load_2d_pair(st + 2 * PA, mBh, kt * BK, blk.b_row + (int)blk.n0 + brow, fb);
+          tma_load_2d_pair(st + 2 * PA + PB, mBl, kt * BK, blk.b_row + (int)blk.n0 + brow, fb);
+        }
+      }
+      // the leader's last commits arrive on our empty barriers: let them land before exit
+      for (uint32_t q = g > (uint32_t)STAGES ? g - STAGES : 0; q < g; ++q)
+        mbar_wait(&empty[q % STAGES], (q / STAGES) & 1);
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer (leader)
+    if (lane == 0 && leader) {
+      uint32_t g = 0, t = 0;
+      tc::Blk blk;
+      for (int64_t item = first; next(item, blk); item += stride, ++t) {
+        const int b = t & 1;
+        mbar_wait(&tempty[b], ((t >> 1) & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t d = tmem + b * BN;
+        for (int kt = 0; kt < KT; ++kt, ++g) {
+          const int s = g % STAGES;
+          mbar_wait(&full[s], (g / STAGES) & 1);
+          tc::fence_after();
+          const uint32_t st = smem_u32(base + (size_t)s * STAGE_BYTES);
+          const uint32_t ahi = st, alo = st + PA, bhi = st + 2 * PA, blo = bhi + PB;
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint32_t off = ks * 32;
+            mma_pair(d, tc::sdesc(alo + off), tc::sdesc(bhi + off), P::IDESC, (kt | ks) != 0);
+            mma_pair(d, tc::sdesc(ahi + off), tc::sdesc(blo + off), P::IDESC, 1);
+            mma_pair(d, tc::sdesc(ahi + off), tc::sdesc(bhi + off), P::IDESC, 1);
+          }
+          commit_pair(&empty[s]);  // both CTAs' stage s reusable once these MMAs read it
+        }
+        commit_pair(&tfull[b]);    // both CTAs' accumulator b ready
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------- epilogue (8 warps, both CTAs)
+    const int q = warp & 3;
+    const int ch = (warp - 4) >> 2;
+    const int row = 32 * q + lane;
+    const uint32_t te = mapa_u32(smem_u32(&tempty[0]), 0);  // the leader's tempty[0]; [1] is 8 bytes on
+    uint32_t t = 0;
+    tc::Blk blk;
+    for (int64_t item = first; next(item, blk); item += stride, ++t) {
+      const int b = t & 1;
+      const int64_t r = blk.m0 + rank * BM + row;
+      float* __restrict__ crow = blk.C + r;
+      auto load_chunk = [&](int c0, float* dst) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int64_t col = blk.n0 + c0 + j;
+          dst[j] = (blk.beta != 0.f && r < blk.M && col < blk.N) ? crow[col * blk.ldc] : 0.f;
+        }
+      };
+      const int cbeg = ch * (BN / 2), cend = cbeg + BN / 2;
+      if (blk.beta != 0.f) {
+        constexpr int PER = BN / 2 / 32;
+        const int64_t col = blk.n0 + cbeg + PER * lane, r0 = blk.m0 + rank * BM + 32 * q;
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+          if (col + j < blk.N && r0 < blk.M) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(blk.C + r0 + (col + j) * blk.ldc));
+      }
+      float old[32], nxt[32];
+      load_chunk(cbeg, old);
+      mbar_wait(&tfull[b], (t >> 1) & 1);
+      tc::fence_after();
+#pragma unroll 1
+      for (int c0 = cbeg; c0 < cend; c0 += 32) {
+        if (c0 + 32 < cend) load_chunk(c0 + 32, nxt);
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + b * BN + c0, v);
+        if (r < blk.M) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int64_t col = blk.n0 + c0 + j;
+            if (col < blk.N) crow[col * blk.ldc] = blk.alpha * v[j] + blk.beta * old[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) old[j] = nxt[j];
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(te + 8 * b);
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();  // both CTAs done with the pair's TMEM and with each other's barriers
+  if (warp == 1) {
+    tc::fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(P::TMEM_COLS));
+  }
+}
+
 }  // namespace tck
 
 // C := alpha * A * B^T + beta * C on pre-split K-major planes (rows x Kp).
@@ -292,7 +504,8 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
     tck_trail_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                      const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, TrailParams p,
                      const int* info) {
-  constexpr int64_t BMX = CL * tc::BM;  // rows per item (a CTA pair covers 256)
+  static_assert(CL != 3 || BNT == 256, "the 2-SM UMMA tile is 256 x 256");
+  constexpr int64_t BMX = (CL == 1 ? 1 : 2) * tc::BM;  // rows per item (a CTA pair covers 256)
   using TZ = TrapR<BMX, BNT>;
   using TZC = TrapR<BMX / 2, BNT>;
   // (a CTA pair must not split on a flag another stream may be writing: only single CTAs skip)
@@ -309,7 +522,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
   const int64_t cm0 = cm;
   auto unit_row = [&](int64_t k) { return ncb == 1 ? (cm0 + k * sc) * p.T : (p.m_first * ncb + k) * BNT; };
   int64_t ku = 0, bg = 0, ba0 = 0, btop = 0;
-  tck::tck_loop<BNT, CL>(&mAh, &mAl, &mBh, &mBl, (int)(p.cplx ? 2 * p.K : p.K), [&](int64_t item, tc::Blk& blk) -> bool {
+  auto next = [&](int64_t item, tc::Blk& blk) -> bool {
     if (p.band > 0) {
       const int64_t RB = p.cplx ? BMX / 2 : BMX;  // matrix rows per row block (complex64: embedded pairs)
       const int64_t step = (ncb == 1 ? sc * p.T : (int64_t)BNT) / RB, aend = (p.N + RB - 1) / RB;
@@ -402,7 +615,10 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
     blk.beta = 1.f;
     blk.nfan = 0;
     return true;
-  });
+  };
+  const int Kx = (int)(p.cplx ? 2 * p.K : p.K);
+  if constexpr (CL == 3) tck::tck_loop_pair(&mAh, &mAl, &mBh, &mBl, Kx, next);
+  else tck::tck_loop<BNT, CL>(&mAh, &mAl, &mBh, &mBl, Kx, next);
 }
 
 }  // namespace bcmg

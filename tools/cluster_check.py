@@ -1,6 +1,6 @@
-"""tcgen05 CTA-pair (B multicast) trailing update vs the single-CTA one: the
-factor must be bit-identical (same MMAs per element, only the CTA-to-row map and
-the B delivery differ).  Runs each variant in its own process (the switch is
+"""tcgen05 2-SM UMMA (CTA pair, BCMG_TCK_CLUSTER=2) trailing update vs the
+single-CTA one: solutions within 10 N eps of each other (bit-identical if the
+pair MMA sums each element in the same order).  Runs each variant in its own process (the switch is
 read once)."""
 import os, subprocess, sys
 import numpy as np
@@ -18,13 +18,14 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
 ok = True
 for n, t, d, dt in ((2048, 512, 1, "f32"), (4096, 1024, 2, "f32"), (3072, 512, 1, "c64"), (4096, 256, 4, "f32")):
     xs = []
-    for cl in ("0", "1"):
+    for cl in ("0", "2"):
         f = f"/tmp/x_{cl}.npy"
         r = subprocess.run([sys.executable, __file__, "child", str(n), str(t), str(d), dt, f],
                            env=dict(os.environ, BCMG_TCK_CLUSTER=cl), capture_output=True, text=True, timeout=300)
         print(n, t, d, dt, "cluster", cl, r.stdout.strip(), r.stderr[-300:])
         xs.append(np.load(f))
     same = np.array_equal(xs[0], xs[1])
-    ok &= same
-    print("bit-identical:", same)
+    rel = float(np.abs(xs[0].astype(np.complex128) - xs[1]).max() / np.abs(xs[0]).max())
+    ok &= rel <= 10 * n * 1.2e-7
+    print("bit-identical:", same, "max rel diff", rel)
 sys.exit(0 if ok else 1)
