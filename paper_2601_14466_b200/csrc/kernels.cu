@@ -745,6 +745,24 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   BCMG_CHECK_LAUNCH();
 }
 
+// clusters of two CTAs (one per SM of a TPC pair), `pairs` clusters
+static void launch_pair(const void* kern, int64_t pairs, size_t smem, cudaStream_t st, void** args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(2 * std::max<int64_t>(pairs, 1)));
+  cfg.blockDim = dim3(tck::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BCMG_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
+  BCMG_CHECK_LAUNCH();
+}
+
 // BCMG_TCK_CLUSTER, the 256-wide trailing update: 0 one CTA per 128 x 256 tile;
 // 1 CTA pairs sharing the B tile through TMA multicast (tck_loop CL = 2);
 // 2 (default) CTA pairs on 256 x 256 tiles with the 2-SM UMMA (tck_loop_pair)
@@ -767,11 +785,26 @@ static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t
 }
 
 // C = alpha*A*B^T + beta*C (float32) on pre-split planes Ah/Al (M x kp) and Bh/Bl (N x kp).
+static int tck_cluster();
+static void launch_pair(const void* kern, int64_t pairs, size_t smem, cudaStream_t st, void** args);
+
 template <int BNT>
 static void tck_gemm_t(int64_t M, int64_t N, int64_t K, const float* ah, const float* al, const float* bh,
                        const float* bl, int64_t kp, float* C, int64_t ldc, float alpha, float beta, const int* info,
                        cudaStream_t st, const FloatFan& fan) {
   const CUtensorMap mah = make_map_kmajor(ah, M, kp), mal = make_map_kmajor(al, M, kp);
+  if constexpr (BNT == 256) {
+    if (fan.n == 0 && M > tc::BM && tck_cluster() == 2) {  // CTA pairs, 2-SM UMMA on 256 x 256 tiles
+      const CUtensorMap mbh = make_map_kmajor(bh, N, kp, BNT / 2), mbl = make_map_kmajor(bl, N, kp, BNT / 2);
+      auto kern = tck_gemm_kernel<256, 3>;
+      set_smem(kern, tck::Pair::SMEM_BYTES);
+      const int64_t tiles = ((M + 2 * tc::BM - 1) / (2 * tc::BM)) * ((N + BNT - 1) / BNT);
+      void* args[] = {(void*)&mah, (void*)&mal, (void*)&mbh, (void*)&mbl, &M, &N, &K, &C, &ldc, &alpha, &beta,
+                      (void*)&info, (void*)&fan};
+      launch_pair((const void*)kern, std::min<int64_t>(tiles, num_sms() / 2), tck::Pair::SMEM_BYTES, st, args);
+      return;
+    }
+  }
   const CUtensorMap mbh = make_map_kmajor(bh, N, kp, BNT), mbl = make_map_kmajor(bl, N, kp, BNT);
   constexpr size_t smem = tck::Cfg<BNT>::SMEM_BYTES;
   set_smem(tck_gemm_kernel<BNT>, smem);

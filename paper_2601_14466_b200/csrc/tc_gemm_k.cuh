@@ -470,19 +470,22 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
 }  // namespace tck
 
 // C := alpha * A * B^T + beta * C on pre-split K-major planes (rows x Kp).
-template <int BNT>
+// CL = 3: CTA pairs on 256 x 256 tiles with the 2-SM UMMA (no fan-out)
+template <int BNT, int CL = 1>
 __global__ void __launch_bounds__(tck::THREADS, 1)
     tck_gemm_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                     const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, int64_t M,
                     int64_t N, int64_t K, float* C, int64_t ldc, float alpha, float beta, const int* info,
                     FloatFan fan) {
-  if (ld_flag(info)) return;
-  const int64_t nbm = (M + tc::BM - 1) / tc::BM, nbn = (N + BNT - 1) / BNT;
-  tck::tck_loop<BNT>(&mAh, &mAl, &mBh, &mBl, (int)K, [&](int64_t item, tc::Blk& blk) -> bool {
+  static_assert(CL == 1 || (CL == 3 && BNT == 256), "pair GEMM tiles are 256 x 256");
+  if (CL == 1 && ld_flag(info)) return;  // (a CTA pair must not split on the flag)
+  constexpr int64_t BMX = CL == 1 ? tc::BM : 2 * tc::BM;
+  const int64_t nbm = (M + BMX - 1) / BMX, nbn = (N + BNT - 1) / BNT;
+  auto next = [&](int64_t item, tc::Blk& blk) -> bool {
     if (item >= nbm * nbn) return false;
     blk.a_row = 0;
     blk.b_row = 0;
-    blk.m0 = (item % nbm) * tc::BM;
+    blk.m0 = (item % nbm) * BMX;
     blk.n0 = (item / nbm) * BNT;
     blk.M = M;
     blk.N = N;
@@ -494,7 +497,9 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
 #pragma unroll
     for (int e = 0; e < MAX_FAN; ++e) blk.fan[e] = e < fan.n ? fan.p[e] : nullptr;
     return true;
-  });
+  };
+  if constexpr (CL == 3) tck::tck_loop_pair(&mAh, &mAl, &mBh, &mBl, (int)K, next);
+  else tck::tck_loop<BNT>(&mAh, &mAl, &mBh, &mBl, (int)K, next);
 }
 
 // potrf trailing update on the pre-split panel (TrailParams::split_*): same
