@@ -430,7 +430,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                      "ms_per_launch": trail["ms"] / max(trail["launches"], 1),
                      "share_of_step": trail["ms"] / ms if ms else None,
                      "step_fraction_of_peak": value / peak.value if peak.value else None},
-        "kernels": other,
+        "kernels": {**other, "note": "CUDA-event brackets on each kind's launching stream over the timed steps; "
+                                     "the diagonal factor and panel solve run on the critical stream next to the "
+                                     "persistent bulk grid, so their times include waiting for SMs (not kernel "
+                                     "durations; tools/kernel_split.py, tools/scale_model.py with "
+                                     "CUDA_LAUNCH_BLOCKING=1 give those)"},
         "clocks": clocks.summary(),
         "nccl": _nccl_summary() if world > 1 else None,
         "gpu_launches": int(launches),
