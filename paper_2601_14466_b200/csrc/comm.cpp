@@ -62,33 +62,51 @@ IpcHandle ipc_export(const void* ptr) {
 
 // Imported allocations, one mapping per exporter allocation (opening the same
 // handle twice in a process is not allowed).
+// At most kMaxOpen mappings are kept (least recently used closed first): a
+// mapping keeps the exporter's allocation alive, and callers that pass new
+// buffers on every call would otherwise accumulate them.  Only mappings used
+// by earlier calls are evicted -- a call's own mappings are its most recent.
 class IpcCache {
  public:
-  void* import(const IpcHandle& h) {
+  static constexpr size_t kMaxOpen = 32;
+  // pin: never evicted (mappings whose addresses live for the whole transport)
+  void* import(const IpcHandle& h, bool pin = false) {
     std::lock_guard<std::mutex> lk(mu_);
     const std::string key(reinterpret_cast<const char*>(h.bytes), sizeof(h.bytes));
     auto it = map_.find(key);
     void* base = nullptr;
+    const uint64_t stamp = pin ? UINT64_MAX : ++tick_;
     if (it != map_.end()) {
-      base = it->second;
+      base = it->second.first;
+      it->second.second = std::max(it->second.second == UINT64_MAX ? UINT64_MAX : 0, stamp);
     } else {
+      if (map_.size() >= kMaxOpen) {
+        auto old = map_.end();
+        for (auto e = map_.begin(); e != map_.end(); ++e)
+          if (e->second.second != UINT64_MAX && (old == map_.end() || e->second.second < old->second.second)) old = e;
+        if (old != map_.end()) {
+          cudaIpcCloseMemHandle(old->second.first);
+          map_.erase(old);
+        }
+      }
       cudaIpcMemHandle_t mh;
       std::memcpy(&mh, h.bytes, sizeof(mh));
       BCMG_CUDA(cudaIpcOpenMemHandle(&base, mh, cudaIpcMemLazyEnablePeerAccess));
-      map_[key] = base;
+      map_[key] = {base, stamp};
     }
     return static_cast<char*>(base) + h.offset;
   }
   void close_all() {
     std::lock_guard<std::mutex> lk(mu_);
-    for (auto& e : map_) cudaIpcCloseMemHandle(e.second);
+    for (auto& e : map_) cudaIpcCloseMemHandle(e.second.first);
     map_.clear();
   }
   ~IpcCache() { close_all(); }
 
  private:
   std::mutex mu_;
-  std::map<std::string, void*> map_;
+  uint64_t tick_ = 0;
+  std::map<std::string, std::pair<void*, uint64_t>> map_;
 };
 
 namespace {
@@ -122,13 +140,17 @@ class NcclComm final : public Comm {
     BCMG_NCCL_CALL(ncclCommInitRankConfig(&c_, world, u, rank, &cfg));
     world_ = world;
     me_ = rank;
-    BCMG_CUDA(cudaMalloc(&scratch_, 256));
-    BCMG_CUDA(cudaMemset(scratch_, 0, 256));
+    // scratch: the barrier word and the all-gather of exchange_pointers (no
+    // allocation -- cudaFree synchronises the device -- on the hot path)
+    scratch_bytes_ = 4096 + 128 * (size_t)(world + 1);
+    BCMG_CUDA(cudaMalloc(&scratch_, scratch_bytes_));
+    BCMG_CUDA(cudaMemset(scratch_, 0, scratch_bytes_));
+    BCMG_CUDA(cudaStreamCreateWithFlags(&xstream_, cudaStreamNonBlocking));
     // flag words of this rank, mapped into every peer (collective, like the init)
     BCMG_CUDA(cudaMalloc(&flags_, kFlagSlots * sizeof(uint32_t)));
     BCMG_CUDA(cudaMemset(flags_, 0, kFlagSlots * sizeof(uint32_t)));
     BCMG_CUDA(cudaDeviceSynchronize());
-    if (stream_wait_supported()) peer_flags_ = exchange_pointers(flags_);
+    if (stream_wait_supported()) peer_flags_ = exchange(flags_, true);  // pinned: used for the comm's lifetime
   }
   bool flags_supported() const override { return (int)peer_flags_.size() == world_; }
   void post_flag(int peer, int slot, uint32_t v, cudaStream_t st) override {
@@ -143,6 +165,7 @@ class NcclComm final : public Comm {
     if (c_) ncclCommDestroy(c_);
     if (scratch_) cudaFree(scratch_);
     if (flags_) cudaFree(flags_);
+    if (xstream_) cudaStreamDestroy(xstream_);
   }
   void barrier(cudaStream_t st) override {
     BCMG_NCCL_CALL(ncclAllReduce(scratch_, scratch_, 1, ncclInt32, ncclSum, c_, st));
@@ -158,8 +181,9 @@ class NcclComm final : public Comm {
     BCMG_NCCL_CALL(ncclRecv(buf, bytes, ncclUint8, peer, c_, st));
   }
   void group_end() override { BCMG_NCCL_CALL(ncclGroupEnd()); }
-  std::vector<void*> exchange_pointers(void* local) override {
-    // every rank's (IPC handle, offset, ok) all-gathered over NCCL, then opened
+  std::vector<void*> exchange_pointers(void* local) override { return exchange(local, false); }
+  // every rank's (IPC handle, offset, ok) all-gathered over NCCL, then opened
+  std::vector<void*> exchange(void* local, bool pin) {
     struct Rec {
       IpcHandle h;
       int32_t ok, pad;
@@ -172,12 +196,10 @@ class NcclComm final : public Comm {
       cudaGetLastError();
       mine.ok = 0;
     }
-    void* dev = nullptr;
-    BCMG_CUDA(cudaMalloc(&dev, sizeof(Rec) * (size_t)(world_ + 1)));
+    static_assert(sizeof(Rec) <= 128, "exchange record fits its scratch slot");
     std::vector<Rec> all(world_);
-    cudaStream_t st;
-    BCMG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    char* d = static_cast<char*>(dev);
+    cudaStream_t st = xstream_;
+    char* d = static_cast<char*>(scratch_) + 4096;
     BCMG_CUDA(cudaMemcpyAsync(d + sizeof(Rec) * world_, &mine, sizeof(Rec), cudaMemcpyHostToDevice, st));
     BCMG_NCCL_CALL(ncclAllGather(d + sizeof(Rec) * world_, d, sizeof(Rec), ncclUint8, c_, st));
     BCMG_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(Rec) * world_, cudaMemcpyDeviceToHost, st));
@@ -192,7 +214,7 @@ class NcclComm final : public Comm {
           continue;
         }
         try {
-          out[r] = ipc_.import(all[r].h);
+          out[r] = ipc_.import(all[r].h, pin);
         } catch (const Error&) {
           cudaGetLastError();
           ok = 0;
@@ -205,8 +227,6 @@ class NcclComm final : public Comm {
     BCMG_NCCL_CALL(ncclAllReduce(flag, flag, 1, ncclInt32, ncclMin, c_, st));
     BCMG_CUDA(cudaMemcpyAsync(&ok, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     BCMG_CUDA(cudaStreamSynchronize(st));
-    cudaStreamDestroy(st);
-    cudaFree(dev);
     if (!ok) return {};
     return out;
   }
@@ -227,6 +247,8 @@ class NcclComm final : public Comm {
   ncclComm_t c_ = nullptr;
   int me_ = 0, world_ = 1;
   void* scratch_ = nullptr;
+  size_t scratch_bytes_ = 0;
+  cudaStream_t xstream_ = nullptr;
   void* flags_ = nullptr;
   std::vector<void*> peer_flags_;
   IpcCache ipc_;
