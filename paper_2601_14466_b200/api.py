@@ -185,8 +185,9 @@ def syevd(A, T_A: int, mesh: DeviceMesh | None = None, in_specs=None, *, return_
 
     mesh = mesh or make_mesh()
     _check_specs(in_specs, mesh, 1)
-    if mesh.world != 1:
-        raise DescriptorError("dimension-mismatch", "syevd runs single-process (DESIGN.md §3b)")
+    if mesh.world != 1:  # (solvers.eigh_hermitian / bcmg_syevd run across processes: DESIGN.md §3b)
+        raise DescriptorError("dimension-mismatch", "the drop-in syevd returns row-major V from one process; "
+                                                    "use eigh_hermitian(mesh, a, tile) across processes")
     A, et, n = _prepare_a(A, mesh, overwrite_a)
     validate_tile(TileSpec(int(T_A)), n)
     real = torch.float32 if et in (ElementType.real32, ElementType.complex64) else torch.float64

@@ -861,10 +861,75 @@ void syevd_t(Session& ss, int64_t n, int64_t T, int ndev, void* const* shards, b
 
 }  // namespace
 
+// world > 1: the eigensolver's chain is serial (a reflector per column, the
+// host QL loop), so the shards are gathered on rank 0 (one point-to-point
+// transfer per logical device, device after device -- the all-shards layout of
+// a single-process session), solved there by the single-process path, and the
+// eigenvector shards / eigenvalues sent back.  The outcome (NO_CONVERGENCE,
+// OUT_OF_MEMORY, ...) is agreed on by every rank before any data returns.
 void Session::syevd(int dt, int64_t n, int64_t T, int ndev, void* const* shards, bool cyclic, void* w) {
-  if (world != 1) throw Error(CONFIG, "syevd runs single-process (all logical devices on the session's GPU)");
   if (ndev > 16) throw Error(CONFIG, "syevd supports at most 16 logical devices");
-  dispatch_dtype(dt, [&](auto s) { syevd_t<decltype(s)>(*this, n, T, ndev, shards, cyclic, w); });
+  if (world == 1) {
+    dispatch_dtype(dt, [&](auto s) { syevd_t<decltype(s)>(*this, n, T, ndev, shards, cyclic, w); });
+    return;
+  }
+  if (ndev % world) throw Error(CONFIG, "logical device count must be a multiple of the process count");
+  const size_t esz = dtype_size(dt), wsz = (dt == R32 || dt == C64) ? 4 : 8;
+  const int nloc = ndev / world, dev0 = rank * nloc;
+  const auto counts = column_counts(n, T, ndev);
+  std::vector<int64_t> off(ndev + 1, 0);
+  for (int d = 0; d < ndev; ++d) off[d + 1] = off[d] + counts[d];
+  cudaStream_t st = user;
+  int status = 0;  // 0 ok, else the error code of the root's solve
+  std::string msg;
+  if (rank == 0) {
+    try {
+      eig[1].ensure((size_t)n * n * esz);  // the gathered matrix, device after device (eig[1] is free)
+    } catch (const Error& e) {
+      status = e.code;
+      msg = e.what();
+    }
+  }
+  tmp.ensure(4096);
+  status = -net->allreduce_min(-status, tmp.p, comm);  // max over ranks
+  if (status) throw Error(status, rank == 0 ? msg : "syevd: the gathering rank failed");
+  char* g = static_cast<char*>(eig[1].p);
+  auto seg = [&](int d) { return (size_t)counts[d] * n * esz; };
+  net->group_start();
+  if (rank == 0) {
+    for (int d = 0; d < nloc; ++d)
+      if (seg(d)) BCMG_CUDA(cudaMemcpyAsync(g + off[d] * n * esz, shards[d], seg(d), cudaMemcpyDeviceToDevice, st));
+    for (int d = nloc; d < ndev; ++d)
+      if (seg(d)) net->recv(g + off[d] * n * esz, seg(d), d / nloc, st);
+  } else {
+    for (int i = 0; i < nloc; ++i)
+      if (seg(dev0 + i)) net->send(shards[i], seg(dev0 + i), 0, st);
+  }
+  net->group_end();
+  if (rank == 0) {
+    std::vector<void*> all(ndev);
+    for (int d = 0; d < ndev; ++d) all[d] = g + off[d] * n * esz;
+    try {
+      dispatch_dtype(dt, [&](auto s) { syevd_t<decltype(s)>(*this, n, T, ndev, all.data(), cyclic, w); });
+    } catch (const Error& e) {
+      status = e.code;
+      msg = e.what();
+    }
+  }
+  status = -net->allreduce_min(-status, tmp.p, comm);
+  if (status) throw Error(status, rank == 0 ? msg : "syevd failed on the solving rank");
+  net->group_start();
+  if (rank == 0) {
+    for (int d = 0; d < nloc; ++d)
+      if (seg(d)) BCMG_CUDA(cudaMemcpyAsync(shards[d], g + off[d] * n * esz, seg(d), cudaMemcpyDeviceToDevice, st));
+    for (int d = nloc; d < ndev; ++d)
+      if (seg(d)) net->send(g + off[d] * n * esz, seg(d), d / nloc, st);
+  } else {
+    for (int i = 0; i < nloc; ++i)
+      if (seg(dev0 + i)) net->recv(shards[i], seg(dev0 + i), 0, st);
+  }
+  net->group_end();
+  net->bcast(w, (size_t)n * wsz, 0, st);
 }
 
 }  // namespace bcmg

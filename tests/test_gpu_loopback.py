@@ -235,3 +235,38 @@ def test_loopback_redistribution_bit_exact(dtype, n_rows, n, t, ndev, world, red
     _run_ranks(world, body)
     for blk, c0, c1 in blocks:
         assert np.array_equal(blk.cpu().numpy().T, a[:, c0:c1]), "round trip differs"
+
+
+@pytest.mark.parametrize("dtype,n,t,ndev,world", [
+    (np.float64, 96, 8, 2, 2), (np.complex128, 80, 8, 4, 2), (np.float32, 64, 16, 4, 4), (np.complex64, 72, 12, 2, 2),
+])
+def test_loopback_syevd_matches_single_process(dtype, n, t, ndev, world):
+    """syevd across processes (the matrix gathered on rank 0, solved there,
+    eigenvector shards and eigenvalues sent back): the single-process bits on
+    every rank (reference eigh_hermitian, solvers.py:1019-1043)."""
+    import torch
+
+    lib = _lib.load()
+    a = O.make_matrix("random_spd", n, dtype, 5)
+    w0, v0, _ = bc.eigh_hermitian(bc.make_mesh(ndev), a, bc.TileSpec(t))
+    real = torch.float32 if dtype in (np.float32, np.complex64) else torch.float64
+    inputs = []
+    for r in range(world):
+        block, ptrs, cols = _local_shards(a, n, t, ndev, world, r, "cuda")
+        inputs.append((block, ptrs, cols, torch.empty(n, dtype=real, device="cuda")))
+    torch.cuda.synchronize()
+
+    def body(r, sess, st):
+        _, ptrs, _, w = inputs[r]
+        info = C.c_int(0)
+        _lib.check(lib.bcmg_syevd(sess, C.c_void_p(st.cuda_stream), CODES[dtype], n, t, ndev, ptrs,
+                                  C.c_void_p(w.data_ptr()), 0, C.byref(info)))
+        assert info.value == 0
+        return r
+
+    _run_ranks(world, body)
+    v = np.zeros((n, n), dtype=dtype, order="F")
+    for block, _, (c0, c1), w in inputs:
+        assert np.array_equal(w.cpu().numpy(), w0), "eigenvalues differ from the single-process bits"
+        v[:, c0:c1] = block.cpu().numpy().T
+    assert np.array_equal(v, v0), "eigenvectors differ from the single-process bits"
