@@ -154,7 +154,8 @@ int bcmg_potri(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile
    elements of the real type: float for dtype 0/2, double for 1/3); A's shards
    (contiguous layout) are overwritten by the eigenvectors, column j belonging
    to w[j], each scaled so that its first largest-magnitude component is real
-   and positive (solvers.py:898-909).  Single-process sessions only.  *info =
+   and positive (solvers.py:898-909).  Across processes the matrix is gathered and
+   solved on rank 0 (same bits on every rank).  *info =
    BCMG_ERR_NO_CONVERGENCE (and the same return code) when the tridiagonal QL
    exceeds 30 iterations for one eigenvalue (solvers.py:806-811). */
 int bcmg_syevd(bcmg_session* s, void* stream, int dtype, int64_t n, int64_t tile, int ndev, void* const* shards,

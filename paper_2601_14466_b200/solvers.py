@@ -422,7 +422,8 @@ def syevd(mesh: DeviceMesh, dmat: DistributedMatrix, ws: Sequence = ()) -> tuple
     a Hermitian matrix on the block-cyclic layout; the eigenvectors overwrite
     the shards, column j of the cyclic layout belonging to w[j], each scaled so
     its first largest-magnitude component is real and positive
-    (solvers.py:862-910).  Single-process meshes (csrc/eigen.cu)."""
+    (solvers.py:862-910).  Across processes the matrix is gathered and solved
+    on rank 0 (csrc/eigen.cu)."""
     _require_layout(dmat, "block_cyclic")
     desc = dmat.descriptor
     _require_hermitian(desc)
