@@ -6,6 +6,7 @@
 //   * small copy / conjugate / mirror helpers.
 #include <algorithm>
 #include <atomic>
+#include <cstring>
 #include <mutex>
 #include <type_traits>
 
@@ -692,7 +693,7 @@ static int tck_width(int64_t n) {
 
 template <int BNT, int CL = 1>
 static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream_t st) {
-  constexpr int64_t BMX = (CL == 1 ? 1 : 2) * tc::BM;
+  constexpr int64_t BMX = (CL == 1 || CL == 4 ? 1 : 2) * tc::BM;
   using TZ = TrapR<BMX, BNT>;
   using TZC = TrapR<BMX / 2, BNT>;
   int64_t total = 0;
@@ -719,13 +720,29 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   const CUtensorMap al = make_map_kmajor(p.split[1], arows, p.split_ld[0]);
   const CUtensorMap bh = make_map_kmajor(p.split[2], prow, p.split_ld[1], CL == 1 ? BNT : BNT / 2);  // pairs: halves
   const CUtensorMap bl = make_map_kmajor(p.split[3], prow, p.split_ld[1], CL == 1 ? BNT : BNT / 2);
-  constexpr size_t smem = CL == 3 ? tck::Pair::SMEM_BYTES : tck::Cfg<BNT>::SMEM_BYTES;
+  constexpr size_t smem = CL == 3 ? tck::Pair::SMEM_BYTES : CL == 4 ? tck::Epi::SMEM_BYTES : tck::Cfg<BNT>::SMEM_BYTES;
   auto kern = tck_trail_kernel<BNT, CL>;
   set_smem(kern, smem);
   const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, num_sms()) : num_sms();
-  if constexpr (CL == 1) {
+  tck::CMaps cmaps;
+  std::memset(&cmaps, 0, sizeof(cmaps));
+  if constexpr (CL == 4) {  // the TMA epilogue's C maps: each local shard as (rows, its columns)
+    const auto counts = column_counts(p.N, p.T, p.D);
+    const int64_t cx = p.cplx ? 2 : 1;
+    for (int i = 0; i < p.nloc; ++i) {
+      cuuint64_t dims[2] = {(cuuint64_t)(cx * p.N), (cuuint64_t)counts[p.dev0 + i]};
+      cuuint64_t strides[1] = {(cuuint64_t)(cx * p.N) * 4};
+      cuuint32_t box[2] = {(cuuint32_t)tc::BM, 128};
+      cuuint32_t es[2] = {1, 1};
+      CUresult r = encode_fn()(&cmaps.m[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, p.shards[i], dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw Error(CUDA, "cuTensorMapEncodeTiled (C tile) failed (" + std::to_string((int)r) + ")");
+    }
+  }
+  if constexpr (CL == 1 || CL == 4) {
     const int64_t grid = std::min<int64_t>(total, sms);
-    kern<<<(unsigned)grid, tck::THREADS, smem, st>>>(ah, al, bh, bl, q, info);
+    kern<<<(unsigned)grid, tck::THREADS, smem, st>>>(ah, al, bh, bl, q, info, cmaps);
   } else {  // clusters of two CTAs (one per SM of a TPC pair)
     const int64_t pairs = std::min<int64_t>(total, sms / 2);
     cudaLaunchConfig_t cfg{};
@@ -740,7 +757,7 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    BCMG_CUDA(cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, q, info));
+    BCMG_CUDA(cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, q, info, cmaps));
   }
   BCMG_CHECK_LAUNCH();
 }
@@ -774,7 +791,19 @@ static int tck_cluster() {
   return v;
 }
 
+// BCMG_TCK_EPI (default 1): T_A = 128 trailing updates on whole 128 x 128
+// tiles use the TMA read-modify-write epilogue (tck_loop_epi)
+static bool tck_epi() {
+  static const bool v = [] {
+    const char* e = getenv("BCMG_TCK_EPI");
+    return !(e && *e && atoi(e) == 0);
+  }();
+  return v;
+}
+
 static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t st) {
+  if (tck_width(p.T) == 128 && p.T == 128 && p.N % p.T == 0 && tck_epi() && p.nloc <= MAX_LOCAL_DEV)
+    return launch_tck_trail_t<128, 4>(p, info, st);
   if (tck_width(p.T) == 256) {
     const int c = tck_cluster();
     if (c == 2) return launch_tck_trail_t<256, 3>(p, info, st);

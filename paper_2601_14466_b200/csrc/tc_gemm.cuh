@@ -99,6 +99,10 @@ struct Blk {
   float alpha, beta;
   float* fan[MAX_FAN];  // peer copies of C (Epilogue::fan)
   int nfan;
+  // TMA epilogue (tck_loop_epi): C's tensor map (local device) and the map
+  // coordinates of the item's row / column 0 (the block adds m0 / n0)
+  int cdev;
+  int64_t crow0, ccol0;
 };
 
 template <class Next>

@@ -467,6 +467,176 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
   }
 }
 
+// ----------------------------------------------------------------- TMA epilogue
+// One CTA per 128 x 128 tile (the narrow-tile trailing update, T_A = 128) with
+// the read-modify-write of C done by TMA instead of per-thread loads: the
+// epilogue leader TMA-loads the next item's C tile (64 KB, column-major, no
+// swizzle) into shared memory as soon as the previous tile's TMA store has
+// read it, i.e. while the MMAs run; the eight epilogue warps combine it with
+// the accumulator in shared memory (row r, 32 consecutive columns per thread:
+// conflict-free), and the leader TMA-stores the tile back.  The per-thread
+// scalar loads of the default epilogue keep only ~32 KB in flight per SM and
+// leave HBM ~35 % busy at T_A = 128; the bulk copies keep a whole tile in
+// flight.  Two 64 KB operand stages + the C tile fill 192 KB.
+struct CMaps {
+  CUtensorMap m[MAX_LOCAL_DEV];  // per local device: its shard as (rows, columns), box {128, 128}
+};
+struct Epi {
+  static constexpr int BN = 128;
+  static constexpr int PA = BM * BK * 4, PB = BN * BK * 4;  // 16 KB each
+  static constexpr int STAGE_BYTES = 2 * (PA + PB);         // 64 KB
+  static constexpr int STAGES = 2;
+  static constexpr int CBUF = BM * BN * 4;                  // 64 KB
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + CBUF + 256;
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                    ((uint32_t)(BM >> 4) << 24);
+};
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+
+template <class Next>
+__device__ __forceinline__ void tck_loop_epi(const CUtensorMap* mAh, const CUtensorMap* mAl, const CUtensorMap* mBh,
+                                             const CUtensorMap* mBl, const CMaps* cmaps, int K, Next&& next) {
+  using E = Epi;
+  constexpr int STAGES = E::STAGES, STAGE_BYTES = E::STAGE_BYTES, PA = E::PA, PB = E::PB, BN = E::BN;
+  extern __shared__ __align__(1024) unsigned char tck_smem_raw[];
+  unsigned char* base = tck_smem_raw + ((1024 - (smem_u32(tck_smem_raw) & 1023)) & 1023);
+  float* cbuf = reinterpret_cast<float*>(base + (size_t)STAGES * STAGE_BYTES);  // C tile, column-major 128 x 128
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)STAGES * STAGE_BYTES + E::CBUF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* cfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int KT = (K + BK - 1) / BK;
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);
+    }
+    mbar_init(cfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(E::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(mAh) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(mAl) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(mBh) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(mBl) : "memory");
+      uint32_t g = 0;
+      tc::Blk blk;
+      for (int64_t item = first; next(item, blk); item += stride) {
+        for (int kt = 0; kt < KT; ++kt, ++g) {
+          const int s = g % STAGES;
+          mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+          unsigned char* st = base + (size_t)s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          tma_load_2d(st, mAh, kt * BK, blk.a_row + (int)blk.m0, &full[s]);
+          tma_load_2d(st + PA, mAl, kt * BK, blk.a_row + (int)blk.m0, &full[s]);
+          tma_load_2d(st + 2 * PA, mBh, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
+          tma_load_2d(st + 2 * PA + PB, mBl, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      uint32_t g = 0, t = 0;
+      tc::Blk blk;
+      for (int64_t item = first; next(item, blk); item += stride, ++t) {
+        const int b = t & 1;
+        mbar_wait(&tempty[b], ((t >> 1) & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t d = tmem + b * BN;
+        for (int kt = 0; kt < KT; ++kt, ++g) {
+          const int s = g % STAGES;
+          mbar_wait(&full[s], (g / STAGES) & 1);
+          tc::fence_after();
+          const uint32_t st = smem_u32(base + (size_t)s * STAGE_BYTES);
+          const uint32_t ahi = st, alo = st + PA, bhi = st + 2 * PA, blo = bhi + PB;
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint32_t off = ks * 32;
+            mma(d, tc::sdesc(alo + off), tc::sdesc(bhi + off), E::IDESC, (kt | ks) != 0);
+            mma(d, tc::sdesc(ahi + off), tc::sdesc(blo + off), E::IDESC, 1);
+            mma(d, tc::sdesc(ahi + off), tc::sdesc(bhi + off), E::IDESC, 1);
+          }
+          tc::commit(&empty[s]);
+        }
+        tc::commit(&tfull[b]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------- epilogue (8 warps)
+    const int q = warp & 3, ch = (warp - 4) >> 2, row = 32 * q + lane;
+    const bool leader = warp == 4 && lane == 0;
+    auto load_c = [&](const tc::Blk& bk) {  // leader: C tile of an item into cbuf
+      mbar_expect_tx(cfull, E::CBUF);
+      tma_load_2d(cbuf, &cmaps->m[bk.cdev], (int)(bk.crow0 + bk.m0), (int)(bk.ccol0 + bk.n0), cfull);
+    };
+    uint32_t t = 0;
+    tc::Blk blk, nblk;
+    bool have = next(first, blk);
+    if (leader && have) load_c(blk);
+    for (int64_t item = first; have; item += stride, ++t) {
+      const int b = t & 1;
+      mbar_wait(&tfull[b], (t >> 1) & 1);
+      tc::fence_after();
+      mbar_wait(cfull, t & 1);  // C of this item in cbuf
+      const int cbeg = ch * (BN / 2), cend = cbeg + BN / 2;
+#pragma unroll 1
+      for (int c0 = cbeg; c0 < cend; c0 += 32) {
+        float v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + b * BN + c0, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float* cp = cbuf + row + (c0 + j) * BM;
+          *cp = blk.alpha * v[j] + blk.beta * *cp;
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);  // TMEM accumulator b drained
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // cbuf writes -> the TMA store
+      asm volatile("bar.sync 1, 256;\n" ::: "memory");                 // all eight warps wrote cbuf
+      have = next(item + stride, nblk);
+      if (leader) {
+        tma_store_2d(&cmaps->m[blk.cdev], (int)(blk.crow0 + blk.m0), (int)(blk.ccol0 + blk.n0), cbuf);
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // cbuf read by the store
+        if (have) load_c(nblk);
+      }
+      blk = nblk;
+    }
+    if (leader) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // stores complete before exit
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(E::TMEM_COLS));
+  }
+}
+
 }  // namespace tck
 
 // C := alpha * A * B^T + beta * C on pre-split K-major planes (rows x Kp).
@@ -478,7 +648,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
                     int64_t N, int64_t K, float* C, int64_t ldc, float alpha, float beta, const int* info,
                     FloatFan fan) {
   static_assert(CL == 1 || (CL == 3 && BNT == 256), "pair GEMM tiles are 256 x 256");
-  if (CL == 1 && ld_flag(info)) return;  // (a CTA pair must not split on the flag)
+  if ((CL == 1 || CL == 4) && ld_flag(info)) return;  // (a CTA pair must not split on the flag)
   constexpr int64_t BMX = CL == 1 ? tc::BM : 2 * tc::BM;
   const int64_t nbm = (M + BMX - 1) / BMX, nbn = (N + BNT - 1) / BNT;
   auto next = [&](int64_t item, tc::Blk& blk) -> bool {
@@ -508,13 +678,14 @@ template <int BNT, int CL = 1>
 __global__ void __launch_bounds__(tck::THREADS, 1)
     tck_trail_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                      const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, TrailParams p,
-                     const int* info) {
+                     const int* info, const __grid_constant__ tck::CMaps cmaps) {
+  static_assert(CL != 4 || BNT == 128, "the TMA-epilogue tile is 128 x 128");
   static_assert(CL != 3 || BNT == 256, "the 2-SM UMMA tile is 256 x 256");
-  constexpr int64_t BMX = (CL == 1 ? 1 : 2) * tc::BM;  // rows per item (a CTA pair covers 256)
+  constexpr int64_t BMX = (CL == 1 || CL == 4 ? 1 : 2) * tc::BM;  // rows per item (a CTA pair covers 256)
   using TZ = TrapR<BMX, BNT>;
   using TZC = TrapR<BMX / 2, BNT>;
   // (a CTA pair must not split on a flag another stream may be writing: only single CTAs skip)
-  if (CL == 1 && ld_flag(info)) return;
+  if ((CL == 1 || CL == 4) && ld_flag(info)) return;
   int64_t cm = p.m_first, cbase = 0, ccnt = -1;
   // band mode (see TrailParams::band).  The band interleaves "units" that all
   // end at row N: owned tile columns (T <= BNT, spaced sc tiles), or, with one
@@ -571,6 +742,9 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
       blk.N = p.T < rows ? p.T : rows;
       blk.C = shard + cx * (ms + (c / p.D) * p.T * p.N);
       blk.ldc = cx * p.N;
+      blk.cdev = dev - p.dev0;
+      blk.crow0 = cx * ms;
+      blk.ccol0 = (c / p.D) * p.T;
       blk.alpha = -1.f;
       blk.beta = 1.f;
       blk.nfan = 0;
@@ -605,6 +779,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
       blk.N = tcw;
       blk.C = shard + 2 * (ms + loc * p.N);
       blk.ldc = 2 * p.N;
+      blk.crow0 = 2 * ms;
     } else {
       TZ::decode(item - cbase, tcw, rb, cb);
       blk.a_row = (int)(ms - p.prow0);
@@ -615,7 +790,10 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
       blk.N = tcw;
       blk.C = shard + ms + loc * p.N;
       blk.ldc = p.N;
+      blk.crow0 = ms;
     }
+    blk.cdev = dev - p.dev0;
+    blk.ccol0 = loc;
     blk.alpha = -1.f;
     blk.beta = 1.f;
     blk.nfan = 0;
@@ -623,6 +801,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
   };
   const int Kx = (int)(p.cplx ? 2 * p.K : p.K);
   if constexpr (CL == 3) tck::tck_loop_pair(&mAh, &mAl, &mBh, &mBl, Kx, next);
+  else if constexpr (CL == 4) tck::tck_loop_epi(&mAh, &mAl, &mBh, &mBl, &cmaps, Kx, next);
   else tck::tck_loop<BNT, CL>(&mAh, &mAl, &mBh, &mBl, Kx, next);
 }
 
