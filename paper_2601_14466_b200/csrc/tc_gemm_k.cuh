@@ -626,6 +626,7 @@ __device__ __forceinline__ void tck_loop_epi(const CUtensorMap* mAh, const CUten
         asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // cbuf read by the store
         if (have) load_c(nblk);
       }
+      __syncwarp();  // warp 4 reconverges before the next warp-collective tcgen05.ld
       blk = nblk;
     }
     if (leader) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // stores complete before exit
