@@ -718,8 +718,9 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   const int64_t prow = p.N - p.prow0, arows = p.cplx ? 2 * prow : prow;
   const CUtensorMap ah = make_map_kmajor(p.split[0], arows, p.split_ld[0]);
   const CUtensorMap al = make_map_kmajor(p.split[1], arows, p.split_ld[0]);
-  const CUtensorMap bh = make_map_kmajor(p.split[2], prow, p.split_ld[1], CL == 1 ? BNT : BNT / 2);  // pairs: halves
-  const CUtensorMap bl = make_map_kmajor(p.split[3], prow, p.split_ld[1], CL == 1 ? BNT : BNT / 2);
+  constexpr int BROWS = (CL == 2 || CL == 3) ? BNT / 2 : BNT;  // CTA pairs load half the B tile each
+  const CUtensorMap bh = make_map_kmajor(p.split[2], prow, p.split_ld[1], BROWS);
+  const CUtensorMap bl = make_map_kmajor(p.split[3], prow, p.split_ld[1], BROWS);
   constexpr size_t smem = CL == 3 ? tck::Pair::SMEM_BYTES : CL == 4 ? tck::Epi::SMEM_BYTES : tck::Cfg<BNT>::SMEM_BYTES;
   auto kern = tck_trail_kernel<BNT, CL>;
   set_smem(kern, smem);
@@ -739,6 +740,22 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) throw Error(CUDA, "cuTensorMapEncodeTiled (C tile) failed (" + std::to_string((int)r) + ")");
     }
+  }
+  if constexpr (CL == 4) {
+    static unsigned* dbg = [] {
+      unsigned* h = nullptr;
+      if (getenv("BCMG_EPI_DEBUG")) {
+        cudaHostAlloc(&h, 148 * 8 * 4 * 4, cudaHostAllocMapped);
+        std::memset(h, 0, 148 * 8 * 4 * 4);
+        unsigned* d = nullptr;
+        cudaHostGetDevicePointer(&d, h, 0);
+        cudaMemcpyToSymbol(tck::g_epi_dbg, &d, sizeof(d));
+        fprintf(stderr, "EPI_DEBUG host buffer %p\n", (void*)h);
+        setenv("BCMG_EPI_DEBUG_PTR", std::to_string((uintptr_t)h).c_str(), 1);
+      }
+      return h;
+    }();
+    (void)dbg;
   }
   if constexpr (CL == 1 || CL == 4) {
     const int64_t grid = std::min<int64_t>(total, sms);

@@ -25,7 +25,7 @@ for n, t, d, dt in CASES:
     for v in (v0, v1):
         f = f"/tmp/x_{v}.npy"
         r = subprocess.run([sys.executable, __file__, "child", str(n), str(t), str(d), dt, f],
-                           env=dict(os.environ, **{var: v}), capture_output=True, text=True, timeout=120)
+                           env=dict(os.environ, **{var: v}), capture_output=True, text=True, timeout=300)
         print(n, t, d, dt, var, v, r.stdout.strip(), r.stderr[-300:])
         xs.append(np.load(f))
     rel = float(np.abs(xs[0].astype(np.complex128) - xs[1]).max() / np.abs(xs[0]).max())
