@@ -741,22 +741,6 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
       if (r != CUDA_SUCCESS) throw Error(CUDA, "cuTensorMapEncodeTiled (C tile) failed (" + std::to_string((int)r) + ")");
     }
   }
-  if constexpr (CL == 4) {
-    static unsigned* dbg = [] {
-      unsigned* h = nullptr;
-      if (getenv("BCMG_EPI_DEBUG")) {
-        cudaHostAlloc(&h, 148 * 8 * 4 * 4, cudaHostAllocMapped);
-        std::memset(h, 0, 148 * 8 * 4 * 4);
-        unsigned* d = nullptr;
-        cudaHostGetDevicePointer(&d, h, 0);
-        cudaMemcpyToSymbol(tck::g_epi_dbg, &d, sizeof(d));
-        fprintf(stderr, "EPI_DEBUG host buffer %p\n", (void*)h);
-        setenv("BCMG_EPI_DEBUG_PTR", std::to_string((uintptr_t)h).c_str(), 1);
-      }
-      return h;
-    }();
-    (void)dbg;
-  }
   if constexpr (CL == 1 || CL == 4) {
     const int64_t grid = std::min<int64_t>(total, sms);
     kern<<<(unsigned)grid, tck::THREADS, smem, st>>>(ah, al, bh, bl, q, info, cmaps);
@@ -808,18 +792,20 @@ static int tck_cluster() {
   return v;
 }
 
-// BCMG_TCK_EPI (default 1): T_A = 128 trailing updates on whole 128 x 128
-// tiles use the TMA read-modify-write epilogue (tck_loop_epi)
-static bool tck_epi() {
-  static const bool v = [] {
+// BCMG_TCK_EPI: T_A = 128 trailing updates on whole 128 x 128 tiles use the
+// TMA read-modify-write epilogue (tck_loop_epi). Unset: real dtypes only
+// (float32 N = 65536: 101 -> 114 TFLOP/s; complex64 150 -> 147, so off);
+// 0 never; 1 real and complex. Same bits either way.
+static bool tck_epi(bool cplx) {
+  static const int v = [] {
     const char* e = getenv("BCMG_TCK_EPI");
-    return !(e && *e && atoi(e) == 0);
+    return e && *e ? atoi(e) : -1;
   }();
-  return v;
+  return v > 0 || (v < 0 && !cplx);
 }
 
 static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t st) {
-  if (tck_width(p.T) == 128 && p.T == 128 && p.N % p.T == 0 && tck_epi() && p.nloc <= MAX_LOCAL_DEV)
+  if (tck_width(p.T) == 128 && p.T == 128 && p.N % p.T == 0 && tck_epi(p.cplx) && p.nloc <= MAX_LOCAL_DEV)
     return launch_tck_trail_t<128, 4>(p, info, st);
   if (tck_width(p.T) == 256) {
     const int c = tck_cluster();

@@ -498,13 +498,6 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int
                : "memory");
 }
 
-__device__ unsigned* g_epi_dbg = nullptr;  // BCMG_EPI_DEBUG: per-CTA progress words (host-mapped)
-__device__ __forceinline__ void epi_dbg(int slot, unsigned v) {
-  if (g_epi_dbg) {
-    reinterpret_cast<volatile unsigned*>(g_epi_dbg)[blockIdx.x * 8 + slot] = v;
-    __threadfence_system();
-  }
-}
 template <class Next>
 __device__ __forceinline__ void tck_loop_epi(const CUtensorMap* mAh, const CUtensorMap* mAl, const CUtensorMap* mBh,
                                              const CUtensorMap* mBl, const CMaps* cmaps, int K, Next&& next) {
@@ -563,10 +556,8 @@ __device__ __forceinline__ void tck_loop_epi(const CUtensorMap* mAh, const CUten
           tma_load_2d(st + PA, mAl, kt * BK, blk.a_row + (int)blk.m0, &full[s]);
           tma_load_2d(st + 2 * PA, mBh, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
           tma_load_2d(st + 2 * PA + PB, mBl, kt * BK, blk.b_row + (int)blk.n0, &full[s]);
-          epi_dbg(0, g + 1);
         }
       }
-      epi_dbg(0, 0xFFFF0000u | g);
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
@@ -591,11 +582,9 @@ __device__ __forceinline__ void tck_loop_epi(const CUtensorMap* mAh, const CUten
             mma(d, tc::sdesc(ahi + off), tc::sdesc(bhi + off), E::IDESC, 1);
           }
           tc::commit(&empty[s]);
-          epi_dbg(1, g + 1);
         }
         tc::commit(&tfull[b]);
       }
-      epi_dbg(1, 0xFFFF0000u | g);
     }
   } else if (warp >= 4) {
     // ---------------------------------------------------------- epilogue (8 warps)
@@ -611,12 +600,9 @@ __device__ __forceinline__ void tck_loop_epi(const CUtensorMap* mAh, const CUten
     if (leader && have) load_c(blk);
     for (int64_t item = first; have; item += stride, ++t) {
       const int b = t & 1;
-      if (lane == 0) epi_dbg(2 + (warp - 4) / 2 , (t << 4) | 1);
       mbar_wait(&tfull[b], (t >> 1) & 1);
       tc::fence_after();
-      if (lane == 0) epi_dbg(2 + (warp - 4) / 2, (t << 4) | 2);
       mbar_wait(cfull, t & 1);  // C of this item in cbuf
-      if (lane == 0) epi_dbg(2 + (warp - 4) / 2, (t << 4) | 3);
       const int cbeg = ch * (BN / 2), cend = cbeg + BN / 2;
 #pragma unroll 1
       for (int c0 = cbeg; c0 < cend; c0 += 32) {
@@ -632,16 +618,13 @@ __device__ __forceinline__ void tck_loop_epi(const CUtensorMap* mAh, const CUten
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);  // TMEM accumulator b drained
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // cbuf writes -> the TMA store
-      if (lane == 0) epi_dbg(2 + (warp - 4) / 2, (t << 4) | 4);
       asm volatile("bar.sync 1, 256;\n" ::: "memory");                 // all eight warps wrote cbuf
-      if (lane == 0) epi_dbg(2 + (warp - 4) / 2, (t << 4) | 5);
       have = next(item + stride, nblk);
       if (leader) {
         tma_store_2d(&cmaps->m[blk.cdev], (int)(blk.crow0 + blk.m0), (int)(blk.ccol0 + blk.n0), cbuf);
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // cbuf read by the store
         if (have) load_c(nblk);
-        epi_dbg(6, (t << 4) | 6);
       }
       __syncwarp();  // warp 4 reconverges before the next warp-collective tcgen05.ld
       blk = nblk;
