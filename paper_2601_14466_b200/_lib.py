@@ -11,7 +11,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libbcmg_b200.so")
+LIB_PATH = os.environ.get("BCMG_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
+                                                           "libbcmg_b200.so")
 
 # Stable error codes (reference pkg/frontend/src/errors.ts:9-23) + CUDA.
 BCMG_OK = 0

@@ -462,6 +462,9 @@ struct TrailParams {
   // row block, so a wave reuses each panel row block across the band from L2
   // instead of streaming the whole panel from HBM once per tile column (0 = off)
   int band;
+  // tcgen05 pair kernel at T_A = 128 (cpu = 2): each item covers two owned tile
+  // columns (c, c + spacing) as one 256-wide UMMA tile; 0 / 1 = one column
+  int cpu;
 };
 
 template <int B>

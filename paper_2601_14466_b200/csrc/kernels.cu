@@ -682,6 +682,15 @@ static bool use_presplit() {
 
 bool tc_presplit_enabled() { return use_tc() && use_presplit(); }
 
+// BCMG_TRAIL_BAND: owned tile columns (units) per band of the tcgen05 trailing update
+static int trail_band() {
+  static const int band = [] {
+    const char* e = getenv("BCMG_TRAIL_BAND");
+    return e && *e ? std::max(0, atoi(e)) : 8;
+  }();
+  return band;
+}
+
 static int tck_width(int64_t n) {
   static const int forced = [] {
     const char* e = getenv("BCMG_TCK_N");
@@ -706,12 +715,10 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   if (total == 0) return;
   TrailParams q = p;
   {
-    static const int band = [] {
-      const char* e = getenv("BCMG_TRAIL_BAND");
-      return e && *e ? std::max(0, atoi(e)) : 8;
-    }();
+    const int band = trail_band();
     const int64_t rb = p.cplx ? BMX / 2 : BMX;
-    const bool cols = p.T <= BNT && p.T % rb == 0 && (p.nloc == 1 || p.nloc == p.D);
+    const int64_t cpu = CL == 3 && p.cpu > 1 ? p.cpu : 1;  // tile columns per unit
+    const bool cols = p.T <= BNT && (cpu * p.T) % rb == 0 && (p.nloc == 1 || p.nloc == p.D);
     const bool blocks = p.T > BNT && p.T % BNT == 0 && p.N % p.T == 0 && p.nloc == p.D;
     q.band = cols || blocks ? band : 0;
   }
@@ -728,6 +735,11 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   tck::CMaps cmaps;
   std::memset(&cmaps, 0, sizeof(cmaps));
   if constexpr (CL == 4) {  // the TMA epilogue's C maps: each local shard as (rows, its columns)
+    static const int mode = [] {
+      const char* e = getenv("BCMG_EPI_MODE");
+      return e && *e ? atoi(e) : 0;
+    }();
+    cmaps.mode = mode;
     const auto counts = column_counts(p.N, p.T, p.D);
     const int64_t cx = p.cplx ? 2 : 1;
     for (int i = 0; i < p.nloc; ++i) {
@@ -804,9 +816,34 @@ static bool tck_epi(bool cplx) {
   return v > 0 || (v < 0 && !cplx);
 }
 
+// BCMG_TCK_UNIT2 (default 1): at T_A = 128, where the TMA epilogue is not used
+// (complex64 by default), the bulk trailing update runs on the 2-SM pair kernel
+// with items of two owned tile columns (one 256 x 256 UMMA tile: 3/4 of the
+// shared-memory operand traffic per SM of the 128 x 128 kernel).  Same bits.
+// N = 65536, 8 devices: complex64 150.6 -> 170.6 TFLOP/s; float32 117.3 -> 112.6
+// (its C read-modify-write per flop is twice complex64's: the TMA epilogue wins)
+static bool tck_unit2() {
+  static const bool v = [] {
+    const char* e = getenv("BCMG_TCK_UNIT2");
+    return !(e && *e && atoi(e) == 0);
+  }();
+  return v;
+}
+
 static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t st) {
-  if (tck_width(p.T) == 128 && p.T == 128 && p.N % p.T == 0 && tck_epi(p.cplx) && p.nloc <= MAX_LOCAL_DEV)
-    return launch_tck_trail_t<128, 4>(p, info, st);
+  const bool epi = tck_width(p.T) == 128 && p.T == 128 && p.N % p.T == 0 && tck_epi(p.cplx) && p.nloc <= MAX_LOCAL_DEV;
+  if (!epi && p.T == 128 && tck_unit2() && tck_cluster() == 2 && trail_band() > 0 && p.N % p.T == 0 &&
+      (p.nloc == 1 || p.nloc == p.D)) {
+    const int64_t sc = p.nloc == p.D ? 1 : p.D;
+    int64_t cm = p.m_first;
+    if (sc > 1) cm += ((p.dev0 - cm % p.D) + p.D) % p.D;
+    if (cm + sc < p.m_last) {  // at least two owned tile columns
+      TrailParams q = p;
+      q.cpu = 2;
+      return launch_tck_trail_t<256, 3>(q, info, st);
+    }
+  }
+  if (epi) return launch_tck_trail_t<128, 4>(p, info, st);
   if (tck_width(p.T) == 256) {
     const int c = tck_cluster();
     if (c == 2) return launch_tck_trail_t<256, 3>(p, info, st);

@@ -103,6 +103,12 @@ struct Blk {
   // coordinates of the item's row / column 0 (the block adds m0 / n0)
   int cdev;
   int64_t crow0, ccol0;
+  // 2-SM pair kernel (tck_loop_pair): B rows of CTA rank 1 (< 0: b_row + 128), and
+  // a second output column tile for tile columns >= 128 (C2, same row base as C;
+  // its rows < skip2 lie above that tile column's diagonal and are not written)
+  int b_row1 = -1;
+  float* C2 = nullptr;
+  int64_t skip2 = 0;
 };
 
 template <class Next>

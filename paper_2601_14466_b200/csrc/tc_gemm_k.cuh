@@ -362,8 +362,9 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(mBl) : "memory");
       uint32_t g = 0;
       tc::Blk blk;
-      const int arow = rank * BM, brow = rank * (BN / 2);
+      const int arow = rank * BM;
       for (int64_t item = first; next(item, blk); item += stride) {
+        const int brow = (rank == 0 ? blk.b_row : blk.b_row1 >= 0 ? blk.b_row1 : blk.b_row + BN / 2) + (int)blk.n0;
         for (int kt = 0; kt < KT; ++kt, ++g) {
           const int s = g % STAGES;
           mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
@@ -372,8 +373,8 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
           if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
           tma_load_2d_pair(st, mAh, kt * BK, blk.a_row + (int)blk.m0 + arow, fb);
           tma_load_2d_pair(st + PA, mAl, kt * BK, blk.a_row + (int)blk.m0 + arow, fb);
-          tma_load_2d_pair(st + 2 * PA, mBh, kt * BK, blk.b_row + (int)blk.n0 + brow, fb);
-          tma_load_2d_pair(st + 2 * PA + PB, mBl, kt * BK, blk.b_row + (int)blk.n0 + brow, fb);
+          tma_load_2d_pair(st + 2 * PA, mBh, kt * BK, brow, fb);
+          tma_load_2d_pair(st + 2 * PA + PB, mBl, kt * BK, brow, fb);
         }
       }
       // the leader's last commits arrive on our empty barriers: let them land before exit
@@ -419,21 +420,27 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
     for (int64_t item = first; next(item, blk); item += stride, ++t) {
       const int b = t & 1;
       const int64_t r = blk.m0 + rank * BM + row;
-      float* __restrict__ crow = blk.C + r;
+      // columns >= 128 of a two-column item go to the second tile column (C2)
+      const bool second = blk.C2 != nullptr && ch == 1;
+      const int64_t coff = second ? BN / 2 : 0;
+      float* __restrict__ crow = (second ? blk.C2 : blk.C) + r;
+      const bool rok = r < blk.M && (!second || r >= blk.skip2);
       auto load_chunk = [&](int c0, float* dst) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int64_t col = blk.n0 + c0 + j;
-          dst[j] = (blk.beta != 0.f && r < blk.M && col < blk.N) ? crow[col * blk.ldc] : 0.f;
+          dst[j] = (blk.beta != 0.f && rok && col < blk.N) ? crow[(col - coff) * blk.ldc] : 0.f;
         }
       };
       const int cbeg = ch * (BN / 2), cend = cbeg + BN / 2;
       if (blk.beta != 0.f) {
         constexpr int PER = BN / 2 / 32;
         const int64_t col = blk.n0 + cbeg + PER * lane, r0 = blk.m0 + rank * BM + 32 * q;
+        const bool live = r0 < blk.M && (!second || r0 + 32 > blk.skip2);
 #pragma unroll
         for (int j = 0; j < PER; ++j)
-          if (col + j < blk.N && r0 < blk.M) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(blk.C + r0 + (col + j) * blk.ldc));
+          if (col + j < blk.N && live)
+            asm volatile("prefetch.global.L2 [%0];\n" ::"l"((second ? blk.C2 : blk.C) + r0 + (col + j - coff) * blk.ldc));
       }
       float old[32], nxt[32];
       load_chunk(cbeg, old);
@@ -444,11 +451,11 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
         if (c0 + 32 < cend) load_chunk(c0 + 32, nxt);
         float v[32];
         tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + b * BN + c0, v);
-        if (r < blk.M) {
+        if (rok) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int64_t col = blk.n0 + c0 + j;
-            if (col < blk.N) crow[col * blk.ldc] = blk.alpha * v[j] + blk.beta * old[j];
+            if (col < blk.N) crow[(col - coff) * blk.ldc] = blk.alpha * v[j] + blk.beta * old[j];
           }
         }
 #pragma unroll
@@ -480,6 +487,12 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
 // flight.  Two 64 KB operand stages + the C tile fill 192 KB.
 struct CMaps {
   CUtensorMap m[MAX_LOCAL_DEV];  // per local device: its shard as (rows, columns), box {128, 128}
+  int mode;                      // EPI_PREFETCH | EPI_DIRECT (BCMG_EPI_MODE)
+};
+enum : int {
+  EPI_PREFETCH = 1,  // the producer prefetches an item's C tile into L2 when it starts the item's operands
+  EPI_DIRECT = 2,    // results stored straight from registers (coalesced 128 B per warp and column):
+                     // cbuf is free for the next item's C as soon as every warp has read it
 };
 struct Epi {
   static constexpr int BN = 128;
@@ -492,6 +505,10 @@ struct Epi {
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                     ((uint32_t)(BM >> 4) << 24);
 };
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(map), "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map), "r"(c0),
                "r"(c1), "r"(smem_u32(src))
@@ -547,6 +564,8 @@ __device__ __forceinline__ void tck_loop_epi(const CUtensorMap* mAh, const CUten
       uint32_t g = 0;
       tc::Blk blk;
       for (int64_t item = first; next(item, blk); item += stride) {
+        if (cmaps->mode & EPI_PREFETCH)
+          tma_prefetch_2d(&cmaps->m[blk.cdev], (int)(blk.crow0 + blk.m0), (int)(blk.ccol0 + blk.n0));
         for (int kt = 0; kt < KT; ++kt, ++g) {
           const int s = g % STAGES;
           mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
@@ -604,26 +623,39 @@ __device__ __forceinline__ void tck_loop_epi(const CUtensorMap* mAh, const CUten
       tc::fence_after();
       mbar_wait(cfull, t & 1);  // C of this item in cbuf
       const int cbeg = ch * (BN / 2), cend = cbeg + BN / 2;
+      const bool direct = cmaps->mode & EPI_DIRECT;
+      float* gc = blk.C + blk.m0 + row + blk.n0 * blk.ldc;
+      const bool live = blk.m0 + row < blk.M;
 #pragma unroll 1
       for (int c0 = cbeg; c0 < cend; c0 += 32) {
         float v[32];
         tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + b * BN + c0, v);
+        if (direct) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float* cp = cbuf + row + (c0 + j) * BM;
-          *cp = blk.alpha * v[j] + blk.beta * *cp;
+          for (int j = 0; j < 32; ++j) {
+            const float out = blk.alpha * v[j] + blk.beta * cbuf[row + (c0 + j) * BM];
+            if (live && c0 + j < blk.N) gc[(int64_t)(c0 + j) * blk.ldc] = out;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float* cp = cbuf + row + (c0 + j) * BM;
+            *cp = blk.alpha * v[j] + blk.beta * *cp;
+          }
         }
       }
       tc::fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);  // TMEM accumulator b drained
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // cbuf writes -> the TMA store
-      asm volatile("bar.sync 1, 256;\n" ::: "memory");                 // all eight warps wrote cbuf
+      if (!direct) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // cbuf writes -> the TMA store
+      asm volatile("bar.sync 1, 256;\n" ::: "memory");  // all eight warps are done with cbuf
       have = next(item + stride, nblk);
       if (leader) {
-        tma_store_2d(&cmaps->m[blk.cdev], (int)(blk.crow0 + blk.m0), (int)(blk.ccol0 + blk.n0), cbuf);
-        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // cbuf read by the store
+        if (!direct) {
+          tma_store_2d(&cmaps->m[blk.cdev], (int)(blk.crow0 + blk.m0), (int)(blk.ccol0 + blk.n0), cbuf);
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // cbuf read by the store
+        }
         if (have) load_c(nblk);
       }
       __syncwarp();  // warp 4 reconverges before the next warp-collective tcgen05.ld
@@ -694,20 +726,24 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
   // blocks of consecutive tiles (spaced BNT rows).
   const int64_t sc = p.nloc == p.D ? 1 : p.D;
   const int64_t ncb = p.T > BNT ? p.T / BNT : 1;
+  // CL = 3 at T_A = 128: a unit is two owned tile columns (c, c + sc), one 256-wide item
+  const int64_t cpu = CL == 3 && ncb == 1 && p.cpu > 1 ? p.cpu : 1, usp = cpu * sc;
   if (p.band > 0 && sc > 1) cm += ((p.dev0 - cm % p.D) + p.D) % p.D;  // first owned column
-  const int64_t nunits = ncb == 1 ? (p.m_last - cm + sc - 1) / sc : (p.m_last - p.m_first) * ncb;
+  const int64_t nunits = ncb == 1 ? ((p.m_last - cm + sc - 1) / sc + cpu - 1) / cpu : (p.m_last - p.m_first) * ncb;
   const int64_t cm0 = cm;
-  auto unit_row = [&](int64_t k) { return ncb == 1 ? (cm0 + k * sc) * p.T : (p.m_first * ncb + k) * BNT; };
+  auto unit_row = [&](int64_t k) { return ncb == 1 ? (cm0 + k * usp) * p.T : (p.m_first * ncb + k) * BNT; };
+  // row blocks are counted from roff (units start a multiple of RB rows apart)
+  const int64_t roff = unit_row(0) % (p.cplx ? BMX / 2 : BMX);
   int64_t ku = 0, bg = 0, ba0 = 0, btop = 0;
   auto next = [&](int64_t item, tc::Blk& blk) -> bool {
     if (p.band > 0) {
       const int64_t RB = p.cplx ? BMX / 2 : BMX;  // matrix rows per row block (complex64: embedded pairs)
-      const int64_t step = (ncb == 1 ? sc * p.T : (int64_t)BNT) / RB, aend = (p.N + RB - 1) / RB;
+      const int64_t step = (ncb == 1 ? usp * p.T : (int64_t)BNT) / RB, aend = (p.N - roff + RB - 1) / RB;
       for (;;) {
         if (ku >= nunits) return false;
         if (ccnt < 0) {
           bg = nunits - ku < p.band ? nunits - ku : p.band;
-          ba0 = unit_row(ku) / RB;
+          ba0 = (unit_row(ku) - roff) / RB;
           btop = step * bg * (bg - 1) / 2;
           ccnt = bg * (aend - ba0) - btop;
         }
@@ -729,7 +765,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
         i = o % bg;
       }
       const int64_t k = ku + i;
-      const int64_t c = ncb == 1 ? cm0 + k * sc : (p.m_first * ncb + k) / ncb;
+      const int64_t c = ncb == 1 ? cm0 + k * usp : (p.m_first * ncb + k) / ncb;
       const int64_t cb = ncb == 1 ? 0 : (p.m_first * ncb + k) % ncb;
       const int64_t ms = c * p.T, rows = p.N - ms;
       const int dev = (int)(c % p.D);
@@ -737,7 +773,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
       const int64_t cx = p.cplx ? 2 : 1;
       blk.a_row = (int)(cx * (ms - p.prow0));
       blk.b_row = (int)(ms - p.prow0);
-      blk.m0 = (A - ms / RB) * BMX;
+      blk.m0 = (A - (ms - roff) / RB) * BMX;
       blk.n0 = cb * BNT;
       blk.M = cx * rows;
       blk.N = p.T < rows ? p.T : rows;
@@ -749,6 +785,16 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
       blk.alpha = -1.f;
       blk.beta = 1.f;
       blk.nfan = 0;
+      blk.C2 = nullptr;
+      blk.b_row1 = -1;
+      if (cpu > 1 && c + sc < p.m_last) {  // the unit's second tile column
+        const int64_t c2 = c + sc;
+        float* shard2 = reinterpret_cast<float*>(p.shards[(int)(c2 % p.D) - p.dev0]);
+        blk.C2 = shard2 + cx * (ms + (c2 / p.D) * p.T * p.N);
+        blk.skip2 = cx * (c2 - c) * p.T;
+        blk.b_row1 = (int)(c2 * p.T - p.prow0);
+        blk.N = 2 * p.T;
+      }
       return true;
     }
     for (;;) {
