@@ -167,6 +167,29 @@ def reference_ladder(bcmg) -> dict:
     out["extrapolated_N3"] = {"n32768_s": c * 32768 ** 3, "n131072_s": c * 131072 ** 3,
                               "n131072_tflops": potrs_flops(131072, 64) / (c * 131072 ** 3) / 1e12,
                               "label": "EXTRAPOLATED proportional to N^3 from the N=4096/8192 points, not measured"}
+    # secondary comparator: LAPACK potrf + potrs through scipy on the same cores
+    try:
+        import scipy.linalg as sl
+        from bcmg import cli as ref_cli
+
+        lap = {}
+        for n in (4096, 8192):
+            a = ref_cli.make_matrix("random_spd", n, bcmg.ElementType.real64, 1)
+            b = np.ones((n, 64))
+            t0 = time.perf_counter()
+            x = sl.cho_solve(sl.cho_factor(a, lower=True, check_finite=False), b, check_finite=False)
+            dt = time.perf_counter() - t0
+            lap[f"n{n}"] = {"s": dt, "tflops": potrs_flops(n, 64) / dt / 1e12,
+                            "residual": float(ref_cli.solve_residual(a, x, b))}
+        try:
+            from threadpoolctl import threadpool_info
+
+            lap["blas"] = [{k: i.get(k) for k in ("internal_api", "version", "num_threads")} for i in threadpool_info()]
+        except Exception:
+            pass
+        out["lapack_cho_solve"] = lap
+    except Exception as e:  # the comparator is optional
+        out["lapack_cho_solve"] = {"unavailable": str(e)[:200]}
     return out
 
 
