@@ -116,6 +116,10 @@ def _potrs_ranks(a, b, n, t, ndev, world, dtype):
 @pytest.mark.parametrize("dtype,n,t,ndev,world", [
     (np.float64, 300, 32, 2, 2), (np.float64, 512, 64, 4, 2), (np.complex128, 260, 24, 4, 2),
     (np.float32, 384, 64, 4, 4), (np.complex64, 200, 40, 2, 2), (np.float64, 2048, 256, 4, 2),
+    # T_A = 128: the TMA-epilogue kernel (f32) and the two-column 2-SM pair items with
+    # owned columns D apart (c64, one device per rank)
+    (np.float32, 2048, 128, 2, 2), (np.float32, 2048, 128, 4, 2), (np.complex64, 2048, 128, 2, 2),
+    (np.complex64, 2560, 128, 4, 4),
 ])
 @pytest.mark.parametrize("paths", ["ce+p2p", "nccl+staged"])
 def test_loopback_potrs_matches_single_process(dtype, n, t, ndev, world, paths, monkeypatch):
