@@ -52,8 +52,11 @@ template <class TL>
 constexpr int tma_box_rows_a() { return TL::LDA; }
 template <class TL>
 constexpr int tma_box_rows_b() { return TL::LDB; }
-template <class TL>
-constexpr unsigned tma_stage_bytes() { return (unsigned)(TL::BK * (TL::LDA + TL::LDB) * 8); }
+// TBK: B stored k-contiguous (N x K with K innermost): its tile is [BN][LDT]
+template <class TL, bool TBK = false>
+constexpr int tma_stage_words() { return TL::BK * TL::LDA + (TBK ? TL::BN * TL::LDT : TL::BK * TL::LDB); }
+template <class TL, bool TBK = false>
+constexpr unsigned tma_stage_bytes() { return (unsigned)(tma_stage_words<TL, TBK>() * 8); }
 // One output block: rows [a_row + m0 ...) of A's map, [b_row + n0 ...) of B's map.
 struct TmaBlock {
   int a_row, b_row;      // tensor-map row coordinate of the block's first A / B row
@@ -61,6 +64,7 @@ struct TmaBlock {
   int64_t M, N;          // output extent (rows >= M / cols >= N are not stored)
   Epilogue ep;
   int live;              // 0: no more items (sentinel slot)
+  int bmap;              // B tensor map of the item (multi-map kernels; MB)
 };
 // Dynamic shared memory: STAGES operand stages | 2*STAGES mbarriers | aux area:
 // producer state [0,384), caller state [384,512), then a ring of decoded work
@@ -69,14 +73,50 @@ struct TmaBlock {
 // current item occupies registers next to the DMMA accumulators.
 constexpr int TMA_RING = 8;
 constexpr int TMA_AUX_BYTES = 512 + TMA_RING * (int)sizeof(TmaBlock);
-template <class TL>
+template <class TL, bool TBK = false>
 constexpr size_t tma_smem_bytes() {
-  return (size_t)TL::STAGES * tma_stage_bytes<TL>() + 2 * TL::STAGES * 8 + TMA_AUX_BYTES;
+  return (size_t)TL::STAGES * tma_stage_bytes<TL, TBK>() + 2 * TL::STAGES * 8 + TMA_AUX_BYTES;
 }
 extern __shared__ __align__(1024) unsigned char tma_dyn_smem[];
-template <class TL>
+template <class TL, bool TBK = false>
 __device__ __forceinline__ unsigned char* tma_aux() {
-  return tma_dyn_smem + (size_t)TL::STAGES * tma_stage_bytes<TL>() + 2 * TL::STAGES * 8;
+  return tma_dyn_smem + (size_t)TL::STAGES * tma_stage_bytes<TL, TBK>() + 2 * TL::STAGES * 8;
+}
+
+// One BK slice with B k-contiguous ([BN][LDT] tile, TBK): thread (r, q) takes
+// k = kk + 2q + j in DMMA step j of each 8-wide k block, so both of its B
+// values are one 16-byte load (conflict-free at LDT = 36: rows 2r + c land on
+// 16-byte bank groups 4r + q); A keeps the paired-row loads of mma_slice.
+template <class TL>
+__device__ __forceinline__ void mma_slice_tbk(Acc<TL, false>& acc, const double* __restrict__ As,
+                                              const double* __restrict__ Bs, int wm0, int wn0, int lane) {
+  static_assert(TL::PAIR && TL::BK % 8 == 0, "paired fragments, 8-wide k blocks");
+  const int r = lane >> 2, q = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < TL::BK; kk += 8) {
+    double b0[TL::FN], b1[TL::FN];
+#pragma unroll
+    for (int f = 0; f < TL::FN; ++f) {
+      const double2 v = *reinterpret_cast<const double2*>(Bs + (wn0 + frag_row<TL>(f, r)) * TL::LDT + kk + 2 * q);
+      b0[f] = v.x;
+      b1[f] = v.y;
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double a[TL::FM];
+#pragma unroll
+      for (int f = 0; f < TL::FM; f += 2) {
+        const double2 v =
+            *reinterpret_cast<const double2*>(As + (kk + 2 * q + j) * TL::LDA + wm0 + frag_row<TL>(f, r));
+        a[f] = v.x;
+        a[f + 1] = v.y;
+      }
+#pragma unroll
+      for (int fm = 0; fm < TL::FM; ++fm)
+#pragma unroll
+        for (int fn = 0; fn < TL::FN; ++fn) dmma(acc.re[fm][fn][0], acc.re[fm][fn][1], a[fm], j ? b1[fn] : b0[fn]);
+    }
+  }
 }
 
 // Persistent producer/consumer loop.  `next_p(item, blk)` fills the block of
@@ -86,13 +126,13 @@ __device__ __forceinline__ unsigned char* tma_aux() {
 // waiting for that slice (mbarrier release / acquire orders the ring store).
 // When the items run out the producer publishes a sentinel (live = 0) and
 // completes the next stage's barrier without a transfer.
-template <class TL, bool FAN = true, bool COPY = false, class NextP>
+template <class TL, bool FAN = true, bool COPY = false, bool TBK = false, bool MB = false, class NextP>
 __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUtensorMap* mapB, int K, NextP&& next_p,
                                               long long stagger_ns = 0) {
   double* smem = reinterpret_cast<double*>(tma_dyn_smem);
   constexpr int NW = TL::THREADS / 32;
-  constexpr unsigned STAGE_BYTES = tma_stage_bytes<TL>();
-  constexpr int STAGE_WORDS = TL::BK * (TL::LDA + TL::LDB);
+  constexpr unsigned STAGE_BYTES = tma_stage_bytes<TL, TBK>();
+  constexpr int STAGE_WORDS = tma_stage_words<TL, TBK>();
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + TL::STAGES * STAGE_WORDS);
   uint64_t* empty = full + TL::STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -117,8 +157,8 @@ __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUt
     int kt, live, done;
   };
   static_assert(sizeof(Prod) <= 384, "producer state must fit its aux slot");
-  Prod& ps = *reinterpret_cast<Prod*>(tma_aux<TL>());
-  TmaBlock* ring = reinterpret_cast<TmaBlock*>(tma_aux<TL>() + 512);
+  Prod& ps = *reinterpret_cast<Prod*>(tma_aux<TL, TBK>());
+  TmaBlock* ring = reinterpret_cast<TmaBlock*>(tma_aux<TL, TBK>() + 512);
   auto produce_one = [&]() {
     if (ps.done) return;
     const uint32_t gp = ps.gp;
@@ -134,7 +174,9 @@ __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUt
     double* st = smem + s * STAGE_WORDS;
     mbar_expect_tx(&full[s], STAGE_BYTES);
     tma_load_2d(st, mapA, blk.a_row + (int)blk.m0, kt * TL::BK, &full[s]);
-    tma_load_2d(st + TL::BK * TL::LDA, mapB, blk.b_row + (int)blk.n0, kt * TL::BK, &full[s]);
+    const CUtensorMap* mb = MB ? mapB + blk.bmap : mapB;
+    if constexpr (TBK) tma_load_2d(st + TL::BK * TL::LDA, mb, kt * TL::BK, blk.b_row + (int)blk.n0, &full[s]);
+    else tma_load_2d(st + TL::BK * TL::LDA, mb, blk.b_row + (int)blk.n0, kt * TL::BK, &full[s]);
     ps.gp = gp + 1;
     if (kt + 1 == KT) {
       ps.kt = 0;
@@ -192,7 +234,8 @@ __device__ __forceinline__ void tma_gemm_loop(const CUtensorMap* mapA, const CUt
       if (kt == 0 && !cb.live) return;  // sentinel (published before this barrier completed)
       if (kt == (KT > PREFETCH_AHEAD ? KT - PREFETCH_AHEAD : 0)) prefetch_c(cb);
       const double* st = smem + s * STAGE_WORDS;
-      mma_slice<TL, false, false, false>(acc, st, st + TL::BK * TL::LDA, nullptr, nullptr, wm0, wn0, lane);
+      if constexpr (TBK) mma_slice_tbk<TL>(acc, st, st + TL::BK * TL::LDA, wm0, wn0, lane);
+      else mma_slice<TL, false, false, false>(acc, st, st + TL::BK * TL::LDA, nullptr, nullptr, wm0, wn0, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       ++g;
@@ -530,9 +573,10 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
       [&](int64_t item, TmaBlock& blk) { return decode(cc, item, blk); }, p.stagger_ns);
 }
 
-// Single GEMM C := alpha A B^H (+ beta C) with A (M x K) and B (N x K) both
-// i-contiguous real double, persistent over the ceil(M/BM) x ceil(N/BN) blocks.
-template <class TL>
+// Single GEMM C := alpha A B^H (+ beta C) with A (M x K) i-contiguous and B
+// (N x K) i-contiguous (TBK = false) or k-contiguous (TBK = true) real double,
+// persistent over the ceil(M/BM) x ceil(N/BN) blocks.
+template <class TL, bool TBK = false>
 __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
     gemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int64_t M,
                     int64_t N, int64_t K, Epilogue ep, const int* info) {
@@ -550,7 +594,46 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
     blk.ep = ep;
     return true;
   };
-  tma_gemm_loop<TL>(&mapA, &mapB, (int)K, decode);
+  tma_gemm_loop<TL, true, false, TBK>(&mapA, &mapB, (int)K, decode);
+}
+
+// Several GEMMs sharing A in one persistent launch: group g is
+// C[:, col0[g] + j] := alpha A Bg(j, :)^T (+ beta C), Bg k-contiguous (TBK)
+// with its own tensor map; column blocks never straddle groups.  (The complex
+// embedding's product sweep: one B per local device, one wave-filling launch.)
+struct BMaps {
+  static constexpr int MAX = 8;
+  CUtensorMap m[MAX];
+  int64_t col0[MAX + 1];  // output column of each group; col0[n] = total
+  int n;
+};
+template <class TL>
+__global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
+    gemm_tma_grouped_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ BMaps bm, int64_t M,
+                            int64_t K, Epilogue ep, const int* info) {
+  if (ld_flag(info)) return;
+  const int64_t nbm = (M + TL::BM - 1) / TL::BM;
+  auto decode = [&](int64_t item, TmaBlock& blk) -> bool {
+    int64_t cb = item / nbm;  // column-block-major, as gemm_tma_kernel
+    for (int g = 0; g < bm.n; ++g) {
+      const int64_t ng = bm.col0[g + 1] - bm.col0[g], nbg = (ng + TL::BN - 1) / TL::BN;
+      if (cb < nbg) {
+        blk.a_row = 0;
+        blk.b_row = 0;
+        blk.bmap = g;
+        blk.m0 = (item % nbm) * TL::BM;
+        blk.n0 = cb * TL::BN;
+        blk.M = M;
+        blk.N = ng;
+        blk.ep = ep;
+        blk.ep.C = static_cast<char*>(ep.C) + bm.col0[g] * ep.ldc * 8;
+        return true;
+      }
+      cb -= nbg;
+    }
+    return false;
+  };
+  tma_gemm_loop<TL, true, false, true, true>(&mapA, &bm.m[0], (int)K, decode);
 }
 
 }  // namespace bcmg

@@ -349,13 +349,15 @@ void expand_panel(int dt, void* P, void* PB, int64_t rows, int64_t K, cudaStream
   BCMG_CHECK_LAUNCH();
 }
 
-template <class TL>
+// TBK: B is k-contiguous (Bhat(n, k) = B[k + n*ld]); its box is {LDT k, BN rows}
+// (4 k columns of over-fetch, zero past K) for the [BN][LDT] tile of mma_slice_tbk
+template <class TL, bool TBK = false>
 static void launch_gemm_tma_t(int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B,
                               const Epilogue& ep, const int* info, cudaStream_t st) {
   const CUtensorMap ma = make_map(A.ptr, M, K, A.ld, TL::LDA, TL::BK);
-  const CUtensorMap mb = make_map(B.ptr, N, K, B.ld, TL::LDB, TL::BK);
-  constexpr size_t smem = tma_smem_bytes<TL>();
-  auto kern = gemm_tma_kernel<TL>;
+  const CUtensorMap mb = TBK ? make_map(B.ptr, K, N, B.ld, TL::LDT, TL::BN) : make_map(B.ptr, N, K, B.ld, TL::LDB, TL::BK);
+  constexpr size_t smem = tma_smem_bytes<TL, TBK>();
+  auto kern = gemm_tma_kernel<TL, TBK>;
   set_smem(kern, smem);
   int per_sm = 1;
   BCMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TL::THREADS, smem));
@@ -384,10 +386,17 @@ static void launch_gemm_tma(int64_t M, int64_t N, int64_t K, const Operand& A, c
 //     row 2r+1: sum Im A Re B + Re A Im B = Im (A B)_rc
 // The gather kernel materialises either operand from any Operand view
 // (transposed / conjugated) through a 32x32 shared-memory tile.
+// With B-hat k-contiguous and unconjugated (complex128), B-hat's own storage is
+// the real operand: Bhat(n, k) -> doubles (Re, Im) at k' = 2k, 2k+1 of a real
+// N x 2K k-contiguous matrix (ld 2 ld).  A is then embedded with interleaved
+// columns, Atilde(:, 2k) = A(:, k), Atilde(:, 2k+1) = i A(:, k):
+//     sum_k A(r,k) Re B(c,k) + i A(r,k) Im B(c,k) = (A B^T)(r,c)
+// so only the (small) A side is gathered; the GEMM reads B in place
+// (launch_gemm_tma_t<TL, true>).
 template <class C, class R>
-__global__ void embed_gather_kernel(Operand X, int64_t I, int64_t kn, C* outc, R* outp, int64_t ldo) {
-  // logical element (i, kk) of X, kk < kn; outc: complex Atilde (ld ldo, cols kk and kn + kk),
-  // outp: planar X (ld ldo, cols kk and kn + kk)
+__global__ void embed_gather_kernel(Operand X, int64_t I, int64_t kn, C* outc, R* outp, int64_t ldo, int inter) {
+  // logical element (i, kk) of X, kk < kn; outc: complex Atilde (ld ldo, cols kk and kn + kk,
+  // or 2kk and 2kk + 1 when inter), outp: planar X (ld ldo, cols kk and kn + kk)
   __shared__ C t[32][33];
   const int64_t i0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
   const C* base = static_cast<const C*>(X.ptr);
@@ -408,7 +417,13 @@ __global__ void embed_gather_kernel(Operand X, int64_t I, int64_t kn, C* outc, R
     const int64_t i = i0 + threadIdx.x, kk = c0 + y;
     if (i >= I || kk >= kn) continue;
     const C v = t[y][threadIdx.x];
-    if (outc) {
+    if (outc && inter) {
+      C q;
+      q.x = -v.y;
+      q.y = v.x;
+      outc[i + 2 * kk * ldo] = v;
+      outc[i + (2 * kk + 1) * ldo] = q;
+    } else if (outc) {
       C q;
       q.x = v.y;
       q.y = -v.x;
@@ -422,10 +437,17 @@ __global__ void embed_gather_kernel(Operand X, int64_t I, int64_t kn, C* outc, R
 }
 
 template <class C, class R>
-static void embed_gather(const Operand& X, int64_t I, int64_t kn, C* outc, R* outp, int64_t ldo, cudaStream_t st) {
+static void embed_gather(const Operand& X, int64_t I, int64_t kn, C* outc, R* outp, int64_t ldo, cudaStream_t st,
+                         int inter = 0) {
   dim3 grid((unsigned)((I + 31) / 32), (unsigned)((kn + 31) / 32)), block(32, 8);
-  embed_gather_kernel<C, R><<<grid, block, 0, st>>>(X, I, kn, outc, outp, ldo);
+  embed_gather_kernel<C, R><<<grid, block, 0, st>>>(X, I, kn, outc, outp, ldo, inter);
   BCMG_CHECK_LAUNCH();
+}
+
+// complex128 B-hat usable in place by the k-contiguous TMA GEMM (see embed_gather_kernel)
+static bool native_b(const Operand& B) {
+  static const bool off = getenv("BCMG_CPLX_NATIVE_B") && atoi(getenv("BCMG_CPLX_NATIVE_B")) == 0;
+  return !off && B.trans && !B.conj && !B.mask && aligned16(B.ptr) && B.ld < ((int64_t)1 << 35);
 }
 
 size_t gemm_cplx_embed_bytes(int dt, int64_t M, int64_t N, int64_t K) {
@@ -447,7 +469,14 @@ bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, 
   // the caller needs a shape-independent choice (bit-identical results across device counts)
   const int64_t blocks = ((2 * M + TileTrail2::BM - 1) / TileTrail2::BM) * ((N + TileTrail2::BN - 1) / TileTrail2::BN);
   if (!always && blocks < num_sms()) return false;
-  if (dt == C128) {
+  if (dt == C128 && native_b(B)) {  // B read in place, A gathered with interleaved columns
+    double2* at = static_cast<double2*>(scratch);
+    embed_gather<double2, double>(A, M, K, at, nullptr, M, st, 1);
+    Epilogue er = ep;
+    er.ldc = 2 * ep.ldc;
+    launch_gemm_tma_t<TileTrail2, true>(2 * M, N, 2 * K, Operand{at, 2 * M, 0, 0, 0, 0},
+                                        Operand{B.ptr, 2 * B.ld, 1, 0, 0, 0}, er, info, st);
+  } else if (dt == C128) {
     double2* at = static_cast<double2*>(scratch);              // M x 2K complex, ld M
     double* xp = reinterpret_cast<double*>(at + 2 * M * K);    // N x 2K real, ld N
     embed_gather<double2, double>(A, M, K, at, nullptr, M, st);
@@ -493,6 +522,49 @@ bool gemm_cplx_embed_grouped(int dt, int64_t M, int64_t K, const Operand& A, con
   if (!aligned16(ep.C) || !aligned16(scratch) || scratch_bytes < gemm_cplx_embed_bytes(dt, M, chunk, K)) return false;
   if (dt == C64 && 2 * M < 256) return false;  // the tcgen05 tile's minimum shape
   const size_t csz = dt == C128 ? 16 : 8;
+  bool native = dt == C128;
+  for (int i = 0; i < ngroups && native; ++i) native = native_b(Bs[i]);
+  if (native) {  // A gathered once (interleaved columns), one GEMM per group reading B in place
+    double2* at = static_cast<double2*>(scratch);
+    embed_gather<double2, double>(A, M, K, at, nullptr, M, st, 1);
+    using TL = TileTrail2;
+    BMaps bm;
+    std::memset(&bm, 0, sizeof(bm));
+    if (ngroups <= BMaps::MAX) {  // one launch over every group's columns
+      int64_t nblk = 0;
+      for (int i = 0; i < ngroups; ++i) {
+        if (ncols[i] == 0) continue;
+        bm.m[bm.n] = make_map(Bs[i].ptr, 2 * K, ncols[i], 2 * Bs[i].ld, TL::LDT, TL::BN);
+        bm.col0[bm.n + 1] = bm.col0[bm.n] + ncols[i];
+        ++bm.n;
+        nblk += (ncols[i] + TL::BN - 1) / TL::BN;
+      }
+      Epilogue er = ep;
+      er.ldc = 2 * ep.ldc;
+      const CUtensorMap ma = make_map(at, 2 * M, 2 * K, 2 * M, TL::LDA, TL::BK);
+      constexpr size_t smem = tma_smem_bytes<TL, true>();
+      auto kern = gemm_tma_grouped_kernel<TL>;
+      set_smem(kern, smem);
+      int per_sm = 1;
+      BCMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TL::THREADS, smem));
+      const int64_t blocks = ((2 * M + TL::BM - 1) / TL::BM) * nblk;
+      const int64_t grid = std::min<int64_t>(blocks, (int64_t)num_sms() * std::max(per_sm, 1));
+      if (grid > 0) kern<<<(unsigned)grid, TL::THREADS, smem, st>>>(ma, bm, 2 * M, 2 * K, er, nullptr);
+      BCMG_CHECK_LAUNCH();
+      return true;
+    }
+    int64_t g0 = 0;
+    for (int i = 0; i < ngroups; ++i) {
+      if (ncols[i] == 0) continue;
+      Epilogue er = ep;
+      er.C = static_cast<char*>(ep.C) + g0 * ep.ldc * (int64_t)csz;
+      er.ldc = 2 * ep.ldc;
+      launch_gemm_tma_t<TL, true>(2 * M, ncols[i], 2 * K, Operand{at, 2 * M, 0, 0, 0, 0},
+                                  Operand{Bs[i].ptr, 2 * Bs[i].ld, 1, 0, 0, 0}, er, nullptr, st);
+      g0 += ncols[i];
+    }
+    return true;
+  }
   // A (M x K, op(A)) gathered ONCE as [A | -iA] (M x 2K complex), then chunk
   // after chunk of the concatenated groups' columns as planar [Re B | -Im B]
   // and one real GEMM per chunk into the concatenated output columns
