@@ -75,3 +75,16 @@ def test_gemm_f32_tcgen05_3xtf32(cuda, m, n, k):
     pad = (-m) % 4
     assert _run(torch, 0, m, n, k, 0, 1, -1.0, 1.0, lda_pad=pad) <= 0
     assert _run(torch, 0, m, n, k, 0, 1, 1.0, 0.0, lda_pad=pad, seed=3) <= 0
+
+
+@pytest.mark.parametrize("m,n,k", [(2100, 1500, 333), (1030, 2050, 517), (4096, 1024, 512)])
+def test_gemm_c128_real_embedding(cuda, m, n, k):
+    """complex128 shapes large enough for the real embedding on the FP64 TMA
+    kernel: op_b = N reads B in place (k-contiguous operand, interleaved A
+    embedding), op_b = C takes the planar gather; odd K and padded lda."""
+    import torch
+
+    for op_a in (0, 1):
+        for op_b in (0, 1):
+            assert _run(torch, 3, m, n, k, op_a, op_b, -1.0, 1.0) <= 0
+            assert _run(torch, 3, m, n, k, op_a, op_b, 1.0, 0.0, lda_pad=3, seed=2) <= 0
