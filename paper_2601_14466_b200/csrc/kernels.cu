@@ -789,7 +789,7 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   {
     const int band = trail_band();
     const int64_t rb = p.cplx ? BMX / 2 : BMX;
-    const int64_t cpu = CL == 3 && p.cpu > 1 ? p.cpu : 1;  // tile columns per unit
+    const int64_t cpu = (CL == 3 || CL == 6) && p.cpu > 1 ? p.cpu : 1;  // tile columns per unit
     const bool cols = p.T <= BNT && (cpu * p.T) % rb == 0 && (p.nloc == 1 || p.nloc == p.D);
     const bool blocks = p.T > BNT && p.T % BNT == 0 && p.N % p.T == 0 && p.nloc == p.D;
     q.band = cols || blocks ? band : 0;
@@ -797,16 +797,19 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   const int64_t prow = p.N - p.prow0, arows = p.cplx ? 2 * prow : prow;
   const CUtensorMap ah = make_map_kmajor(p.split[0], arows, p.split_ld[0]);
   const CUtensorMap al = make_map_kmajor(p.split[1], arows, p.split_ld[0]);
-  constexpr int BROWS = (CL == 2 || CL == 3) ? BNT / 2 : BNT;  // CTA pairs load half the B tile each
+  constexpr int BROWS = (CL == 2 || CL == 3 || CL == 6) ? BNT / 2 : BNT;  // CTA pairs load half the B tile each
   const CUtensorMap bh = make_map_kmajor(p.split[2], prow, p.split_ld[1], BROWS);
   const CUtensorMap bl = make_map_kmajor(p.split[3], prow, p.split_ld[1], BROWS);
-  constexpr size_t smem = CL == 3 ? tck::Pair::SMEM_BYTES : CL == 4 ? tck::Epi::SMEM_BYTES : tck::Cfg<BNT>::SMEM_BYTES;
+  constexpr size_t smem = CL == 3   ? tck::Pair::SMEM_BYTES
+                          : CL == 6 ? tck::PairT<true>::SMEM_BYTES
+                          : CL == 4 ? tck::Epi::SMEM_BYTES
+                                    : tck::Cfg<BNT>::SMEM_BYTES;
   auto kern = tck_trail_kernel<BNT, CL>;
   set_smem(kern, smem);
   const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, num_sms()) : num_sms();
   tck::CMaps cmaps;
   std::memset(&cmaps, 0, sizeof(cmaps));
-  if constexpr (CL == 4) {  // the TMA epilogue's C maps: each local shard as (rows, its columns)
+  if constexpr (CL == 4 || CL == 6) {  // the TMA epilogue's C maps: each local shard as (rows, its columns)
     static const int mode = [] {
       const char* e = getenv("BCMG_EPI_MODE");
       return e && *e ? atoi(e) : 0;
@@ -902,20 +905,31 @@ static bool tck_unit2() {
   return v;
 }
 
+// BCMG_TCK_PAIR_EPI: the two-column 2-SM pair items of BCMG_TCK_UNIT2 with the
+// TMA read-modify-write epilogue in 128-column halves (tck_loop_pair<true>)
+static int tck_pair_epi() {
+  static const int v = [] {
+    const char* e = getenv("BCMG_TCK_PAIR_EPI");
+    return e && *e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t st) {
-  const bool epi = tck_width(p.T) == 128 && p.T == 128 && p.N % p.T == 0 && tck_epi(p.cplx) && p.nloc <= MAX_LOCAL_DEV;
-  if (!epi && p.T == 128 && tck_unit2() && tck_cluster() == 2 && trail_band() > 0 && p.N % p.T == 0 &&
-      (p.nloc == 1 || p.nloc == p.D)) {
+  bool unit2 = false;  // at least two owned 128-wide tile columns, pair kernels usable
+  if (p.T == 128 && tck_cluster() == 2 && trail_band() > 0 && p.N % p.T == 0 && (p.nloc == 1 || p.nloc == p.D) &&
+      p.nloc <= MAX_LOCAL_DEV) {
     const int64_t sc = p.nloc == p.D ? 1 : p.D;
     int64_t cm = p.m_first;
     if (sc > 1) cm += ((p.dev0 - cm % p.D) + p.D) % p.D;
-    if (cm + sc < p.m_last) {  // at least two owned tile columns
-      TrailParams q = p;
-      q.cpu = 2;
-      return launch_tck_trail_t<256, 3>(q, info, st);
-    }
+    unit2 = cm + sc < p.m_last;
   }
+  TrailParams q = p;
+  q.cpu = 2;
+  if (unit2 && tck_pair_epi() > 0) return launch_tck_trail_t<256, 6>(q, info, st);
+  const bool epi = tck_width(p.T) == 128 && p.T == 128 && p.N % p.T == 0 && tck_epi(p.cplx) && p.nloc <= MAX_LOCAL_DEV;
   if (epi) return launch_tck_trail_t<128, 4>(p, info, st);
+  if (unit2 && tck_unit2()) return launch_tck_trail_t<256, 3>(q, info, st);
   if (tck_width(p.T) == 256) {
     const int c = tck_cluster();
     if (c == 2) return launch_tck_trail_t<256, 3>(p, info, st);

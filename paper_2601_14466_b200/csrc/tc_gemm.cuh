@@ -109,6 +109,8 @@ struct Blk {
   int b_row1 = -1;
   float* C2 = nullptr;
   int64_t skip2 = 0;
+  int cdev2 = 0;        // TMA epilogue: C2's local device and map column
+  int64_t ccol02 = 0;
 };
 
 template <class Next>

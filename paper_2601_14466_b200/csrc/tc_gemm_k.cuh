@@ -301,30 +301,56 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar_cluster) : "memory");
 }
 
-struct Pair {
+struct CMaps {
+  CUtensorMap m[MAX_LOCAL_DEV];  // per local device: its shard as (rows, columns), box {128, 128}
+  int mode;                      // EPI_PREFETCH | EPI_DIRECT (BCMG_EPI_MODE)
+};
+enum : int {
+  EPI_PREFETCH = 1,  // the producer prefetches an item's C tile into L2 when it starts the item's operands
+  EPI_DIRECT = 2,    // results stored straight from registers (coalesced 128 B per warp and column):
+                     // cbuf is free for the next item's C as soon as every warp has read it
+};
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(map), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+
+// EPI: the TMA read-modify-write epilogue (see tck_loop_epi) in two 128-column
+// halves per CTA through one 64 KB C buffer; two operand stages then fit.
+template <bool EPI = false>
+struct PairT {
   static constexpr int BN = 256;                      // output columns per tile (UMMA N)
   static constexpr int PA = BM * BK * 4;              // 16 KB: 128 A rows x 32 k
   static constexpr int PB = (BN / 2) * BK * 4;        // 16 KB: this CTA's 128 B rows
   static constexpr int STAGE_BYTES = 2 * (PA + PB);   // A hi, A lo, B hi, B lo
-  static constexpr int STAGES = 3;
+  static constexpr int STAGES = EPI ? 2 : 3;
+  static constexpr int CBUF = EPI ? BM * 128 * 4 : 0;  // one 128 x 128 C half
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+  static constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + CBUF + 256;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                     ((uint32_t)(256 >> 4) << 24);
 };
+using Pair = PairT<false>;
 
-template <class Next>
+template <bool EPI = false, class Next>
 __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUtensorMap* mAl, const CUtensorMap* mBh,
-                                              const CUtensorMap* mBl, int K, Next&& next) {
-  using P = Pair;
+                                              const CUtensorMap* mBl, const CMaps* cmaps, int K, Next&& next) {
+  using P = PairT<EPI>;
   constexpr int STAGES = P::STAGES, STAGE_BYTES = P::STAGE_BYTES, PA = P::PA, PB = P::PB, BN = P::BN;
   extern __shared__ __align__(1024) unsigned char tck_smem_raw[];
   unsigned char* base = tck_smem_raw + ((1024 - (smem_u32(tck_smem_raw) & 1023)) & 1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)STAGES * STAGE_BYTES);
+  float* cbuf = reinterpret_cast<float*>(base + (size_t)STAGES * STAGE_BYTES);  // EPI: 128 x 128, column-major
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)STAGES * STAGE_BYTES + P::CBUF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* cfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KT = (K + BK - 1) / BK;
   const int rank = (int)cluster_rank();
@@ -340,6 +366,7 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 16);  // leader: 8 epilogue warps of each CTA
     }
+    mbar_init(cfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {  // pair allocation: the same columns in both CTAs' TMEM
@@ -409,7 +436,86 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
         commit_pair(&tfull[b]);    // both CTAs' accumulator b ready
       }
     }
-  } else if (warp >= 4) {
+  } else if (EPI && warp >= 4) {
+    // ------------------------------------- TMA epilogue (8 warps, both CTAs)
+    // Each CTA updates its 128 rows of the item in two 128-column halves
+    // (h = 0: the item's first tile column; h = 1: columns 128.. or, for a
+    // two-column item, the second tile column C2), each through cbuf: the
+    // leader TMA-loads the half, the warps combine it with TMEM, the leader
+    // TMA-stores it and loads the next live half.  Halves whose rows lie
+    // outside the matrix or above C2's diagonal are skipped by both sides.
+    const int q = warp & 3, ch = (warp - 4) >> 2, row = 32 * q + lane;
+    const bool lead = warp == 4 && lane == 0;
+    const uint32_t te = mapa_u32(smem_u32(&tempty[0]), 0);
+    auto live = [&](const tc::Blk& bk, int h) {
+      const int64_t r0 = bk.m0 + rank * BM;
+      return r0 < bk.M && (h == 0 || (bk.C2 != nullptr && r0 >= bk.skip2));
+    };
+    auto coord = [&](const tc::Blk& bk, int h, int& dev, int& r, int& c) {
+      dev = h && bk.C2 ? bk.cdev2 : bk.cdev;
+      r = (int)(bk.crow0 + bk.m0 + rank * BM);
+      c = (int)(h && bk.C2 ? bk.ccol02 : bk.ccol0 + bk.n0 + h * 128);
+    };
+    auto load_half = [&](const tc::Blk& bk, int h) {
+      int dev, r, c;
+      coord(bk, h, dev, r, c);
+      mbar_expect_tx(cfull, P::CBUF);
+      tma_load_2d(cbuf, &cmaps->m[dev], r, c, cfull);
+    };
+    auto load_first = [&](const tc::Blk& bk) {
+      for (int h = 0; h < 2; ++h)
+        if (live(bk, h)) {
+          load_half(bk, h);
+          return;
+        }
+    };
+    uint32_t t = 0, nw = 0;
+    tc::Blk blk, nblk;
+    bool have = next(first, blk);
+    if (lead && have) load_first(blk);
+    for (int64_t item = first; have; item += stride, ++t) {
+      const int b = t & 1;
+      const bool more = next(item + stride, nblk);
+      mbar_wait(&tfull[b], (t >> 1) & 1);
+      tc::fence_after();
+      bool any = false;
+      for (int h = 0; h < 2; ++h) {
+        if (!live(blk, h)) continue;
+        any = true;
+        mbar_wait(cfull, nw & 1);
+        ++nw;
+#pragma unroll 1
+        for (int c0 = ch * 64; c0 < ch * 64 + 64; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + b * BN + h * 128 + c0, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float* cp = cbuf + row + (c0 + j) * BM;
+            *cp = blk.alpha * v[j] + blk.beta * *cp;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // cbuf writes -> the TMA store
+        asm volatile("bar.sync 1, 256;\n" ::: "memory");
+        if (lead) {
+          int dev, r, c;
+          coord(blk, h, dev, r, c);
+          tma_store_2d(&cmaps->m[dev], r, c, cbuf);
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // cbuf read by the store
+          if (h == 0 && live(blk, 1)) load_half(blk, 1);
+          else if (more) load_first(nblk);
+        }
+        __syncwarp();  // warp 4 reconverges before the next warp-collective tcgen05.ld
+      }
+      if (lead && !any && more) load_first(nblk);  // nothing of this item is ours: keep the chain going
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(te + 8 * b);  // TMEM accumulator b drained (both halves read)
+      have = more;
+      blk = nblk;
+    }
+    if (lead) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // stores complete before exit
+  } else if (!EPI && warp >= 4) {
     // ---------------------------------------------------------- epilogue (8 warps, both CTAs)
     const int q = warp & 3;
     const int ch = (warp - 4) >> 2;
@@ -485,15 +591,6 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
 // scalar loads of the default epilogue keep only ~32 KB in flight per SM and
 // leave HBM ~35 % busy at T_A = 128; the bulk copies keep a whole tile in
 // flight.  Two 64 KB operand stages + the C tile fill 192 KB.
-struct CMaps {
-  CUtensorMap m[MAX_LOCAL_DEV];  // per local device: its shard as (rows, columns), box {128, 128}
-  int mode;                      // EPI_PREFETCH | EPI_DIRECT (BCMG_EPI_MODE)
-};
-enum : int {
-  EPI_PREFETCH = 1,  // the producer prefetches an item's C tile into L2 when it starts the item's operands
-  EPI_DIRECT = 2,    // results stored straight from registers (coalesced 128 B per warp and column):
-                     // cbuf is free for the next item's C as soon as every warp has read it
-};
 struct Epi {
   static constexpr int BN = 128;
   static constexpr int PA = BM * BK * 4, PB = BN * BK * 4;  // 16 KB each
@@ -505,16 +602,6 @@ struct Epi {
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                     ((uint32_t)(BM >> 4) << 24);
 };
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(map), "r"(c0), "r"(c1)
-               : "memory");
-}
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map), "r"(c0),
-               "r"(c1), "r"(smem_u32(src))
-               : "memory");
-}
-
 template <class Next>
 __device__ __forceinline__ void tck_loop_epi(const CUtensorMap* mAh, const CUtensorMap* mAl, const CUtensorMap* mBh,
                                              const CUtensorMap* mBl, const CMaps* cmaps, int K, Next&& next) {
@@ -701,7 +788,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
     for (int e = 0; e < MAX_FAN; ++e) blk.fan[e] = e < fan.n ? fan.p[e] : nullptr;
     return true;
   };
-  if constexpr (CL == 3) tck::tck_loop_pair(&mAh, &mAl, &mBh, &mBl, (int)K, next);
+  if constexpr (CL == 3) tck::tck_loop_pair(&mAh, &mAl, &mBh, &mBl, nullptr, (int)K, next);
   else tck::tck_loop<BNT>(&mAh, &mAl, &mBh, &mBl, (int)K, next);
 }
 
@@ -713,7 +800,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
                      const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, TrailParams p,
                      const int* info, const __grid_constant__ tck::CMaps cmaps) {
   static_assert(CL != 4 || BNT == 128, "the TMA-epilogue tile is 128 x 128");
-  static_assert(CL != 3 || BNT == 256, "the 2-SM UMMA tile is 256 x 256");
+  static_assert((CL != 3 && CL != 6) || BNT == 256, "the 2-SM UMMA tile is 256 x 256");
   constexpr int64_t BMX = (CL == 1 || CL == 4 ? 1 : 2) * tc::BM;  // rows per item (a CTA pair covers 256)
   using TZ = TrapR<BMX, BNT>;
   using TZC = TrapR<BMX / 2, BNT>;
@@ -727,7 +814,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
   const int64_t sc = p.nloc == p.D ? 1 : p.D;
   const int64_t ncb = p.T > BNT ? p.T / BNT : 1;
   // CL = 3 at T_A = 128: a unit is two owned tile columns (c, c + sc), one 256-wide item
-  const int64_t cpu = CL == 3 && ncb == 1 && p.cpu > 1 ? p.cpu : 1, usp = cpu * sc;
+  const int64_t cpu = (CL == 3 || CL == 6) && ncb == 1 && p.cpu > 1 ? p.cpu : 1, usp = cpu * sc;
   if (p.band > 0 && sc > 1) cm += ((p.dev0 - cm % p.D) + p.D) % p.D;  // first owned column
   const int64_t nunits = ncb == 1 ? ((p.m_last - cm + sc - 1) / sc + cpu - 1) / cpu : (p.m_last - p.m_first) * ncb;
   const int64_t cm0 = cm;
@@ -794,6 +881,8 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
         blk.skip2 = cx * (c2 - c) * p.T;
         blk.b_row1 = (int)(c2 * p.T - p.prow0);
         blk.N = 2 * p.T;
+        blk.cdev2 = (int)(c2 % p.D) - p.dev0;
+        blk.ccol02 = (c2 / p.D) * p.T;
       }
       return true;
     }
@@ -847,7 +936,8 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
     return true;
   };
   const int Kx = (int)(p.cplx ? 2 * p.K : p.K);
-  if constexpr (CL == 3) tck::tck_loop_pair(&mAh, &mAl, &mBh, &mBl, Kx, next);
+  if constexpr (CL == 3) tck::tck_loop_pair(&mAh, &mAl, &mBh, &mBl, nullptr, Kx, next);
+  else if constexpr (CL == 6) tck::tck_loop_pair<true>(&mAh, &mAl, &mBh, &mBl, &cmaps, Kx, next);
   else if constexpr (CL == 4) tck::tck_loop_epi(&mAh, &mAl, &mBh, &mBl, &cmaps, Kx, next);
   else tck::tck_loop<BNT, CL>(&mAh, &mAl, &mBh, &mBl, Kx, next);
 }
