@@ -905,12 +905,16 @@ static bool tck_unit2() {
   return v;
 }
 
-// BCMG_TCK_PAIR_EPI: the two-column 2-SM pair items of BCMG_TCK_UNIT2 with the
-// TMA read-modify-write epilogue in 128-column halves (tck_loop_pair<true>)
+// BCMG_TCK_PAIR_EPI (default 1): at T_A = 128 the bulk update runs on the
+// two-column 2-SM pair items of BCMG_TCK_UNIT2 with the TMA read-modify-write
+// epilogue in 128-column halves (tck_loop_pair<true>).  Same bits.  N = 65536,
+// 8 devices: float32 118.8 -> 139.6 TFLOP/s (trailing update 652 -> 529 ms,
+// against the one-CTA TMA-epilogue kernel), complex64 176.7 -> 177.7 (against
+// the pair kernel's per-thread epilogue)
 static int tck_pair_epi() {
   static const int v = [] {
     const char* e = getenv("BCMG_TCK_PAIR_EPI");
-    return e && *e ? atoi(e) : 0;
+    return e && *e ? atoi(e) : 1;
   }();
   return v;
 }
