@@ -449,7 +449,9 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
     const uint32_t te = mapa_u32(smem_u32(&tempty[0]), 0);
     auto live = [&](const tc::Blk& bk, int h) {
       const int64_t r0 = bk.m0 + rank * BM;
-      return r0 < bk.M && (h == 0 || (bk.C2 != nullptr && r0 >= bk.skip2));
+      if (r0 >= bk.M) return false;
+      if (h == 0) return true;
+      return bk.C2 != nullptr ? r0 >= bk.skip2 : bk.n0 + 128 < bk.N;
     };
     auto coord = [&](const tc::Blk& bk, int h, int& dev, int& r, int& c) {
       dev = h && bk.C2 ? bk.cdev2 : bk.cdev;

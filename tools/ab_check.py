@@ -7,7 +7,8 @@ bit-identity and the max relative difference (must be within 10 N eps).
 import os, subprocess, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-CASES = ((2048, 128, 1, "f32"), (4096, 128, 2, "f32"), (3072, 128, 1, "c64"), (4096, 128, 8, "f32"), (2048, 256, 4, "c64"))
+CASES = ((2048, 128, 1, "f32"), (4096, 128, 2, "f32"), (3072, 128, 1, "c64"), (4096, 128, 8, "f32"), (2048, 256, 4, "c64"),
+         (3072, 256, 1, "f32"), (4096, 512, 2, "f32"), (4096, 1024, 1, "c64"))
 if len(sys.argv) > 1 and sys.argv[1] == "child":
     import paper_2601_14466_b200 as bc
     from oracle import bcmg_oracle as O
