@@ -507,7 +507,7 @@ __device__ __forceinline__ void tma_gemm_loop_v1(const CUtensorMap* mapA, const 
 }
 
 // Round-1 form of trail_tma_kernel (consumers decode their own items; kept for A/B
-// measurement, BCMG_TRAIL_V1=1).
+// measurement; the default, BCMG_TRAIL_VARIANT=1).
 template <class TL>
 __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
     trail_tma_kernel_v1(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TrailParams p,
