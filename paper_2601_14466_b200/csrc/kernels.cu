@@ -1479,6 +1479,260 @@ void diag_factor(int dt, void* A, int64_t lda, void* X, int64_t ldx, void* W, in
   zero_upper(dt, at(X, ldx, 0, n1), ldx, n1, n2, n1, st);
 }
 
+// ============================================================== substitution (small N_RHS)
+// Bandwidth kernels for the triangular sweeps of potrs when the right-hand
+// side is narrow (N_RHS <= 16): the split-K GEMM path pads N_RHS to its 16-wide
+// tile and runs ~7x (T_A = 1024) to ~27x (T_A = 128) above the HBM floor of
+// reading the factor twice.  Accumulation in double / double2; every sum has a
+// fixed order that depends on (n, T_A, k) only, so the bits do not depend on
+// the device or process count.
+template <bool CPLX> struct SubAcc { using T = double; };
+template <> struct SubAcc<true> { using T = double2; };
+__device__ __forceinline__ double sub_ld(float v) { return v; }
+__device__ __forceinline__ double sub_ld(double v) { return v; }
+__device__ __forceinline__ double2 sub_ld(float2 v) { return make_double2(v.x, v.y); }
+__device__ __forceinline__ double2 sub_ld(double2 v) { return v; }
+__device__ __forceinline__ double sub_conj(double v) { return v; }
+__device__ __forceinline__ double2 sub_conj(double2 v) { return make_double2(v.x, -v.y); }
+__device__ __forceinline__ double sub_fma(double acc, double a, double b) { return fma(a, b, acc); }
+__device__ __forceinline__ double2 sub_fma(double2 acc, double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
+}
+__device__ __forceinline__ double sub_add(double a, double b) { return a + b; }
+__device__ __forceinline__ double2 sub_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double sub_zero(double) { return 0.0; }
+__device__ __forceinline__ double2 sub_zero(double2) { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ double sub_shfl(double v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+__device__ __forceinline__ double2 sub_shfl(double2 v, int m) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
+}
+template <class S> __device__ __forceinline__ S sub_st(double v) { return (S)v; }
+template <class S> __device__ __forceinline__ S sub_st(double2 v) { return from_c<S>(v); }
+
+// Forward GEMV out[r, j] = (beta ? out[r, j] : 0) + alpha * sum_c A[r + c lda] y[c, j]
+// for r in [ncopy, rows); out[r, j] = y[r, j] for r < ncopy.  A CTA owns 32 rows
+// (one per lane); its W warps split the columns (contiguous ranges, loads
+// coalesced across the lanes, U in flight per lane) and their sums meet in
+// shared memory in warp order.  (128 rows per CTA with 4 rows per lane was
+// measured slower: fewer CTAs, fewer loads in flight.)
+template <class S, int NR>
+constexpr int subst_gemv_warps() { return 8; }
+template <class S, int NR>
+__global__ void __launch_bounds__(256) subst_gemv_kernel(const S* __restrict__ A, int64_t lda, const S* __restrict__ y,
+                                                         int64_t ldy, S* __restrict__ out, int64_t ldo, int64_t rows,
+                                                         int tc, int nrhs, int64_t ncopy, double alpha, int beta) {
+  using Acc = typename SubAcc<Traits<S>::cplx>::T;
+  constexpr int W = subst_gemv_warps<S, NR>();
+  __shared__ Acc red[W][32][NR];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * 32 + lane;
+  const bool live = r < rows && r >= ncopy;
+  Acc acc[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) acc[j] = sub_zero(Acc{});
+  const int cpw = (tc + W - 1) / W, c0 = warp * cpw, c1 = c0 + cpw < tc ? c0 + cpw : tc;
+  if (live) {
+    const S* a = A + r;
+    int c = c0;
+    constexpr int U = 8;  // column loads in flight per lane
+    for (; c + U <= c1; c += U) {
+      Acc av[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) av[u] = sub_ld(a[(int64_t)(c + u) * lda]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < NR; ++j)
+          if (j < nrhs) acc[j] = sub_fma(acc[j], av[u], sub_ld(__ldg(y + (c + u) + j * ldy)));
+    }
+    for (; c < c1; ++c) {
+      const Acc av = sub_ld(a[(int64_t)c * lda]);
+#pragma unroll
+      for (int j = 0; j < NR; ++j)
+        if (j < nrhs) acc[j] = sub_fma(acc[j], av, sub_ld(__ldg(y + c + j * ldy)));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NR; ++j) red[warp][lane][j] = acc[j];
+  __syncthreads();
+  if (warp != 0 || r >= rows) return;
+  if (r < ncopy) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+      if (j < nrhs) out[r + j * ldo] = y[r + j * ldy];
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    if (j >= nrhs) break;
+    Acc v = red[0][lane][j];
+    for (int w = 1; w < W; ++w) v = sub_add(v, red[w][lane][j]);
+    if constexpr (Traits<S>::cplx) v = make_double2(alpha * v.x, alpha * v.y);
+    else v = alpha * v;
+    if (beta) v = sub_add(v, sub_ld(out[r + j * ldo]));
+    out[r + j * ldo] = sub_st<S>(v);
+  }
+}
+
+// Backward partial sums P[chunk][c][j] = sum_{r in chunk} conj(L[r, c]) x[r, j]
+// over chunks of SUBST_CH rows.  Grid (chunk, column group): a CTA stages its
+// chunk of x in shared memory and its warps take the group's columns two at a
+// time (lanes stride the rows, coalesced; one fixed butterfly reduction per
+// sum), so the partial of (chunk, c) does not depend on the grid shape.
+constexpr int SUBST_CH = 512;
+template <class S, int NR>
+__global__ void __launch_bounds__(256) subst_partials_kernel(const S* __restrict__ L, int64_t ldl,
+                                                             const S* __restrict__ x, int64_t ldx, int64_t rows, int tc,
+                                                             int nrhs, int cpg, void* parts) {
+  using Acc = typename SubAcc<Traits<S>::cplx>::T;
+  constexpr int CH = SUBST_CH, PER = CH / 32;
+  extern __shared__ __align__(16) unsigned char subst_smem[];
+  Acc* xs = reinterpret_cast<Acc*>(subst_smem);  // [NR][CH]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * CH;
+  const int sn = (int)(rows - r0 < CH ? rows - r0 : CH);
+  for (int e = threadIdx.x; e < CH * NR; e += blockDim.x) {
+    const int r = e % CH, j = e / CH;
+    xs[j * CH + r] = (r < sn && j < nrhs) ? sub_ld(x[(r0 + r) + j * ldx]) : sub_zero(Acc{});
+  }
+  __syncthreads();
+  Acc* P = static_cast<Acc*>(parts) + (int64_t)blockIdx.x * tc * nrhs;
+  const int cb = blockIdx.y * cpg, ce = cb + cpg < tc ? cb + cpg : tc;
+  auto one = [&](const Acc* lv, int c) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      if (j >= nrhs) break;
+      Acc v = sub_zero(Acc{});
+#pragma unroll
+      for (int i = 0; i < PER; ++i) v = sub_fma(v, lv[i], xs[j * CH + lane + 32 * i]);
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) v = sub_add(v, sub_shfl(v, m));
+      if (lane == 0) P[(int64_t)c * nrhs + j] = v;
+    }
+  };
+  for (int c = cb + 2 * warp; c < ce; c += 2 * nw) {
+    const bool two = c + 1 < ce;
+    const S* l0 = L + (int64_t)c * ldl + r0;
+    const S* l1 = l0 + ldl;
+    Acc a0[PER], a1[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int r = lane + 32 * i;
+      a0[i] = r < sn ? sub_conj(sub_ld(l0[r])) : sub_zero(Acc{});
+      a1[i] = (two && r < sn) ? sub_conj(sub_ld(l1[r])) : sub_zero(Acc{});
+    }
+    one(a0, c);
+    if (two) one(a1, c + 1);
+  }
+}
+
+// mode 0: z[c, j] = x[c, j] - sum_p P[p][c][j];  mode 1: z[c, j] = sum_p P[p][c][j]
+// (p ascending); z has leading dimension ldz
+template <class S>
+__global__ void subst_reduce_kernel(const S* __restrict__ x, int64_t ldx, const void* parts, int np, int tc, int nrhs,
+                                    S* __restrict__ z, int64_t ldz, int mode) {
+  using Acc = typename SubAcc<Traits<S>::cplx>::T;
+  const Acc* P = static_cast<const Acc*>(parts);
+  const int64_t total = (int64_t)tc * nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / nrhs), j = (int)(e % nrhs);
+    Acc s = sub_zero(Acc{});
+#pragma unroll 8
+    for (int p = 0; p < np; ++p) s = sub_add(s, P[((int64_t)p * tc + c) * nrhs + j]);
+    if (mode == 0) {
+      Acc v = sub_ld(x[c + j * ldx]);
+      if constexpr (Traits<S>::cplx) s = make_double2(v.x - s.x, v.y - s.y);
+      else s = v - s;
+    }
+    z[c + j * ldz] = sub_st<S>(s);
+  }
+}
+
+bool subst_gemv_ok(int dt, int64_t nrhs) {
+  static const bool on = [] {
+    const char* e = getenv("BCMG_SUBST_GEMV");
+    return !(e && *e && atoi(e) == 0);
+  }();
+  // measured (tools/potrs_phase.py, N=65536, ms new / split-K): f32 T=128 N_RHS=1 29.9 / 73.8,
+  // T=1024 13.9 / 18.5, T=256 N_RHS=2 18.1 / 41.4; c64 21.9 / 38.1; c128 N_RHS=1 / 4 28.9 / 56.9,
+  // 37.8 / 57.0; f64 N_RHS=1 / 4 14.1 / 10.4, 16.8 / 10.5 -- float64 keeps the DMMA split-K GEMMs
+  return on && nrhs >= 1 && nrhs <= 4 && dt != R64;
+}
+size_t subst_parts_bytes(int64_t n, int64_t T, int64_t nrhs) {
+  return (size_t)((n + SUBST_CH - 1) / SUBST_CH + 1) * T * nrhs * 16 + (size_t)T * nrhs * 16;
+}
+
+static int subst_nr(int64_t nrhs) { return nrhs <= 1 ? 1 : nrhs <= 2 ? 2 : 4; }
+
+template <class S>
+static void launch_subst_gemv(int nr, const S* A, int64_t lda, const S* y, int64_t ldy, S* out, int64_t ldo,
+                              int64_t rows, int tc, int nrhs, int64_t ncopy, double alpha, int beta, cudaStream_t st) {
+  if (rows <= 0) return;
+  const unsigned grid = (unsigned)((rows + 31) / 32);
+  auto go = [&](auto kern, int warps) {
+    kern<<<grid, 32 * warps, 0, st>>>(A, lda, y, ldy, out, ldo, rows, tc, nrhs, ncopy, alpha, beta);
+  };
+  if (nr == 1) go(subst_gemv_kernel<S, 1>, subst_gemv_warps<S, 1>());
+  else if (nr == 2) go(subst_gemv_kernel<S, 2>, subst_gemv_warps<S, 2>());
+  else go(subst_gemv_kernel<S, 4>, subst_gemv_warps<S, 4>());
+  BCMG_CHECK_LAUNCH();
+}
+
+// P[chunk] over `rows` rows of L (ld ldl) against x; returns the chunk count
+template <class S>
+static int launch_subst_partials(int nr, const S* L, int64_t ldl, const S* x, int64_t ldx, int64_t rows, int tc,
+                                 int nrhs, void* parts, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  using Acc = typename SubAcc<Traits<S>::cplx>::T;
+  const int np = (int)((rows + SUBST_CH - 1) / SUBST_CH);
+  const size_t smem = (size_t)SUBST_CH * nr * sizeof(Acc);
+  // column groups of >= 16 columns so that the grid covers ~8 CTAs per SM
+  const int groups = (int)std::max<int64_t>(1, std::min<int64_t>((tc + 15) / 16, ((int64_t)num_sms() * 8 + np - 1) / np));
+  const int cpg = (tc + groups - 1) / groups;
+  auto go = [&](auto kern) {
+    set_smem(kern, smem);
+    kern<<<dim3((unsigned)np, (unsigned)((tc + cpg - 1) / cpg)), 256, smem, st>>>(L, ldl, x, ldx, rows, tc, nrhs, cpg,
+                                                                                 parts);
+  };
+  if (nr == 1) go(subst_partials_kernel<S, 1>);
+  else if (nr == 2) go(subst_partials_kernel<S, 2>);
+  else go(subst_partials_kernel<S, 4>);
+  BCMG_CHECK_LAUNCH();
+  return np;
+}
+
+// forward step: tmp = X_kk x_k; x_k = tmp; x[s0 + tc + r] -= L[tc + r, :] tmp
+void subst_fwd(int dt, int64_t rows, int64_t tc, int64_t nrhs, const void* Xkk, int64_t ldxk, const void* Lk,
+               int64_t ldl, void* xk, int64_t ldx, void* tmp, cudaStream_t st) {
+  const int nr = subst_nr(nrhs);
+  dispatch_dtype(dt, [&](auto s) {
+    using S = decltype(s);
+    launch_subst_gemv<S>(nr, static_cast<const S*>(Xkk), ldxk, static_cast<const S*>(xk), ldx, static_cast<S*>(tmp),
+                         tc, tc, (int)tc, (int)nrhs, 0, 1.0, 0, st);
+    launch_subst_gemv<S>(nr, static_cast<const S*>(Lk), ldl, static_cast<const S*>(tmp), tc, static_cast<S*>(xk), ldx,
+                         rows, (int)tc, (int)nrhs, tc, -1.0, 1, st);
+  });
+}
+
+// backward step: z = x_k - L[tc:, :]^H x[s0 + tc:]; x_k = X_kk^H z
+void subst_bwd(int dt, int64_t rows, int64_t tc, int64_t nrhs, const void* Xkk, int64_t ldxk, const void* Lk,
+               int64_t ldl, void* xk, int64_t ldx, void* parts, void* tmp, cudaStream_t st) {
+  const int nr = subst_nr(nrhs);
+  dispatch_dtype(dt, [&](auto s) {
+    using S = decltype(s);
+    const S* L = static_cast<const S*>(Lk);
+    S* x = static_cast<S*>(xk);
+    S* z = static_cast<S*>(tmp);
+    const int np = launch_subst_partials<S>(nr, L + tc, ldl, x + tc, ldx, rows - tc, (int)tc, (int)nrhs, parts, st);
+    subst_reduce_kernel<S><<<ew_grid(tc * nrhs), 256, 0, st>>>(x, ldx, parts, np, (int)tc, (int)nrhs, z, tc, 0);
+    BCMG_CHECK_LAUNCH();
+    const int nd = launch_subst_partials<S>(nr, static_cast<const S*>(Xkk), ldxk, z, tc, tc, (int)tc, (int)nrhs, parts,
+                                            st);
+    subst_reduce_kernel<S><<<ew_grid(tc * nrhs), 256, 0, st>>>(x, ldx, parts, nd, (int)tc, (int)nrhs, x, ldx, 1);
+    BCMG_CHECK_LAUNCH();
+  });
+}
+
 // ============================================================== elementwise helpers
 template <class S>
 __global__ void copy2d_kernel(const S* __restrict__ src, int64_t lds, S* __restrict__ dst, int64_t ldd, int64_t rows,

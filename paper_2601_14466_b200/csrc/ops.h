@@ -99,6 +99,16 @@ void ct_scatter(int dt, const void* src, int64_t lds, int64_t rows, int64_t cols
 void realify_diag(int dt, void* a, int64_t lda, int64_t n, cudaStream_t st);
 void mirror_diag(int dt, void* a, int64_t lda, int64_t n, cudaStream_t st);
 
+// potrs sweeps for N_RHS <= 4 (bandwidth kernels, fixed-order sums).  rows =
+// n - start_k; Lk = tile k's column block from row start_k (ld ldl); xk = x +
+// start_k.  parts: subst_parts_bytes(T, nrhs) (partials + a tile of z / tmp).
+bool subst_gemv_ok(int dt, int64_t nrhs);
+size_t subst_parts_bytes(int64_t n, int64_t T, int64_t nrhs);
+void subst_fwd(int dt, int64_t rows, int64_t tc, int64_t nrhs, const void* Xkk, int64_t ldxk, const void* Lk,
+               int64_t ldl, void* xk, int64_t ldx, void* tmp, cudaStream_t st);
+void subst_bwd(int dt, int64_t rows, int64_t tc, int64_t nrhs, const void* Xkk, int64_t ldxk, const void* Lk,
+               int64_t ldl, void* xk, int64_t ldx, void* parts, void* tmp, cudaStream_t st);
+
 // Split-K deterministic reduction: dst = beta*dst + alpha*sum_s part[s] (fixed order).
 void reduce_parts(int dt, const void* parts, int64_t part_stride, int nparts, void* dst, int64_t ldd, int64_t rows,
                   int64_t cols, double alpha, cudaStream_t st, double beta = 1.0);

@@ -612,7 +612,7 @@ WsPlan workspace_plan(int routine, int dt, int64_t n, int64_t T, int ndev, int w
   w.wdiag = (size_t)T * T * esz;
   w.info = sizeof(int);
   if (routine == 1) {  // potrs: split-K slabs + (multi-process) the solution hand-off buffer
-    const size_t parts_bytes = (size_t)64 * T * nrhs * esz;
+    const size_t parts_bytes = std::max((size_t)64 * T * nrhs * esz, subst_gemv_ok(dt, nrhs) ? subst_parts_bytes(n, T, nrhs) : 0);
     w.tmp = std::max<size_t>(4096, parts_bytes + (world > 1 ? (size_t)n * nrhs * esz : 0));
     if (dt == R32)  // forward substitution x[stop:] -= L x_k when the split-K slabs do not fit
       for (int64_t k = 0; k < nt; ++k) {
@@ -1139,7 +1139,8 @@ void Session::potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* 
                         "(same shards, order, element type, tile width and device count)");
   // split-K slabs (fixed count per shape: bits independent of the device count)
   const int64_t max_parts = 64;
-  const size_t parts_bytes = (size_t)max_parts * T * nrhs * g.esz;
+  const bool fast = subst_gemv_ok(dt, nrhs);  // bandwidth kernels for narrow right-hand sides
+  const size_t parts_bytes = std::max((size_t)max_parts * T * nrhs * g.esz, fast ? subst_parts_bytes(n, T, nrhs) : 0);
   const size_t pack_bytes = world > 1 ? (size_t)n * nrhs * g.esz : 0;
   tmp.ensure(std::max<size_t>(4096, parts_bytes + pack_bytes));
   char* parts = static_cast<char*>(tmp.p);
@@ -1161,6 +1162,14 @@ void Session::potrs(int dt, int64_t n, int64_t nrhs, int64_t T, int ndev, void* 
       continue;
     }
     void* sh = shards[(k % g.D) - g.dev0];
+    if (fast) {
+      char* tmpz = parts + subst_parts_bytes(n, T, nrhs) - (size_t)T * nrhs * 16;
+      if (op.kind == S_FWD)
+        subst_fwd(dt, n - s0, tc, nrhs, dinv_k(k), T, colp(sh, g, s0, g.loc(k)), n, xrow(s0), ldx, tmpz, st);
+      else
+        subst_bwd(dt, n - s0, tc, nrhs, dinv_k(k), T, colp(sh, g, s0, g.loc(k)), n, xrow(s0), ldx, parts, tmpz, st);
+      continue;
+    }
     if (op.kind == S_FWD) {
       // x_k <- X_kk x_k: split-K straight into x_k (the slabs hold the product)
       const int npd = gemm_splitk(dt, tc, nrhs, tc, opA(dinv_k(k), T, OP_N), opB(xrow(s0), ldx, OP_N), parts,
