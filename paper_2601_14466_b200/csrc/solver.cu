@@ -60,6 +60,7 @@ Session::Session(int device_, int rank_, int world_, const unsigned char* nccl_i
   BCMG_CUDA(cudaStreamCreateWithPriority(&crit, cudaStreamNonBlocking, hi));
   BCMG_CUDA(cudaStreamCreateWithPriority(&bulk, cudaStreamNonBlocking, lo));
   BCMG_CUDA(cudaStreamCreateWithPriority(&comm, cudaStreamNonBlocking, hi));
+  BCMG_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
   for (auto& e : ev_pool) BCMG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : ev_time) BCMG_CUDA(cudaEventCreate(&e));
   BCMG_CUDA(cudaMallocHost(&info_host, sizeof(int)));
@@ -89,7 +90,7 @@ Session::~Session() {
     }
   for (auto& e : ev_spare) cudaEventDestroy(e);
   if (info_host) cudaFreeHost(info_host);
-  for (cudaStream_t st : {crit, bulk, comm}) {
+  for (cudaStream_t st : {crit, bulk, comm, side}) {
     release_split_scratch(st);
     cudaStreamDestroy(st);
   }
@@ -139,15 +140,15 @@ void Session::begin(cudaStream_t user_stream) {
   user = user_stream;
   BCMG_CUDA(cudaSetDevice(device));
   BCMG_CUDA(cudaEventRecord(ev(kJoin + 4), user));
-  for (cudaStream_t s : {crit, bulk, comm}) BCMG_CUDA(cudaStreamWaitEvent(s, ev(kJoin + 4), 0));
+  for (cudaStream_t s : {crit, bulk, comm, side}) BCMG_CUDA(cudaStreamWaitEvent(s, ev(kJoin + 4), 0));
 }
 
 void Session::join() {
   // user stream waits for every internal stream
   int i = 0;
-  for (cudaStream_t s : {crit, bulk, comm}) {
-    BCMG_CUDA(cudaEventRecord(ev(kJoin + i), s));
-    BCMG_CUDA(cudaStreamWaitEvent(user, ev(kJoin + i), 0));
+  for (cudaStream_t s : {crit, bulk, comm, side}) {
+    BCMG_CUDA(cudaEventRecord(ev(kJoin + (i < 3 ? i : 5)), s));
+    BCMG_CUDA(cudaStreamWaitEvent(user, ev(kJoin + (i < 3 ? i : 5)), 0));
     ++i;
   }
 }
@@ -1014,7 +1015,8 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
   //   R[k]    panel k usable on this process     C[k] broadcast of panel k done
   //   B[k]    bulk update + copy-back of step k  U[k] lookahead update of step k
   //   FREE[k] panel buffer k%2 reusable
-  enum { R = 0, C = 1, B = 2, U = 3, FREE = 4 };
+  //   CB[k]   copy-back of panel k into A done (side stream, copy engine)
+  enum { R = 0, C = 1, B = 2, U = 3, FREE = 4, CB = 5 };
   auto E = [&](int type, int64_t k) { return ev(type * 8 + (int)(k % 8)); };
   for (const SchedOp& op : potrf_schedule(n, T, ndev, world, rank)) {
     if (op.k < k0) continue;  // factored left-looking during a streamed upload
@@ -1022,8 +1024,9 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
     const bool mine = g.owns(k);
     const int b = (int)(k % 2);
     switch (op.kind) {
-      case S_FACTOR:  // F(k) overwrites panel buffer k%2, last used by panel k-2
+      case S_FACTOR:  // F(k) overwrites panel buffer k%2, last used by panel k-2 (and its copy-back)
         if (k >= 2) BCMG_CUDA(cudaStreamWaitEvent(crit, E(FREE, k - 2), 0));
+        if (k >= 2 && g.owns(k - 2) && k - 2 >= k0) BCMG_CUDA(cudaStreamWaitEvent(crit, E(CB, k - 2), 0));
         if (bc_mode == BC_FAN && s1 < n) wait_peers_free(k, crit);
         factor(k);
         if (bc_mode == BC_FAN && s1 < n) {  // panel k is in every peer's buffer: raise their ready flags
@@ -1088,8 +1091,14 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
         }
         break;
       case S_COPYBACK:  // factor below the diagonal back into A (potrs/potri read it there)
-        copy2d(dt, panel[b].p, n - s1, colp(shard_of(k), g, s1, g.loc(k)), n, n - s1, s1 - g.start(k), false, info,
-               bulk);
+        // on the copy engines, off the bulk stream: nothing in potrf reads it, and
+        // between two bulk launches it was part of the gap the critical path sees
+        BCMG_CUDA(cudaStreamWaitEvent(side, E(R, k), 0));
+        if (s1 < n)
+          BCMG_CUDA(cudaMemcpy2DAsync(colp(shard_of(k), g, s1, g.loc(k)), (size_t)n * g.esz, panel[b].p,
+                                      (size_t)(n - s1) * g.esz, (size_t)(n - s1) * g.esz, (size_t)(s1 - g.start(k)),
+                                      cudaMemcpyDeviceToDevice, side));
+        BCMG_CUDA(cudaEventRecord(E(CB, k), side));
         break;
       case S_STEP_END:  // panel buffer k%2 reusable once bulk(k), U(k) and the broadcast are done
         BCMG_CUDA(cudaEventRecord(E(B, k), bulk));

@@ -71,6 +71,7 @@ struct Session {
   int device, rank, world;
   std::unique_ptr<Comm> net;  // world > 1: NCCL or in-process loopback transport
   cudaStream_t crit = nullptr, bulk = nullptr, comm = nullptr, user = nullptr;
+  cudaStream_t side = nullptr;  // copy-engine work off the critical path (potrf copy-back)
   static constexpr int kEvents = 64, kJoin = 56, kTimeEvents = 5;
   cudaEvent_t ev_pool[kEvents];
   cudaEvent_t ev_time[kTimeEvents];
