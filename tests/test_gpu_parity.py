@@ -406,3 +406,25 @@ def test_out_of_memory_before_any_data_movement(meshes):
     a = O.make_matrix("random_spd", 64, np.float64, 1)
     xs, _ = bc.solve_positive_definite(mesh, a, np.ones((64, 1)), bc.TileSpec(16))
     assert O.solve_residual(a, xs, np.ones((64, 1))) <= 100 * 64 * O.eps_of(np.float64)
+
+
+@pytest.mark.parametrize("dtype", ALL_DTYPES)
+@pytest.mark.parametrize("nrhs", [1, 2, 3, 4, 5])
+def test_potrs_narrow_rhs_sweeps(meshes, dtype, nrhs):
+    """The substitution's bandwidth kernels (N_RHS <= 4, not float64) and the
+    split-K path (N_RHS = 5, float64): ragged n, chunks of 512 rows crossed,
+    against the unblocked oracle, and the same bits for D = 1 and 3."""
+    n, t = 1100, 96
+    a = O.make_matrix("random_spd", n, dtype, 30 + nrhs)
+    rng = np.random.default_rng(nrhs)
+    b = rng.standard_normal((n, nrhs))
+    if np.iscomplexobj(np.zeros(1, dtype)):
+        b = b + 1j * rng.standard_normal((n, nrhs))
+    b = np.asfortranarray(b.astype(dtype))
+    xr = O.solve_unblocked(a, b)
+    eps = O.eps_of(dtype)
+    base, _ = bc.solve_positive_definite(meshes(1), a, b, bc.TileSpec(t))
+    assert np.abs(base - xr).max() <= 10 * n * eps * max(1.0, np.abs(xr).max())
+    assert O.solve_residual(a, base, b) <= 100 * n * eps
+    x3, _ = bc.solve_positive_definite(meshes(3), a, b, bc.TileSpec(t))
+    assert np.array_equal(x3, base)
