@@ -15,7 +15,7 @@ mesh = bc.make_mesh(1)
 st = torch.cuda.current_stream()
 for name, code, dt in (("f64", 1, torch.float64), ("f32", 0, torch.float32), ("c64", 2, torch.complex64),
                        ("c128", 3, torch.complex128)):
-    for t in (256, 512, 1024, 2048):
+    for t in [int(v) for v in os.environ.get("DIAG_TILES", "256,512,1024,2048").split(",")]:
         A0 = torch.empty(t, t, dtype=dt, device="cuda")
         _lib.check(lib.bcmg_generate_spd(C.c_void_p(st.cuda_stream), code, t, 0, t, C.c_void_p(A0.data_ptr()), t, 3,
                                          float(t)))
