@@ -181,6 +181,18 @@ int gemm_splitk(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const
   return np;
 }
 
+// The kernel choice of gemm() depends on N (the tcgen05 path needs N >= 64).
+// potri's per-device products have N = that device's columns, so the same
+// block would take different kernels (different bits) at different device
+// counts; this variant decides from M and K only.
+void gemm_shape_fixed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+                      const int* info, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return;
+  if (dt == R32 && use_tc() && use_presplit() && !A.mask && !B.mask && aligned16(ep.C) && M >= 256 && K >= 32)
+    return gemm_tck_generic(M, N, K, A, B, ep, info, st);
+  gemm(dt, M, N, K, A, B, ep, info, st);
+}
+
 void gemm(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
           const int* info, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
@@ -463,7 +475,8 @@ bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, 
   if (M <= 0 || N <= 0 || K <= 0 || N % align || (2 * M) % align || !aligned16(ep.C) || !aligned16(scratch))
     return false;
   if (scratch_bytes < gemm_cplx_embed_bytes(dt, M, N, K)) return false;
-  if (dt == C64 && (2 * M < 256 || N < 64)) return false;  // the tcgen05 tile's minimum shape
+  // the tcgen05 tile's minimum shape (N only when the caller allows a shape-dependent choice)
+  if (dt == C64 && (2 * M < 256 || (!always && N < 64))) return false;
   if (dt == C64 && ep.nfan && !use_presplit()) return false;  // the inline-split kernel has no fan-out
   // enough real blocks to fill the GPU (smaller GEMMs stay on the complex kernels), unless
   // the caller needs a shape-independent choice (bit-identical results across device counts)

@@ -21,6 +21,9 @@ void generate_spd(int dt, void* p, int64_t ld, int64_t n, int64_t row0, int64_t 
 
 // C := alpha*op(A)*op(B) + beta*C, any dtype (dt), any shape; dispatches to
 // the cp.async DMMA kernel when the operands qualify, else the REG kernel.
+// gemm() with a kernel choice that does not depend on N (device-count invariant bits)
+void gemm_shape_fixed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
+                      const int* info, cudaStream_t st);
 void gemm(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, const Operand& B, const Epilogue& ep,
           const int* info, cudaStream_t st);
 

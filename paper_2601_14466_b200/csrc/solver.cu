@@ -1339,7 +1339,7 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
           const Operand wa = opA(W, ldw, OP_N), lb = opB(stage, c, OP_C);
           const Epilogue ep{sh, n, 1.0, 1.0, 0, 0};
           if (!(emb && gemm_cplx_embed(dt, n - ss, c, tcs, wa, lb, ep, embed_buf.p, emb_bytes, nullptr, st, true)))
-            gemm(dt, n - ss, c, tcs, wa, lb, ep, nullptr, st);
+            gemm_shape_fixed(dt, n - ss, c, tcs, wa, lb, ep, nullptr, st);
         }
         break;
       }
@@ -1382,15 +1382,15 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
                                      Epilogue{blk + c0 * tcs * g.esz, tcs, 1.0, 0.0, 0, 0}, embed_buf.p,
                                      emb_bytes, nullptr, st, true);
               if (!done && c0 > 0) {  // finish the remaining columns on the complex kernels
-                gemm(dt, tcs, c - c0, n - ss, wh, opB(sh + c0 * n * g.esz, n, OP_N),
-                     Epilogue{blk + c0 * tcs * g.esz, tcs, 1.0, 0.0, 0, 0}, nullptr, st);
+                gemm_shape_fixed(dt, tcs, c - c0, n - ss, wh, opB(sh + c0 * n * g.esz, n, OP_N),
+                                 Epilogue{blk + c0 * tcs * g.esz, tcs, 1.0, 0.0, 0, 0}, nullptr, st);
                 done = true;
                 break;
               }
             }
             if (done) continue;
           }
-          gemm(dt, tcs, c, n - ss, wh, opB(sh, n, OP_N), Epilogue{blk, tcs, 1.0, 0.0, 0, 0}, nullptr, st);
+          gemm_shape_fixed(dt, tcs, c, n - ss, wh, opB(sh, n, OP_N), Epilogue{blk, tcs, 1.0, 0.0, 0, 0}, nullptr, st);
         }
         // written back only after every GEMM: with one process W_s is read from tile s itself
         for (int d = g.dev0; d < g.dev0 + g.nloc; ++d) {

@@ -428,3 +428,17 @@ def test_potrs_narrow_rhs_sweeps(meshes, dtype, nrhs):
     assert O.solve_residual(a, base, b) <= 100 * n * eps
     x3, _ = bc.solve_positive_definite(meshes(3), a, b, bc.TileSpec(t))
     assert np.array_equal(x3, base)
+
+
+@pytest.mark.parametrize("dtype", ALL_DTYPES)
+def test_potri_device_count_bit_exact_ragged(meshes, dtype):
+    """potri bits do not depend on D for every dtype, with a ragged last tile
+    and devices whose column counts fall under the tcgen05 tile width (found
+    by tools/stress.py: float32 n=649, T_A=64, D=2)."""
+    n, t = 649, 64
+    a = O.make_matrix("random_spd", n, dtype, 1172)
+    base, _ = bc.invert_positive_definite(meshes(1), a, bc.TileSpec(t))
+    assert O.inverse_residual(a, base) <= 100 * n * O.eps_of(dtype)
+    for d in (2, 3, 8):
+        inv, _ = bc.invert_positive_definite(meshes(d), a, bc.TileSpec(t))
+        assert np.array_equal(inv, base), d
