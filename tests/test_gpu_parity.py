@@ -442,3 +442,18 @@ def test_potri_device_count_bit_exact_ragged(meshes, dtype):
     for d in (2, 3, 8):
         inv, _ = bc.invert_positive_definite(meshes(d), a, bc.TileSpec(t))
         assert np.array_equal(inv, base), d
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.complex64])
+def test_potrs_device_count_bit_exact_odd_n_wide_tile(meshes, dtype):
+    """Odd n puts later devices' shards at 4-byte offsets of the flat buffer;
+    the diagonal factor's GEMMs must not pick a different kernel for them
+    (found by tools/stress.py: float32 n=1441, T_A=512, D=2)."""
+    n, t = 1441, 512
+    a = O.make_matrix("random_spd", n, dtype, 77)
+    b = np.asfortranarray(np.ones((n, 2), dtype=dtype))
+    base, _ = bc.solve_positive_definite(meshes(1), a, b, bc.TileSpec(t))
+    assert O.solve_residual(a, base, b) <= 100 * n * O.eps_of(dtype)
+    for d in (2, 3):
+        x, _ = bc.solve_positive_definite(meshes(d), a, b, bc.TileSpec(t))
+        assert np.array_equal(x, base), d

@@ -15,6 +15,10 @@ from oracle import bcmg_oracle as O  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--cases", type=int, default=200)
 ap.add_argument("--seed", type=int, default=1)
+ap.add_argument("--dtypes", default="f32,f64,c64,c128")
+ap.add_argument("--tiles", default="16,32,48,64,96,128,192,256,384,512")
+ap.add_argument("--nmax", type=int, default=3000)
+ap.add_argument("--dcheck", type=int, default=4, help="check D-invariance on every k-th case")
 a = ap.parse_args()
 rng = np.random.default_rng(a.seed)
 meshes = {}
@@ -22,12 +26,14 @@ def mesh(d):
     if d not in meshes:
         meshes[d] = bc.make_mesh(d)
     return meshes[d]
-dtypes = [np.float32, np.float64, np.complex64, np.complex128]
+dtypes = [{"f32": np.float32, "f64": np.float64, "c64": np.complex64, "c128": np.complex128}[x]
+          for x in a.dtypes.split(",")]
+tiles = [int(x) for x in a.tiles.split(",")]
 fails, done = 0, 0
 for i in range(a.cases):
-    dt = dtypes[rng.integers(4)]
-    n = int(rng.integers(65, 3001))
-    t = int(rng.choice([16, 32, 48, 64, 96, 128, 192, 256, 384, 512]))
+    dt = dtypes[rng.integers(len(dtypes))]
+    n = int(rng.integers(65, a.nmax + 1))
+    t = int(rng.choice(tiles))
     t = min(t, n)
     d = int(rng.choice([1, 2, 3, 4, 8]))
     routine = "potri" if rng.random() < 0.25 else "potrs"
@@ -46,7 +52,7 @@ for i in range(a.cases):
             err = float(np.abs(x - xr).max() / max(1.0, np.abs(xr).max()))
             res = float(O.solve_residual(A, x, b))
             ok = err <= 10 * n * eps and res <= 100 * n * eps
-            if ok and i % 4 == 0:
+            if ok and i % a.dcheck == 0:
                 x1, _ = bc.solve_positive_definite(mesh(1), A, b, bc.TileSpec(t))
                 ok = np.array_equal(x1, x)
                 case["d_invariant"] = bool(ok)
@@ -55,7 +61,7 @@ for i in range(a.cases):
             res = float(O.inverse_residual(A, inv))
             err = None
             ok = res <= 100 * n * eps and np.array_equal(inv, inv.conj().T)
-            if ok and i % 4 == 0:
+            if ok and i % a.dcheck == 0:
                 inv1, _ = bc.invert_positive_definite(mesh(1), A, bc.TileSpec(t))
                 ok = np.array_equal(inv1, inv)
                 case["d_invariant"] = bool(ok)
