@@ -885,7 +885,10 @@ int Session::potrf(int dt, int64_t n, int64_t T, int ndev, void* const* shards, 
   if (const char* e = getenv("BCMG_RESERVE_SMS"); e && *e) reserve_fixed = std::max(0, atoi(e));
   auto reserve_at = [&](int64_t k) {
     if (reserve_fixed >= 0) return reserve_fixed;
-    if (presplit) return 2;
+    // complex64 at T_A >= 2048: the diagonal factor (7.4 ms per 2048 tile) needs more
+    // than 2 SMs to hide (N=65536, 8 devices, reserve 2 / 8 / 12: 189.4, 187.5 / 196.2,
+    // 197.4 / 193.1, 194.0 TFLOP/s; float32 flat, complex64 T_A=1024 -1 % at 8)
+    if (presplit) return dt == C64 && T >= 2048 ? 8 : 2;
     return (n - g.stop(k)) / T >= 32 ? 0 : 2;
   };
   // world > 1 with the NCCL broadcast: the NCCL kernels need SMs on every
