@@ -9,10 +9,13 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 CASES = ((2048, 128, 1, "f32"), (4096, 128, 2, "f32"), (3072, 128, 1, "c64"), (4096, 128, 8, "f32"), (2048, 256, 4, "c64"),
          (3072, 256, 1, "f32"), (4096, 512, 2, "f32"), (4096, 1024, 1, "c64"))
+if os.environ.get("AB_CASES") == "all":
+    CASES = CASES + ((1500, 64, 1, "f64"), (2100, 100, 3, "c128"), (1441, 512, 2, "f64"), (777, 60, 1, "f32"),
+                     (1000, 200, 1, "c64"))
 if len(sys.argv) > 1 and sys.argv[1] == "child":
     import paper_2601_14466_b200 as bc
     from oracle import bcmg_oracle as O
-    n, t, d, dt = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), {"f32": np.float32, "c64": np.complex64}[sys.argv[5]]
+    n, t, d, dt = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), {"f32": np.float32, "c64": np.complex64, "f64": np.float64, "c128": np.complex128}[sys.argv[5]]
     a = O.make_matrix("random_spd", n, dt, 3)
     b = np.ones((n, 2), dtype=dt, order="F")
     x, _ = bc.solve_positive_definite(bc.DeviceMesh(d), a, b, bc.TileSpec(t))
@@ -24,7 +27,7 @@ ok = True
 for n, t, d, dt in CASES:
     xs = []
     for v in (v0, v1):
-        f = f"/tmp/x_{v}.npy"
+        f = f"/tmp/ab_x_{(v0, v1).index(v)}.npy"
         r = subprocess.run([sys.executable, __file__, "child", str(n), str(t), str(d), dt, f],
                            env=dict(os.environ, **{var: v}), capture_output=True, text=True, timeout=300)
         print(n, t, d, dt, var, v, r.stdout.strip(), r.stderr[-300:])

@@ -42,23 +42,23 @@ mesh.close()
 if len(sys.argv) > 1 and sys.argv[1] == "--trace":  # per-kernel CUPTI trace of one f64 / c64 1024 tile
     mesh = bc.make_mesh(1)
     for name, code, dt in (("f64", 1, torch.float64), ("c64", 2, torch.complex64)):
-        t = 1024
-        A = torch.empty(t, t, dtype=dt, device="cuda")
-        _lib.check(lib.bcmg_generate_spd(C.c_void_p(st.cuda_stream), code, t, 0, t, C.c_void_p(A.data_ptr()), t, 3,
-                                         float(t)))
-        A0 = A.clone()
-        ptrs = (C.c_void_p * 1)(A.data_ptr())
-        info = C.c_int(0)
-        _lib.check(lib.bcmg_potrf(mesh.session, C.c_void_p(st.cuda_stream), code, t, t, 1, ptrs, C.byref(info)))
-        A.copy_(A0)
-        torch.cuda.synchronize()
-        with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
-            _lib.check(lib.bcmg_potrf(mesh.session, C.c_void_p(st.cuda_stream), code, t, t, 1, ptrs, C.byref(info)))
-            torch.cuda.synchronize()
-        evs = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA],
-                     key=lambda e: e.time_range.start)
-        t0 = evs[0].time_range.start
-        for e in evs:
-            print(json.dumps({"dtype": name, "kernel": e.name.split("(")[0][:80], "start_us": e.time_range.start - t0,
-                              "dur_us": e.time_range.end - e.time_range.start}))
+      for t in [int(v) for v in os.environ.get("TRACE_TILES", "1024").split(",")]:
+          A = torch.empty(t, t, dtype=dt, device="cuda")
+          _lib.check(lib.bcmg_generate_spd(C.c_void_p(st.cuda_stream), code, t, 0, t, C.c_void_p(A.data_ptr()), t, 3,
+                                           float(t)))
+          A0 = A.clone()
+          ptrs = (C.c_void_p * 1)(A.data_ptr())
+          info = C.c_int(0)
+          _lib.check(lib.bcmg_potrf(mesh.session, C.c_void_p(st.cuda_stream), code, t, t, 1, ptrs, C.byref(info)))
+          A.copy_(A0)
+          torch.cuda.synchronize()
+          with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+              _lib.check(lib.bcmg_potrf(mesh.session, C.c_void_p(st.cuda_stream), code, t, t, 1, ptrs, C.byref(info)))
+              torch.cuda.synchronize()
+          evs = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA],
+                       key=lambda e: e.time_range.start)
+          t0 = evs[0].time_range.start
+          for e in evs:
+              print(json.dumps({"dtype": name, "kernel": e.name.split("(")[0][:80], "start_us": e.time_range.start - t0,
+                                "dur_us": e.time_range.end - e.time_range.start}))
     mesh.close()
