@@ -1592,6 +1592,76 @@ __global__ void __launch_bounds__(256) subst_gemv_kernel(const S* __restrict__ A
   }
 }
 
+// float32, N_RHS = 1: the same GEMV with 4 consecutive rows per lane (one
+// 16-byte load per column: 512-byte runs per warp instead of 128), 128 rows
+// per CTA.  Same column split and warp-order sums as subst_gemv_kernel, so the
+// same bits; used when every column start is 16-byte aligned.
+#ifndef BCMG_NO_GEMV4
+#define BCMG_NO_GEMV4 0
+#endif
+__global__ void __launch_bounds__(256) subst_gemv4_kernel(const float* __restrict__ A, int64_t lda,
+                                                          const float* __restrict__ y, float* __restrict__ out,
+                                                          int64_t rows, int tc, int64_t ncopy, double alpha, int beta) {
+  constexpr int W = 8;
+  __shared__ double red[W][128];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = (int64_t)blockIdx.x * 128 + 4 * lane;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int cpw = (tc + W - 1) / W, c0 = warp * cpw, c1 = c0 + cpw < tc ? c0 + cpw : tc;
+  const bool full = r0 + 3 < rows;
+  if (r0 < rows) {
+    const float* a = A + r0;
+    int c = c0;
+    if (full) {
+      for (; c + 4 <= c1; c += 4) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(a + (int64_t)(c + u) * lda));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double yv = __ldg(y + c + u);
+          acc[0] = fma((double)v[u].x, yv, acc[0]);
+          acc[1] = fma((double)v[u].y, yv, acc[1]);
+          acc[2] = fma((double)v[u].z, yv, acc[2]);
+          acc[3] = fma((double)v[u].w, yv, acc[3]);
+        }
+      }
+      for (; c < c1; ++c) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(a + (int64_t)c * lda));
+        const double yv = __ldg(y + c);
+        acc[0] = fma((double)v.x, yv, acc[0]);
+        acc[1] = fma((double)v.y, yv, acc[1]);
+        acc[2] = fma((double)v.z, yv, acc[2]);
+        acc[3] = fma((double)v.w, yv, acc[3]);
+      }
+    } else {
+      for (; c < c1; ++c) {
+        const double yv = __ldg(y + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (r0 + i < rows) acc[i] = fma((double)a[(int64_t)c * lda + i], yv, acc[i]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) red[warp][4 * lane + i] = acc[i];
+  __syncthreads();
+  if (threadIdx.x >= 128) return;
+  const int e = threadIdx.x;
+  const int64_t r = (int64_t)blockIdx.x * 128 + e;
+  if (r >= rows) return;
+  if (r < ncopy) {
+    out[r] = y[r];
+    return;
+  }
+  double v = red[0][e];
+#pragma unroll
+  for (int w = 1; w < W; ++w) v += red[w][e];
+  v = alpha * v;
+  if (beta) v += (double)out[r];
+  out[r] = (float)v;
+}
+
 // Backward partial sums P[chunk][c][j] = sum_{r in chunk} conj(L[r, c]) x[r, j]
 // over chunks of SUBST_CH rows.  Grid (chunk, column group): a CTA stages its
 // chunk of x in shared memory and its warps take the group's columns two at a
@@ -1686,6 +1756,14 @@ template <class S>
 static void launch_subst_gemv(int nr, const S* A, int64_t lda, const S* y, int64_t ldy, S* out, int64_t ldo,
                               int64_t rows, int tc, int nrhs, int64_t ncopy, double alpha, int beta, cudaStream_t st) {
   if (rows <= 0) return;
+  if constexpr (std::is_same_v<S, float> && !BCMG_NO_GEMV4) {
+    if (nr == 1 && nrhs == 1 && lda % 4 == 0 && aligned16(A)) {
+      subst_gemv4_kernel<<<(unsigned)((rows + 127) / 128), 256, 0, st>>>(A, lda, y, out, rows, tc, ncopy, alpha,
+                                                                          beta);
+      BCMG_CHECK_LAUNCH();
+      return;
+    }
+  }
   const unsigned grid = (unsigned)((rows + 31) / 32);
   auto go = [&](auto kern, int warps) {
     kern<<<grid, 32 * warps, 0, st>>>(A, lda, y, ldy, out, ldo, rows, tc, nrhs, ncopy, alpha, beta);
