@@ -406,13 +406,13 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
 // Persistent producer/consumer loop.  `next_p(item, blk)` / `next_c(item, blk)`
 // fill the block of work item `item` (producer / consumer view; separate so
 // stateful cursors stay monotone) and return false when there is none.
-template <class TL, bool FAN = true, class NextP, class NextC>
+template <class TL, bool FAN = true, bool TBK = false, bool MB = false, class NextP, class NextC>
 __device__ __forceinline__ void tma_gemm_loop_v1(const CUtensorMap* mapA, const CUtensorMap* mapB, int K, NextP&& next_p,
                                               NextC&& next_c, long long stagger_ns = 0) {
   double* smem = reinterpret_cast<double*>(tma_dyn_smem);
   constexpr int NW = TL::THREADS / 32;
-  constexpr unsigned STAGE_BYTES = tma_stage_bytes<TL>();
-  constexpr int STAGE_WORDS = TL::BK * (TL::LDA + TL::LDB);
+  constexpr unsigned STAGE_BYTES = tma_stage_bytes<TL, TBK>();
+  constexpr int STAGE_WORDS = tma_stage_words<TL, TBK>();
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + TL::STAGES * STAGE_WORDS);
   uint64_t* empty = full + TL::STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -438,7 +438,7 @@ __device__ __forceinline__ void tma_gemm_loop_v1(const CUtensorMap* mapA, const 
     int kt, live;
   };
   static_assert(sizeof(Prod) <= 384, "producer state must fit its aux slot");
-  Prod& ps = *reinterpret_cast<Prod*>(tma_aux<TL>());
+  Prod& ps = *reinterpret_cast<Prod*>(tma_aux<TL, TBK>());
   auto produce_one = [&]() {
     if (!ps.live) return;
     const uint32_t gp = ps.gp;
@@ -447,7 +447,9 @@ __device__ __forceinline__ void tma_gemm_loop_v1(const CUtensorMap* mapA, const 
     double* st = smem + s * STAGE_WORDS;
     mbar_expect_tx(&full[s], STAGE_BYTES);
     tma_load_2d(st, mapA, ps.blk.a_row + (int)ps.blk.m0, kt * TL::BK, &full[s]);
-    tma_load_2d(st + TL::BK * TL::LDA, mapB, ps.blk.b_row + (int)ps.blk.n0, kt * TL::BK, &full[s]);
+    const CUtensorMap* mb = MB ? mapB + ps.blk.bmap : mapB;
+    if constexpr (TBK) tma_load_2d(st + TL::BK * TL::LDA, mb, kt * TL::BK, ps.blk.b_row + (int)ps.blk.n0, &full[s]);
+    else tma_load_2d(st + TL::BK * TL::LDA, mb, ps.blk.b_row + (int)ps.blk.n0, kt * TL::BK, &full[s]);
     ps.gp = gp + 1;
     if (kt + 1 == KT) {
       ps.kt = 0;
@@ -497,7 +499,8 @@ __device__ __forceinline__ void tma_gemm_loop_v1(const CUtensorMap* mapA, const 
       const int s = g % TL::STAGES;
       mbar_wait(&full[s], (g / TL::STAGES) & 1);
       const double* st = smem + s * STAGE_WORDS;
-      mma_slice<TL, false, false, false>(acc, st, st + TL::BK * TL::LDA, nullptr, nullptr, wm0, wn0, lane);
+      if constexpr (TBK) mma_slice_tbk<TL>(acc, st, st + TL::BK * TL::LDA, wm0, wn0, lane);
+      else mma_slice<TL, false, false, false>(acc, st, st + TL::BK * TL::LDA, nullptr, nullptr, wm0, wn0, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       ++g;
@@ -605,9 +608,10 @@ struct BMaps {
   static constexpr int MAX = 8;
   CUtensorMap m[MAX];
   int64_t col0[MAX + 1];  // output column of each group; col0[n] = total
+  char* cbase[MAX];       // nullptr: group g writes ep.C + col0[g] * ldc; else its own C
   int n;
 };
-template <class TL>
+template <class TL, bool TBK = true>
 __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
     gemm_tma_grouped_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ BMaps bm, int64_t M,
                             int64_t K, Epilogue ep, const int* info) {
@@ -626,14 +630,18 @@ __global__ void __launch_bounds__(TL::THREADS, min_blocks<TL>())
         blk.M = M;
         blk.N = ng;
         blk.ep = ep;
-        blk.ep.C = static_cast<char*>(ep.C) + bm.col0[g] * ep.ldc * 8;
+        blk.ep.C = bm.cbase[g] ? bm.cbase[g] : static_cast<char*>(ep.C) + bm.col0[g] * ep.ldc * 8;
         return true;
       }
       cb -= nbg;
     }
     return false;
   };
-  tma_gemm_loop<TL, true, false, true, true>(&mapA, &bm.m[0], (int)K, decode);
+  // i-contiguous B (potri's W sweep): the consumer-decoded loop of
+  // trail_tma_kernel_v1, 2.3 % faster there (10.86 vs 11.12 s at config 4);
+  // k-contiguous B (product sweep): the item ring, 1.7 % faster there
+  if constexpr (TBK) tma_gemm_loop<TL, true, false, true, true>(&mapA, &bm.m[0], (int)K, decode);
+  else tma_gemm_loop_v1<TL, false, false, true>(&mapA, &bm.m[0], (int)K, decode, decode);
 }
 
 }  // namespace bcmg

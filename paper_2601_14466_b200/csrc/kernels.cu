@@ -524,6 +524,55 @@ bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, 
   return true;
 }
 
+// complex128: C_g (+)= alpha A B_g^T for several groups sharing A, each with its
+// own C (potri's W sweep: one product per local device into its own shard).
+// A is gathered once as [A | -iA]; each B_g planar [Re B | -Im B]; ONE launch
+// of the multi-map TMA kernel.  Per element the same tile kernel, K order and
+// epilogue as gemm_cplx_embed, so the same bits.  False when a group would not
+// take the embedding on its own (the caller then runs the groups one by one).
+bool gemm_cplx_embed_multi(int dt, int64_t M, int64_t K, const Operand& A, const Operand* Bs, const int64_t* ncols,
+                           void* const* Cs, int ngroups, const Epilogue& ep, void* scratch, size_t scratch_bytes,
+                           cudaStream_t st) {
+  if (dt != C128 || getenv("BCMG_NO_CPLX_EMBED") || !use_tma() || A.mask || ep.lower_only || ep.nfan) return false;
+  if (ngroups < 1 || ngroups > BMaps::MAX || M <= 0 || K <= 0 || (2 * M) % 2 || !aligned16(scratch)) return false;
+  int64_t total = 0;
+  for (int i = 0; i < ngroups; ++i) {
+    if (Bs[i].mask || native_b(Bs[i]) || ncols[i] <= 0 || ncols[i] % 2 || !aligned16(Cs[i])) return false;
+    total += ncols[i];
+  }
+  if (scratch_bytes < gemm_cplx_embed_bytes(dt, M, total, K)) return false;
+  using TL = TileTrail2;
+  double2* at = static_cast<double2*>(scratch);              // M x 2K complex, ld M
+  double* xp = reinterpret_cast<double*>(at + 2 * M * K);    // per group: N_g x 2K real, ld N_g
+  embed_gather<double2, double>(A, M, K, at, nullptr, M, st);
+  BMaps bm;
+  std::memset(&bm, 0, sizeof(bm));
+  int64_t nblk = 0, off = 0;
+  for (int i = 0; i < ngroups; ++i) {
+    double* xg = xp + off;
+    embed_gather<double2, double>(Bs[i], ncols[i], K, nullptr, xg, ncols[i], st);
+    bm.m[i] = make_map(xg, ncols[i], 2 * K, ncols[i], TL::LDB, TL::BK);
+    bm.col0[i + 1] = bm.col0[i] + ncols[i];
+    bm.cbase[i] = static_cast<char*>(Cs[i]);
+    off += ncols[i] * 2 * K;
+    nblk += (ncols[i] + TL::BN - 1) / TL::BN;
+  }
+  bm.n = ngroups;
+  Epilogue er = ep;
+  er.ldc = 2 * ep.ldc;
+  const CUtensorMap ma = make_map(at, 2 * M, 2 * K, 2 * M, TL::LDA, TL::BK);
+  constexpr size_t smem = tma_smem_bytes<TL, false>();
+  auto kern = gemm_tma_grouped_kernel<TL, false>;
+  set_smem(kern, smem);
+  int per_sm = 1;
+  BCMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TL::THREADS, smem));
+  const int64_t blocks = ((2 * M + TL::BM - 1) / TL::BM) * nblk;
+  const int64_t grid = std::min<int64_t>(blocks, (int64_t)num_sms() * std::max(per_sm, 1));
+  kern<<<(unsigned)grid, TL::THREADS, smem, st>>>(ma, bm, 2 * M, 2 * K, er, nullptr);
+  BCMG_CHECK_LAUNCH();
+  return true;
+}
+
 bool gemm_cplx_embed_grouped(int dt, int64_t M, int64_t K, const Operand& A, const Operand* Bs, const int64_t* ncols,
                              int ngroups, const Epilogue& ep, void* scratch, size_t scratch_bytes, int64_t chunk,
                              cudaStream_t st) {
@@ -561,7 +610,7 @@ bool gemm_cplx_embed_grouped(int dt, int64_t M, int64_t K, const Operand& A, con
       er.ldc = 2 * ep.ldc;
       const CUtensorMap ma = make_map(at, 2 * M, 2 * K, 2 * M, TL::LDA, TL::BK);
       constexpr size_t smem = tma_smem_bytes<TL, true>();
-      auto kern = gemm_tma_grouped_kernel<TL>;
+      auto kern = gemm_tma_grouped_kernel<TL, true>;
       set_smem(kern, smem);
       int per_sm = 1;
       BCMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TL::THREADS, smem));

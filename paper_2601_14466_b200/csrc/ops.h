@@ -54,6 +54,9 @@ bool gemm_cplx_embed(int dt, int64_t M, int64_t N, int64_t K, const Operand& A, 
 // concatenated in ep.C (ld ep.ldc): A is gathered (and split) once, the
 // groups' columns chunk by chunk (`chunk` columns per GEMM; scratch >=
 // gemm_cplx_embed_bytes(dt, M, chunk, K)).  False: nothing launched.
+bool gemm_cplx_embed_multi(int dt, int64_t M, int64_t K, const Operand& A, const Operand* Bs, const int64_t* ncols,
+                           void* const* Cs, int ngroups, const Epilogue& ep, void* scratch, size_t scratch_bytes,
+                           cudaStream_t st);
 bool gemm_cplx_embed_grouped(int dt, int64_t M, int64_t K, const Operand& A, const Operand* Bs, const int64_t* ncols,
                              int ngroups, const Epilogue& ep, void* scratch, size_t scratch_bytes, int64_t chunk,
                              cudaStream_t st);

@@ -1331,18 +1331,36 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
       case S_WACC: {
         int64_t ldw = 0;
         const void* W = w_of(s, &ldw);
+        const Operand wa = opA(W, ldw, OP_N);
+        // L21_k rows [ss, se) of all k < s, staged per device as (L21 rows)^H (c x tcs, one
+        // region each) so that the GEMM's B operand is in natural orientation (TMA-eligible)
+        std::vector<Operand> bs;
+        std::vector<int64_t> nc_d;
+        std::vector<void*> cs;
+        int64_t soff = 0;
         for (int d = g.dev0; d < g.dev0 + g.nloc; ++d) {
           const int64_t c = cols_below(g, d, s);
           if (c == 0) continue;
           char* sh = colp(shards[d - g.dev0], g, ss, 0);
-          // L21_k rows [ss, se) of all k < s, staged as (L21 rows)^H (c x tcs) so that the
-          // GEMM's B operand is in natural orientation (TMA-eligible)
-          conj_transpose(dt, sh, n, stage, c, c, tcs, st);
+          char* sd = stage + soff * g.esz;
+          conj_transpose(dt, sh, n, sd, c, c, tcs, st);
           BCMG_CUDA(cudaMemset2DAsync(sh, n * g.esz, 0, tcs * g.esz, c, st));  // first touch of acc rows [ss, se)
-          const Operand wa = opA(W, ldw, OP_N), lb = opB(stage, c, OP_C);
-          const Epilogue ep{sh, n, 1.0, 1.0, 0, 0};
-          if (!(emb && gemm_cplx_embed(dt, n - ss, c, tcs, wa, lb, ep, embed_buf.p, emb_bytes, nullptr, st, true)))
-            gemm_shape_fixed(dt, n - ss, c, tcs, wa, lb, ep, nullptr, st);
+          bs.push_back(opB(sd, c, OP_C));
+          nc_d.push_back(c);
+          cs.push_back(sh);
+          soff += c * tcs;
+        }
+        const Epilogue ep{nullptr, n, 1.0, 1.0, 0, 0};
+        // complex128 with several local devices: W embedded once, one launch over every device's columns
+        if (emb && bs.size() > 1 &&
+            gemm_cplx_embed_multi(dt, n - ss, tcs, wa, bs.data(), nc_d.data(), cs.data(), (int)bs.size(), ep,
+                                  embed_buf.p, emb_bytes, st))
+          break;
+        for (size_t i = 0; i < bs.size(); ++i) {
+          Epilogue e = ep;
+          e.C = cs[i];
+          if (!(emb && gemm_cplx_embed(dt, n - ss, nc_d[i], tcs, wa, bs[i], e, embed_buf.p, emb_bytes, nullptr, st, true)))
+            gemm_shape_fixed(dt, n - ss, nc_d[i], tcs, wa, bs[i], e, nullptr, st);
         }
         break;
       }
