@@ -1351,8 +1351,9 @@ void Session::potri(int dt, int64_t n, int64_t T, int ndev, void* const* shards)
           soff += c * tcs;
         }
         const Epilogue ep{nullptr, n, 1.0, 1.0, 0, 0};
-        // complex128 with several local devices: W embedded once, one launch over every device's columns
-        if (emb && bs.size() > 1 &&
+        // complex128: W embedded once, one launch over every local device's columns (also the
+        // faster loop with one device)
+        if (emb && !bs.empty() &&
             gemm_cplx_embed_multi(dt, n - ss, tcs, wa, bs.data(), nc_d.data(), cs.data(), (int)bs.size(), ep,
                                   embed_buf.p, emb_bytes, st))
           break;
