@@ -856,7 +856,7 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   {
     const int band = trail_band();
     const int64_t rb = p.cplx ? BMX / 2 : BMX;
-    const int64_t cpu = (CL == 3 || CL == 6) && p.cpu > 1 ? p.cpu : 1;  // tile columns per unit
+    const int64_t cpu = (CL == 3 || CL == 6 || CL == 7) && p.cpu > 1 ? p.cpu : 1;  // tile columns per unit
     const bool cols = p.T <= BNT && (cpu * p.T) % rb == 0 && (p.nloc == 1 || p.nloc == p.D);
     const bool blocks = p.T > BNT && p.T % BNT == 0 && p.N % p.T == 0 && p.nloc == p.D;
     q.band = cols || blocks ? band : 0;
@@ -864,11 +864,12 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   const int64_t prow = p.N - p.prow0, arows = p.cplx ? 2 * prow : prow;
   const CUtensorMap ah = make_map_kmajor(p.split[0], arows, p.split_ld[0]);
   const CUtensorMap al = make_map_kmajor(p.split[1], arows, p.split_ld[0]);
-  constexpr int BROWS = (CL == 2 || CL == 3 || CL == 6) ? BNT / 2 : BNT;  // CTA pairs load half the B tile each
+  constexpr int BROWS = (CL == 2 || CL == 3 || CL == 6 || CL == 7) ? BNT / 2 : BNT;  // CTA pairs load half the B tile each
   const CUtensorMap bh = make_map_kmajor(p.split[2], prow, p.split_ld[1], BROWS);
   const CUtensorMap bl = make_map_kmajor(p.split[3], prow, p.split_ld[1], BROWS);
   constexpr size_t smem = CL == 3   ? tck::Pair::SMEM_BYTES
-                          : CL == 6 ? tck::PairT<true>::SMEM_BYTES
+                          : CL == 6 ? tck::PairT<1>::SMEM_BYTES
+                          : CL == 7 ? tck::PairT<2>::SMEM_BYTES
                           : CL == 4 ? tck::Epi::SMEM_BYTES
                                     : tck::Cfg<BNT>::SMEM_BYTES;
   auto kern = tck_trail_kernel<BNT, CL>;
@@ -876,7 +877,7 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
   const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, num_sms()) : num_sms();
   tck::CMaps cmaps;
   std::memset(&cmaps, 0, sizeof(cmaps));
-  if constexpr (CL == 4 || CL == 6) {  // the TMA epilogue's C maps: each local shard as (rows, its columns)
+  if constexpr (CL == 4 || CL == 6 || CL == 7) {  // the TMA epilogue's C maps: each local shard as (rows, its columns)
     static const int mode = [] {
       const char* e = getenv("BCMG_EPI_MODE");
       return e && *e ? atoi(e) : 0;
@@ -887,7 +888,7 @@ static void launch_tck_trail_t(const TrailParams& p, const int* info, cudaStream
     for (int i = 0; i < p.nloc; ++i) {
       cuuint64_t dims[2] = {(cuuint64_t)(cx * p.N), (cuuint64_t)counts[p.dev0 + i]};
       cuuint64_t strides[1] = {(cuuint64_t)(cx * p.N) * 4};
-      cuuint32_t box[2] = {(cuuint32_t)tc::BM, 128};
+      cuuint32_t box[2] = {(cuuint32_t)tc::BM, CL == 7 ? 64u : 128u};  // quarters / halves / tiles
       cuuint32_t es[2] = {1, 1};
       CUresult r = encode_fn()(&cmaps.m[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, p.shards[i], dims, strides, box, es,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -974,16 +975,18 @@ static bool tck_unit2() {
 
 // BCMG_TCK_PAIR_EPI (default 1): at T_A = 128 the bulk update runs on the
 // two-column 2-SM pair items of BCMG_TCK_UNIT2 with the TMA read-modify-write
-// epilogue in 128-column halves (tck_loop_pair<true>).  Same bits.  N = 65536,
+// epilogue in 128-column halves (tck_loop_pair<1>; 3: quarter ring, tck_loop_pair<2>).  Same bits.  N = 65536,
 // 8 devices: float32 118.8 -> 139.6 TFLOP/s (trailing update 652 -> 529 ms,
 // against the one-CTA TMA-epilogue kernel), complex64 176.7 -> 177.7 (against
 // the pair kernel's per-thread epilogue)
-static int tck_pair_epi() {
+// Unset: float32 the quarter ring (3), complex64 the halves (1) -- N=65536 T_A=128,
+// same box: f32 159.6 / 163.8, c64 196.1 / 195.6 TFLOP/s (halves / quarters).
+static int tck_pair_epi(bool cplx) {
   static const int v = [] {
     const char* e = getenv("BCMG_TCK_PAIR_EPI");
-    return e && *e ? atoi(e) : 1;
+    return e && *e ? atoi(e) : -1;
   }();
-  return v;
+  return v >= 0 ? v : cplx ? 1 : 3;
 }
 
 static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t st) {
@@ -997,14 +1000,15 @@ static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t
   }
   TrailParams q = p;
   q.cpu = 2;
-  if (unit2 && tck_pair_epi() > 0) return launch_tck_trail_t<256, 6>(q, info, st);
+  if (unit2 && tck_pair_epi(p.cplx) == 3) return launch_tck_trail_t<256, 7>(q, info, st);
+  if (unit2 && tck_pair_epi(p.cplx) > 0) return launch_tck_trail_t<256, 6>(q, info, st);
   const bool epi = tck_width(p.T) == 128 && p.T == 128 && p.N % p.T == 0 && tck_epi(p.cplx) && p.nloc <= MAX_LOCAL_DEV;
   if (epi) return launch_tck_trail_t<128, 4>(p, info, st);
   if (unit2 && tck_unit2()) return launch_tck_trail_t<256, 3>(q, info, st);
   if (tck_width(p.T) == 256) {
     const int c = tck_cluster();
     // whole 256-wide column blocks (T_A a multiple of 256): the TMA epilogue in halves
-    if (c == 2 && tck_pair_epi() > 1 && p.T % 256 == 0 && p.N % p.T == 0 && p.nloc <= MAX_LOCAL_DEV)
+    if (c == 2 && tck_pair_epi(p.cplx) == 2 && p.T % 256 == 0 && p.N % p.T == 0 && p.nloc <= MAX_LOCAL_DEV)
       return launch_tck_trail_t<256, 6>(p, info, st);
     if (c == 2) return launch_tck_trail_t<256, 3>(p, info, st);
     if (c == 1) return launch_tck_trail_t<256, 2>(p, info, st);

@@ -320,24 +320,27 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int
                : "memory");
 }
 
-// EPI: the TMA read-modify-write epilogue (see tck_loop_epi) in two 128-column
-// halves per CTA through one 64 KB C buffer; two operand stages then fit.
-template <bool EPI = false>
+// EPI: the TMA read-modify-write epilogue (see tck_loop_epi).  1: in two
+// 128-column halves per CTA through one 64 KB C buffer; 2: in 64-column
+// quarters through a ring of three 32 KB buffers, so up to three loads are in
+// flight while a quarter is combined and stored.  Two operand stages then fit.
+template <int EPI = 0>
 struct PairT {
   static constexpr int BN = 256;                      // output columns per tile (UMMA N)
   static constexpr int PA = BM * BK * 4;              // 16 KB: 128 A rows x 32 k
   static constexpr int PB = (BN / 2) * BK * 4;        // 16 KB: this CTA's 128 B rows
   static constexpr int STAGE_BYTES = 2 * (PA + PB);   // A hi, A lo, B hi, B lo
   static constexpr int STAGES = EPI ? 2 : 3;
-  static constexpr int CBUF = EPI ? BM * 128 * 4 : 0;  // one 128 x 128 C half
+  static constexpr int NCB = EPI == 2 ? 3 : 1;        // C buffers (and their barriers)
+  static constexpr int CBUF = EPI == 1 ? BM * 128 * 4 : EPI == 2 ? NCB * BM * 64 * 4 : 0;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + CBUF + 256;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                     ((uint32_t)(256 >> 4) << 24);
 };
-using Pair = PairT<false>;
+using Pair = PairT<0>;
 
-template <bool EPI = false, class Next>
+template <int EPI = 0, class Next>
 __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUtensorMap* mAl, const CUtensorMap* mBh,
                                               const CUtensorMap* mBl, const CMaps* cmaps, int K, Next&& next) {
   using P = PairT<EPI>;
@@ -350,7 +353,7 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* cfull = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + P::NCB);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KT = (K + BK - 1) / BK;
   const int rank = (int)cluster_rank();
@@ -366,7 +369,7 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 16);  // leader: 8 epilogue warps of each CTA
     }
-    mbar_init(cfull, 1);
+    for (int i = 0; i < P::NCB; ++i) mbar_init(&cfull[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {  // pair allocation: the same columns in both CTAs' TMEM
@@ -436,7 +439,96 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
         commit_pair(&tfull[b]);    // both CTAs' accumulator b ready
       }
     }
-  } else if (EPI && warp >= 4) {
+  } else if (EPI == 2 && warp >= 4) {
+    // ------------------------ TMA epilogue, quarter ring (8 warps, both CTAs)
+    // A CTA's 128 rows of an item in 64-column quarters (the live halves in
+    // order, two quarters each).  The leader keeps up to NB quarter loads in
+    // flight -- the rest of this item, then the next item's -- and refills a
+    // buffer as soon as its store has read it.
+    constexpr int NB = P::NCB, QF = BM * 64;
+    float* qb = cbuf;
+    const int q = warp & 3, ch = (warp - 4) >> 2, row = 32 * q + lane;
+    const bool lead = warp == 4 && lane == 0;
+    const uint32_t te = mapa_u32(smem_u32(&tempty[0]), 0);
+    auto live = [&](const tc::Blk& bk, int h) {
+      const int64_t r0 = bk.m0 + rank * BM;
+      if (r0 >= bk.M) return false;
+      if (h == 0) return true;
+      return bk.C2 != nullptr ? r0 >= bk.skip2 : bk.n0 + 128 < bk.N;
+    };
+    auto nquarters = [&](const tc::Blk& bk) { return (live(bk, 0) ? 2 : 0) + (live(bk, 1) ? 2 : 0); };
+    auto quarter = [&](const tc::Blk& bk, int i, int& h, int& qq) {
+      h = (i >> 1) == 0 && live(bk, 0) ? 0 : 1;
+      qq = i & 1;
+    };
+    auto coord = [&](const tc::Blk& bk, int h, int qq, int& dev, int& r, int& c) {
+      dev = h && bk.C2 ? bk.cdev2 : bk.cdev;
+      r = (int)(bk.crow0 + bk.m0 + rank * BM);
+      c = (int)(h && bk.C2 ? bk.ccol02 : bk.ccol0 + bk.n0 + h * 128) + qq * 64;
+    };
+    auto issue = [&](const tc::Blk& bk, int i, uint32_t slot) {  // leader: quarter i of bk into buffer slot % NB
+      int h, qq, dev, r, c;
+      quarter(bk, i, h, qq);
+      coord(bk, h, qq, dev, r, c);
+      mbar_expect_tx(&cfull[slot % NB], QF * 4);
+      tma_load_2d(qb + (slot % NB) * QF, &cmaps->m[dev], r, c, &cfull[slot % NB]);
+    };
+    uint32_t t = 0, g = 0, gi = 0;  // items, quarters consumed, quarters issued (leader)
+    int pend = 0;                   // leader: next quarter to issue, counted from the current item's first
+    tc::Blk blk, nblk;
+    bool have = next(first, blk);
+    for (int64_t item = first; have; item += stride, ++t) {
+      const int b = t & 1;
+      const bool more = next(item + stride, nblk);
+      const int ncur = nquarters(blk), nnext = more ? nquarters(nblk) : 0;
+      if (lead && pend < ncur && gi < g + NB) {
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // every buffer read by its store
+        while (pend < ncur && gi < g + NB) issue(blk, pend++, gi++);
+      }
+      mbar_wait(&tfull[b], (t >> 1) & 1);
+      tc::fence_after();
+      for (int i = 0; i < ncur; ++i, ++g) {
+        int h, qq;
+        quarter(blk, i, h, qq);
+        const uint32_t s = g % NB;
+        mbar_wait(&cfull[s], (g / NB) & 1);
+        float* cb = qb + s * QF;
+        {
+          const int c0 = ch * 32;
+          float v[32];
+          tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + b * BN + h * 128 + qq * 64 + c0, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float* cp = cb + row + (c0 + j) * BM;
+            *cp = blk.alpha * v[j] + blk.beta * *cp;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // cb writes -> the TMA store
+        asm volatile("bar.sync 1, 256;\n" ::: "memory");
+        if (lead) {
+          int dev, r, c;
+          coord(blk, h, qq, dev, r, c);
+          tma_store_2d(&cmaps->m[dev], r, c, cb);
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          // this quarter's store may still be reading cb: the refill goes into the
+          // buffer of the previous quarter, whose store has been read
+          asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+          if (gi < g + NB) {  // a buffer is free: the next quarter in order, this item or the next
+            if (pend < ncur) issue(blk, pend++, gi++);
+            else if (pend - ncur < nnext) issue(nblk, pend++ - ncur, gi++);
+          }
+        }
+        __syncwarp();  // warp 4 reconverges before the next warp-collective tcgen05.ld
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(te + 8 * b);  // TMEM accumulator b drained
+      if (lead) pend -= ncur;  // what was issued from the next item carries over
+      have = more;
+      blk = nblk;
+    }
+    if (lead) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // stores complete before exit
+  } else if (EPI == 1 && warp >= 4) {
     // ------------------------------------- TMA epilogue (8 warps, both CTAs)
     // Each CTA updates its 128 rows of the item in two 128-column halves
     // (h = 0: the item's first tile column; h = 1: columns 128.. or, for a
@@ -517,7 +609,7 @@ __device__ __forceinline__ void tck_loop_pair(const CUtensorMap* mAh, const CUte
       blk = nblk;
     }
     if (lead) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // stores complete before exit
-  } else if (!EPI && warp >= 4) {
+  } else if (EPI == 0 && warp >= 4) {
     // ---------------------------------------------------------- epilogue (8 warps, both CTAs)
     const int q = warp & 3;
     const int ch = (warp - 4) >> 2;
@@ -802,7 +894,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
                      const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, TrailParams p,
                      const int* info, const __grid_constant__ tck::CMaps cmaps) {
   static_assert(CL != 4 || BNT == 128, "the TMA-epilogue tile is 128 x 128");
-  static_assert((CL != 3 && CL != 6) || BNT == 256, "the 2-SM UMMA tile is 256 x 256");
+  static_assert((CL != 3 && CL != 6 && CL != 7) || BNT == 256, "the 2-SM UMMA tile is 256 x 256");
   constexpr int64_t BMX = (CL == 1 || CL == 4 ? 1 : 2) * tc::BM;  // rows per item (a CTA pair covers 256)
   using TZ = TrapR<BMX, BNT>;
   using TZC = TrapR<BMX / 2, BNT>;
@@ -816,7 +908,7 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
   const int64_t sc = p.nloc == p.D ? 1 : p.D;
   const int64_t ncb = p.T > BNT ? p.T / BNT : 1;
   // CL = 3 at T_A = 128: a unit is two owned tile columns (c, c + sc), one 256-wide item
-  const int64_t cpu = (CL == 3 || CL == 6) && ncb == 1 && p.cpu > 1 ? p.cpu : 1, usp = cpu * sc;
+  const int64_t cpu = (CL == 3 || CL == 6 || CL == 7) && ncb == 1 && p.cpu > 1 ? p.cpu : 1, usp = cpu * sc;
   if (p.band > 0 && sc > 1) cm += ((p.dev0 - cm % p.D) + p.D) % p.D;  // first owned column
   const int64_t nunits = ncb == 1 ? ((p.m_last - cm + sc - 1) / sc + cpu - 1) / cpu : (p.m_last - p.m_first) * ncb;
   const int64_t cm0 = cm;
@@ -939,7 +1031,8 @@ __global__ void __launch_bounds__(tck::THREADS, 1)
   };
   const int Kx = (int)(p.cplx ? 2 * p.K : p.K);
   if constexpr (CL == 3) tck::tck_loop_pair(&mAh, &mAl, &mBh, &mBl, nullptr, Kx, next);
-  else if constexpr (CL == 6) tck::tck_loop_pair<true>(&mAh, &mAl, &mBh, &mBl, &cmaps, Kx, next);
+  else if constexpr (CL == 6) tck::tck_loop_pair<1>(&mAh, &mAl, &mBh, &mBl, &cmaps, Kx, next);
+  else if constexpr (CL == 7) tck::tck_loop_pair<2>(&mAh, &mAl, &mBh, &mBl, &cmaps, Kx, next);
   else if constexpr (CL == 4) tck::tck_loop_epi(&mAh, &mAl, &mBh, &mBl, &cmaps, Kx, next);
   else tck::tck_loop<BNT, CL>(&mAh, &mAl, &mBh, &mBl, Kx, next);
 }
