@@ -1010,6 +1010,8 @@ static void launch_tck_trail(const TrailParams& p, const int* info, cudaStream_t
     // whole 256-wide column blocks (T_A a multiple of 256): the TMA epilogue in halves
     if (c == 2 && tck_pair_epi(p.cplx) == 2 && p.T % 256 == 0 && p.N % p.T == 0 && p.nloc <= MAX_LOCAL_DEV)
       return launch_tck_trail_t<256, 6>(p, info, st);
+    if (c == 2 && tck_pair_epi(p.cplx) == 4 && p.T % 256 == 0 && p.N % p.T == 0 && p.nloc <= MAX_LOCAL_DEV)
+      return launch_tck_trail_t<256, 7>(p, info, st);  // (measurement switch: the quarter ring at T_A >= 256)
     if (c == 2) return launch_tck_trail_t<256, 3>(p, info, st);
     if (c == 1) return launch_tck_trail_t<256, 2>(p, info, st);
     return launch_tck_trail_t<256, 1>(p, info, st);
