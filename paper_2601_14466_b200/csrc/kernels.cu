@@ -1717,6 +1717,49 @@ __global__ void __launch_bounds__(256) subst_gemv4_kernel(const float* __restric
   out[r] = (float)v;
 }
 
+// complex64, N_RHS = 1: two consecutive rows per lane (one 16-byte load per
+// column), 64 rows per CTA; same column split and sums as subst_gemv_kernel.
+__global__ void __launch_bounds__(256) subst_gemv2c_kernel(const float2* __restrict__ A, int64_t lda,
+                                                           const float2* __restrict__ y, float2* __restrict__ out,
+                                                           int64_t rows, int tc, int64_t ncopy, double alpha, int beta) {
+  constexpr int W = 8;
+  __shared__ double2 red[W][64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = (int64_t)blockIdx.x * 64 + 2 * lane;
+  double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  const int cpw = (tc + W - 1) / W, c0 = warp * cpw, c1 = c0 + cpw < tc ? c0 + cpw : tc;
+  if (r0 < rows) {
+    const float2* a = A + r0;
+    if (r0 + 1 < rows) {
+      for (int c = c0; c < c1; ++c) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(a + (int64_t)c * lda));
+        const double2 yv = sub_ld(__ldg(y + c));
+        acc[0] = sub_fma(acc[0], make_double2(v.x, v.y), yv);
+        acc[1] = sub_fma(acc[1], make_double2(v.z, v.w), yv);
+      }
+    } else {
+      for (int c = c0; c < c1; ++c) acc[0] = sub_fma(acc[0], sub_ld(a[(int64_t)c * lda]), sub_ld(__ldg(y + c)));
+    }
+  }
+  red[warp][2 * lane] = acc[0];
+  red[warp][2 * lane + 1] = acc[1];
+  __syncthreads();
+  if (threadIdx.x >= 64) return;
+  const int e = threadIdx.x;
+  const int64_t r = (int64_t)blockIdx.x * 64 + e;
+  if (r >= rows) return;
+  if (r < ncopy) {
+    out[r] = y[r];
+    return;
+  }
+  double2 v = red[0][e];
+#pragma unroll
+  for (int w = 1; w < W; ++w) v = sub_add(v, red[w][e]);
+  v = make_double2(alpha * v.x, alpha * v.y);
+  if (beta) v = sub_add(v, sub_ld(out[r]));
+  out[r] = sub_st<float2>(v);
+}
+
 // Backward partial sums P[chunk][c][j] = sum_{r in chunk} conj(L[r, c]) x[r, j]
 // over chunks of SUBST_CH rows.  Grid (chunk, column group): a CTA stages its
 // chunk of x in shared memory and its warps take the group's columns two at a
@@ -1815,6 +1858,14 @@ static void launch_subst_gemv(int nr, const S* A, int64_t lda, const S* y, int64
     if (nr == 1 && nrhs == 1 && lda % 4 == 0 && aligned16(A)) {
       subst_gemv4_kernel<<<(unsigned)((rows + 127) / 128), 256, 0, st>>>(A, lda, y, out, rows, tc, ncopy, alpha,
                                                                           beta);
+      BCMG_CHECK_LAUNCH();
+      return;
+    }
+  }
+  if constexpr (std::is_same_v<S, float2> && !BCMG_NO_GEMV4) {
+    if (nr == 1 && nrhs == 1 && lda % 2 == 0 && aligned16(A)) {
+      subst_gemv2c_kernel<<<(unsigned)((rows + 63) / 64), 256, 0, st>>>(A, lda, y, out, rows, tc, ncopy, alpha,
+                                                                         beta);
       BCMG_CHECK_LAUNCH();
       return;
     }
