@@ -794,7 +794,8 @@ bool pair_panels(int dt, int64_t T) {
   }();
   // 2 (default): T_A <= 512; 1: T_A <= 256 (N=65536, 8 devices, T_A=512, same box, two
   // rounds: f32 191.0 / 193.0 -> 198.8 / 201.0, c64 215.4 / 215.2 -> 215.2 / 216.0 TFLOP/s)
-  return v && (dt == R32 || dt == C64) && tc_presplit_enabled() && T <= (v >= 2 ? 512 : 256) && T % 32 == 0;
+  return v && (dt == R32 || dt == C64) && tc_presplit_enabled() && T <= (v >= 3 ? 1024 : v >= 2 ? 512 : 256) &&
+         T % 32 == 0;
 }
 
 // K-major plane map: dims {kp, rows}, box {32 k, 128 rows}, SWIZZLE_128B (the
